@@ -1,0 +1,219 @@
+// extern "C" entry points of libkfb200.so and the native fold-loop runtime:
+// per-iteration kernel sequence, CUDA-graph capture/replay, error plumbing.
+// See include/kfb200.h for the contract of each entry point.
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "kf_common.cuh"
+
+// launchers defined in the kernel translation units
+int kf_fk_launch(const kf_chain_t *c, kf_batch_t *w, const kf_status_t *status, cudaStream_t s);
+int kf_bin_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s);
+int kf_pairs_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s);
+int kf_clash_report_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s);
+int kf_solvation_launch(const kf_field_t *f, kf_batch_t *w, int n, int n_solv, const int32_t *solv_atoms,
+                        cudaStream_t s);
+int kf_sasa_api_launch(const double *pos, int n, const double *r_off, const double *r_off2,
+                       const double *samples, int N, const int64_t *nb_off, const int64_t *nb, double pad,
+                       uint8_t *counts, int32_t *critical, int64_t *covered, const double *gamma,
+                       double four_pi, double *f_exp, double *a_exp, double *cav, int nb_cap, int *overflow,
+                       cudaStream_t s);
+int kf_fixed_to_f64_launch(const long long *acc, int64_t m, double quantum, double *out, cudaStream_t s);
+int kf_solv_forces_api_launch(const double *pos, int n, const double *r_off, const double *r_off2,
+                              const int64_t *w_int, const double *samples, int N, const int64_t *nb_off,
+                              const int64_t *nb, const uint8_t *counts, const int32_t *critical, double dr,
+                              double pad, long long *acc, int nb_cap, int *overflow, cudaStream_t s);
+int kf_wrench_launch(const kf_chain_t *c, int B, const double *pos, const double *forces, double *wrench,
+                     const kf_status_t *status, cudaStream_t s);
+int kf_torque_launch(const kf_chain_t *c, const kf_field_t *f, kf_batch_t *w, const double *link_T,
+                     const double *wrench, double *side_tot, double *bb_suffix, double *tau,
+                     const kf_step_t *step, int mode, cudaStream_t s);
+int kf_kcm_step_launch(const double *tau, const double *theta, const uint8_t *frozen, int D, double kappa,
+                       double *theta_out, double *deltas, cudaStream_t s);
+
+namespace {
+thread_local std::string g_last_error;
+std::mutex g_graph_mu;
+std::unordered_map<std::string, cudaGraphExec_t> g_graphs;
+
+std::string graph_key(const kf_chain_t *c, const kf_field_t *f, const kf_batch_t *w, const kf_step_t *st,
+                      int n_iters, cudaStream_t s) {
+    std::string k;
+    k.append(reinterpret_cast<const char *>(c), sizeof(*c));
+    k.append(reinterpret_cast<const char *>(f), sizeof(*f));
+    k.append(reinterpret_cast<const char *>(w), sizeof(*w));
+    k.append(reinterpret_cast<const char *>(st), sizeof(*st));
+    k.append(reinterpret_cast<const char *>(&n_iters), sizeof(n_iters));
+    (void)s;
+    return k;
+}
+
+// One KCM iteration body (kcm.py:313-350): FK -> bin -> pairs -> [solvation] ->
+// wrenches -> torques + record + stop tests + step.
+int enqueue_iteration(const kf_chain_t *c, const kf_field_t *f, kf_batch_t *w, const kf_step_t *st,
+                      cudaStream_t s) {
+    const int n = c->n_atoms;
+    if (kf_fk_launch(c, w, w->status, s)) return 1;
+    if (kf_bin_launch(f, w, n, s)) return 1;
+    if (kf_pairs_launch(f, w, n, s)) return 1;
+    if (f->solvation && kf_solvation_launch(f, w, n, f->n_solv, f->solv_atoms, s)) return 1;
+    if (kf_wrench_launch(c, w->B, w->pos, w->forces, w->wrench, w->status, s)) return 1;
+    if (kf_torque_launch(c, f, w, w->link_T, w->wrench, w->side_tot, w->bb_suffix, w->tau, st, 1, s)) return 1;
+    return 0;
+}
+}  // namespace
+
+void kf_set_error(const char *where, cudaError_t e) {
+    g_last_error = std::string(where) + ": " + cudaGetErrorString(e);
+}
+
+extern "C" {
+
+int kf_abi_version(void) { return KF_ABI_VERSION; }
+
+size_t kf_struct_size(int which) {
+    switch (which) {
+        case 0: return sizeof(kf_chain_t);
+        case 1: return sizeof(kf_field_t);
+        case 2: return sizeof(kf_status_t);
+        case 3: return sizeof(kf_batch_t);
+        case 4: return sizeof(kf_step_t);
+        default: return 0;
+    }
+}
+
+const char *kf_last_error(void) { return g_last_error.c_str(); }
+
+int kf_device_sm_count(void) {
+    int dev = 0, sms = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
+    return sms;
+}
+
+int kf_fk(const kf_chain_t *c, kf_batch_t *w, void *stream) {
+    return kf_fk_launch(c, w, w->status, (cudaStream_t)stream);
+}
+
+int kf_nonbonded(const kf_field_t *f, kf_batch_t *w, void *stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (kf_bin_launch(f, w, f->n_atoms, s)) return 1;
+    return kf_pairs_launch(f, w, f->n_atoms, s);
+}
+
+int kf_solvation(const kf_field_t *f, kf_batch_t *w, void *stream) {
+    return kf_solvation_launch(f, w, f->n_atoms, f->n_solv, f->solv_atoms, (cudaStream_t)stream);
+}
+
+int kf_energy_reduce(const kf_field_t *f, kf_batch_t *w, int n, void *stream) {
+    kf_chain_t c;
+    std::memset(&c, 0, sizeof(c));
+    c.n_atoms = n;
+    return kf_torque_launch(&c, f, w, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 2,
+                            (cudaStream_t)stream);
+}
+
+int kf_torques_step(const kf_chain_t *c, const kf_field_t *f, kf_batch_t *w, const kf_step_t *step,
+                    void *stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (kf_wrench_launch(c, w->B, w->pos, w->forces, w->wrench, w->status, s)) return 1;
+    return kf_torque_launch(c, f, w, w->link_T, w->wrench, w->side_tot, w->bb_suffix, w->tau, step,
+                            step ? 1 : 0, s);
+}
+
+int kf_fold_iterations(const kf_chain_t *c, const kf_field_t *f, kf_batch_t *w, const kf_step_t *step,
+                       int n_iters, void *stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (n_iters <= 0) return 0;
+    const std::string key = graph_key(c, f, w, step, n_iters, s);
+    cudaGraphExec_t exec = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(g_graph_mu);
+        auto it = g_graphs.find(key);
+        if (it != g_graphs.end()) exec = it->second;
+    }
+    if (!exec) {
+        cudaGraph_t graph = nullptr;
+        KF_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "begin capture");
+        int rc = 0;
+        for (int k = 0; k < n_iters && !rc; ++k) rc = enqueue_iteration(c, f, w, step, s);
+        cudaError_t e = cudaStreamEndCapture(s, &graph);
+        if (rc) { if (graph) cudaGraphDestroy(graph); return 1; }
+        KF_CUDA(e, "end capture");
+        e = cudaGraphInstantiate(&exec, graph, 0);
+        cudaGraphDestroy(graph);
+        KF_CUDA(e, "graph instantiate");
+        std::lock_guard<std::mutex> lk(g_graph_mu);
+        g_graphs[key] = exec;
+    }
+    KF_CUDA(cudaGraphLaunch(exec, s), "graph launch");
+    return 0;
+}
+
+void kf_graph_cache_clear(void) {
+    std::lock_guard<std::mutex> lk(g_graph_mu);
+    for (auto &kv : g_graphs) cudaGraphExecDestroy(kv.second);
+    g_graphs.clear();
+}
+
+int kf_fold_iterations_eager(const kf_chain_t *c, const kf_field_t *f, kf_batch_t *w, const kf_step_t *step,
+                             int n_iters, void *stream) {
+    for (int k = 0; k < n_iters; ++k)
+        if (enqueue_iteration(c, f, w, step, (cudaStream_t)stream)) return 1;
+    return 0;
+}
+
+int kf_clash_report(const kf_field_t *f, kf_batch_t *w, void *stream) {
+    return kf_clash_report_launch(f, w, f->n_atoms, (cudaStream_t)stream);
+}
+
+int kf_sasa_pass(const double *pos, int n, const double *r_off, const double *r_off2, const double *samples,
+                 int n_samples, const int64_t *nb_off, const int64_t *nb, double pad, int nb_cap,
+                 uint8_t *counts, int32_t *critical, int64_t *covered, const double *gamma, double four_pi,
+                 double *f_exp, double *a_exp, double *cav, int *overflow, void *stream) {
+    return kf_sasa_api_launch(pos, n, r_off, r_off2, samples, n_samples, nb_off, nb, pad, counts, critical, covered,
+                              gamma, four_pi, f_exp, a_exp, cav, nb_cap, overflow, (cudaStream_t)stream);
+}
+
+int kf_fixed_to_f64(const long long *acc, int64_t m, double quantum, double *out, void *stream) {
+    return kf_fixed_to_f64_launch(acc, m, quantum, out, (cudaStream_t)stream);
+}
+
+int kf_bin(const kf_field_t *f, kf_batch_t *w, void *stream) {
+    return kf_bin_launch(f, w, f->n_atoms, (cudaStream_t)stream);
+}
+
+int kf_pairs(const kf_field_t *f, kf_batch_t *w, void *stream) {
+    return kf_pairs_launch(f, w, f->n_atoms, (cudaStream_t)stream);
+}
+
+int kf_solvation_forces(const double *pos, int n, const double *r_off, const double *r_off2, const int64_t *w_int,
+                         const double *samples, int n_samples, const int64_t *nb_off, const int64_t *nb,
+                         const uint8_t *counts, const int32_t *critical, double delta_r, double pad, int nb_cap,
+                         long long *acc, int *overflow, void *stream) {
+    return kf_solv_forces_api_launch(pos, n, r_off, r_off2, w_int, samples, n_samples, nb_off, nb, counts, critical,
+                                     delta_r, pad, acc, nb_cap, overflow, (cudaStream_t)stream);
+}
+
+int kf_link_wrenches(const kf_chain_t *c, const double *pos, const double *forces, double *wrench, void *stream) {
+    return kf_wrench_launch(c, 1, pos, forces, wrench, nullptr, (cudaStream_t)stream);
+}
+
+int kf_joint_torques(const kf_chain_t *c, const double *link_T, const double *wrench, double *side_tot,
+                     double *bb_suffix, double *tau, void *stream) {
+    kf_batch_t w;
+    std::memset(&w, 0, sizeof(w));
+    w.B = 1;
+    return kf_torque_launch(c, nullptr, &w, link_T, wrench, side_tot, bb_suffix, tau, nullptr, 0,
+                            (cudaStream_t)stream);
+}
+
+int kf_kcm_step(const double *tau, const double *theta, const uint8_t *frozen, int n_dof, double kappa,
+                double *theta_out, double *deltas, void *stream) {
+    return kf_kcm_step_launch(tau, theta, frozen, n_dof, kappa, theta_out, deltas, (cudaStream_t)stream);
+}
+
+}  // extern "C"

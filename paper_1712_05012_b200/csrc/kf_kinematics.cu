@@ -1,0 +1,142 @@
+// Forward kinematics as a parallel scan of rigid transforms (K4).
+//
+// Reference: chain.kinematic_state (/root/reference/pkg/src/kinefold/chain.py:
+// 240-261) walks links sequentially: M_l = M_parent R(axis0_l, theta_l),
+// P_l = P_parent + M_parent body0_parent, pos_a = P_l + M_l (zp_a - point0_l).
+// Written as affine maps that is T_l = T_parent o A_l with
+// A_l = (R(axis0_l, theta_l), body0_parent), an associative composition, so the
+// backbone path (phi/psi links) is a prefix scan and the <= 4-deep side
+// branches follow level by level.  fp64 throughout; the scan re-associates the
+// products, so positions differ from the sequential walk at the 1e-13 A level.
+#include "kf_common.cuh"
+
+namespace {
+
+constexpr int FK_THREADS = 256;
+
+// Rodrigues R = I + sin(t) K + (1 - cos(t)) K^2 (geometry.py:26-41), t in radians
+// from degrees as math.radians does (x * (pi / 180)).
+KF_DEV Xf local_transform(const double *axis, double theta_deg, const double *body_parent) {
+    const double deg2rad = 0.017453292519943295;
+    double s, c;
+    sincos(theta_deg * deg2rad, &s, &c);
+    const double x = axis[0], y = axis[1], z = axis[2];
+    const double omc = 1.0 - c;
+    Xf t;
+    // K^2 = a a^T - |a|^2 I, written out as the reference's (k @ k) entries
+    const double k00 = -(y * y + z * z), k11 = -(x * x + z * z), k22 = -(x * x + y * y);
+    const double k01 = x * y, k02 = x * z, k12 = y * z;
+    t.m[0] = 1.0 + omc * k00;   t.m[1] = -s * z + omc * k01; t.m[2] = s * y + omc * k02;
+    t.m[3] = s * z + omc * k01; t.m[4] = 1.0 + omc * k11;    t.m[5] = -s * x + omc * k12;
+    t.m[6] = -s * y + omc * k02; t.m[7] = s * x + omc * k12; t.m[8] = 1.0 + omc * k22;
+    t.p[0] = body_parent[0]; t.p[1] = body_parent[1]; t.p[2] = body_parent[2];
+    return t;
+}
+
+// One CTA per trajectory: local transforms, blocked backbone scan, side levels.
+__global__ void __launch_bounds__(FK_THREADS)
+fk_scan_kernel(kf_chain_t c, const double *__restrict__ theta_all, double *__restrict__ T_all,
+               const kf_status_t *__restrict__ status) {
+    const int b = blockIdx.x;
+    if (status && status[b].done) return;
+    const int L = c.n_links, D = c.n_dof;
+    const double *theta = theta_all + (size_t)b * D;
+    double *T = T_all + (size_t)b * L * KF_XF_STRIDE;
+    __shared__ double chunk[FK_THREADS][12];
+
+    // 1. local transforms (ground = identity)
+    for (int l = threadIdx.x; l < L; l += blockDim.x) {
+        Xf a;
+        if (l == 0 || c.link_dof[l] < 0) {
+            a = xf_identity();
+        } else {
+            const int p = c.link_parent[l];
+            a = local_transform(c.link_axis0 + 3 * l, theta[c.link_dof[l]], c.link_body0 + 3 * p);
+        }
+        xf_store(T + KF_XF_STRIDE * l, a);
+    }
+    __syncthreads();
+
+    // 2. backbone path: per-thread chunk prefix, then a scan of chunk totals
+    const int nb = c.n_bb;
+    const int per = (nb + blockDim.x - 1) / blockDim.x;
+    const int lo = min(nb, (int)threadIdx.x * per), hi = min(nb, lo + per);
+    Xf acc = xf_identity();
+    for (int k = lo; k < hi; ++k) {
+        double *slot = T + KF_XF_STRIDE * c.bb_order[k];
+        acc = xf_compose(acc, xf_load(slot));
+        xf_store(slot, acc);
+    }
+    {
+        double *s = chunk[threadIdx.x];
+        for (int k = 0; k < 9; ++k) s[k] = acc.m[k];
+        for (int k = 0; k < 3; ++k) s[9 + k] = acc.p[k];
+    }
+    __syncthreads();
+    for (int off = 1; off < (int)blockDim.x; off <<= 1) {
+        Xf mine = xf_load(chunk[threadIdx.x]);
+        Xf r = mine;
+        if ((int)threadIdx.x >= off) r = xf_compose(xf_load(chunk[threadIdx.x - off]), mine);
+        __syncthreads();
+        xf_store(chunk[threadIdx.x], r);
+        __syncthreads();
+    }
+    if (threadIdx.x > 0 && lo < hi) {
+        const Xf pre = xf_load(chunk[threadIdx.x - 1]);
+        for (int k = lo; k < hi; ++k) {
+            double *slot = T + KF_XF_STRIDE * c.bb_order[k];
+            xf_store(slot, xf_compose(pre, xf_load(slot)));
+        }
+    }
+    __syncthreads();
+
+    // 3. side branches, one depth level at a time
+    for (int d = 0; d < c.side_depth; ++d) {
+        for (int k = c.side_depth_off[d] + threadIdx.x; k < c.side_depth_off[d + 1]; k += blockDim.x) {
+            const int l = c.side_order[k];
+            double *slot = T + KF_XF_STRIDE * l;
+            xf_store(slot, xf_compose(xf_load(T + KF_XF_STRIDE * c.link_parent[l]), xf_load(slot)));
+        }
+        __syncthreads();
+    }
+
+    // 4. current joint axes U_l = M_l axis0_l (chain.py:257); ground keeps 0
+    for (int l = threadIdx.x; l < L; l += blockDim.x) {
+        double *slot = T + KF_XF_STRIDE * l;
+        const double *a = c.link_axis0 + 3 * l;
+        for (int r = 0; r < 3; ++r)
+            slot[12 + r] = (l == 0 || c.link_dof[l] < 0)
+                               ? 0.0 : slot[3 * r] * a[0] + slot[3 * r + 1] * a[1] + slot[3 * r + 2] * a[2];
+        slot[15] = 0.0;
+    }
+}
+
+// pos_a = P_l + M_l zrel_a over every (trajectory, atom)
+__global__ void fk_positions_kernel(kf_chain_t c, int B, const double *__restrict__ T_all,
+                                    double *__restrict__ pos_all,
+                                    const kf_status_t *__restrict__ status) {
+    const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int n = c.n_atoms;
+    if (gid >= (long long)B * n) return;
+    const int b = (int)(gid / n), a = (int)(gid % n);
+    if (status && status[b].done) return;
+    const double *t = T_all + ((size_t)b * c.n_links + c.atom_link[a]) * KF_XF_STRIDE;
+    const double zx = c.atom_zrel[3 * a], zy = c.atom_zrel[3 * a + 1], zz = c.atom_zrel[3 * a + 2];
+    double *out = pos_all + 3 * gid;
+    out[0] = t[9] + (t[0] * zx + t[1] * zy + t[2] * zz);
+    out[1] = t[10] + (t[3] * zx + t[4] * zy + t[5] * zz);
+    out[2] = t[11] + (t[6] * zx + t[7] * zy + t[8] * zz);
+}
+
+}  // namespace
+
+int kf_fk_launch(const kf_chain_t *c, kf_batch_t *w, const kf_status_t *status, cudaStream_t s) {
+    fk_scan_kernel<<<w->B, FK_THREADS, 0, s>>>(*c, w->theta, w->link_T, status);
+    KF_LAUNCH_CHECK("fk_scan_kernel");
+    const long long total = (long long)w->B * c->n_atoms;
+    if (total > 0) {
+        fk_positions_kernel<<<kf_blocks(total, 256), 256, 0, s>>>(*c, w->B, w->link_T, w->pos, status);
+        KF_LAUNCH_CHECK("fk_positions_kernel");
+    }
+    return 0;
+}

@@ -1,0 +1,262 @@
+// Link wrenches, suffix-scan joint torques, energy reduction, records, stop
+// tests and the max-normalised compliance step (K6 + K7).
+//
+// Reference: link_wrenches (/root/reference/pkg/src/kinefold/kcm.py:177-188),
+// joint_torques (:196-240), kcm_step (:264-274) with apply_deltas
+// (chain.py:93-101), and fold's per-iteration bookkeeping (kcm.py:325-350).
+//
+// Wrenches repeat the reference's arithmetic (numpy cross product, bincount
+// summation in ascending atom order), so they are bit-identical given the
+// same positions and forces.  Joint torques replace the sequential suffix
+// loop with a blocked parallel suffix scan of 6-vectors (one CTA per
+// trajectory); tau_max is an exact max-reduction and the step reproduces
+// numpy's float remainder twice, so theta' is bit-identical given tau.
+#include "kf_common.cuh"
+
+namespace {
+
+constexpr int TQ_THREADS = 512;
+
+struct W6 { double f[3], t[3]; };
+
+KF_DEV W6 w6_zero() { W6 r; for (int k = 0; k < 3; ++k) r.f[k] = r.t[k] = 0.0; return r; }
+KF_DEV W6 w6_load(const double *s) { W6 r; for (int k = 0; k < 3; ++k) { r.f[k] = s[k]; r.t[k] = s[3 + k]; } return r; }
+KF_DEV void w6_store(double *d, const W6 &r) { for (int k = 0; k < 3; ++k) { d[k] = r.f[k]; d[3 + k] = r.t[k]; } }
+KF_DEV void w6_add(W6 &a, const W6 &b) { for (int k = 0; k < 3; ++k) { a.f[k] += b.f[k]; a.t[k] += b.t[k]; } }
+
+// tau = u . T - (u x p) . F  (kcm.py:204-207), u = current axis, p = joint point
+KF_DEV double project(const double *X, const W6 &w) {
+    const double u0 = X[12], u1 = X[13], u2 = X[14];
+    const double p0 = X[9], p1 = X[10], p2 = X[11];
+    const double c0 = u1 * p2 - u2 * p1, c1 = u2 * p0 - u0 * p2, c2 = u0 * p1 - u1 * p0;
+    return (u0 * w.t[0] + u1 * w.t[1] + u2 * w.t[2]) - (c0 * w.f[0] + c1 * w.f[1] + c2 * w.f[2]);
+}
+
+// F_l = sum F_a, T_l = sum r_a x F_a over the link's atoms in ascending order
+// (np.cross + np.bincount, kcm.py:181-187): exact same roundings.
+__global__ void wrench_kernel(kf_chain_t c, int B, const double *__restrict__ pos_all,
+                              const double *__restrict__ f_all, double *__restrict__ wrench_all,
+                              const kf_status_t *status) {
+    const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int L = c.n_links, n = c.n_atoms;
+    if (gid >= (long long)B * L) return;
+    const int b = (int)(gid / L), l = (int)(gid % L);
+    if (status && (status[b].done || status[b].error)) return;
+    const double *pos = pos_all + (size_t)b * n * 3;
+    const double *frc = f_all + (size_t)b * n * 3;
+    double F0 = 0.0, F1 = 0.0, F2 = 0.0, T0 = 0.0, T1 = 0.0, T2 = 0.0;
+    for (int e = c.link_atom_off[l]; e < c.link_atom_off[l + 1]; ++e) {
+        const int a = c.link_atoms[e];
+        const double r0 = pos[3 * a], r1 = pos[3 * a + 1], r2 = pos[3 * a + 2];
+        const double g0 = frc[3 * a], g1 = frc[3 * a + 1], g2 = frc[3 * a + 2];
+        F0 = xadd(F0, g0); F1 = xadd(F1, g1); F2 = xadd(F2, g2);
+        T0 = xadd(T0, xsub(xmul(r1, g2), xmul(r2, g1)));
+        T1 = xadd(T1, xsub(xmul(r2, g0), xmul(r0, g2)));
+        T2 = xadd(T2, xsub(xmul(r0, g1), xmul(r1, g0)));
+    }
+    double *o = wrench_all + 6 * gid;
+    o[0] = F0; o[1] = F1; o[2] = F2; o[3] = T0; o[4] = T1; o[5] = T2;
+}
+
+struct TorqueArgs {
+    const double *link_T;      // [B][L][KF_XF_STRIDE]
+    const double *wrench;      // [B][L][6]
+    double *side_tot;          // [B][n_res][6]
+    double *bb_suffix;         // [B][n_bb][6]
+    double *tau;               // [B][D]
+};
+
+// One CTA per trajectory.  mode: 0 = torques only (API), 1 = fold iteration,
+// 2 = energy reduction only (Field.evaluate)
+__global__ void __launch_bounds__(TQ_THREADS)
+torque_step_kernel(kf_chain_t c, kf_field_t f, TorqueArgs ta, kf_batch_t w, kf_step_t step, int mode) {
+    const int b = blockIdx.x;
+    kf_status_t *st = w.status ? w.status + b : nullptr;
+    if (st && st->done) return;
+    __shared__ double red[32];
+    __shared__ double chunk[TQ_THREADS][6];
+    __shared__ int stop_reason;
+    if (st && st->error) {   // domain error this iteration: freeze, no record, no step
+        if (threadIdx.x == 0) st->done = 1;
+        return;
+    }
+    const int L = c.n_links, D = c.n_dof, R = c.n_res, nb = c.n_bb;
+    const double *T = ta.link_T + (size_t)b * L * KF_XF_STRIDE;
+    const double *Wr = ta.wrench + (size_t)b * L * 6;
+    double *side = ta.side_tot + (size_t)b * R * 6;
+    double *suf = ta.bb_suffix + (size_t)b * nb * 6;
+    double *tau = ta.tau + (size_t)b * D;
+
+    if (mode != 2) {
+    // 1. side branches: plain suffix in chi order, total folded into phi (kcm.py:209-225)
+    for (int r = threadIdx.x; r < R; r += blockDim.x) {
+        W6 agg = w6_zero();
+        for (int e = c.chi_res_off[r + 1] - 1; e >= c.chi_res_off[r]; --e) {
+            const int l = c.chi_links[e];
+            w6_add(agg, w6_load(Wr + 6 * l));
+            tau[c.link_dof[l]] = project(T + KF_XF_STRIDE * l, agg);
+        }
+        w6_store(side + 6 * r, agg);
+    }
+    __syncthreads();
+
+    // 2. backbone reverse suffix over links in dof order (kcm.py:227-239)
+    const int per = (nb + blockDim.x - 1) / blockDim.x;
+    const int lo = min(nb, (int)threadIdx.x * per), hi = min(nb, lo + per);
+    W6 acc = w6_zero();
+    for (int k = hi - 1; k >= lo; --k) {
+        w6_add(acc, w6_load(Wr + 6 * c.bb_by_dof[k]));
+        const int r = c.bb_side_res[k];          // phi link: its residue's side total joins here
+        if (r >= 0) w6_add(acc, w6_load(side + 6 * r));
+        w6_store(suf + 6 * k, acc);
+    }
+    for (int q = 0; q < 3; ++q) { chunk[threadIdx.x][q] = acc.f[q]; chunk[threadIdx.x][3 + q] = acc.t[q]; }
+    __syncthreads();
+    // inclusive suffix scan of chunk totals (Hillis-Steele, right to left)
+    for (int off = 1; off < (int)blockDim.x; off <<= 1) {
+        double v[6];
+        for (int q = 0; q < 6; ++q) v[q] = chunk[threadIdx.x][q];
+        if (threadIdx.x + off < blockDim.x)
+            for (int q = 0; q < 6; ++q) v[q] += chunk[threadIdx.x + off][q];
+        __syncthreads();
+        for (int q = 0; q < 6; ++q) chunk[threadIdx.x][q] = v[q];
+        __syncthreads();
+    }
+    W6 later = w6_zero();
+    if (threadIdx.x + 1 < blockDim.x) later = w6_load(chunk[threadIdx.x + 1]);
+    for (int k = lo; k < hi; ++k) {
+        const int l = c.bb_by_dof[k];
+        W6 s = w6_load(suf + 6 * k);
+        w6_add(s, later);
+        tau[c.link_dof[l]] = project(T + KF_XF_STRIDE * l, s);
+    }
+    __syncthreads();
+    }
+    if (mode == 0) return;
+
+    // 3. tau_max over free joints (kcm.py:325-326)
+    const uint8_t *frozen = w.frozen + (size_t)b * D;
+    double tmax = 0.0;
+    if (mode == 1) {
+        for (int d = threadIdx.x; d < D; d += blockDim.x)
+            if (!frozen[d]) tmax = fmax(tmax, fabs(tau[d]));
+        tmax = block_max(tmax, red);
+    }
+
+    // 4. energies: full-list halves summed in a fixed order
+    const int n = c.n_atoms;
+    const double *ea = w.e_atom + (size_t)b * n * 2;
+    double se = 0.0, sv = 0.0, sc = 0.0, sp = 0.0;
+    for (int a = threadIdx.x; a < n; a += blockDim.x) {
+        se += ea[2 * a]; sv += ea[2 * a + 1];
+        if (f.solvation) sc += w.cav_atom[(size_t)b * n + a];
+        sp += (double)w.pair_count[(size_t)b * n + a];
+    }
+    se = block_sum(se, red);
+    sv = block_sum(sv, red);
+    sc = f.solvation ? block_sum(sc, red) : 0.0;
+    sp = block_sum(sp, red);
+    const double ge = 0.5 * se, gv = 0.5 * sv, gc = sc;
+    if (mode == 2) {   // Field.evaluate: energies only
+        if (threadIdx.x == 0) {
+            double *e = w.energy + 3 * (size_t)b;
+            e[0] = ge; e[1] = gv; e[2] = gc;
+            if (st) st->n_pairs = (long long)(0.5 * sp);
+        }
+        return;
+    }
+    double *th = w.theta + (size_t)b * D;
+
+    // 5. record + stop tests (thread 0), theta copy (all)
+    const int it = st->iter;
+    if (threadIdx.x == 0) {
+        double *e = w.energy + 3 * (size_t)b;
+        e[0] = ge; e[1] = gv; e[2] = gc;
+        st->n_pairs = (long long)(0.5 * sp);
+        int reason = KF_REASON_NONE;
+        if (it < w.max_records) {
+            double *rec = w.rec_energy + ((size_t)b * w.max_records + it) * 4;
+            rec[0] = ge; rec[1] = gv; rec[2] = gc; rec[3] = tmax;
+        }
+        if (it == 0) st->tau0 = tmax;
+        if (mode == 1) {
+            const double tau0 = st->tau0;
+            if (tmax == 0.0) reason = KF_REASON_TORQUE_FREE;
+            else if (step.torque_tol > 0 && tmax < step.torque_tol) reason = KF_REASON_TORQUE_TOL;
+            else if (step.torque_tol_rel > 0 && tmax < step.torque_tol_rel * tau0) reason = KF_REASON_TORQUE_TOL_REL;
+            else if (step.energy_window && it >= step.energy_window && it < w.max_records) {
+                const double *r0 = w.rec_energy + ((size_t)b * w.max_records + it) * 4;
+                const double *r1 = w.rec_energy + ((size_t)b * w.max_records + it - step.energy_window) * 4;
+                const double g0 = (r0[0] + r0[1]) + r0[2], g1 = (r1[0] + r1[1]) + r1[2];
+                if (fabs(g0 - g1) < step.energy_tol) reason = KF_REASON_PLATEAU;
+            }
+        }
+        stop_reason = reason;
+    }
+    if (w.record_theta && it < w.max_records) {
+        double *rt = w.rec_theta + ((size_t)b * w.max_records + it) * D;
+        for (int d = threadIdx.x; d < D; d += blockDim.x) rt[d] = th[d];
+    }
+    __syncthreads();
+    const int reason = stop_reason;
+
+    // 6. compliance step: theta' = mod(mod(theta + kappa*tau/tau_max)) on free joints
+    if (reason == KF_REASON_NONE) {
+        for (int d = threadIdx.x; d < D; d += blockDim.x) {
+            const double delta = frozen[d] ? 0.0 : __ddiv_rn(xmul(step.kappa, tau[d]), tmax);
+            th[d] = np_mod360(np_mod360(xadd(th[d], delta)));
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        st->iter = it + 1;
+        if (reason != KF_REASON_NONE) { st->done = 1; st->reason = reason; }
+        else if (it + 1 >= step.max_iters) { st->done = 1; st->reason = KF_REASON_MAX_ITERS; }
+    }
+}
+
+// kcm_step for the API (B = 1): deltas and theta' (kcm.py:264-274).
+__global__ void kcm_step_api_kernel(const double *tau, const double *theta, const uint8_t *frozen, int D,
+                                    double kappa, double *theta_out, double *deltas) {
+    __shared__ double red[32];
+    double tmax = 0.0;
+    for (int d = threadIdx.x; d < D; d += blockDim.x)
+        if (!frozen[d]) tmax = fmax(tmax, fabs(tau[d]));
+    tmax = block_max(tmax, red);
+    for (int d = threadIdx.x; d < D; d += blockDim.x) {
+        double delta = 0.0;
+        if (tmax != 0.0 && !frozen[d]) delta = __ddiv_rn(xmul(kappa, tau[d]), tmax);
+        deltas[d] = delta;
+        theta_out[d] = tmax == 0.0 ? theta[d] : np_mod360(np_mod360(xadd(theta[d], delta)));
+    }
+}
+
+}  // namespace
+
+int kf_wrench_launch(const kf_chain_t *c, int B, const double *pos, const double *forces, double *wrench,
+                     const kf_status_t *status, cudaStream_t s) {
+    const long long total = (long long)B * c->n_links;
+    wrench_kernel<<<kf_blocks(total, 128), 128, 0, s>>>(*c, B, pos, forces, wrench, status);
+    KF_LAUNCH_CHECK("wrench_kernel");
+    return 0;
+}
+
+int kf_torque_launch(const kf_chain_t *c, const kf_field_t *f, kf_batch_t *w, const double *link_T,
+                     const double *wrench, double *side_tot, double *bb_suffix, double *tau,
+                     const kf_step_t *step, int mode, cudaStream_t s) {
+    TorqueArgs ta{link_T, wrench, side_tot, bb_suffix, tau};
+    kf_step_t st{};
+    if (step) st = *step;
+    kf_field_t fz{};
+    if (f) fz = *f;
+    torque_step_kernel<<<w->B, TQ_THREADS, 0, s>>>(*c, fz, ta, *w, st, mode);
+    KF_LAUNCH_CHECK("torque_step_kernel");
+    return 0;
+}
+
+int kf_kcm_step_launch(const double *tau, const double *theta, const uint8_t *frozen, int D, double kappa,
+                       double *theta_out, double *deltas, cudaStream_t s) {
+    kcm_step_api_kernel<<<1, 512, 0, s>>>(tau, theta, frozen, D, kappa, theta_out, deltas);
+    KF_LAUNCH_CHECK("kcm_step_api_kernel");
+    return 0;
+}

@@ -1,0 +1,129 @@
+"""Cavity (SASA) solvation by sample enumeration: types and the drop-in API.
+
+Types and setup mirror /root/reference/pkg/src/kinefold/solvation.py:32-126
+(``SolvationConfig``, the deterministic geodesic ``generate_samples``,
+``ExposureStates``, ``SasaResult``, ``check_cav_cutoff``) and the fixed-point
+quantum (:184-191).  ``sasa_pass`` (:135-181) and ``solvation_forces``
+(:194-255) run on the GPU (csrc/kf_solvation.cu) and are bit-identical to the
+reference: same fp64 coverage tests, same int64 fixed point.  ``threads`` is
+accepted for API compatibility; the GPU result is schedule-independent like
+the reference's.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from .errors import ConfigurationError
+
+MIN_SAMPLES = 12
+FIXED_POINT_BITS = 36
+
+
+@dataclass(frozen=True)
+class SolvationConfig:
+    probe_radius: float = 1.4
+    delta_r: float = 1e-2
+    samples: int = 1024
+    sampling: str = "geodesic"
+    seed: int = 0
+    threads: int = 1
+
+    def __post_init__(self):
+        if min(self.probe_radius, self.delta_r) <= 0 or self.samples < MIN_SAMPLES:
+            raise ConfigurationError(
+                "probe radius and delta_r must be positive, samples >= 12")
+
+
+@dataclass(frozen=True)
+class SampleSphere:
+    points: np.ndarray
+    mode: str = "geodesic"
+
+    @property
+    def n(self) -> int:
+        return len(self.points)
+
+
+def generate_samples(n: int, mode: str = "geodesic", seed: int = 0) -> SampleSphere:
+    """Latitude orbits, points per orbit proportional to sin(polar), golden-ratio
+    azimuth offsets (solvation.py:64-97).  Once per system, host numpy."""
+    if n < MIN_SAMPLES:
+        raise ConfigurationError(f"need at least {MIN_SAMPLES} sample points, got {n}")
+    if mode == "random":
+        v = np.random.default_rng(seed).normal(size=(n, 3))
+        return SampleSphere(v / np.linalg.norm(v, axis=1, keepdims=True), mode)
+    if mode != "geodesic":
+        raise ConfigurationError(f"unknown sampling mode {mode!r}")
+    n_orb = max(2 * int(round(math.sqrt(math.pi * n) / 4.0)), 2)
+    polar = (np.arange(n_orb) + 0.5) * math.pi / n_orb
+    w = np.sin(polar)
+    ideal = n * w / w.sum()
+    per_orbit = np.floor(ideal).astype(int)
+    short = n - per_orbit.sum()
+    per_orbit[np.argsort(-(ideal - per_orbit), kind="stable")[:short]] += 1
+    pts = np.empty((n, 3))
+    at = 0
+    golden = 0.618033988749895
+    for t, cnt in enumerate(per_orbit):
+        if cnt == 0:
+            continue
+        az = 2.0 * math.pi * (np.arange(cnt) + (t * golden) % 1.0) / cnt
+        s, z = math.sin(polar[t]), math.cos(polar[t])
+        pts[at:at + cnt, 0] = s * np.cos(az)
+        pts[at:at + cnt, 1] = s * np.sin(az)
+        pts[at:at + cnt, 2] = z
+        at += cnt
+    pts /= np.linalg.norm(pts, axis=1, keepdims=True)
+    return SampleSphere(pts, mode)
+
+
+@dataclass
+class ExposureStates:
+    counts: np.ndarray    # uint8 0/1/2 per (atom, sample)
+    critical: np.ndarray  # int32 coverer where count == 1, else -1
+
+
+@dataclass(frozen=True)
+class SasaResult:
+    f_exp: np.ndarray
+    a_exp: np.ndarray
+    g_cav: float
+
+
+def offset_radii(params, config: SolvationConfig) -> np.ndarray:
+    return params.R + config.probe_radius
+
+
+def check_cav_cutoff(params, config: SolvationConfig, d_cut_cav: float) -> None:
+    """Setup check 2 (R_max + probe) <= d_cav (solvation.py:119-126)."""
+    needed = 2.0 * (float(np.max(params.R)) + config.probe_radius)
+    if needed > d_cut_cav:
+        raise ConfigurationError(
+            f"cavity cutoff {d_cut_cav} A below 2(R_max + probe) = {needed:.2f} A")
+
+
+def force_quantum(params, r_off: np.ndarray, nq: int, delta_r: float):
+    """Integer event magnitudes and the power-of-two quantum (solvation.py:184-191)."""
+    delta = 4.0 * math.pi * params.gamma * r_off * r_off / (nq * delta_r)
+    peak = float(np.max(np.abs(delta))) if len(delta) else 0.0
+    if peak == 0.0:
+        return np.zeros(len(delta), np.int64), 1.0
+    quantum = 2.0 ** (math.floor(math.log2(peak)) - FIXED_POINT_BITS)
+    return np.round(delta / quantum).astype(np.int64), quantum
+
+
+def sasa_pass(positions, params, neighbors, sphere: SampleSphere,
+              config: SolvationConfig = SolvationConfig()):
+    from . import device
+    return device.sasa_pass(positions, params, neighbors, sphere, config)
+
+
+def solvation_forces(positions, params, neighbors, sphere: SampleSphere,
+                     states: ExposureStates,
+                     config: SolvationConfig = SolvationConfig()) -> np.ndarray:
+    from . import device
+    return device.solvation_forces(positions, params, neighbors, sphere, states, config)
