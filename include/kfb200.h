@@ -102,6 +102,7 @@ typedef struct {
     unsigned long long clash_key;  /* (i << 32) | j of the reported clash pair     */
     double tau0;
     long long n_pairs;     /* pairs with d <= elec cutoff, last evaluation        */
+    long long n_pairs_vdw; /* pairs with d <= vdW cutoff, last evaluation         */
 } kf_status_t;
 
 enum { KF_REASON_NONE = 0, KF_REASON_MAX_ITERS = 1, KF_REASON_TORQUE_FREE = 2,
@@ -121,13 +122,21 @@ typedef struct {
     double  *link_T;                /* [B][L][16]: rotation (row-major 9), joint point (3), axis (3), pad */
     double  *pos;                   /* [B][n][3]                                   */
     double  *forces;                /* [B][n][3]                                   */
-    /* spatial hash */
-    int32_t *bucket_count;          /* [B][n_buckets]                              */
-    int32_t *bucket_start;          /* [B][n_buckets+1]                            */
-    int32_t *atom_slot;             /* [B][n] slot inside its bucket               */
-    int32_t *atom_cell;             /* [B][n][3] integer cell                      */
-    int32_t *sorted_atom;           /* [B][n] atoms in bucket order                */
-    double  *sorted_pos;            /* [B][n][4] x, y, z, packed cell (bit cast)    */
+    /* spatial hash: per trajectory an open-addressing table of H = n_buckets
+       slots, one slot per occupied cell (key = packed integer cell)          */
+    unsigned long long *cell_key;   /* [B][H], ~0 = empty                          */
+    int32_t *cell_cnt;              /* [B][H] atoms in the slot's cell             */
+    int32_t *cell_start;            /* [B][H] first sorted index of the cell       */
+    int32_t *occ;                   /* [B][H] occupied slots (first occ_count[b])  */
+    int32_t *occ_count;             /* [B]                                         */
+    int32_t *occ_offset;            /* [B+1] prefix of occ_count (work items)      */
+    int32_t *atom_slot;             /* [B][n] slot of the atom's cell              */
+    int32_t *atom_rank;             /* [B][n] arrival rank inside the cell         */
+    int32_t *sorted_atom;           /* [B][n] atoms grouped by cell, ascending     */
+    float   *s_rel;                 /* [B][n][4] fp32 offset from the cell centre  */
+    double  *s_pos;                 /* [B][n][4] fp64 position (4th: unused)       */
+    float   *s_par;                 /* [B][n][4] q, R, sqrt(eps), 0                */
+    int32_t *s_aux;                 /* [B][n][4] atom, residue, chain flag, 0      */
     /* nonbonded */
     double  *e_atom;                /* [B][n][2] per-atom elec / vdw (full list)   */
     int32_t *pair_count;            /* [B][n] elec-cutoff partners per atom        */
@@ -205,6 +214,12 @@ void kf_graph_cache_clear(void);
 /* Smallest-(i, j) clashing pair among pairs at the minimum distance, for the
  * StericClashError message (forcefield.py:84-88).  Run only on error. */
 int kf_clash_report(const kf_field_t *f, kf_batch_t *w, void *stream);
+
+/* Kernel launches enqueued per loop iteration (bench bookkeeping). */
+int kf_kernels_per_iteration(int solvation);
+/* Issue-rate microbenchmark of this GPU: kind 0 = FP32 FFMA, 1 = FP64 DFMA.
+ * Writes FLOP/s (FMA = 2 FLOP) measured with events on `stream` to *out. */
+int kf_peak_flops(int kind, double *out, void *stream);
 
 /* ---- reference-API entry points (B = 1, parity and drop-in calls) -------- */
 

@@ -46,15 +46,16 @@ class KfStatus(C.Structure):
     _fields_ = [("iter", I32), ("done", I32), ("reason", I32), ("error", I32),
                 ("err_iter", I32), ("clash_i", I32), ("clash_j", I32), ("overflow", I32),
                 ("dmin_bits", C.c_uint64), ("clash_key", C.c_uint64), ("tau0", F64),
-                ("n_pairs", C.c_int64)]
+                ("n_pairs", C.c_int64), ("n_pairs_vdw", C.c_int64)]
 
 
 class KfBatch(C.Structure):
     _fields_ = [("B", I32), ("n_buckets", I32), ("nb_cap", I32), ("record_theta", I32),
                 ("max_records", I32), ("_pad", I32)] + [
         (name, P) for name in (
-            "theta", "frozen", "link_T", "pos", "forces", "bucket_count", "bucket_start",
-            "atom_slot", "atom_cell", "sorted_atom", "sorted_pos", "e_atom", "pair_count",
+            "theta", "frozen", "link_T", "pos", "forces", "cell_key", "cell_cnt", "cell_start",
+            "occ", "occ_count", "occ_offset", "atom_slot", "atom_rank", "sorted_atom", "s_rel",
+            "s_pos", "s_par", "s_aux", "e_atom", "pair_count",
             "solv_acc", "cav_atom", "f_exp", "a_exp", "wrench", "side_tot", "bb_suffix", "tau", "energy", "status",
             "rec_energy", "rec_theta")]
 
@@ -103,6 +104,8 @@ _PROTOS = {
                            P, P, P, P, P]),
     "kf_fixed_to_f64": (I32, [P, C.c_int64, F64, P, P]),
     "kf_bin": (I32, [P, P, P]),
+    "kf_kernels_per_iteration": (I32, [C.c_int]),
+    "kf_peak_flops": (I32, [C.c_int, P, P]),
     "kf_pairs": (I32, [P, P, P]),
     "kf_solvation_forces": (I32, [P, C.c_int, P, P, P, P, C.c_int, P, P, P, P, F64, F64,
                                   C.c_int, P, P, P]),

@@ -166,6 +166,12 @@ int kf_fold_iterations_eager(const kf_chain_t *c, const kf_field_t *f, kf_batch_
     return 0;
 }
 
+int kf_kernels_per_iteration(int solvation) {
+    // fk: scan + positions; bin: count, scan, scatter, finalize; pairs; wrench; torque
+    // (+ solvation: hot kernel, combine).  Memsets are not counted.
+    return 9 + (solvation ? 2 : 0);
+}
+
 int kf_clash_report(const kf_field_t *f, kf_batch_t *w, void *stream) {
     return kf_clash_report_launch(f, w, f->n_atoms, (cudaStream_t)stream);
 }

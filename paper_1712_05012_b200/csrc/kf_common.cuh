@@ -89,6 +89,33 @@ KF_DEV long long pack_cell(int cx, int cy, int cz) {
     return ((long long)(cx & m) << 42) | ((long long)(cy & m) << 21) | (long long)(cz & m);
 }
 
+KF_DEV void unpack_cell(long long p, int &cx, int &cy, int &cz) {
+    const unsigned long long u = (unsigned long long)p;
+    cx = (int)((long long)(u << 1) >> 43);
+    cy = (int)((long long)(u << 22) >> 43);
+    cz = (int)((long long)(u << 43) >> 43);
+}
+// Slot of cell (cx, cy, cz) in a trajectory's open-addressing table, or -1.
+KF_DEV int cell_probe(const unsigned long long *tk, uint32_t H, int cx, int cy, int cz) {
+    const unsigned long long key = (unsigned long long)pack_cell(cx, cy, cz);
+    uint32_t slot = cell_hash(cx, cy, cz, H - 1);
+    for (;;) {
+        const unsigned long long k = tk[slot];
+        if (k == key) return (int)slot;
+        if (k == ~0ull) return -1;
+        slot = (slot + 1) & (H - 1);
+    }
+}
+// Trajectory owning work item `item` given the exclusive prefix off[0..B].
+KF_DEV int item_owner(const int32_t *off, int B, int item) {
+    int lo = 0, hi = B;
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (off[mid] <= item) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
 // Interaction class 1..4 (topology.py:153-178): tree neighbours only when both
 // atoms are chain atoms within one residue of each other; 1-2 beats 1-3 beats 1-4.
 KF_DEV int classify_pair(const kf_field_t &f, int i, int j, int pi, int gpi, int ggi, int ri, bool ci) {

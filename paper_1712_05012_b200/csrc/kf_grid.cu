@@ -1,20 +1,29 @@
-// Spatial binning (K1) for the hot path: per-atom cell key, warp-aggregated
-// bucket histogram, per-trajectory exclusive scan, scatter, and a
-// deterministic in-bucket order (ascending atom index).
+// Spatial binning (K1) for the hot path.
 //
 // Reference: spatial.build_grid (/root/reference/pkg/src/kinefold/spatial.py:
-// 83-114).  The reference sizes cells from the bounding box (~alpha*n cells);
-// its pair sets are filtered exactly afterwards (spatial.py:233-241), so any
-// superset gives bit-identical pairs.  The hot path therefore
-// bins on a fixed cell edge into a power-of-two hash table per trajectory —
-// no bounding-box reduction and no host round trip inside the loop.  The
-// reference grid itself (bit-exact cell_index / occupied / starts / order) is
-// produced by the API kernels in kf_refgrid.cu.
+// 83-114) sizes cells from the bounding box (~alpha*n cells) and the pair sets
+// are filtered exactly afterwards (spatial.py:233-241), so any superset grid
+// gives bit-identical pairs.  The hot path therefore bins on
+// a fixed cell edge >= the largest interaction reach (9 A: a 27-cell stencil)
+// into a per-trajectory open-addressing table with ONE slot per occupied cell:
+// no bounding-box reduction, no host round trip, and a probe either finds the
+// cell or proves it empty, so stencil walks never see foreign atoms.
+//
+//   insert   per atom: cell key -> CAS into the table (linear probing), the
+//            first inserter appends the slot to the trajectory's occupied list,
+//            rank = warp-aggregated atomicAdd on the slot count
+//   scan     per trajectory: starts of occupied cells (list order) and the
+//            work-item prefix over trajectories
+//   scatter  sorted_atom[start + rank] = atom
+//   finalize per occupied cell: members sorted by atom index (deterministic
+//            visit order) and the cell-ordered SoA the pair kernel stages:
+//            fp32 offset from the cell centre, fp64 position, params, aux ints
 #include "kf_common.cuh"
 
 namespace {
 
-constexpr int CELL_LIM = (1 << 20) - 1;
+constexpr int CELL_LIM = (1 << 20) - 2;
+constexpr unsigned long long EMPTY = ~0ull;
 
 KF_DEV int cell_coord(double x, double inv_cell) {
     double c = floor(x * inv_cell);
@@ -22,9 +31,11 @@ KF_DEV int cell_coord(double x, double inv_cell) {
     return (int)c;
 }
 
-__global__ void bin_count_kernel(kf_field_t f, int B, int n, const double *__restrict__ pos,
-                                 int32_t *__restrict__ atom_cell, int32_t *__restrict__ atom_slot,
-                                 int32_t *__restrict__ bucket_count, kf_status_t *status) {
+__global__ void bin_insert_kernel(kf_field_t f, int B, int n, const double *__restrict__ pos,
+                                  unsigned long long *__restrict__ keys, int32_t *__restrict__ cnt,
+                                  int32_t *__restrict__ occ, int32_t *__restrict__ occ_count,
+                                  int32_t *__restrict__ atom_slot, int32_t *__restrict__ atom_rank,
+                                  kf_status_t *status) {
     const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (gid >= (long long)B * n) return;
     const int b = (int)(gid / n);
@@ -39,38 +50,54 @@ __global__ void bin_count_kernel(kf_field_t f, int B, int n, const double *__res
         const double inv = 1.0 / f.cell;
         cx = cell_coord(x, inv); cy = cell_coord(y, inv); cz = cell_coord(z, inv);
     }
-    atom_cell[3 * gid] = cx; atom_cell[3 * gid + 1] = cy; atom_cell[3 * gid + 2] = cz;
-    const uint32_t key = (uint32_t)b * H + cell_hash(cx, cy, cz, H - 1);
-    // warp-aggregated atomics: consecutive chain atoms usually share a cell
+    const unsigned long long key = (unsigned long long)pack_cell(cx, cy, cz);
+    unsigned long long *tk = keys + (size_t)b * H;
+    uint32_t slot = cell_hash(cx, cy, cz, H - 1);
+    // warp leaders insert each distinct key once
     const unsigned active = __activemask();
-    const unsigned peers = __match_any_sync(active, key);
+    const unsigned same = __match_any_sync(active, key) & __match_any_sync(active, b);
     const int lane = threadIdx.x & 31;
-    const int leader = __ffs(peers) - 1;
-    const int rank = __popc(peers & ((1u << lane) - 1u));
+    const int leader = __ffs(same) - 1;
+    if (lane == leader) {
+        for (;;) {
+            const unsigned long long prev = atomicCAS(&tk[slot], EMPTY, key);
+            if (prev == EMPTY) {
+                occ[(size_t)b * H + atomicAdd(&occ_count[b], 1)] = (int32_t)slot;
+                break;
+            }
+            if (prev == key) break;
+            slot = (slot + 1) & (H - 1);
+        }
+    }
+    slot = __shfl_sync(same, slot, leader);
+    const int rank_in = __popc(same & ((1u << lane) - 1u));
     int base = 0;
-    if (lane == leader) base = atomicAdd(&bucket_count[key], __popc(peers));
-    base = __shfl_sync(peers, base, leader);
-    atom_slot[gid] = base + rank;
+    if (lane == leader) base = atomicAdd(&cnt[(size_t)b * H + slot], __popc(same));
+    base = __shfl_sync(same, base, leader);
+    atom_slot[gid] = (int32_t)slot;
+    atom_rank[gid] = base + rank_in;
 }
 
-// Exclusive scan of each trajectory's bucket counts (one CTA per trajectory).
+// Per trajectory: exclusive scan of the occupied cells' counts in list order.
 __global__ void __launch_bounds__(1024)
-bucket_scan_kernel(int H, const int32_t *__restrict__ count, int32_t *__restrict__ start,
-                   const kf_status_t *status) {
+cell_scan_kernel(int H, const int32_t *__restrict__ occ, const int32_t *__restrict__ occ_count,
+                 const int32_t *__restrict__ cnt, int32_t *__restrict__ start, const kf_status_t *status) {
     const int b = blockIdx.x;
     if (status[b].done) return;
-    const int32_t *cnt = count + (size_t)b * H;
-    int32_t *out = start + (size_t)b * (H + 1);
-    const int per = (H + blockDim.x - 1) / blockDim.x;
-    const int lo = min(H, (int)threadIdx.x * per), hi = min(H, lo + per);
+    const int m = occ_count[b];
+    const int32_t *ob = occ + (size_t)b * H;
+    const int32_t *cb = cnt + (size_t)b * H;
+    int32_t *sb = start + (size_t)b * H;
+    const int per = (m + blockDim.x - 1) / blockDim.x;
+    const int lo = min(m, (int)threadIdx.x * per), hi = min(m, lo + per);
     int local = 0;
-    for (int k = lo; k < hi; ++k) local += cnt[k];
+    for (int k = lo; k < hi; ++k) local += cb[ob[k]];
     __shared__ int wsum[32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     int incl = local;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-        int v = __shfl_up_sync(0xffffffffu, incl, o);
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
         if (lane >= o) incl += v;
     }
     if (lane == 31) wsum[wid] = incl;
@@ -79,55 +106,104 @@ bucket_scan_kernel(int H, const int32_t *__restrict__ count, int32_t *__restrict
         int v = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            int u = __shfl_up_sync(0xffffffffu, v, o);
+            const int u = __shfl_up_sync(0xffffffffu, v, o);
             if (lane >= o) v += u;
         }
         wsum[lane] = v;
     }
     __syncthreads();
     int run = incl - local + (wid > 0 ? wsum[wid - 1] : 0);
-    for (int k = lo; k < hi; ++k) { out[k] = run; run += cnt[k]; }
-    if (threadIdx.x == blockDim.x - 1) out[H] = run;
+    for (int k = lo; k < hi; ++k) { sb[ob[k]] = run; run += cb[ob[k]]; }
 }
 
-__global__ void bucket_scatter_kernel(kf_field_t f, int B, int n, const int32_t *__restrict__ atom_cell,
-                                      const int32_t *__restrict__ atom_slot,
-                                      const int32_t *__restrict__ start, int32_t *__restrict__ sorted_atom,
-                                      const kf_status_t *status) {
+// Work-item prefix over trajectories (one item = one occupied cell).
+__global__ void __launch_bounds__(1024)
+occ_prefix_kernel(int B, const int32_t *__restrict__ occ_count, int32_t *__restrict__ occ_offset,
+                  const kf_status_t *status) {
+    __shared__ int carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int base = 0; base < B; base += blockDim.x) {
+        const int b = base + threadIdx.x;
+        const int v = (b < B && !status[b].done) ? occ_count[b] : 0;
+        __shared__ int ws[32];
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+        int incl = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int u = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += u;
+        }
+        if (lane == 31) ws[wid] = incl;
+        __syncthreads();
+        if (wid == 0) {
+            int t = lane < (int)(blockDim.x >> 5) ? ws[lane] : 0;
+            for (int o = 1; o < 32; o <<= 1) {
+                const int u = __shfl_up_sync(0xffffffffu, t, o);
+                if (lane >= o) t += u;
+            }
+            ws[lane] = t;
+        }
+        __syncthreads();
+        const int excl = carry + incl - v + (wid > 0 ? ws[wid - 1] : 0);
+        if (b < B) occ_offset[b] = excl;
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) carry = excl + v;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) occ_offset[B] = carry;
+}
+
+__global__ void bin_scatter_kernel(kf_field_t f, int B, int n, const int32_t *__restrict__ atom_slot,
+                                   const int32_t *__restrict__ atom_rank, const int32_t *__restrict__ start,
+                                   int32_t *__restrict__ sorted_atom, const kf_status_t *status) {
     const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (gid >= (long long)B * n) return;
     const int b = (int)(gid / n), a = (int)(gid % n);
     if (status[b].done) return;
-    const uint32_t H = 1u << f.hash_bits;
-    const uint32_t h = cell_hash(atom_cell[3 * gid], atom_cell[3 * gid + 1], atom_cell[3 * gid + 2], H - 1);
-    sorted_atom[(size_t)b * n + start[(size_t)b * (H + 1) + h] + atom_slot[gid]] = a;
+    const size_t H = (size_t)1 << f.hash_bits;
+    sorted_atom[(size_t)b * n + start[b * H + atom_slot[gid]] + atom_rank[gid]] = a;
 }
 
-// Sort each bucket by atom index (buckets hold a few atoms) and gather the
-// bucket-ordered coordinates with the packed cell in the 4th lane.
-__global__ void bucket_finalize_kernel(kf_field_t f, int B, int n, const double *__restrict__ pos,
-                                       const int32_t *__restrict__ atom_cell,
-                                       const int32_t *__restrict__ start, int32_t *__restrict__ sorted_atom,
-                                       double *__restrict__ sorted_pos, const kf_status_t *status) {
-    const int H = 1 << f.hash_bits;
-    const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (gid >= (long long)B * H) return;
-    const int b = (int)(gid / H), h = (int)(gid % H);
-    if (status[b].done) return;
-    const int s0 = start[(size_t)b * (H + 1) + h], s1 = start[(size_t)b * (H + 1) + h + 1];
+// One thread per occupied cell: sort members by atom index, gather the SoA.
+__global__ void bin_finalize_kernel(kf_field_t f, int B, int n, const double *__restrict__ pos,
+                                    const unsigned long long *__restrict__ keys, const int32_t *__restrict__ occ,
+                                    const int32_t *__restrict__ occ_offset, const int32_t *__restrict__ cnt,
+                                    const int32_t *__restrict__ start, int32_t *__restrict__ sorted_atom,
+                                    float4 *__restrict__ s_rel, double4 *__restrict__ s_pos,
+                                    float4 *__restrict__ s_par, int4 *__restrict__ s_aux,
+                                    const kf_status_t *status) {
+    const int item = blockIdx.x * blockDim.x + threadIdx.x;
+    if (item >= occ_offset[B]) return;
+    int lo = 0, hi = B;   // b: last trajectory with occ_offset[b] <= item
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (occ_offset[mid] <= item) lo = mid; else hi = mid;
+    }
+    const int b = lo;
+    const size_t H = (size_t)1 << f.hash_bits;
+    const int slot = occ[b * H + (item - occ_offset[b])];
+    const int s0 = start[b * H + slot], c = cnt[b * H + slot];
     int32_t *ids = sorted_atom + (size_t)b * n;
-    for (int k = s0 + 1; k < s1; ++k) {
+    for (int k = s0 + 1; k < s0 + c; ++k) {
         const int v = ids[k];
         int m = k - 1;
         while (m >= s0 && ids[m] > v) { ids[m + 1] = ids[m]; --m; }
         ids[m + 1] = v;
     }
-    for (int k = s0; k < s1; ++k) {
-        const size_t a = (size_t)b * n + ids[k];
-        double4 v;
-        v.x = pos[3 * a]; v.y = pos[3 * a + 1]; v.z = pos[3 * a + 2];
-        v.w = __longlong_as_double(pack_cell(atom_cell[3 * a], atom_cell[3 * a + 1], atom_cell[3 * a + 2]));
-        reinterpret_cast<double4 *>(sorted_pos)[(size_t)b * n + k] = v;
+    const long long key = (long long)keys[b * H + slot];
+    const unsigned long long u = (unsigned long long)key;
+    const int cx = (int)((long long)(u << 1) >> 43), cy = (int)((long long)(u << 22) >> 43),
+              cz = (int)((long long)(u << 43) >> 43);
+    const double ctr[3] = {((double)cx + 0.5) * f.cell, ((double)cy + 0.5) * f.cell, ((double)cz + 0.5) * f.cell};
+    const bool tree = !f.uniform_weights;
+    for (int k = s0; k < s0 + c; ++k) {
+        const int a = ids[k];
+        const size_t ga = (size_t)b * n + a, gs = (size_t)b * n + k;
+        const double x = pos[3 * ga], y = pos[3 * ga + 1], z = pos[3 * ga + 2];
+        s_pos[gs] = make_double4(x, y, z, 0.0);
+        s_rel[gs] = make_float4((float)(x - ctr[0]), (float)(y - ctr[1]), (float)(z - ctr[2]), 0.f);
+        s_par[gs] = make_float4(f.q32[a], f.R32[a], f.seps32[a], 0.f);
+        s_aux[gs] = make_int4(a, tree ? f.tres[a] : 0, tree ? (int)f.tchain[a] : 0, 0);
     }
 }
 
@@ -135,18 +211,24 @@ __global__ void bucket_finalize_kernel(kf_field_t f, int B, int n, const double 
 
 int kf_bin_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s) {
     const int B = w->B, H = 1 << f->hash_bits;
-    KF_CUDA(cudaMemsetAsync(w->bucket_count, 0, sizeof(int32_t) * (size_t)B * H, s), "memset buckets");
+    KF_CUDA(cudaMemsetAsync(w->cell_key, 0xFF, sizeof(unsigned long long) * (size_t)B * H, s), "memset keys");
+    KF_CUDA(cudaMemsetAsync(w->cell_cnt, 0, sizeof(int32_t) * (size_t)B * H, s), "memset cnt");
+    KF_CUDA(cudaMemsetAsync(w->occ_count, 0, sizeof(int32_t) * (size_t)B, s), "memset occ");
     const long long total = (long long)B * n;
-    bin_count_kernel<<<kf_blocks(total, 256), 256, 0, s>>>(*f, B, n, w->pos, w->atom_cell, w->atom_slot,
-                                                           w->bucket_count, w->status);
-    KF_LAUNCH_CHECK("bin_count_kernel");
-    bucket_scan_kernel<<<B, 1024, 0, s>>>(H, w->bucket_count, w->bucket_start, w->status);
-    KF_LAUNCH_CHECK("bucket_scan_kernel");
-    bucket_scatter_kernel<<<kf_blocks(total, 256), 256, 0, s>>>(*f, B, n, w->atom_cell, w->atom_slot,
-                                                                w->bucket_start, w->sorted_atom, w->status);
-    KF_LAUNCH_CHECK("bucket_scatter_kernel");
-    bucket_finalize_kernel<<<kf_blocks((long long)B * H, 256), 256, 0, s>>>(
-        *f, B, n, w->pos, w->atom_cell, w->bucket_start, w->sorted_atom, w->sorted_pos, w->status);
-    KF_LAUNCH_CHECK("bucket_finalize_kernel");
+    bin_insert_kernel<<<kf_blocks(total, 256), 256, 0, s>>>(*f, B, n, w->pos, w->cell_key, w->cell_cnt, w->occ,
+                                                            w->occ_count, w->atom_slot, w->atom_rank, w->status);
+    KF_LAUNCH_CHECK("bin_insert_kernel");
+    cell_scan_kernel<<<B, 1024, 0, s>>>(H, w->occ, w->occ_count, w->cell_cnt, w->cell_start, w->status);
+    KF_LAUNCH_CHECK("cell_scan_kernel");
+    occ_prefix_kernel<<<1, 1024, 0, s>>>(B, w->occ_count, w->occ_offset, w->status);
+    KF_LAUNCH_CHECK("occ_prefix_kernel");
+    bin_scatter_kernel<<<kf_blocks(total, 256), 256, 0, s>>>(*f, B, n, w->atom_slot, w->atom_rank, w->cell_start,
+                                                             w->sorted_atom, w->status);
+    KF_LAUNCH_CHECK("bin_scatter_kernel");
+    bin_finalize_kernel<<<kf_blocks(total, 128), 128, 0, s>>>(
+        *f, B, n, w->pos, w->cell_key, w->occ, w->occ_offset, w->cell_cnt, w->cell_start, w->sorted_atom,
+        reinterpret_cast<float4 *>(w->s_rel), reinterpret_cast<double4 *>(w->s_pos),
+        reinterpret_cast<float4 *>(w->s_par), reinterpret_cast<int4 *>(w->s_aux), w->status);
+    KF_LAUNCH_CHECK("bin_finalize_kernel");
     return 0;
 }

@@ -89,19 +89,13 @@ KF_DEV int enumerate_samples(const double *xi, double r_off_i, const double *sam
     return covered;
 }
 
-KF_DEV void unpack_cell(long long p, int &cx, int &cy, int &cz) {
-    const unsigned long long u = (unsigned long long)p;
-    cx = (int)((long long)(u << 1) >> 43);
-    cy = (int)((long long)(u << 22) >> 43);
-    cz = (int)((long long)(u << 43) >> 43);
-}
-
 // Hot path: neighbours come from the spatial hash of this iteration.
 __global__ void __launch_bounds__(SOLV_THREADS)
 solv_hot_kernel(kf_field_t f, int n, int n_solv, const int32_t *__restrict__ solv_atoms,
-                const double *__restrict__ pos_all, const double *__restrict__ sorted_pos_d,
-                const int32_t *__restrict__ sorted_atom, const int32_t *__restrict__ bstart,
-                const int32_t *__restrict__ atom_cell, long long *__restrict__ solv_acc,
+                const double *__restrict__ pos_all, const unsigned long long *__restrict__ keys,
+                const int32_t *__restrict__ cnt, const int32_t *__restrict__ start,
+                const int32_t *__restrict__ atom_slot, const double4 *__restrict__ s_pos,
+                const int4 *__restrict__ s_aux, long long *__restrict__ solv_acc,
                 double *__restrict__ cav_atom, double *__restrict__ f_exp_out,
                 double *__restrict__ a_exp_out, int nb_cap, kf_status_t *status) {
     const int b = blockIdx.x / n_solv;
@@ -120,20 +114,18 @@ solv_hot_kernel(kf_field_t f, int n, int n_solv, const int32_t *__restrict__ sol
     const size_t ai = (size_t)b * n + i;
     const double xi[3] = {pos_all[3 * ai], pos_all[3 * ai + 1], pos_all[3 * ai + 2]};
     const double r_off_i = f.r_off[i];
-    const double4 *spos = reinterpret_cast<const double4 *>(sorted_pos_d) + (size_t)b * n;
-    const int32_t *sid = sorted_atom + (size_t)b * n;
-    const int H = 1 << f.hash_bits;
-    const int32_t *st = bstart + (size_t)b * (H + 1);
-    const int cx = atom_cell[3 * ai], cy = atom_cell[3 * ai + 1], cz = atom_cell[3 * ai + 2];
+    const uint32_t H = 1u << f.hash_bits;
+    const size_t hb = (size_t)b * H, nbase = (size_t)b * n;
+    int cx, cy, cz;
+    unpack_cell((long long)keys[hb + atom_slot[ai]], cx, cy, cz);
 
     for (int s = threadIdx.x; s < f.n_stencil; s += blockDim.x) {
-        const int ox = cx + f.stencil[3 * s], oy = cy + f.stencil[3 * s + 1], oz = cz + f.stencil[3 * s + 2];
-        const long long key = pack_cell(ox, oy, oz);
-        const uint32_t h = cell_hash(ox, oy, oz, (uint32_t)H - 1);
-        for (int kk = st[h]; kk < st[h + 1]; ++kk) {
-            const double4 pj = spos[kk];
-            if (__double_as_longlong(pj.w) != key) continue;
-            const int j = sid[kk];
+        const int js = cell_probe(keys + hb, H, cx + f.stencil[3 * s], cy + f.stencil[3 * s + 1],
+                                  cz + f.stencil[3 * s + 2]);
+        if (js < 0) continue;
+        for (int kk = start[hb + js]; kk < start[hb + js] + cnt[hb + js]; ++kk) {
+            const double4 pj = s_pos[nbase + kk];
+            const int j = s_aux[nbase + kk].x;
             if (j == i) continue;
             const double dx = xi[0] - pj.x, dy = xi[1] - pj.y, dz = xi[2] - pj.z;
             const double lim = r_off_i + f.r_off[j] + f.reach_pad;
@@ -352,8 +344,8 @@ int kf_solvation_launch(const kf_field_t *f, kf_batch_t *w, int n, int n_solv, c
             opted = smem;
         }
         solv_hot_kernel<<<(unsigned)((long long)B * n_solv), SOLV_THREADS, smem, s>>>(
-            *f, n, n_solv, solv_atoms, w->pos, w->sorted_pos, w->sorted_atom, w->bucket_start, w->atom_cell,
-            w->solv_acc, w->cav_atom, w->f_exp, w->a_exp, w->nb_cap, w->status);
+            *f, n, n_solv, solv_atoms, w->pos, w->cell_key, w->cell_cnt, w->cell_start, w->atom_slot,
+            reinterpret_cast<const double4 *>(w->s_pos), reinterpret_cast<const int4 *>(w->s_aux), w->solv_acc, w->cav_atom, w->f_exp, w->a_exp, w->nb_cap, w->status);
         KF_LAUNCH_CHECK("solv_hot_kernel");
     }
     const long long total = (long long)B * n * 3;

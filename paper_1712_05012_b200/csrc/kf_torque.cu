@@ -146,22 +146,25 @@ torque_step_kernel(kf_chain_t c, kf_field_t f, TorqueArgs ta, kf_batch_t w, kf_s
     // 4. energies: full-list halves summed in a fixed order
     const int n = c.n_atoms;
     const double *ea = w.e_atom + (size_t)b * n * 2;
-    double se = 0.0, sv = 0.0, sc = 0.0, sp = 0.0;
+    double se = 0.0, sv = 0.0, sc = 0.0, sp = 0.0, sp5 = 0.0;
     for (int a = threadIdx.x; a < n; a += blockDim.x) {
         se += ea[2 * a]; sv += ea[2 * a + 1];
         if (f.solvation) sc += w.cav_atom[(size_t)b * n + a];
-        sp += (double)w.pair_count[(size_t)b * n + a];
+        const int pc = w.pair_count[(size_t)b * n + a];
+        sp += (double)(pc & 0xffff);
+        sp5 += (double)(pc >> 16);
     }
     se = block_sum(se, red);
     sv = block_sum(sv, red);
     sc = f.solvation ? block_sum(sc, red) : 0.0;
     sp = block_sum(sp, red);
+    sp5 = block_sum(sp5, red);
     const double ge = 0.5 * se, gv = 0.5 * sv, gc = sc;
     if (mode == 2) {   // Field.evaluate: energies only
         if (threadIdx.x == 0) {
             double *e = w.energy + 3 * (size_t)b;
             e[0] = ge; e[1] = gv; e[2] = gc;
-            if (st) st->n_pairs = (long long)(0.5 * sp);
+            if (st) { st->n_pairs = (long long)(0.5 * sp); st->n_pairs_vdw = (long long)(0.5 * sp5); }
         }
         return;
     }
@@ -173,6 +176,7 @@ torque_step_kernel(kf_chain_t c, kf_field_t f, TorqueArgs ta, kf_batch_t w, kf_s
         double *e = w.energy + 3 * (size_t)b;
         e[0] = ge; e[1] = gv; e[2] = gc;
         st->n_pairs = (long long)(0.5 * sp);
+        st->n_pairs_vdw = (long long)(0.5 * sp5);
         int reason = KF_REASON_NONE;
         if (it < w.max_records) {
             double *rec = w.rec_energy + ((size_t)b * w.max_records + it) * 4;

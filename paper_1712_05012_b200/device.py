@@ -303,7 +303,7 @@ class DeviceField(ParamTables):
                 setattr(s, name, t[name].data_ptr())
             self.n_solv_nz = int(np.count_nonzero(gamma != 0.0))
         reach *= 1.0 + 1e-9
-        s.cell = reach / 2.0
+        s.cell = reach              # one cell per reach: the 27-cell stencil
         sten = _stencil(s.cell, reach)
         t["stencil"] = _up(sten, np.int32)
         s.stencil = t["stencil"].data_ptr()
@@ -363,9 +363,11 @@ class Batch:
             t = self.t = dict(
                 theta=z(B, max(D, 1)), frozen=z(B, max(D, 1), dtype=torch.uint8),
                 link_T=z(B, L, 16), pos=z(B, n, 3), forces=z(B, n, 3),
-                bucket_count=z(B, H, dtype=i32), bucket_start=z(B, H + 1, dtype=i32),
-                atom_slot=z(B, n, dtype=i32), atom_cell=z(B, n, 3, dtype=i32),
-                sorted_atom=z(B, n, dtype=i32), sorted_pos=z(B, n, 4),
+                cell_key=z(B, H, dtype=torch.int64), cell_cnt=z(B, H, dtype=i32),
+                cell_start=z(B, H, dtype=i32), occ=z(B, H, dtype=i32), occ_count=z(B, dtype=i32),
+                occ_offset=z(B + 1, dtype=i32), atom_slot=z(B, n, dtype=i32), atom_rank=z(B, n, dtype=i32),
+                sorted_atom=z(B, n, dtype=i32), s_rel=z(B, n, 4, dtype=torch.float32), s_pos=z(B, n, 4),
+                s_par=z(B, n, 4, dtype=torch.float32), s_aux=z(B, n, 4, dtype=i32),
                 e_atom=z(B, n, 2), pair_count=z(B, n, dtype=i32),
                 solv_acc=z(B, n, 3, dtype=torch.int64), cav_atom=z(B, n),
                 f_exp=z(B, n) if store_sasa else None, a_exp=z(B, n) if store_sasa else None,
@@ -669,9 +671,14 @@ class EnsembleRunner:
                               thetas=thetas, n_pairs=np.array([st.n_pairs for st in sts]))
 
 
+_runner_cache = _IdCache()
+
+
 def fold_ensemble(chain, confs, fld, step, record_theta: bool = False) -> EnsembleResult:
     confs = list(confs)
-    runner = EnsembleRunner(chain, fld, len(confs), step, record_theta=record_theta)
+    key = (len(confs), repr(step), bool(record_theta), id(fld))
+    runner = _runner_cache.get(chain, hash(key),
+                               lambda: EnsembleRunner(chain, fld, len(confs), step, record_theta=record_theta))
     if runner.df.solvation and step.max_iters > 0:
         check_cav_cutoff(fld.params, fld.config.solvation_cfg, fld.config.cutoffs.cav)
     runner.load(np.stack([c.theta for c in confs]), np.stack([c.frozen for c in confs]))
