@@ -133,13 +133,20 @@ typedef struct {
     int32_t *atom_slot;             /* [B][n] slot of the atom's cell              */
     int32_t *atom_rank;             /* [B][n] arrival rank inside the cell         */
     int32_t *sorted_atom;           /* [B][n] atoms grouped by cell, ascending     */
-    float   *s_rel;                 /* [B][n][4] fp32 offset from the cell centre  */
+    float   *s_hi;                  /* [B][n][4] offset from the cell centre, fp32 */
+    float   *s_lo;                  /* [B][n][4] fp32 remainder (hi + lo = fp64)   */
     double  *s_pos;                 /* [B][n][4] fp64 position (4th: unused)       */
     float   *s_par;                 /* [B][n][4] q, R, sqrt(eps), 0                */
     int32_t *s_aux;                 /* [B][n][4] atom, residue, chain flag, 0      */
+    int32_t *s_tree;                /* [B][n][4] parent, grandparent, great-grand  */
+    float   *cell_box;              /* [B][H][8] member bounding box (lo4, hi4)    */
+    int32_t *work;                  /* [1] dynamic work counter (zeroed per launch)*/
     /* nonbonded */
-    double  *e_atom;                /* [B][n][2] per-atom elec / vdw (full list)   */
-    int32_t *pair_count;            /* [B][n] elec-cutoff partners per atom        */
+    double  *e_atom;                /* [B][n][2] elec / vdW energy (full list: twice
+                                       the pair sum); per-cell totals at the cell's
+                                       lowest atom, 0 elsewhere                      */
+    long long *pair_count;          /* [B][n] partner counts (elec | vdW << 32),
+                                       per-cell totals stored at the cell's lowest atom */
     /* solvation */
     long long *solv_acc;            /* [B][n][3] int64 fixed point                 */
     double  *cav_atom;              /* [B][n] gamma_i * a_exp_i                    */

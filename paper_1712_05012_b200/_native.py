@@ -54,8 +54,8 @@ class KfBatch(C.Structure):
                 ("max_records", I32), ("_pad", I32)] + [
         (name, P) for name in (
             "theta", "frozen", "link_T", "pos", "forces", "cell_key", "cell_cnt", "cell_start",
-            "occ", "occ_count", "occ_offset", "atom_slot", "atom_rank", "sorted_atom", "s_rel",
-            "s_pos", "s_par", "s_aux", "e_atom", "pair_count",
+            "occ", "occ_count", "occ_offset", "atom_slot", "atom_rank", "sorted_atom", "s_hi", "s_lo",
+            "s_pos", "s_par", "s_aux", "s_tree", "cell_box", "work", "e_atom", "pair_count",
             "solv_acc", "cav_atom", "f_exp", "a_exp", "wrench", "side_tot", "bb_suffix", "tau", "energy", "status",
             "rec_energy", "rec_theta")]
 

@@ -169,9 +169,10 @@ __global__ void bin_finalize_kernel(kf_field_t f, int B, int n, const double *__
                                     const unsigned long long *__restrict__ keys, const int32_t *__restrict__ occ,
                                     const int32_t *__restrict__ occ_offset, const int32_t *__restrict__ cnt,
                                     const int32_t *__restrict__ start, int32_t *__restrict__ sorted_atom,
-                                    float4 *__restrict__ s_rel, double4 *__restrict__ s_pos,
-                                    float4 *__restrict__ s_par, int4 *__restrict__ s_aux,
-                                    const kf_status_t *status) {
+                                    float4 *__restrict__ s_hi, float4 *__restrict__ s_lo,
+                                    double4 *__restrict__ s_pos, float4 *__restrict__ s_par,
+                                    int4 *__restrict__ s_aux, int4 *__restrict__ s_tree,
+                                    float4 *__restrict__ cell_box, const kf_status_t *status) {
     const int item = blockIdx.x * blockDim.x + threadIdx.x;
     if (item >= occ_offset[B]) return;
     int lo = 0, hi = B;   // b: last trajectory with occ_offset[b] <= item
@@ -196,15 +197,31 @@ __global__ void bin_finalize_kernel(kf_field_t f, int B, int n, const double *__
               cz = (int)((long long)(u << 43) >> 43);
     const double ctr[3] = {((double)cx + 0.5) * f.cell, ((double)cy + 0.5) * f.cell, ((double)cz + 0.5) * f.cell};
     const bool tree = !f.uniform_weights;
+    float bl[3] = {INFINITY, INFINITY, INFINITY}, bh[3] = {-INFINITY, -INFINITY, -INFINITY};
     for (int k = s0; k < s0 + c; ++k) {
         const int a = ids[k];
         const size_t ga = (size_t)b * n + a, gs = (size_t)b * n + k;
         const double x = pos[3 * ga], y = pos[3 * ga + 1], z = pos[3 * ga + 2];
         s_pos[gs] = make_double4(x, y, z, 0.0);
-        s_rel[gs] = make_float4((float)(x - ctr[0]), (float)(y - ctr[1]), (float)(z - ctr[2]), 0.f);
+        // offset from the cell centre as an fp32 pair: hi + lo == the fp64 offset
+        // to ~1e-14 A, so fp32 arithmetic on them recovers fp64-accurate
+        // difference vectors without absolute coordinates
+        const double r[3] = {x - ctr[0], y - ctr[1], z - ctr[2]};
+        float h[3], l[3];
+        for (int q = 0; q < 3; ++q) {
+            h[q] = (float)r[q];
+            l[q] = (float)(r[q] - (double)h[q]);
+            bl[q] = fminf(bl[q], h[q]);
+            bh[q] = fmaxf(bh[q], h[q]);
+        }
+        s_hi[gs] = make_float4(h[0], h[1], h[2], 0.f);
+        s_lo[gs] = make_float4(l[0], l[1], l[2], 0.f);
         s_par[gs] = make_float4(f.q32[a], f.R32[a], f.seps32[a], 0.f);
         s_aux[gs] = make_int4(a, tree ? f.tres[a] : 0, tree ? (int)f.tchain[a] : 0, 0);
+        s_tree[gs] = tree ? make_int4(f.tparent[a], f.tgp[a], f.tggp[a], 0) : make_int4(-1, -1, -1, 0);
     }
+    cell_box[2 * (b * H + slot)] = make_float4(bl[0], bl[1], bl[2], 0.f);
+    cell_box[2 * (b * H + slot) + 1] = make_float4(bh[0], bh[1], bh[2], 0.f);
 }
 
 }  // namespace
@@ -227,8 +244,10 @@ int kf_bin_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s) {
     KF_LAUNCH_CHECK("bin_scatter_kernel");
     bin_finalize_kernel<<<kf_blocks(total, 128), 128, 0, s>>>(
         *f, B, n, w->pos, w->cell_key, w->occ, w->occ_offset, w->cell_cnt, w->cell_start, w->sorted_atom,
-        reinterpret_cast<float4 *>(w->s_rel), reinterpret_cast<double4 *>(w->s_pos),
-        reinterpret_cast<float4 *>(w->s_par), reinterpret_cast<int4 *>(w->s_aux), w->status);
+        reinterpret_cast<float4 *>(w->s_hi), reinterpret_cast<float4 *>(w->s_lo),
+        reinterpret_cast<double4 *>(w->s_pos), reinterpret_cast<float4 *>(w->s_par),
+        reinterpret_cast<int4 *>(w->s_aux), reinterpret_cast<int4 *>(w->s_tree),
+        reinterpret_cast<float4 *>(w->cell_box), w->status);
     KF_LAUNCH_CHECK("bin_finalize_kernel");
     return 0;
 }

@@ -6,51 +6,63 @@
 // TreeWeights.weights_for (topology.py:153-195), elec/vdw_pair_quantities
 // (forcefield.py:98-113) and the bincount scatter (forcefield.py:162-172).
 //
-// Layout: one warp per occupied 9 A cell (persistent grid over the work list
-// of all trajectories); lanes own the cell's atoms.  For each of the 27
-// neighbour cells the warp stages 32-atom j-tiles in shared memory (one
-// coalesced load per lane, then broadcast reads) and each lane
-//   1. prefilters the tile in fp32 from cell-centre offsets (no absolute
-//      coordinates, so |error| < 1e-5 A^2, far inside a 1e-2 A^2 band), into
-//      a bit mask;
-//   2. walks the mask: exact reference membership in fp64 — d2 in einsum
-//      order (dx*dx + dz*dz) + dy*dy vs max(elec, vdw)^2, and sqrt(d2) <= cut
-//      per term via the equivalent d2 thresholds — then the pair energy and
-//      force in fp32 from the fp64 difference vector, fp64 per-atom sums
-//      (pairs closer than 0.1 A take the reference's fp64 formulas).
+// Work: one warp per occupied 9 A cell (dynamic work counter over the cells of
+// all trajectories); the cell's atoms (<= 32 per pass) are the warp's i-tile.
+// For each of the 27 neighbour cells that some lane can reach (per-lane
+// distance to the cell's bounding box, warp vote) the warp stages 32-atom
+// j-tiles in shared memory and runs two stages:
+//   1. prefilter: each lane tests its i against the tile in fp32 from
+//      cell-centre offsets into a 32-bit mask (band 1e-2 A^2 around cut^2);
+//   2. compacted pairs: the set bits of all lanes are dealt out one pair per
+//      lane (warp scan + __fns), so every lane does useful pair work; each
+//      pair gets its difference vector from the hi/lo fp32 offset pairs
+//      (fp64-accurate), decides membership exactly as the reference
+//      (d2 = (dx*dx + dz*dz) + dy*dy in fp64 vs max(elec, vdw)^2, and
+//      sqrt(d2) <= cut per term) — recomputed from the fp64 positions only in
+//      a 1e-3 A^2 band around each threshold — and evaluates energy and
+//      force in fp32; pairs under 1 A take the reference's fp64 formulas.
+//   The per-pair results are summed per owner lane in pair order, i.e. in a
+//   fixed order, into fp64 accumulators.
 // Both directions of each unordered pair are evaluated by their owners
-// ("full list"): no atomics, fixed accumulation order, run-to-run bitwise
-// deterministic.
+// ("full list"): no atomics on forces, run-to-run bitwise deterministic.
 #include "kf_common.cuh"
 
 namespace {
 
 constexpr double COULOMB_K = 332.06;
 constexpr double MIN_DISTANCE = 1e-6;
-constexpr double FP64_BELOW_D2 = 1e-2;
 constexpr int PAIR_WARPS = 4;
+constexpr unsigned FULL = 0xffffffffu;
 
-struct JTile {
-    float4 rel[32];
-    double4 pos[32];
+struct Tile {
+    float4 hi[32];
+    float4 lo[32];
     float4 par[32];
     int4 aux[32];
 };
 
-struct Acc {
-    double fx, fy, fz, ee, ev;
-    int cnt;   // elec-cutoff partners (low 16 bits) | vdW-cutoff partners << 16
+struct WarpSmem {
+    Tile J;
+    Tile I;
+    int4 itree[32];
+    float acc[3][32];          // per-owner fp32 force sums of the current tile
+    unsigned short list[1024]; // accepted (owner << 5 | t) pairs of the tile, owner-major
 };
 
-// Reference fp64 formulas for one pair (used at d < 0.1 A).
+struct Acc {
+    double fx, fy, fz, ee, ev;
+    long long cnt;   // elec-cutoff partners (low 32 bits) | vdW-cutoff partners << 32
+};
+
+// Reference fp64 formulas for one pair (used below 1 A).
 KF_DEV void pair_fp64(const kf_field_t &f, int i, int j, double d2, double dx, double dy, double dz,
-                      double we, double wv, bool ke, bool kv, Acc &a) {
+                      double we, double wv, bool ke, bool kv, float *out) {
     const double d = sqrt(d2);
-    double mag = 0.0;
+    double mag = 0.0, ee = 0.0, ev = 0.0;
     if (ke) {
         const double kap = f.dielectric_const ? f.kappa : d;
         const double num = COULOMB_K * we * f.q[i] * f.q[j];
-        a.ee += num / (kap * d);
+        ee = num / (kap * d);
         mag += num / (kap * d * d);
     }
     if (kv) {
@@ -58,145 +70,250 @@ KF_DEV void pair_fp64(const kf_field_t &f, int i, int j, double d2, double dx, d
         const double dd = f.R[i] + f.R[j];
         const double dd6 = pow(dd, 6.0), d6 = pow(d, 6.0);
         const double ratio6 = dd6 / d6;
-        a.ev += wv * eps * (ratio6 * ratio6 - 2.0 * ratio6);
+        ev = wv * eps * (ratio6 * ratio6 - 2.0 * ratio6);
         mag += 12.0 * wv * eps * (pow(dd, 12.0) / pow(d, 13.0) - dd6 / pow(d, 7.0));
     }
     const double g = mag / d;
-    a.fx += g * dx; a.fy += g * dy; a.fz += g * dz;
+    out[0] = (float)(g * dx); out[1] = (float)(g * dy); out[2] = (float)(g * dz);
+    out[3] = (float)ee; out[4] = (float)ev;
 }
 
-__global__ void __launch_bounds__(PAIR_WARPS * 32)
+#ifndef PAIR_MINB
+#define PAIR_MINB 6
+#endif
+__global__ void __launch_bounds__(PAIR_WARPS * 32, PAIR_MINB)
 pair_kernel(kf_field_t f, int B, int n, const unsigned long long *__restrict__ keys,
             const int32_t *__restrict__ cnt, const int32_t *__restrict__ start, const int32_t *__restrict__ occ,
-            const int32_t *__restrict__ occ_offset, const float4 *__restrict__ s_rel,
-            const double4 *__restrict__ s_pos, const float4 *__restrict__ s_par, const int4 *__restrict__ s_aux,
-            double *__restrict__ forces, double *__restrict__ e_atom, int32_t *__restrict__ pair_count,
-            kf_status_t *status) {
-    __shared__ JTile tiles[PAIR_WARPS];
+            const int32_t *__restrict__ occ_offset, const float4 *__restrict__ s_hi,
+            const float4 *__restrict__ s_lo, const double4 *__restrict__ s_pos, const float4 *__restrict__ s_par,
+            const int4 *__restrict__ s_aux, const int4 *__restrict__ s_tree, const float4 *__restrict__ cell_box,
+            int32_t *__restrict__ work, double *__restrict__ forces, double *__restrict__ e_atom,
+            long long *__restrict__ pair_count, kf_status_t *status) {
+    __shared__ WarpSmem smem[PAIR_WARPS];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    JTile &T = tiles[warp];
+    WarpSmem &S = smem[warp];
     const uint32_t H = 1u << f.hash_bits;
     const int total = occ_offset[B];
     const float cellf = (float)f.cell;
     const float pre2 = (float)(f.cut_pair2 + 1e-2);
+    const float cut2f = (float)f.cut_pair2, tvf = (float)f.thr_vdw2, tef = (float)f.thr_elec2;
+    const float band = 1e-3f;
     const float kap_inv = f.dielectric_const ? (float)(1.0 / f.kappa) : 1.0f;
 
-    for (int item = blockIdx.x * PAIR_WARPS + warp; item < total; item += gridDim.x * PAIR_WARPS) {
+    for (;;) {
+        int item = 0;
+        if (lane == 0) item = atomicAdd(work, 1);
+        item = __shfl_sync(FULL, item, 0);
+        if (item >= total) break;
         const int b = item_owner(occ_offset, B, item);
         const size_t hb = (size_t)b * H, nb = (size_t)b * n;
         const int slot = occ[hb + (item - occ_offset[b])];
         int cx, cy, cz;
         unpack_cell((long long)keys[hb + slot], cx, cy, cz);
         const int s0 = start[hb + slot], c = cnt[hb + slot];
+        double ee = 0.0, ev = 0.0;   // cell totals (per computing lane)
+        long long pcount = 0;
         for (int ic = 0; ic < c; ic += 32) {
-            const bool valid = ic + lane < c;
-            const size_t ki = nb + s0 + ic + (valid ? lane : 0);
-            const float4 ri = s_rel[ki];
-            const double4 pi4 = s_pos[ki];
-            const float4 qi4 = s_par[ki];
-            const int4 ai = s_aux[ki];
-            const int i = ai.x;
-            int pi = -1, gpi = -1, ggi = -1;
-            const bool ci = !f.uniform_weights && ai.z != 0;
-            if (ci) { pi = f.tparent[i]; gpi = f.tgp[i]; ggi = f.tggp[i]; }
-            const float qi = qi4.x * (float)COULOMB_K;
+            const int ci_n = min(32, c - ic);
+            const bool valid = lane < ci_n;
+            __syncwarp();
+            if (valid) {
+                const size_t ki = nb + s0 + ic + lane;
+                S.I.hi[lane] = s_hi[ki];
+                S.I.lo[lane] = s_lo[ki];
+                S.I.par[lane] = s_par[ki];
+                S.I.aux[lane] = s_aux[ki];
+                S.itree[lane] = s_tree[ki];
+            }
+            __syncwarp();
+            const float4 hi_i = S.I.hi[valid ? lane : 0];
             Acc a = {0.0, 0.0, 0.0, 0.0, 0.0, 0};
 
             for (int s = 0; s < f.n_stencil; ++s) {
                 const int ox = f.stencil[3 * s], oy = f.stencil[3 * s + 1], oz = f.stencil[3 * s + 2];
                 const int js = cell_probe(keys + hb, H, cx + ox, cy + oy, cz + oz);
                 if (js < 0) continue;
+                // i in the neighbour cell's frame; skip the cell unless some lane reaches its box
+                const float sx = (float)ox * cellf, sy = (float)oy * cellf, sz = (float)oz * cellf;
+                const float px = hi_i.x - sx, py = hi_i.y - sy, pz = hi_i.z - sz;
+                const float4 blo = cell_box[2 * (hb + js)], bhi = cell_box[2 * (hb + js) + 1];
+                const float gx = fmaxf(fmaxf(blo.x - px, px - bhi.x), 0.f);
+                const float gy = fmaxf(fmaxf(blo.y - py, py - bhi.y), 0.f);
+                const float gz = fmaxf(fmaxf(blo.z - pz, pz - bhi.z), 0.f);
+                const bool need = valid && gx * gx + gy * gy + gz * gz <= pre2;
+                if (!__any_sync(FULL, need)) continue;
                 const int j0 = start[hb + js], jc = cnt[hb + js];
-                // i relative to the neighbour cell's centre
-                const float xs = ri.x - (float)ox * cellf, ys = ri.y - (float)oy * cellf,
-                            zs = ri.z - (float)oz * cellf;
                 for (int jb = 0; jb < jc; jb += 32) {
                     const int nt = min(32, jc - jb);
                     __syncwarp();
                     if (lane < nt) {
                         const size_t kj = nb + j0 + jb + lane;
-                        T.rel[lane] = s_rel[kj];
-                        T.pos[lane] = s_pos[kj];
-                        T.par[lane] = s_par[kj];
-                        T.aux[lane] = s_aux[kj];
+                        S.J.hi[lane] = s_hi[kj];
+                        S.J.lo[lane] = s_lo[kj];
+                        S.J.par[lane] = s_par[kj];
+                        S.J.aux[lane] = s_aux[kj];
                     }
                     __syncwarp();
-                    if (!valid) continue;
+                    // ---- stage 1: fp32 prefilter into a mask
                     unsigned mask = 0u;
-                    for (int t = 0; t < nt; ++t) {
-                        const float4 r = T.rel[t];
-                        const float dx = xs - r.x, dy = ys - r.y, dz = zs - r.z;
-                        const float d2 = dx * dx + dy * dy + dz * dz;
-                        mask |= (d2 <= pre2 ? 1u : 0u) << t;
-                    }
-                    float fx = 0.f, fy = 0.f, fz = 0.f, fe = 0.f, fv = 0.f;
-                    while (mask) {
-                        const int t = __ffs(mask) - 1;
-                        mask &= mask - 1u;
-                        const int4 aj = T.aux[t];
-                        const int j = aj.x;
-                        if (j == i) continue;
-                        const double4 pj = T.pos[t];
-                        const double dx = xsub(pi4.x, pj.x), dy = xsub(pi4.y, pj.y), dz = xsub(pi4.z, pj.z);
-                        const double d2 = d2_einsum(dx, dy, dz);
-                        if (d2 > f.cut_pair2) continue;
-                        const bool ke = d2 <= f.thr_elec2, kv = d2 <= f.thr_vdw2;
-                        a.cnt += (int)ke + ((int)kv << 16);
-                        double we, wv;
-                        if (f.uniform_weights) {
-                            we = wv = f.uniform_value;
-                        } else {
-                            int cls = 4;
-                            if (ci && aj.z != 0 && abs(ai.y - aj.y) <= 1)
-                                cls = classify_pair(f, i, j, pi, gpi, ggi, ai.y, true);
-                            we = f.w_elec[cls - 1]; wv = f.w_vdw[cls - 1];
+                    if (need) {
+                        for (int t = 0; t < nt; ++t) {
+                            const float4 r = S.J.hi[t];
+                            const float dx = px - r.x, dy = py - r.y, dz = pz - r.z;
+                            mask |= (dx * dx + dy * dy + dz * dz <= pre2 ? 1u : 0u) << t;
                         }
-                        if (d2 < FP64_BELOW_D2) {
-                            if (d2 < 1e-11) {
-                                const double d = sqrt(d2);
-                                if (d < MIN_DISTANCE) {
-                                    atomicMin(&status[b].dmin_bits, (unsigned long long)__double_as_longlong(d));
-                                    if (atomicCAS(&status[b].error, KF_ERR_NONE, KF_ERR_CLASH) == KF_ERR_NONE)
-                                        status[b].err_iter = status[b].iter;
-                                    continue;
+                    }
+                    // ---- stage 2: the tile's candidate pairs, owner-major, one per lane
+                    const int own = __popc(mask);
+                    int incl = own;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int v = __shfl_up_sync(FULL, incl, o);
+                        if (lane >= o) incl += v;
+                    }
+                    const int tot = __shfl_sync(FULL, incl, 31);
+                    {
+                        unsigned m = mask;
+                        int wpos = incl - own;
+                        while (m) {
+                            const int t = __ffs(m) - 1;
+                            m &= m - 1u;
+                            S.list[wpos++] = (unsigned short)((lane << 5) | t);
+                        }
+                    }
+                    for (int q = 0; q < 3; ++q) S.acc[q][lane] = 0.f;
+                    __syncwarp();
+                    float fe = 0.f, fv = 0.f;
+                    for (int base = 0; base < tot; base += 32) {
+                        const int k = base + lane;
+                        const bool act = k < tot;
+                        const int e = act ? (int)S.list[k] : 0;
+                        const int o = act ? e >> 5 : 32 + lane;   // inactive lanes: own segments
+                        float out[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
+                        long long pc = 0;
+                        if (act) {
+                            const int t = e & 31;
+                            const int4 ai = S.I.aux[o], aj = S.J.aux[t];
+                            const int i = ai.x, j = aj.x;
+                            if (i != j) {
+                                const float4 hi = S.I.hi[o], li = S.I.lo[o], hj = S.J.hi[t], lj = S.J.lo[t];
+                                const float dxf = ((hi.x - hj.x) - sx) + (li.x - lj.x);
+                                const float dyf = ((hi.y - hj.y) - sy) + (li.y - lj.y);
+                                const float dzf = ((hi.z - hj.z) - sz) + (li.z - lj.z);
+                                const float d2f = dxf * dxf + dyf * dyf + dzf * dzf;
+                                bool member = d2f <= cut2f, ke = d2f <= tef, kv = d2f <= tvf;
+                                const bool exact = fabsf(d2f - cut2f) <= band || fabsf(d2f - tvf) <= band ||
+                                                   fabsf(d2f - tef) <= band || d2f < 1.0f;
+                                double d2 = d2f, dx = dxf, dy = dyf, dz = dzf;
+                                if (exact) {
+                                    const double4 p_i = s_pos[nb + s0 + ic + o], p_j = s_pos[nb + j0 + jb + t];
+                                    dx = xsub(p_i.x, p_j.x); dy = xsub(p_i.y, p_j.y); dz = xsub(p_i.z, p_j.z);
+                                    d2 = d2_einsum(dx, dy, dz);
+                                    member = d2 <= f.cut_pair2;
+                                    ke = d2 <= f.thr_elec2;
+                                    kv = d2 <= f.thr_vdw2;
+                                }
+                                if (member) {
+                                    pc = (long long)ke + ((long long)kv << 32);
+                                    double we, wv;
+                                    if (f.uniform_weights) {
+                                        we = wv = f.uniform_value;
+                                    } else {
+                                        int cls = 4;
+                                        if (ai.z != 0 && aj.z != 0 && abs(ai.y - aj.y) <= 1) {
+                                            const int4 tr = S.itree[o];
+                                            cls = classify_pair(f, i, j, tr.x, tr.y, tr.z, ai.y, true);
+                                        }
+                                        we = f.w_elec[cls - 1]; wv = f.w_vdw[cls - 1];
+                                    }
+                                    if (d2 < 1.0) {
+                                        bool clash = false;
+                                        if (d2 < 1e-11) {
+                                            const double d = sqrt(d2);
+                                            if (d < MIN_DISTANCE) {
+                                                clash = true;
+                                                atomicMin(&status[b].dmin_bits,
+                                                          (unsigned long long)__double_as_longlong(d));
+                                                if (atomicCAS(&status[b].error, KF_ERR_NONE, KF_ERR_CLASH) == KF_ERR_NONE)
+                                                    status[b].err_iter = status[b].iter;
+                                            }
+                                        }
+                                        if (!clash) pair_fp64(f, i, j, d2, dx, dy, dz, we, wv, ke, kv, out);
+                                    } else {
+                                        const float4 qi = S.I.par[o], qj = S.J.par[t];
+                                        const float inv_r = rsqrtf(d2f);
+                                        const float inv_r2 = inv_r * inv_r;
+                                        float g = 0.f;
+                                        if (ke) {
+                                            // kappa = d: E = K w qi qj / d^2; constant: E = K w qi qj / (kappa d);
+                                            // |F| / d = E / d^2 in both cases
+                                            const float qq = (float)COULOMB_K * qi.x * qj.x * (float)we;
+                                            const float e = f.dielectric_const ? qq * kap_inv * inv_r : qq * inv_r2;
+                                            out[3] = e;
+                                            g += e * inv_r2;
+                                        }
+                                        if (kv) {
+                                            const float weps = (float)wv * qi.z * qj.z;
+                                            const float D = qi.y + qj.y;
+                                            const float sr = D * D * inv_r2;
+                                            const float s3 = sr * sr * sr;
+                                            const float s6 = s3 * s3;
+                                            out[4] = weps * (s6 - 2.f * s3);
+                                            g += 12.f * weps * (s6 - s3) * inv_r2;
+                                        }
+                                        out[0] = g * dxf; out[1] = g * dyf; out[2] = g * dzf;
+                                    }
                                 }
                             }
-                            pair_fp64(f, i, j, d2, dx, dy, dz, we, wv, ke, kv, a);
-                            continue;
                         }
-                        const float4 qj = T.par[t];
-                        const float inv_r = rsqrtf((float)d2);
-                        const float inv_r2 = inv_r * inv_r;
-                        float g = 0.f;
-                        if (ke) {
-                            // kappa = d: E = K w qi qj / d^2, |F|/d = E / d^2;
-                            // constant kappa: E = K w qi qj / (kappa d), |F|/d = E / d^2
-                            const float qq = qi * qj.x * (float)we;
-                            const float e = f.dielectric_const ? qq * kap_inv * inv_r : qq * inv_r2;
-                            fe += e;
-                            g += e * inv_r2;
+                        // energies and counts only enter per-cell totals: the computing lane keeps them
+                        fe += out[3]; fv += out[4];
+                        a.cnt += pc;
+                        // forces: segmented inclusive scan by owner (segments are contiguous
+                        // lanes) on a fixed shuffle tree, so per-owner sums are deterministic
+#pragma unroll
+                        for (int d = 1; d < 32; d <<= 1) {
+                            const int ov = __shfl_up_sync(FULL, o, d);
+                            float up[3];
+#pragma unroll
+                            for (int q = 0; q < 3; ++q) up[q] = __shfl_up_sync(FULL, out[q], d);
+                            if (lane >= d && ov == o)
+#pragma unroll
+                                for (int q = 0; q < 3; ++q) out[q] += up[q];
                         }
-                        if (kv) {
-                            const float weps = (float)wv * qi4.z * qj.z;
-                            const float D = qi4.y + qj.y;
-                            const float sr = D * D * inv_r2;
-                            const float s3 = sr * sr * sr;
-                            const float s6 = s3 * s3;
-                            fv += weps * (s6 - 2.f * s3);
-                            g += 12.f * weps * (s6 - s3) * inv_r2;
-                        }
-                        fx += g * (float)dx; fy += g * (float)dy; fz += g * (float)dz;
+                        const int on = __shfl_down_sync(FULL, o, 1);
+                        if (act && (lane == 31 || on != o))
+#pragma unroll
+                            for (int q = 0; q < 3; ++q) S.acc[q][o] += out[q];
+                        __syncwarp();
                     }
+                    const float fx = S.acc[0][lane], fy = S.acc[1][lane], fz = S.acc[2][lane];
+                    __syncwarp();
                     a.fx += (double)fx; a.fy += (double)fy; a.fz += (double)fz;
                     a.ee += (double)fe; a.ev += (double)fv;
                 }
             }
             if (valid) {
-                const size_t o = nb + i;
+                const size_t o = nb + S.I.aux[lane].x;
                 forces[3 * o] = a.fx; forces[3 * o + 1] = a.fy; forces[3 * o + 2] = a.fz;
-                e_atom[2 * o] = a.ee; e_atom[2 * o + 1] = a.ev;
-                pair_count[o] = a.cnt;
+                e_atom[2 * o] = 0.0; e_atom[2 * o + 1] = 0.0;
+                pair_count[o] = 0;
             }
+            ee += a.ee; ev += a.ev; pcount += a.cnt;
+        }
+        // cell totals on a fixed xor tree, stored at the cell's lowest atom
+        // (cells are a function of the positions, so the layout is deterministic)
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+            ee += __shfl_xor_sync(FULL, ee, d);
+            ev += __shfl_xor_sync(FULL, ev, d);
+            pcount += __shfl_xor_sync(FULL, pcount, d);
+        }
+        __syncwarp();
+        if (lane == 0) {
+            const size_t o = nb + s_aux[nb + s0].x;
+            e_atom[2 * o] = ee; e_atom[2 * o + 1] = ev;
+            pair_count[o] = pcount;
         }
     }
 }
@@ -243,13 +360,16 @@ int kf_pairs_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s) {
         int dev = 0, sms = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        g_pair_grid = sms * 8;
+        g_pair_grid = sms * 4;
     }
+    KF_CUDA(cudaMemsetAsync(w->work, 0, sizeof(int32_t), s), "memset work");
     pair_kernel<<<g_pair_grid, PAIR_WARPS * 32, 0, s>>>(
         *f, w->B, n, w->cell_key, w->cell_cnt, w->cell_start, w->occ, w->occ_offset,
-        reinterpret_cast<const float4 *>(w->s_rel), reinterpret_cast<const double4 *>(w->s_pos),
-        reinterpret_cast<const float4 *>(w->s_par), reinterpret_cast<const int4 *>(w->s_aux), w->forces,
-        w->e_atom, w->pair_count, w->status);
+        reinterpret_cast<const float4 *>(w->s_hi), reinterpret_cast<const float4 *>(w->s_lo),
+        reinterpret_cast<const double4 *>(w->s_pos), reinterpret_cast<const float4 *>(w->s_par),
+        reinterpret_cast<const int4 *>(w->s_aux), reinterpret_cast<const int4 *>(w->s_tree),
+        reinterpret_cast<const float4 *>(w->cell_box), w->work, w->forces, w->e_atom, w->pair_count,
+        w->status);
     KF_LAUNCH_CHECK("pair_kernel");
     return 0;
 }

@@ -150,9 +150,9 @@ torque_step_kernel(kf_chain_t c, kf_field_t f, TorqueArgs ta, kf_batch_t w, kf_s
     for (int a = threadIdx.x; a < n; a += blockDim.x) {
         se += ea[2 * a]; sv += ea[2 * a + 1];
         if (f.solvation) sc += w.cav_atom[(size_t)b * n + a];
-        const int pc = w.pair_count[(size_t)b * n + a];
-        sp += (double)(pc & 0xffff);
-        sp5 += (double)(pc >> 16);
+        const long long pc = w.pair_count[(size_t)b * n + a];
+        sp += (double)(pc & 0xffffffffLL);
+        sp5 += (double)(pc >> 32);
     }
     se = block_sum(se, red);
     sv = block_sum(sv, red);

@@ -366,9 +366,12 @@ class Batch:
                 cell_key=z(B, H, dtype=torch.int64), cell_cnt=z(B, H, dtype=i32),
                 cell_start=z(B, H, dtype=i32), occ=z(B, H, dtype=i32), occ_count=z(B, dtype=i32),
                 occ_offset=z(B + 1, dtype=i32), atom_slot=z(B, n, dtype=i32), atom_rank=z(B, n, dtype=i32),
-                sorted_atom=z(B, n, dtype=i32), s_rel=z(B, n, 4, dtype=torch.float32), s_pos=z(B, n, 4),
+                sorted_atom=z(B, n, dtype=i32), s_hi=z(B, n, 4, dtype=torch.float32),
+                s_lo=z(B, n, 4, dtype=torch.float32), s_pos=z(B, n, 4),
                 s_par=z(B, n, 4, dtype=torch.float32), s_aux=z(B, n, 4, dtype=i32),
-                e_atom=z(B, n, 2), pair_count=z(B, n, dtype=i32),
+                s_tree=z(B, n, 4, dtype=i32), cell_box=z(B, H, 8, dtype=torch.float32),
+                work=z(4, dtype=i32),
+                e_atom=z(B, n, 2), pair_count=z(B, n, dtype=torch.int64),
                 solv_acc=z(B, n, 3, dtype=torch.int64), cav_atom=z(B, n),
                 f_exp=z(B, n) if store_sasa else None, a_exp=z(B, n) if store_sasa else None,
                 wrench=z(B, L, 6), side_tot=z(B, max(R, 1), 6), bb_suffix=z(B, max(nbb, 1), 6),
