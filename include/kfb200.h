@@ -64,6 +64,9 @@ typedef struct {
     const double *q, *R, *eps;              /* fp64 (clash-range path)             */
     const int32_t *tparent, *tgp, *tggp, *tres;  /* bond tree (topology.py:73-91)  */
     const uint8_t *tchain;                  /* chain (non-hetero) mask             */
+    const int32_t *class_map;   /* [n][4]: 2-bit (4 - class) codes for partners
+                                   j = i - 32 .. i + 31 (static topology, host-built) */
+    const uint8_t *class_slow;  /* [n]: atom has a tree partner outside that window */
     double w_elec[4], w_vdw[4];     /* weight by class 1..4 (index class-1)        */
     double uniform_value;
     double kappa;

@@ -33,7 +33,8 @@ class KfField(C.Structure):
     _fields_ = [
         ("n_atoms", I32), ("uniform_weights", I32), ("dielectric_const", I32), ("solvation", I32),
         ("q32", P), ("R32", P), ("seps32", P), ("q", P), ("R", P), ("eps", P),
-        ("tparent", P), ("tgp", P), ("tggp", P), ("tres", P), ("tchain", P),
+        ("tparent", P), ("tgp", P), ("tggp", P), ("tres", P), ("tchain", P), ("class_map", P),
+        ("class_slow", P),
         ("w_elec", F64 * 4), ("w_vdw", F64 * 4), ("uniform_value", F64), ("kappa", F64),
         ("cut_pair2", F64), ("thr_elec2", F64), ("thr_vdw2", F64),
         ("cell", F64), ("hash_bits", I32), ("n_stencil", I32), ("stencil", P),

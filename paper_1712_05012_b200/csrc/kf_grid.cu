@@ -217,8 +217,9 @@ __global__ void bin_finalize_kernel(kf_field_t f, int B, int n, const double *__
         s_hi[gs] = make_float4(h[0], h[1], h[2], 0.f);
         s_lo[gs] = make_float4(l[0], l[1], l[2], 0.f);
         s_par[gs] = make_float4(f.q32[a], f.R32[a], f.seps32[a], 0.f);
-        s_aux[gs] = make_int4(a, tree ? f.tres[a] : 0, tree ? (int)f.tchain[a] : 0, 0);
-        s_tree[gs] = tree ? make_int4(f.tparent[a], f.tgp[a], f.tggp[a], 0) : make_int4(-1, -1, -1, 0);
+        s_aux[gs] = make_int4(a, tree ? f.tres[a] : 0, tree ? (int)f.tchain[a] : 0,
+                              tree ? (int)f.class_slow[a] : 0);
+        s_tree[gs] = tree ? reinterpret_cast<const int4 *>(f.class_map)[a] : make_int4(0, 0, 0, 0);
     }
     cell_box[2 * (b * H + slot)] = make_float4(bl[0], bl[1], bl[2], 0.f);
     cell_box[2 * (b * H + slot) + 1] = make_float4(bh[0], bh[1], bh[2], 0.f);

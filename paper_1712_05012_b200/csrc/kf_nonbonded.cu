@@ -79,7 +79,7 @@ KF_DEV void pair_fp64(const kf_field_t &f, int i, int j, double d2, double dx, d
 }
 
 #ifndef PAIR_MINB
-#define PAIR_MINB 6
+#define PAIR_MINB 4
 #endif
 __global__ void __launch_bounds__(PAIR_WARPS * 32, PAIR_MINB)
 pair_kernel(kf_field_t f, int B, int n, const unsigned long long *__restrict__ keys,
@@ -219,10 +219,17 @@ pair_kernel(kf_field_t f, int B, int n, const unsigned long long *__restrict__ k
                                     if (f.uniform_weights) {
                                         we = wv = f.uniform_value;
                                     } else {
+                                        // static class window: 2-bit codes for j - i in [-32, 32)
                                         int cls = 4;
-                                        if (ai.z != 0 && aj.z != 0 && abs(ai.y - aj.y) <= 1) {
-                                            const int4 tr = S.itree[o];
-                                            cls = classify_pair(f, i, j, tr.x, tr.y, tr.z, ai.y, true);
+                                        const int off = j - i + 32;
+                                        if ((unsigned)off < 64u) {
+                                            const int4 cm = S.itree[o];
+                                            const unsigned wd = off < 32 ? (off < 16 ? cm.x : cm.y)
+                                                                         : (off < 48 ? cm.z : cm.w);
+                                            cls = 4 - (int)((wd >> (2 * (off & 15))) & 3u);
+                                        } else if (ai.w != 0 && aj.z != 0 && abs(ai.y - aj.y) <= 1) {
+                                            cls = classify_pair(f, i, j, f.tparent[i], f.tgp[i], f.tggp[i], ai.y,
+                                                                ai.z != 0);
                                         }
                                         we = f.w_elec[cls - 1]; wv = f.w_vdw[cls - 1];
                                     }

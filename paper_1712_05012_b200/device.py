@@ -229,6 +229,57 @@ def _stencil(cell: float, reach_dist: float) -> np.ndarray:
     return offs[(gap * gap).sum(axis=1) <= reach_dist * reach_dist]
 
 
+def tree_classes(tree, i, j) -> np.ndarray:
+    """Reference interaction classes of pairs (topology.py:153-178), host numpy;
+    used only to build the static per-atom class window below."""
+    p, gp, gg = (np.asarray(a, np.int64) for a in (tree.parent, tree.grandparent, tree.greatgrand))
+    res = np.asarray(tree.residue_of, np.int64)
+    chain = np.asarray(tree.chain_mask, bool)
+    eq = lambda a, b: (a == b) & (a >= 0)  # noqa: E731
+    near = chain[i] & chain[j] & (np.abs(res[i] - res[j]) <= 1)
+    c = np.full(len(i), 4, np.int64)
+    c[near & (eq(gg[i], j) | eq(gg[j], i) | eq(gp[i], p[j]) | eq(gp[j], p[i]))] = 3
+    c[near & (eq(gp[i], j) | eq(gp[j], i) | eq(p[i], p[j]))] = 2
+    c[near & (eq(p[i], j) | eq(p[j], i))] = 1
+    return c
+
+
+def class_window(tree):
+    """Static topology table for the pair kernel: per atom, 2-bit codes
+    (4 - class) for partners j = i-32 .. i+31 packed in 4 int32 words, and a
+    flag for atoms with a class < 4 partner outside the window (those fall
+    back to the tree predicate on the device)."""
+    n = len(tree.parent)
+    off = np.arange(64) - 32
+    ii = np.repeat(np.arange(n), 64)
+    jj = ii + np.tile(off, n)
+    ok = (jj >= 0) & (jj < n) & (jj != ii)
+    codes = np.zeros(n * 64, np.uint64)
+    c = tree_classes(tree, ii[ok], jj[ok])
+    codes[ok] = (4 - c).astype(np.uint64)
+    codes = codes.reshape(n, 4, 16)
+    words = (codes << (2 * np.arange(16, dtype=np.uint64))).sum(axis=2).astype(np.uint32)
+    # partners beyond the window: same or adjacent residue, any index distance
+    slow = np.zeros(n, bool)
+    res = np.asarray(tree.residue_of, np.int64)
+    chain = np.asarray(tree.chain_mask, bool)
+    order = np.argsort(res, kind="stable")
+    bounds = np.searchsorted(res[order], np.unique(res))
+    groups = np.split(order, bounds[1:])
+    by_res = {int(res[g[0]]): g for g in groups if len(g)}
+    for r, g in by_res.items():
+        nb = np.concatenate([by_res.get(r + d, np.zeros(0, np.int64)) for d in (0, 1)])
+        a = np.repeat(g, len(nb))
+        b = np.tile(nb, len(g))
+        far = (np.abs(a - b) >= 32) & chain[a] & chain[b]
+        if far.any():
+            cc = tree_classes(tree, a[far], b[far])
+            hit = cc < 4
+            slow[a[far][hit]] = True
+            slow[b[far][hit]] = True
+    return words.view(np.int32), slow
+
+
 class ParamTables:
     """Per-atom parameters + pair-weight provider + dielectric on the device."""
 
@@ -246,9 +297,11 @@ class ParamTables:
         s.n_atoms = n
         if hasattr(weights, "tree") and hasattr(weights, "table"):
             tree = weights.tree
+            cmap, slow = class_window(tree)
             t.update(tparent=_up(tree.parent, np.int32), tgp=_up(tree.grandparent, np.int32),
                      tggp=_up(tree.greatgrand, np.int32), tres=_up(tree.residue_of, np.int32),
-                     tchain=_up(tree.chain_mask, np.uint8))
+                     tchain=_up(tree.chain_mask, np.uint8), class_map=_up(cmap, np.int32),
+                     class_slow=_up(slow, np.uint8))
             s.uniform_weights = 0
             for k, v in enumerate(np.asarray(weights.table.elec_by_class())[1:5]):
                 s.w_elec[k] = float(v)

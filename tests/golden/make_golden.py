@@ -84,7 +84,7 @@ def trajectory(name, seq, conf, fld, ch, **step_kw):
         os.path.join(OUT, f"{name}.npz"), seq=np.array(seq), theta0=conf.theta, frozen=conf.frozen,
         energies=np.array([[r.energy.g_elec, r.energy.g_vdw, r.energy.g_cav] for r in tr.records]),
         tau_max=np.array([r.tau_max for r in tr.records]),
-        thetas=np.array([r.theta for r in tr.records]), final=tr.final.theta,
+        thetas=np.array([r.theta for r in tr.records][:60]), final=tr.final.theta,
         reason=np.array(tr.reason), converged=np.array(tr.converged),
         snap_iters=np.array([k for k, _ in tr.snapshots]),
         step=np.array([step_kw.get(k, getattr(K.StepConfig(), k)) for k in
@@ -120,6 +120,10 @@ def main():
     ch, params, w, fld = system(seq3)
     conf = random_conf(ch, 4).freeze([0, 1, 5])
     trajectory("fold_frozen", seq3, conf, fld, ch, max_iters=25, torque_tol_rel=0.0, energy_window=0)
+    # C1 trajectory criterion: 1000 vacuum iterations
+    ch, params, w, fld = system(["ALA"] * 30)
+    trajectory("fold_c1_1000", ["ALA"] * 30, ch.conf_from_backbone(-10.0, -10.0), fld, ch,
+               max_iters=1000, torque_tol_rel=0.0, energy_window=0, snapshot_every=0)
     # clash message (test_kcm.py:204-213 pattern)
     ch, params, w, fld = system(["ALA", "ALA"])
     bad = K.build_chain(["ALA", "ALA"])
