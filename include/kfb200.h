@@ -89,7 +89,7 @@ typedef struct {
     const int32_t *solv_atoms;      /* atoms with gamma != 0 (the only ones whose
                                        exposure enters g_cav or the forces)        */
     int32_t n_solv;
-    int32_t _pad2;
+    int32_t precision;              /* pair math: 0 = fp32 (fp64 sums), 1 = fp64   */
 } kf_field_t;
 
 /* ---- per-trajectory status block ----------------------------------------- */

@@ -17,6 +17,7 @@ __version__ = "0.1.0"
 from .chain import (Chain, Conformation, KinematicState, LinkRecord, PeptideGeometry,
                     apply_deltas, build_chain, forward_kinematics, kinematic_state,
                     link_transforms)
+from .device import pair_precision, set_pair_precision
 from .errors import (ConfigurationError, KinefoldError, NativeLibraryError,
                      StericClashError)
 from .forcefield import (AtomParams, DielectricModel, EnergyBreakdown, elec_energy,

@@ -40,7 +40,7 @@ class KfField(C.Structure):
         ("cell", F64), ("hash_bits", I32), ("n_stencil", I32), ("stencil", P),
         ("n_samples", I32), ("_pad1", I32), ("samples", P), ("r_off", P), ("r_off2", P),
         ("gamma", P), ("w_int", P), ("quantum", F64), ("delta_r", F64), ("four_pi", F64),
-        ("reach_pad", F64), ("solv_atoms", P), ("n_solv", I32), ("_pad2", I32)]
+        ("reach_pad", F64), ("solv_atoms", P), ("n_solv", I32), ("precision", I32)]
 
 
 class KfStatus(C.Structure):

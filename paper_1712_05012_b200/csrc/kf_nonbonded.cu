@@ -25,6 +25,8 @@
 //   fixed order, into fp64 accumulators.
 // Both directions of each unordered pair are evaluated by their owners
 // ("full list"): no atomics on forces, run-to-run bitwise deterministic.
+#include <type_traits>
+
 #include "kf_common.cuh"
 
 namespace {
@@ -41,11 +43,12 @@ struct Tile {
     int4 aux[32];
 };
 
+template <typename T>
 struct WarpSmem {
     Tile J;
     Tile I;
     int4 itree[32];
-    float acc[3][32];          // per-owner fp32 force sums of the current tile
+    T acc[3][32];              // per-owner force sums of the current tile
     unsigned short list[1024]; // accepted (owner << 5 | t) pairs of the tile, owner-major
 };
 
@@ -54,33 +57,38 @@ struct Acc {
     long long cnt;   // elec-cutoff partners (low 32 bits) | vdW-cutoff partners << 32
 };
 
-// Reference fp64 formulas for one pair (used below 1 A).
+// One pair in fp64 (the reference's formulas, forcefield.py:98-113, with the
+// powers written as products): used below 1 A, and for every pair in the
+// fp64 precision mode.
+template <typename T>
 KF_DEV void pair_fp64(const kf_field_t &f, int i, int j, double d2, double dx, double dy, double dz,
-                      double we, double wv, bool ke, bool kv, float *out) {
+                      double we, double wv, bool ke, bool kv, T *out) {
     const double d = sqrt(d2);
+    const double inv_d = 1.0 / d;
     double mag = 0.0, ee = 0.0, ev = 0.0;
     if (ke) {
-        const double kap = f.dielectric_const ? f.kappa : d;
         const double num = COULOMB_K * we * f.q[i] * f.q[j];
-        ee = num / (kap * d);
-        mag += num / (kap * d * d);
+        ee = f.dielectric_const ? num * inv_d / f.kappa : num * inv_d * inv_d;   // num / (kappa d)
+        mag += ee * inv_d;                                                       // num / (kappa d^2)
     }
     if (kv) {
         const double eps = sqrt(f.eps[i] * f.eps[j]);
-        const double dd = f.R[i] + f.R[j];
-        const double dd6 = pow(dd, 6.0), d6 = pow(d, 6.0);
-        const double ratio6 = dd6 / d6;
-        ev = wv * eps * (ratio6 * ratio6 - 2.0 * ratio6);
-        mag += 12.0 * wv * eps * (pow(dd, 12.0) / pow(d, 13.0) - dd6 / pow(d, 7.0));
+        const double r = (f.R[i] + f.R[j]) * inv_d;
+        const double r2 = r * r, r6 = r2 * r2 * r2;
+        ev = wv * eps * (r6 * r6 - 2.0 * r6);
+        mag += 12.0 * wv * eps * (r6 * r6 - r6) * inv_d;
     }
-    const double g = mag / d;
-    out[0] = (float)(g * dx); out[1] = (float)(g * dy); out[2] = (float)(g * dz);
-    out[3] = (float)ee; out[4] = (float)ev;
+    const double g = mag * inv_d;
+    out[0] = (T)(g * dx); out[1] = (T)(g * dy); out[2] = (T)(g * dz);
+    out[3] = (T)ee; out[4] = (T)ev;
 }
 
 #ifndef PAIR_MINB
 #define PAIR_MINB 4
 #endif
+// F64 = false: fp32 pair math (the north-star configuration); true: fp64
+// pair math and fp64 per-tile sums (strict trajectory parity mode).
+template <bool F64>
 __global__ void __launch_bounds__(PAIR_WARPS * 32, PAIR_MINB)
 pair_kernel(kf_field_t f, int B, int n, const unsigned long long *__restrict__ keys,
             const int32_t *__restrict__ cnt, const int32_t *__restrict__ start, const int32_t *__restrict__ occ,
@@ -89,9 +97,10 @@ pair_kernel(kf_field_t f, int B, int n, const unsigned long long *__restrict__ k
             const int4 *__restrict__ s_aux, const int4 *__restrict__ s_tree, const float4 *__restrict__ cell_box,
             int32_t *__restrict__ work, double *__restrict__ forces, double *__restrict__ e_atom,
             long long *__restrict__ pair_count, kf_status_t *status) {
-    __shared__ WarpSmem smem[PAIR_WARPS];
+    using T = typename std::conditional<F64, double, float>::type;
+    __shared__ WarpSmem<T> smem[PAIR_WARPS];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    WarpSmem &S = smem[warp];
+    WarpSmem<T> &S = smem[warp];
     const uint32_t H = 1u << f.hash_bits;
     const int total = occ_offset[B];
     const float cellf = (float)f.cell;
@@ -181,15 +190,15 @@ pair_kernel(kf_field_t f, int B, int n, const unsigned long long *__restrict__ k
                             S.list[wpos++] = (unsigned short)((lane << 5) | t);
                         }
                     }
-                    for (int q = 0; q < 3; ++q) S.acc[q][lane] = 0.f;
+                    for (int q = 0; q < 3; ++q) S.acc[q][lane] = (T)0;
                     __syncwarp();
-                    float fe = 0.f, fv = 0.f;
+                    T fe = 0, fv = 0;
                     for (int base = 0; base < tot; base += 32) {
                         const int k = base + lane;
                         const bool act = k < tot;
                         const int e = act ? (int)S.list[k] : 0;
                         const int o = act ? e >> 5 : 32 + lane;   // inactive lanes: own segments
-                        float out[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
+                        T out[5] = {0, 0, 0, 0, 0};
                         long long pc = 0;
                         if (act) {
                             const int t = e & 31;
@@ -202,7 +211,7 @@ pair_kernel(kf_field_t f, int B, int n, const unsigned long long *__restrict__ k
                                 const float dzf = ((hi.z - hj.z) - sz) + (li.z - lj.z);
                                 const float d2f = dxf * dxf + dyf * dyf + dzf * dzf;
                                 bool member = d2f <= cut2f, ke = d2f <= tef, kv = d2f <= tvf;
-                                const bool exact = fabsf(d2f - cut2f) <= band || fabsf(d2f - tvf) <= band ||
+                                const bool exact = F64 || fabsf(d2f - cut2f) <= band || fabsf(d2f - tvf) <= band ||
                                                    fabsf(d2f - tef) <= band || d2f < 1.0f;
                                 double d2 = d2f, dx = dxf, dy = dyf, dz = dzf;
                                 if (exact) {
@@ -233,7 +242,7 @@ pair_kernel(kf_field_t f, int B, int n, const unsigned long long *__restrict__ k
                                         }
                                         we = f.w_elec[cls - 1]; wv = f.w_vdw[cls - 1];
                                     }
-                                    if (d2 < 1.0) {
+                                    if (F64 || d2 < 1.0) {
                                         bool clash = false;
                                         if (d2 < 1e-11) {
                                             const double d = sqrt(d2);
@@ -281,7 +290,7 @@ pair_kernel(kf_field_t f, int B, int n, const unsigned long long *__restrict__ k
 #pragma unroll
                         for (int d = 1; d < 32; d <<= 1) {
                             const int ov = __shfl_up_sync(FULL, o, d);
-                            float up[3];
+                            T up[3];
 #pragma unroll
                             for (int q = 0; q < 3; ++q) up[q] = __shfl_up_sync(FULL, out[q], d);
                             if (lane >= d && ov == o)
@@ -294,7 +303,7 @@ pair_kernel(kf_field_t f, int B, int n, const unsigned long long *__restrict__ k
                             for (int q = 0; q < 3; ++q) S.acc[q][o] += out[q];
                         __syncwarp();
                     }
-                    const float fx = S.acc[0][lane], fy = S.acc[1][lane], fz = S.acc[2][lane];
+                    const T fx = S.acc[0][lane], fy = S.acc[1][lane], fz = S.acc[2][lane];
                     __syncwarp();
                     a.fx += (double)fx; a.fy += (double)fy; a.fz += (double)fz;
                     a.ee += (double)fe; a.ev += (double)fv;
@@ -370,7 +379,8 @@ int kf_pairs_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s) {
         g_pair_grid = sms * 4;
     }
     KF_CUDA(cudaMemsetAsync(w->work, 0, sizeof(int32_t), s), "memset work");
-    pair_kernel<<<g_pair_grid, PAIR_WARPS * 32, 0, s>>>(
+    auto kern = f->precision ? pair_kernel<true> : pair_kernel<false>;
+    kern<<<g_pair_grid, PAIR_WARPS * 32, 0, s>>>(
         *f, w->B, n, w->cell_key, w->cell_cnt, w->cell_start, w->occ, w->occ_offset,
         reinterpret_cast<const float4 *>(w->s_hi), reinterpret_cast<const float4 *>(w->s_lo),
         reinterpret_cast<const double4 *>(w->s_pos), reinterpret_cast<const float4 *>(w->s_par),

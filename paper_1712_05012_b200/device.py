@@ -15,6 +15,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 import time
 import weakref
 import zlib
@@ -29,6 +30,21 @@ from .forcefield import MIN_DISTANCE, EnergyBreakdown
 from .solvation import ExposureStates, SasaResult, check_cav_cutoff, force_quantum
 
 _streams: dict = {}
+_precision = {"pair": os.environ.get("KFB200_PAIR_PRECISION", "fp32")}
+
+
+def set_pair_precision(mode: str) -> None:
+    """Pair-kernel arithmetic: "fp32" (fp32 pair math, fp64 sums; the default)
+    or "fp64" (reference formulas in fp64 for every pair: strict trajectory
+    parity).  Membership decisions, solvation, FK, torques and the step are
+    fp64 / exact in both modes."""
+    if mode not in ("fp32", "fp64"):
+        raise ConfigurationError(f"pair precision must be fp32 or fp64, got {mode!r}")
+    _precision["pair"] = mode
+
+
+def pair_precision() -> str:
+    return _precision["pair"]
 
 
 def _device() -> torch.device:
@@ -362,6 +378,7 @@ class DeviceField(ParamTables):
         s.stencil = t["stencil"].data_ptr()
         s.n_stencil = len(sten)
         s.hash_bits = max(6, int(math.ceil(math.log2(max(2 * n, 2)))))
+        s.precision = 1 if _precision["pair"] == "fp64" else 0
         self.n = n
         self._batches = {}
 
@@ -389,7 +406,8 @@ class DeviceField(ParamTables):
 def device_field(fld, n: int) -> DeviceField:
     p = fld.params
     fp = _fingerprint(np.asarray(p.q, float), np.asarray(p.R, float), np.asarray(p.eps, float),
-                      np.asarray(p.gamma, float), np.array([n])) ^ hash(repr(fld.config)) ^ id(fld.weights)
+                      np.asarray(p.gamma, float), np.array([n])) ^ hash(repr(fld.config)) ^ id(fld.weights) \
+        ^ hash(_precision["pair"])
     return _field_cache.get(fld, fp, lambda: DeviceField(fld, n))
 
 
