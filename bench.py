@@ -218,6 +218,8 @@ def main():
     theta_dev = torch.as_tensor(thetas_all[lo:hi], device=dev)
     runner.load_device(theta_dev)
     runner.batch.t["frozen"].zero_()
+    runner.prepare(W)
+    runner.prepare(K)
     with torch.cuda.stream(s):
         runner.run_graph(W)
     s.synchronize()
@@ -299,8 +301,7 @@ def main():
     # ---- e2e: the public API with host conformations in, host results out
     confs = [P.Conformation(thetas_all[r], np.zeros(D, bool), ch.n_residues) for r in range(lo, hi)]
     e2e_step = P.StepConfig(kappa=0.5, max_iters=K, torque_tol_rel=0.0, energy_window=0)
-    P.fold_ensemble(ch, confs[:2], fld, P.StepConfig(kappa=0.5, max_iters=2, torque_tol_rel=0.0,
-                                                     energy_window=0))
+    P.fold_ensemble(ch, confs, fld, e2e_step)      # warm: buffers and graphs cached
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -326,6 +327,8 @@ def main():
             r1 = DV.EnsembleRunner(c_ch, c_f, 1, P.StepConfig(max_iters=W + K, torque_tol_rel=0.0,
                                                             energy_window=0), chunk=16)
             r1.load(workloads.start_theta(cfg, c_ch)[None, :], np.zeros((1, c_ch.n_dof), bool))
+            r1.prepare(W)
+            r1.prepare(K)
             with torch.cuda.stream(s):
                 r1.run_graph(W)
                 s.synchronize()

@@ -215,6 +215,10 @@ int kf_torques_step(const kf_chain_t *c, const kf_field_t *f, kf_batch_t *w,
  * is done; the host polls status between chunks. */
 int kf_fold_iterations(const kf_chain_t *c, const kf_field_t *f, kf_batch_t *w,
                        const kf_step_t *step, int n_iters, void *stream);
+/* Capture and instantiate the graph kf_fold_iterations would replay for
+ * n_iters, without launching it (keeps graph construction out of timings). */
+int kf_fold_graph_prepare(const kf_chain_t *c, const kf_field_t *f, kf_batch_t *w,
+                          const kf_step_t *step, int n_iters, void *stream);
 /* Same loop body launched eagerly (no graph), for debugging and profiling. */
 int kf_fold_iterations_eager(const kf_chain_t *c, const kf_field_t *f, kf_batch_t *w,
                              const kf_step_t *step, int n_iters, void *stream);

@@ -83,6 +83,7 @@ _PROTOS = {
     "kf_torques_step": (I32, [P, P, P, P, P]),
     "kf_fold_iterations": (I32, [P, P, P, P, C.c_int, P]),
     "kf_fold_iterations_eager": (I32, [P, P, P, P, C.c_int, P]),
+    "kf_fold_graph_prepare": (I32, [P, P, P, P, C.c_int, P]),
     "kf_graph_cache_clear": (None, []),
     "kf_clash_report": (I32, [P, P, P]),
     "kf_bbox": (I32, [P, C.c_int, P, P]),

@@ -124,9 +124,21 @@ int kf_torques_step(const kf_chain_t *c, const kf_field_t *f, kf_batch_t *w, con
                             step ? 1 : 0, s);
 }
 
+static int fold_graph(const kf_chain_t *c, const kf_field_t *f, kf_batch_t *w, const kf_step_t *step,
+                      int n_iters, cudaStream_t s, bool launch);
+
 int kf_fold_iterations(const kf_chain_t *c, const kf_field_t *f, kf_batch_t *w, const kf_step_t *step,
                        int n_iters, void *stream) {
-    cudaStream_t s = (cudaStream_t)stream;
+    return fold_graph(c, f, w, step, n_iters, (cudaStream_t)stream, true);
+}
+
+int kf_fold_graph_prepare(const kf_chain_t *c, const kf_field_t *f, kf_batch_t *w, const kf_step_t *step,
+                          int n_iters, void *stream) {
+    return fold_graph(c, f, w, step, n_iters, (cudaStream_t)stream, false);
+}
+
+static int fold_graph(const kf_chain_t *c, const kf_field_t *f, kf_batch_t *w, const kf_step_t *step,
+                      int n_iters, cudaStream_t s, bool launch) {
     if (n_iters <= 0) return 0;
     const std::string key = graph_key(c, f, w, step, n_iters, s);
     cudaGraphExec_t exec = nullptr;
@@ -149,7 +161,7 @@ int kf_fold_iterations(const kf_chain_t *c, const kf_field_t *f, kf_batch_t *w, 
         std::lock_guard<std::mutex> lk(g_graph_mu);
         g_graphs[key] = exec;
     }
-    KF_CUDA(cudaGraphLaunch(exec, s), "graph launch");
+    if (launch) KF_CUDA(cudaGraphLaunch(exec, s), "graph launch");
     return 0;
 }
 

@@ -164,43 +164,57 @@ __global__ void bin_scatter_kernel(kf_field_t f, int B, int n, const int32_t *__
     sorted_atom[(size_t)b * n + start[b * H + atom_slot[gid]] + atom_rank[gid]] = a;
 }
 
-// One thread per occupied cell: sort members by atom index, gather the SoA.
-__global__ void bin_finalize_kernel(kf_field_t f, int B, int n, const double *__restrict__ pos,
-                                    const unsigned long long *__restrict__ keys, const int32_t *__restrict__ occ,
-                                    const int32_t *__restrict__ occ_offset, const int32_t *__restrict__ cnt,
-                                    const int32_t *__restrict__ start, int32_t *__restrict__ sorted_atom,
-                                    float4 *__restrict__ s_hi, float4 *__restrict__ s_lo,
-                                    double4 *__restrict__ s_pos, float4 *__restrict__ s_par,
-                                    int4 *__restrict__ s_aux, int4 *__restrict__ s_tree,
-                                    float4 *__restrict__ cell_box, const kf_status_t *status) {
-    const int item = blockIdx.x * blockDim.x + threadIdx.x;
+// One warp per occupied cell: members ranked by atom index in parallel
+// (deterministic visit order), then the cell-ordered SoA gathered one atom per
+// lane: fp32 hi/lo offsets from the cell centre, fp64 position, params, aux,
+// the static class window, and the members' bounding box.
+constexpr int FIN_WARPS = 4;
+constexpr int FIN_CAP = 1024;
+
+__global__ void __launch_bounds__(FIN_WARPS * 32)
+bin_finalize_kernel(kf_field_t f, int B, int n, const double *__restrict__ pos,
+                    const unsigned long long *__restrict__ keys, const int32_t *__restrict__ occ,
+                    const int32_t *__restrict__ occ_offset, const int32_t *__restrict__ cnt,
+                    const int32_t *__restrict__ start, int32_t *__restrict__ sorted_atom,
+                    float4 *__restrict__ s_hi, float4 *__restrict__ s_lo,
+                    double4 *__restrict__ s_pos, float4 *__restrict__ s_par,
+                    int4 *__restrict__ s_aux, int4 *__restrict__ s_tree,
+                    float4 *__restrict__ cell_box, const kf_status_t *status) {
+    __shared__ int buf[FIN_WARPS][FIN_CAP];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int item = blockIdx.x * FIN_WARPS + warp;
     if (item >= occ_offset[B]) return;
-    int lo = 0, hi = B;   // b: last trajectory with occ_offset[b] <= item
-    while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (occ_offset[mid] <= item) lo = mid; else hi = mid;
-    }
-    const int b = lo;
+    const int b = item_owner(occ_offset, B, item);
     const size_t H = (size_t)1 << f.hash_bits;
     const int slot = occ[b * H + (item - occ_offset[b])];
     const int s0 = start[b * H + slot], c = cnt[b * H + slot];
-    int32_t *ids = sorted_atom + (size_t)b * n;
-    for (int k = s0 + 1; k < s0 + c; ++k) {
-        const int v = ids[k];
-        int m = k - 1;
-        while (m >= s0 && ids[m] > v) { ids[m + 1] = ids[m]; --m; }
-        ids[m + 1] = v;
+    int32_t *ids = sorted_atom + (size_t)b * n + s0;
+    if (c <= FIN_CAP) {
+        for (int k = lane; k < c; k += 32) buf[warp][k] = ids[k];
+        __syncwarp();
+        for (int k = lane; k < c; k += 32) {
+            const int v = buf[warp][k];
+            int rank = 0;
+            for (int m = 0; m < c; ++m) rank += buf[warp][m] < v;
+            ids[rank] = v;
+        }
+    } else if (lane == 0) {   // pathological cell: serial insertion sort
+        for (int k = 1; k < c; ++k) {
+            const int v = ids[k];
+            int m = k - 1;
+            while (m >= 0 && ids[m] > v) { ids[m + 1] = ids[m]; --m; }
+            ids[m + 1] = v;
+        }
     }
-    const long long key = (long long)keys[b * H + slot];
-    const unsigned long long u = (unsigned long long)key;
-    const int cx = (int)((long long)(u << 1) >> 43), cy = (int)((long long)(u << 22) >> 43),
-              cz = (int)((long long)(u << 43) >> 43);
+    __syncwarp();
+    int cx, cy, cz;
+    unpack_cell((long long)keys[b * H + slot], cx, cy, cz);
     const double ctr[3] = {((double)cx + 0.5) * f.cell, ((double)cy + 0.5) * f.cell, ((double)cz + 0.5) * f.cell};
     const bool tree = !f.uniform_weights;
     float bl[3] = {INFINITY, INFINITY, INFINITY}, bh[3] = {-INFINITY, -INFINITY, -INFINITY};
-    for (int k = s0; k < s0 + c; ++k) {
+    for (int k = lane; k < c; k += 32) {
         const int a = ids[k];
-        const size_t ga = (size_t)b * n + a, gs = (size_t)b * n + k;
+        const size_t ga = (size_t)b * n + a, gs = (size_t)b * n + s0 + k;
         const double x = pos[3 * ga], y = pos[3 * ga + 1], z = pos[3 * ga + 2];
         s_pos[gs] = make_double4(x, y, z, 0.0);
         // offset from the cell centre as an fp32 pair: hi + lo == the fp64 offset
@@ -221,8 +235,16 @@ __global__ void bin_finalize_kernel(kf_field_t f, int B, int n, const double *__
                               tree ? (int)f.class_slow[a] : 0);
         s_tree[gs] = tree ? reinterpret_cast<const int4 *>(f.class_map)[a] : make_int4(0, 0, 0, 0);
     }
-    cell_box[2 * (b * H + slot)] = make_float4(bl[0], bl[1], bl[2], 0.f);
-    cell_box[2 * (b * H + slot) + 1] = make_float4(bh[0], bh[1], bh[2], 0.f);
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1)
+        for (int q = 0; q < 3; ++q) {
+            bl[q] = fminf(bl[q], __shfl_xor_sync(0xffffffffu, bl[q], d));
+            bh[q] = fmaxf(bh[q], __shfl_xor_sync(0xffffffffu, bh[q], d));
+        }
+    if (lane == 0) {
+        cell_box[2 * (b * H + slot)] = make_float4(bl[0], bl[1], bl[2], 0.f);
+        cell_box[2 * (b * H + slot) + 1] = make_float4(bh[0], bh[1], bh[2], 0.f);
+    }
 }
 
 }  // namespace
@@ -243,7 +265,7 @@ int kf_bin_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s) {
     bin_scatter_kernel<<<kf_blocks(total, 256), 256, 0, s>>>(*f, B, n, w->atom_slot, w->atom_rank, w->cell_start,
                                                              w->sorted_atom, w->status);
     KF_LAUNCH_CHECK("bin_scatter_kernel");
-    bin_finalize_kernel<<<kf_blocks(total, 128), 128, 0, s>>>(
+    bin_finalize_kernel<<<kf_blocks(total, FIN_WARPS), FIN_WARPS * 32, 0, s>>>(
         *f, B, n, w->pos, w->cell_key, w->occ, w->occ_offset, w->cell_cnt, w->cell_start, w->sorted_atom,
         reinterpret_cast<float4 *>(w->s_hi), reinterpret_cast<float4 *>(w->s_lo),
         reinterpret_cast<double4 *>(w->s_pos), reinterpret_cast<float4 *>(w->s_par),

@@ -46,10 +46,8 @@ struct Tile {
 template <typename T>
 struct WarpSmem {
     Tile J;
-    Tile I;
-    int4 itree[32];
     T acc[3][32];              // per-owner force sums of the current tile
-    unsigned short list[1024]; // accepted (owner << 5 | t) pairs of the tile, owner-major
+    unsigned short list[1024]; // candidate (owner << 5 | t) pairs of the tile, owner-major
 };
 
 struct Acc {
@@ -84,12 +82,15 @@ KF_DEV void pair_fp64(const kf_field_t &f, int i, int j, double d2, double dx, d
 }
 
 #ifndef PAIR_MINB
-#define PAIR_MINB 4
+#define PAIR_MINB 3
 #endif
 // F64 = false: fp32 pair math (the north-star configuration); true: fp64
 // pair math and fp64 per-tile sums (strict trajectory parity mode).
-template <bool F64>
-__global__ void __launch_bounds__(PAIR_WARPS * 32, PAIR_MINB)
+// SPLIT = true: one CTA per cell, its 4 warps split the 27 neighbour cells
+// (short per-cell latency: single trajectories); false: one warp per cell
+// (throughput: ensembles).
+template <bool F64, bool SPLIT>
+__global__ void __launch_bounds__(PAIR_WARPS * 32, SPLIT ? PAIR_MINB : 4)
 pair_kernel(kf_field_t f, int B, int n, const unsigned long long *__restrict__ keys,
             const int32_t *__restrict__ cnt, const int32_t *__restrict__ start, const int32_t *__restrict__ occ,
             const int32_t *__restrict__ occ_offset, const float4 *__restrict__ s_hi,
@@ -98,9 +99,18 @@ pair_kernel(kf_field_t f, int B, int n, const unsigned long long *__restrict__ k
             int32_t *__restrict__ work, double *__restrict__ forces, double *__restrict__ e_atom,
             long long *__restrict__ pair_count, kf_status_t *status) {
     using T = typename std::conditional<F64, double, float>::type;
+    constexpr int NI = SPLIT ? 1 : PAIR_WARPS;
+    __shared__ Tile Itile[NI];               // the i-chunk (shared by the CTA's warps if SPLIT)
+    __shared__ int4 itree_s[NI][32];
     __shared__ WarpSmem<T> smem[PAIR_WARPS];
+    __shared__ double part[SPLIT ? PAIR_WARPS : 1][3][32];
+    __shared__ double epart[PAIR_WARPS][2];
+    __shared__ long long cpart[PAIR_WARPS];
+    __shared__ int item_s[PAIR_WARPS];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     WarpSmem<T> &S = smem[warp];
+    Tile &I = Itile[SPLIT ? 0 : warp];
+    int4 *itree = itree_s[SPLIT ? 0 : warp];
     const uint32_t H = 1u << f.hash_bits;
     const int total = occ_offset[B];
     const float cellf = (float)f.cell;
@@ -110,9 +120,17 @@ pair_kernel(kf_field_t f, int B, int n, const unsigned long long *__restrict__ k
     const float kap_inv = f.dielectric_const ? (float)(1.0 / f.kappa) : 1.0f;
 
     for (;;) {
-        int item = 0;
-        if (lane == 0) item = atomicAdd(work, 1);
-        item = __shfl_sync(FULL, item, 0);
+        int item;
+        if (SPLIT) {
+            __syncthreads();
+            if (threadIdx.x == 0) item_s[0] = atomicAdd(work, 1);
+            __syncthreads();
+            item = item_s[0];
+        } else {
+            item = 0;
+            if (lane == 0) item = atomicAdd(work, 1);
+            item = __shfl_sync(FULL, item, 0);
+        }
         if (item >= total) break;
         const int b = item_owner(occ_offset, B, item);
         const size_t hb = (size_t)b * H, nb = (size_t)b * n;
@@ -125,20 +143,21 @@ pair_kernel(kf_field_t f, int B, int n, const unsigned long long *__restrict__ k
         for (int ic = 0; ic < c; ic += 32) {
             const int ci_n = min(32, c - ic);
             const bool valid = lane < ci_n;
-            __syncwarp();
-            if (valid) {
+            if ((!SPLIT || warp == 0) && valid) {
                 const size_t ki = nb + s0 + ic + lane;
-                S.I.hi[lane] = s_hi[ki];
-                S.I.lo[lane] = s_lo[ki];
-                S.I.par[lane] = s_par[ki];
-                S.I.aux[lane] = s_aux[ki];
-                S.itree[lane] = s_tree[ki];
+                I.hi[lane] = s_hi[ki];
+                I.lo[lane] = s_lo[ki];
+                I.par[lane] = s_par[ki];
+                I.aux[lane] = s_aux[ki];
+                itree[lane] = s_tree[ki];
             }
-            __syncwarp();
-            const float4 hi_i = S.I.hi[valid ? lane : 0];
+            if (SPLIT) __syncthreads(); else __syncwarp();
+            const float4 hi_i = I.hi[valid ? lane : 0];
             Acc a = {0.0, 0.0, 0.0, 0.0, 0.0, 0};
 
-            for (int s = 0; s < f.n_stencil; ++s) {
+            // the 27 neighbour cells are dealt to the warps round-robin; each warp
+            // keeps per-owner fp64 sums over its cells in a fixed order
+            for (int s = SPLIT ? warp : 0; s < f.n_stencil; s += SPLIT ? PAIR_WARPS : 1) {
                 const int ox = f.stencil[3 * s], oy = f.stencil[3 * s + 1], oz = f.stencil[3 * s + 2];
                 const int js = cell_probe(keys + hb, H, cx + ox, cy + oy, cz + oz);
                 if (js < 0) continue;
@@ -202,10 +221,10 @@ pair_kernel(kf_field_t f, int B, int n, const unsigned long long *__restrict__ k
                         long long pc = 0;
                         if (act) {
                             const int t = e & 31;
-                            const int4 ai = S.I.aux[o], aj = S.J.aux[t];
+                            const int4 ai = I.aux[o], aj = S.J.aux[t];
                             const int i = ai.x, j = aj.x;
                             if (i != j) {
-                                const float4 hi = S.I.hi[o], li = S.I.lo[o], hj = S.J.hi[t], lj = S.J.lo[t];
+                                const float4 hi = I.hi[o], li = I.lo[o], hj = S.J.hi[t], lj = S.J.lo[t];
                                 const float dxf = ((hi.x - hj.x) - sx) + (li.x - lj.x);
                                 const float dyf = ((hi.y - hj.y) - sy) + (li.y - lj.y);
                                 const float dzf = ((hi.z - hj.z) - sz) + (li.z - lj.z);
@@ -232,7 +251,7 @@ pair_kernel(kf_field_t f, int B, int n, const unsigned long long *__restrict__ k
                                         int cls = 4;
                                         const int off = j - i + 32;
                                         if ((unsigned)off < 64u) {
-                                            const int4 cm = S.itree[o];
+                                            const int4 cm = itree[o];
                                             const unsigned wd = off < 32 ? (off < 16 ? cm.x : cm.y)
                                                                          : (off < 48 ? cm.z : cm.w);
                                             cls = 4 - (int)((wd >> (2 * (off & 15))) & 3u);
@@ -256,7 +275,7 @@ pair_kernel(kf_field_t f, int B, int n, const unsigned long long *__restrict__ k
                                         }
                                         if (!clash) pair_fp64(f, i, j, d2, dx, dy, dz, we, wv, ke, kv, out);
                                     } else {
-                                        const float4 qi = S.I.par[o], qj = S.J.par[t];
+                                        const float4 qi = I.par[o], qj = S.J.par[t];
                                         const float inv_r = rsqrtf(d2f);
                                         const float inv_r2 = inv_r * inv_r;
                                         float g = 0.f;
@@ -309,27 +328,58 @@ pair_kernel(kf_field_t f, int B, int n, const unsigned long long *__restrict__ k
                     a.ee += (double)fe; a.ev += (double)fv;
                 }
             }
-            if (valid) {
-                const size_t o = nb + S.I.aux[lane].x;
+            ee += a.ee; ev += a.ev; pcount += a.cnt;
+            if (SPLIT) {
+                // combine the warps' partial forces in warp order (deterministic)
+                part[SPLIT ? warp : 0][0][lane] = a.fx;
+                part[SPLIT ? warp : 0][1][lane] = a.fy;
+                part[SPLIT ? warp : 0][2][lane] = a.fz;
+                __syncthreads();
+                if (warp == 0 && valid) {
+                    double fx = 0.0, fy = 0.0, fz = 0.0;
+#pragma unroll
+                    for (int w = 0; w < (SPLIT ? PAIR_WARPS : 1); ++w) {
+                        fx += part[w][0][lane]; fy += part[w][1][lane]; fz += part[w][2][lane];
+                    }
+                    const size_t o = nb + I.aux[lane].x;
+                    forces[3 * o] = fx; forces[3 * o + 1] = fy; forces[3 * o + 2] = fz;
+                    e_atom[2 * o] = 0.0; e_atom[2 * o + 1] = 0.0;
+                    pair_count[o] = 0;
+                }
+                __syncthreads();
+            } else if (valid) {
+                const size_t o = nb + I.aux[lane].x;
                 forces[3 * o] = a.fx; forces[3 * o + 1] = a.fy; forces[3 * o + 2] = a.fz;
                 e_atom[2 * o] = 0.0; e_atom[2 * o + 1] = 0.0;
                 pair_count[o] = 0;
             }
-            ee += a.ee; ev += a.ev; pcount += a.cnt;
         }
-        // cell totals on a fixed xor tree, stored at the cell's lowest atom
-        // (cells are a function of the positions, so the layout is deterministic)
+        // cell totals: fixed xor tree per warp, then warps in order, stored at the
+        // cell's lowest atom (cells are a function of the positions: deterministic)
 #pragma unroll
         for (int d = 16; d > 0; d >>= 1) {
             ee += __shfl_xor_sync(FULL, ee, d);
             ev += __shfl_xor_sync(FULL, ev, d);
             pcount += __shfl_xor_sync(FULL, pcount, d);
         }
-        __syncwarp();
-        if (lane == 0) {
-            const size_t o = nb + s_aux[nb + s0].x;
-            e_atom[2 * o] = ee; e_atom[2 * o + 1] = ev;
-            pair_count[o] = pcount;
+        if (SPLIT) {
+            if (lane == 0) { epart[warp][0] = ee; epart[warp][1] = ev; cpart[warp] = pcount; }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                double te = 0.0, tv = 0.0;
+                long long tc = 0;
+                for (int w = 0; w < PAIR_WARPS; ++w) { te += epart[w][0]; tv += epart[w][1]; tc += cpart[w]; }
+                const size_t o = nb + s_aux[nb + s0].x;
+                e_atom[2 * o] = te; e_atom[2 * o + 1] = tv;
+                pair_count[o] = tc;
+            }
+        } else {
+            __syncwarp();
+            if (lane == 0) {
+                const size_t o = nb + s_aux[nb + s0].x;
+                e_atom[2 * o] = ee; e_atom[2 * o + 1] = ev;
+                pair_count[o] = pcount;
+            }
         }
     }
 }
@@ -379,7 +429,10 @@ int kf_pairs_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s) {
         g_pair_grid = sms * 4;
     }
     KF_CUDA(cudaMemsetAsync(w->work, 0, sizeof(int32_t), s), "memset work");
-    auto kern = f->precision ? pair_kernel<true> : pair_kernel<false>;
+    // one CTA per cell when the whole batch is small (latency), one warp per cell otherwise
+    const bool split = (long long)w->B * n < 200000;
+    auto kern = f->precision ? (split ? pair_kernel<true, true> : pair_kernel<true, false>)
+                             : (split ? pair_kernel<false, true> : pair_kernel<false, false>);
     kern<<<g_pair_grid, PAIR_WARPS * 32, 0, s>>>(
         *f, w->B, n, w->cell_key, w->cell_cnt, w->cell_start, w->occ, w->occ_offset,
         reinterpret_cast<const float4 *>(w->s_hi), reinterpret_cast<const float4 *>(w->s_lo),

@@ -41,20 +41,91 @@ KF_DEV bool covers_shifted(double px, double py, double pz, const NbSlot &s, int
     return d2_rowsum(xsub(px, sx), xsub(py, sy), xsub(pz, sz)) <= s.r2;
 }
 
-// Shared body: states + (optionally) events for atom i against nn staged slots.
-// Returns the number of covered samples.
+// Staged neighbour set of one atom (shared memory): coordinates + R_off^2,
+// an fp32 spherical-cap prefilter per neighbour, and a nearest-first order.
+//
+// Cap prefilter: for a sample p = r_i + R_i q (|q| = 1) and a neighbour at
+// distance d in direction u, |p - r_j|^2 = R_i^2 + d^2 - 2 R_i d (q.u), so j can
+// cover p only if q.u >= c1 = (R_i^2 + d^2 - R_j^2) / (2 R_i d), and j displaced
+// by dr only if q.u >= c2 = (R_i^2 + d^2 - (R_j + dr)^2) / (2 R_i d).  The fp32
+// test q.u >= c - 1e-3 is a strict superset (all rounding is ~1e-7); every
+// sample that passes gets the exact fp64 test of the reference.
+struct NbSet {
+    NbSlot *nb;
+    float4 *cap;          // u.x, u.y, u.z, c1
+    float *c2;
+    unsigned short *ord;  // nearest first
+    int32_t *atom;
+    double *key;          // sort scratch
+};
+
+constexpr float CAP_MARGIN = 1e-3f;
+
+KF_DEV void prepare_neighbors(const double *xi, double r_i, int count, double dr, const NbSet &S) {
+    const int P = count <= 1 ? 1 : 1 << (32 - __clz(count - 1));
+    for (int m = threadIdx.x; m < P; m += blockDim.x) {
+        if (m < count) {
+            const NbSlot q = S.nb[m];
+            const double dx = q.x - xi[0], dy = q.y - xi[1], dz = q.z - xi[2];
+            const double d2 = dx * dx + dy * dy + dz * dz;
+            const double d = sqrt(d2);
+            const double rj = sqrt(q.r2);
+            float4 cp;
+            float c2 = -3.f;
+            if (d > 1e-6) {
+                const double inv = 1.0 / d;
+                const double c1 = (r_i * r_i + d2 - q.r2) / (2.0 * r_i * d);
+                c2 = (float)((r_i * r_i + d2 - (rj + dr) * (rj + dr)) / (2.0 * r_i * d)) - CAP_MARGIN;
+                cp = make_float4((float)(dx * inv), (float)(dy * inv), (float)(dz * inv), (float)c1 - CAP_MARGIN);
+            } else {
+                cp = make_float4(0.f, 0.f, 0.f, -3.f);
+            }
+            S.cap[m] = cp;
+            S.c2[m] = c2;
+            S.key[m] = d2;
+        } else {
+            S.key[m] = INFINITY;
+        }
+        S.ord[m] = (unsigned short)m;
+    }
+    __syncthreads();
+    // bitonic sort of (key, ord) ascending
+    for (int size = 2; size <= P; size <<= 1)
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int t = threadIdx.x; t < P; t += blockDim.x) {
+                const int u = t ^ stride;
+                if (u > t) {
+                    const bool up = (t & size) == 0;
+                    const double a = S.key[t], b = S.key[u];
+                    if ((a > b) == up) {
+                        S.key[t] = b; S.key[u] = a;
+                        const unsigned short o = S.ord[t];
+                        S.ord[t] = S.ord[u]; S.ord[u] = o;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+}
+
+// States + (optionally) forward-difference events of atom i's samples against
+// the staged set; returns the number of covered samples.
 template <bool WITH_FORCES>
 KF_DEV int enumerate_samples(const double *xi, double r_off_i, const double *samples, int N,
-                             const NbSlot *nb, int nn, long long wi, double dr, long long *acc_nb,
-                             long long *acc_i, uint8_t *counts_out, int32_t *crit_out,
-                             const int32_t *nb_atom) {
+                             const NbSet &S, int nn, long long wi, double dr, long long *acc_nb,
+                             long long *acc_i, uint8_t *counts_out, int32_t *crit_out) {
     int covered = 0;
     for (int k = threadIdx.x; k < N; k += blockDim.x) {
+        const double *q = samples + 3 * k;
+        const float qx = (float)q[0], qy = (float)q[1], qz = (float)q[2];
         double px, py, pz;
-        sample_point(xi, r_off_i, samples + 3 * k, px, py, pz);
+        sample_point(xi, r_off_i, q, px, py, pz);
         int cnt = 0, crit = -1;
-        for (int m = 0; m < nn; ++m) {
-            if (covers(px, py, pz, nb[m])) {
+        for (int r = 0; r < nn; ++r) {
+            const int m = S.ord[r];
+            const float4 cp = S.cap[m];
+            if (qx * cp.x + qy * cp.y + qz * cp.z < cp.w) continue;
+            if (covers(px, py, pz, S.nb[m])) {
                 crit = m;
                 if (++cnt == 2) break;
             }
@@ -62,13 +133,16 @@ KF_DEV int enumerate_samples(const double *xi, double r_off_i, const double *sam
         covered += cnt > 0;
         if (counts_out) {
             counts_out[k] = (uint8_t)cnt;
-            crit_out[k] = cnt == 1 ? nb_atom[crit] : -1;
+            crit_out[k] = cnt == 1 ? S.atom[crit] : -1;
         }
         if (WITH_FORCES && wi != 0) {
             if (cnt == 0) {
-                for (int s = 0; s < 3; ++s) {
-                    for (int m = 0; m < nn; ++m) {
-                        if (covers_shifted(px, py, pz, nb[m], s, dr)) {
+                for (int m = 0; m < nn; ++m) {
+                    const float4 cp = S.cap[m];
+                    if (qx * cp.x + qy * cp.y + qz * cp.z < S.c2[m]) continue;
+                    const NbSlot nbm = S.nb[m];
+                    for (int s = 0; s < 3; ++s) {
+                        if (covers_shifted(px, py, pz, nbm, s, dr)) {
                             atomicAdd(reinterpret_cast<unsigned long long *>(&acc_nb[3 * m + s]),
                                       (unsigned long long)wi);
                             acc_i[s] -= wi;
@@ -77,7 +151,7 @@ KF_DEV int enumerate_samples(const double *xi, double r_off_i, const double *sam
                 }
             } else if (cnt == 1) {
                 for (int s = 0; s < 3; ++s) {
-                    if (!covers_shifted(px, py, pz, nb[crit], s, dr)) {
+                    if (!covers_shifted(px, py, pz, S.nb[crit], s, dr)) {
                         acc_i[s] += wi;
                         atomicAdd(reinterpret_cast<unsigned long long *>(&acc_nb[3 * crit + s]),
                                   (unsigned long long)(-wi));
@@ -87,6 +161,25 @@ KF_DEV int enumerate_samples(const double *xi, double r_off_i, const double *sam
         }
     }
     return covered;
+}
+
+// shared-memory carve-up: nb | cap | acc (also the sort keys) | c2 | atom | ord
+KF_DEV NbSet carve(unsigned char *smem, int cap, long long **acc) {
+    NbSet S;
+    S.nb = reinterpret_cast<NbSlot *>(smem);
+    S.cap = reinterpret_cast<float4 *>(S.nb + cap);
+    *acc = reinterpret_cast<long long *>(S.cap + cap);
+    S.key = reinterpret_cast<double *>(*acc);
+    S.c2 = reinterpret_cast<float *>(*acc + 3 * cap);
+    S.atom = reinterpret_cast<int32_t *>(S.c2 + cap);
+    S.ord = reinterpret_cast<unsigned short *>(S.atom + cap);
+    return S;
+}
+
+size_t set_smem(int cap) {
+    const int P = cap <= 1 ? 1 : 1 << (32 - __builtin_clz(cap - 1));
+    return (size_t)P * (sizeof(NbSlot) + sizeof(float4) + 3 * sizeof(long long) + sizeof(float) +
+                        sizeof(int32_t) + sizeof(unsigned short));
 }
 
 // Hot path: neighbours come from the spatial hash of this iteration.
@@ -102,9 +195,10 @@ solv_hot_kernel(kf_field_t f, int n, int n_solv, const int32_t *__restrict__ sol
     const int i = solv_atoms[blockIdx.x % n_solv];
     if (status[b].done) return;
     extern __shared__ __align__(16) unsigned char smem[];
-    NbSlot *nb = reinterpret_cast<NbSlot *>(smem);
-    long long *acc_nb = reinterpret_cast<long long *>(nb + nb_cap);
-    int32_t *nb_atom = reinterpret_cast<int32_t *>(acc_nb + 3 * nb_cap);
+    long long *acc_nb;
+    const NbSet S = carve(smem, nb_cap, &acc_nb);
+    NbSlot *nb = S.nb;
+    int32_t *nb_atom = S.atom;
     __shared__ int nn;
     __shared__ long long acc_i_s[3];
     __shared__ double red[32];
@@ -119,22 +213,47 @@ solv_hot_kernel(kf_field_t f, int n, int n_solv, const int32_t *__restrict__ sol
     int cx, cy, cz;
     unpack_cell((long long)keys[hb + atom_slot[ai]], cx, cy, cz);
 
-    for (int s = threadIdx.x; s < f.n_stencil; s += blockDim.x) {
-        const int js = cell_probe(keys + hb, H, cx + f.stencil[3 * s], cy + f.stencil[3 * s + 1],
-                                  cz + f.stencil[3 * s + 2]);
-        if (js < 0) continue;
-        for (int kk = start[hb + js]; kk < start[hb + js] + cnt[hb + js]; ++kk) {
-            const double4 pj = s_pos[nbase + kk];
-            const int j = s_aux[nbase + kk].x;
-            if (j == i) continue;
-            const double dx = xi[0] - pj.x, dy = xi[1] - pj.y, dz = xi[2] - pj.z;
-            const double lim = r_off_i + f.r_off[j] + f.reach_pad;
-            if (dx * dx + dy * dy + dz * dz > lim * lim) continue;
-            const int slot = atomicAdd(&nn, 1);
-            if (slot < nb_cap) {
-                nb[slot] = NbSlot{pj.x, pj.y, pj.z, f.r_off2[j]};
-                nb_atom[slot] = j;
-            }
+    // gather: probe the stencil cells (one thread each), then sweep all their
+    // members with every thread of the block
+    __shared__ int cell_first[32], cell_len[32], cell_pre[33];
+    if (threadIdx.x < 32) {
+        int first = 0, len = 0;
+        if ((int)threadIdx.x < f.n_stencil) {
+            const int s = threadIdx.x;
+            const int js = cell_probe(keys + hb, H, cx + f.stencil[3 * s], cy + f.stencil[3 * s + 1],
+                                      cz + f.stencil[3 * s + 2]);
+            if (js >= 0) { first = start[hb + js]; len = cnt[hb + js]; }
+        }
+        cell_first[threadIdx.x] = first;
+        cell_len[threadIdx.x] = len;
+        int incl = len;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, o);
+            if ((int)threadIdx.x >= o) incl += v;
+        }
+        cell_pre[threadIdx.x + 1] = incl;
+        if (threadIdx.x == 0) cell_pre[0] = 0;
+    }
+    __syncthreads();
+    const int cand = cell_pre[32];
+    for (int c = threadIdx.x; c < cand; c += blockDim.x) {
+        int lo = 0, hi = 32;
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (cell_pre[mid] <= c) lo = mid; else hi = mid;
+        }
+        const int kk = cell_first[lo] + (c - cell_pre[lo]);
+        const double4 pj = s_pos[nbase + kk];
+        const int j = s_aux[nbase + kk].x;
+        if (j == i) continue;
+        const double dx = xi[0] - pj.x, dy = xi[1] - pj.y, dz = xi[2] - pj.z;
+        const double lim = r_off_i + f.r_off[j] + f.reach_pad;
+        if (dx * dx + dy * dy + dz * dz > lim * lim) continue;
+        const int slot = atomicAdd(&nn, 1);
+        if (slot < nb_cap) {
+            nb[slot] = NbSlot{pj.x, pj.y, pj.z, f.r_off2[j]};
+            nb_atom[slot] = j;
         }
     }
     __syncthreads();
@@ -147,13 +266,14 @@ solv_hot_kernel(kf_field_t f, int n, int n_solv, const int32_t *__restrict__ sol
         }
         return;
     }
+    prepare_neighbors(xi, r_off_i, count, f.delta_r, S);
     for (int m = threadIdx.x; m < 3 * count; m += blockDim.x) acc_nb[m] = 0;
     __syncthreads();
 
     long long acc_i[3] = {0, 0, 0};
     const long long wi = f.w_int[i];
-    const int covered = enumerate_samples<true>(xi, r_off_i, f.samples, f.n_samples, nb, count, wi,
-                                                f.delta_r, acc_nb, acc_i, nullptr, nullptr, nb_atom);
+    const int covered = enumerate_samples<true>(xi, r_off_i, f.samples, f.n_samples, S, count, wi,
+                                                f.delta_r, acc_nb, acc_i, nullptr, nullptr);
     const double cov_total = block_sum((double)covered, red);
     for (int s = 0; s < 3; ++s) {
         const long long v = warp_sum_ll(acc_i[s]);
@@ -221,22 +341,22 @@ sasa_api_kernel(const double *__restrict__ pos, const double *__restrict__ r_off
                 int nb_cap, int *overflow) {
     const int i = blockIdx.x;
     extern __shared__ __align__(16) unsigned char smem[];
-    NbSlot *nb = reinterpret_cast<NbSlot *>(smem);
-    int32_t *nb_atom = reinterpret_cast<int32_t *>(nb + nb_cap);
+    long long *scratch;
+    const NbSet S = carve(smem, nb_cap, &scratch);
     __shared__ int nn;
     __shared__ double red[32];
     if (threadIdx.x == 0) nn = 0;
     __syncthreads();
-    const int count = stage_from_list(pos, r_off, r_off2, i, nb_off, nbl, pad, nb, nb_atom, nb_cap, &nn);
+    const int count = stage_from_list(pos, r_off, r_off2, i, nb_off, nbl, pad, S.nb, S.atom, nb_cap, &nn);
     if (count > nb_cap) {
         if (threadIdx.x == 0) atomicMax(overflow, count);
         return;
     }
     const double xi[3] = {pos[3 * (size_t)i], pos[3 * (size_t)i + 1], pos[3 * (size_t)i + 2]};
+    prepare_neighbors(xi, r_off[i], count, 0.0, S);
     const bool empty_list = nb_off[i + 1] == nb_off[i];
-    const int cov = enumerate_samples<false>(xi, r_off[i], samples, N, nb, count, 0, 0.0, nullptr,
-                                             nullptr, counts + (size_t)i * N, critical + (size_t)i * N,
-                                             nb_atom);
+    const int cov = enumerate_samples<false>(xi, r_off[i], samples, N, S, count, 0, 0.0, nullptr,
+                                             nullptr, counts + (size_t)i * N, critical + (size_t)i * N);
     const double total = block_sum((double)cov, red);
     if (threadIdx.x == 0) {
         const int64_t c = empty_list ? 0 : (int64_t)total;
@@ -259,9 +379,10 @@ solv_forces_api_kernel(const double *__restrict__ pos, const double *__restrict_
     const long long wi = w_int[i];
     if (wi == 0 || nb_off[i + 1] == nb_off[i]) return;
     extern __shared__ __align__(16) unsigned char smem[];
-    NbSlot *nb = reinterpret_cast<NbSlot *>(smem);
-    long long *acc_nb = reinterpret_cast<long long *>(nb + nb_cap);
-    int32_t *nb_atom = reinterpret_cast<int32_t *>(acc_nb + 3 * nb_cap);
+    long long *acc_nb;
+    const NbSet S = carve(smem, nb_cap, &acc_nb);
+    NbSlot *nb = S.nb;
+    int32_t *nb_atom = S.atom;
     __shared__ int nn;
     __shared__ long long acc_i_s[3];
     if (threadIdx.x == 0) { nn = 0; acc_i_s[0] = acc_i_s[1] = acc_i_s[2] = 0; }
@@ -271,9 +392,10 @@ solv_forces_api_kernel(const double *__restrict__ pos, const double *__restrict_
         if (threadIdx.x == 0) atomicMax(overflow, count);
         return;
     }
+    const double xi[3] = {pos[3 * (size_t)i], pos[3 * (size_t)i + 1], pos[3 * (size_t)i + 2]};
+    prepare_neighbors(xi, r_off[i], count, dr, S);
     for (int m = threadIdx.x; m < 3 * count; m += blockDim.x) acc_nb[m] = 0;
     __syncthreads();
-    const double xi[3] = {pos[3 * (size_t)i], pos[3 * (size_t)i + 1], pos[3 * (size_t)i + 2]};
     long long acc_i[3] = {0, 0, 0};
     for (int k = threadIdx.x; k < N; k += blockDim.x) {
         const int c = counts[(size_t)i * N + k];
@@ -281,13 +403,17 @@ solv_forces_api_kernel(const double *__restrict__ pos, const double *__restrict_
         double px, py, pz;
         sample_point(xi, r_off[i], samples + 3 * k, px, py, pz);
         if (c == 0) {
-            for (int s = 0; s < 3; ++s)
-                for (int m = 0; m < count; ++m)
+            const float qx = (float)samples[3 * k], qy = (float)samples[3 * k + 1], qz = (float)samples[3 * k + 2];
+            for (int m = 0; m < count; ++m) {
+                const float4 cp = S.cap[m];
+                if (qx * cp.x + qy * cp.y + qz * cp.z < S.c2[m]) continue;
+                for (int s = 0; s < 3; ++s)
                     if (covers_shifted(px, py, pz, nb[m], s, dr)) {
                         atomicAdd(reinterpret_cast<unsigned long long *>(&acc_nb[3 * m + s]),
                                   (unsigned long long)wi);
                         acc_i[s] -= wi;
                     }
+            }
         } else {
             const int jo = critical[(size_t)i * N + k];
             const NbSlot so{pos[3 * (size_t)jo], pos[3 * (size_t)jo + 1], pos[3 * (size_t)jo + 2], r_off2[jo]};
@@ -327,7 +453,7 @@ __global__ void fixed_to_f64_kernel(const long long *acc, int64_t m, double quan
     if (k < m) out[k] = xmul(__ll2double_rn(acc[k]), quantum);
 }
 
-size_t hot_smem(int cap) { return (size_t)cap * (sizeof(NbSlot) + 3 * sizeof(long long) + sizeof(int32_t)); }
+
 
 }  // namespace
 
@@ -336,7 +462,7 @@ int kf_solvation_launch(const kf_field_t *f, kf_batch_t *w, int n, int n_solv, c
     const int B = w->B;
     KF_CUDA(cudaMemsetAsync(w->solv_acc, 0, sizeof(long long) * (size_t)B * n * 3, s), "memset solv_acc");
     if (n_solv > 0) {
-        const size_t smem = hot_smem(w->nb_cap);
+        const size_t smem = set_smem(w->nb_cap);
         static size_t opted = 0;
         if (smem > 48 * 1024 && smem > opted) {
             KF_CUDA(cudaFuncSetAttribute(solv_hot_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
@@ -367,7 +493,7 @@ int kf_sasa_api_launch(const double *pos, int n, const double *r_off, const doub
                        double four_pi, double *f_exp, double *a_exp, double *cav, int nb_cap, int *overflow,
                        cudaStream_t s) {
     if (n == 0) return 0;
-    const size_t smem = (size_t)nb_cap * (sizeof(NbSlot) + sizeof(int32_t));
+    const size_t smem = set_smem(nb_cap);
     if (smem > 48 * 1024)
         KF_CUDA(cudaFuncSetAttribute(sasa_api_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                 "smem attr");
@@ -383,7 +509,7 @@ int kf_solv_forces_api_launch(const double *pos, int n, const double *r_off, con
                               const int64_t *nb, const uint8_t *counts, const int32_t *critical, double dr,
                               double pad, long long *acc, int nb_cap, int *overflow, cudaStream_t s) {
     if (n == 0) return 0;
-    const size_t smem = hot_smem(nb_cap);
+    const size_t smem = set_smem(nb_cap);
     if (smem > 48 * 1024)
         KF_CUDA(cudaFuncSetAttribute(solv_forces_api_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem), "smem attr");

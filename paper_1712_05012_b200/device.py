@@ -377,6 +377,7 @@ class DeviceField(ParamTables):
         t["stencil"] = _up(sten, np.int32)
         s.stencil = t["stencil"].data_ptr()
         s.n_stencil = len(sten)
+        assert s.n_stencil <= 32, "one-cell reach stencil expected (27 cells)"
         s.hash_bits = max(6, int(math.ceil(math.log2(max(2 * n, 2)))))
         s.precision = 1 if _precision["pair"] == "fp64" else 0
         self.n = n
@@ -710,6 +711,18 @@ class EnsembleRunner:
             b.reset_status()
             _prep_clash_key(b)
             b.t["theta"][:, :D].copy_(theta_dev)
+
+    def prepare(self, n_iters: int):
+        """Capture the graphs run_graph(n_iters) will replay (no launch)."""
+        lib = N.lib()
+        cs, fs, bs = N.ref(self.dc.struct), N.ref(self.df.struct_for(False)), N.ref(self.batch.struct)
+        ss = N.ref(_step_struct(self.step))
+        sizes = {min(self.chunk, n_iters)}
+        if n_iters % self.chunk:
+            sizes.add(n_iters % self.chunk)
+        with torch.cuda.stream(stream()):
+            for k in sizes:
+                N.check(lib.kf_fold_graph_prepare(cs, fs, bs, ss, k, _sp()), "kf_fold_graph_prepare")
 
     def run_graph(self, n_iters: int):
         """Enqueue n_iters iterations (no host sync)."""
@@ -1068,6 +1081,11 @@ def classify_pairs(tree, i, j) -> np.ndarray:
 # solvation API
 # --------------------------------------------------------------------------
 
+def _pow2_cap(longest: int) -> int:
+    # staged neighbours per atom: a power of two (the in-block bitonic sort), <= 2048 (smem)
+    return int(min(max(1, 1 << int(math.ceil(math.log2(max(longest, 1))))), 2048))
+
+
 def _csr(neighbors, n):
     lens = np.array([len(x) for x in neighbors], np.int64)
     if len(lens) != n:
@@ -1084,7 +1102,7 @@ def sasa_pass(positions, params, neighbors, sphere, config):
     r_off = np.asarray(params.R, float) + config.probe_radius
     r_off2 = r_off * r_off
     off, flat, longest = _csr(neighbors, n)
-    cap = max(1, min(longest, 6000))
+    cap = _pow2_cap(longest)
     with torch.cuda.stream(stream()):
         p = _up(pos, np.float64)
         dev = p.device
@@ -1116,7 +1134,7 @@ def solvation_forces(positions, params, neighbors, sphere, states, config) -> np
     r_off2 = r_off * r_off
     w_int, quantum = force_quantum(params, r_off, N_s, config.delta_r)
     off, flat, longest = _csr(neighbors, n)
-    cap = max(1, min(longest, 3500))
+    cap = _pow2_cap(longest)
     with torch.cuda.stream(stream()):
         p = _up(pos, np.float64)
         dev = p.device
