@@ -43,10 +43,12 @@ struct Tile {
     int4 aux[32];
 };
 
+constexpr int RES_BATCH = 128;
+
 template <typename T>
 struct WarpSmem {
     Tile J;
-    T acc[3][32];              // per-owner force sums of the current tile
+    T res[RES_BATCH][3];       // per-pair forces of the current batch of the tile's list
     unsigned short list[1024]; // candidate (owner << 5 | t) pairs of the tile, owner-major
 };
 
@@ -79,6 +81,64 @@ KF_DEV void pair_fp64(const kf_field_t &f, int i, int j, double d2, double dx, d
     const double g = mag * inv_d;
     out[0] = (T)(g * dx); out[1] = (T)(g * dy); out[2] = (T)(g * dz);
     out[3] = (T)ee; out[4] = (T)ev;
+}
+
+// Everything the exact / fp64 pair path needs, kept out of the kernel's
+// register allocation (the path runs for pairs within 1e-3 A^2 of a cut-off,
+// below 1 A, or always in fp64 mode).
+struct SlowArgs {
+    const double *q, *R, *eps;
+    double kappa, cut2, te2, tv2, wel[4], wvd[4];
+    int dconst;
+};
+
+__device__ __noinline__ int slow_class(const int32_t *tp, const int32_t *tgp, const int32_t *tgg,
+                                       const int32_t *tres, const uint8_t *tchain, int i, int j) {
+    if (!tchain[i] || !tchain[j] || abs(tres[i] - tres[j]) > 1) return 4;
+    const int pi = tp[i], gpi = tgp[i], ggi = tgg[i], pj = tp[j], gpj = tgp[j], ggj = tgg[j];
+    if (pi == j || pj == i) return 1;
+    if (gpi == j || gpj == i || (pi >= 0 && pi == pj)) return 2;
+    if (ggi == j || ggj == i || (gpi >= 0 && gpi == pj) || (gpj >= 0 && gpj == pi)) return 3;
+    return 4;
+}
+
+template <typename T>
+__device__ __noinline__ void slow_pair(bool f64, const SlowArgs &A, const double4 *pi_, const double4 *pj_, int i,
+                                       int j, int cls, T *out, int *pce, int *pcv, kf_status_t *st) {
+    const double4 p_i = *pi_, p_j = *pj_;
+    const double dx = xsub(p_i.x, p_j.x), dy = xsub(p_i.y, p_j.y), dz = xsub(p_i.z, p_j.z);
+    const double d2 = d2_einsum(dx, dy, dz);
+    if (d2 > A.cut2) return;
+    const bool ke = d2 <= A.te2, kv = d2 <= A.tv2;
+    *pce = ke; *pcv = kv;
+    const double we = A.wel[cls - 1], wv = A.wvd[cls - 1];
+    if (d2 < 1e-11) {
+        const double d = sqrt(d2);
+        if (d < MIN_DISTANCE) {
+            atomicMin(&st->dmin_bits, (unsigned long long)__double_as_longlong(d));
+            if (atomicCAS(&st->error, KF_ERR_NONE, KF_ERR_CLASH) == KF_ERR_NONE) st->err_iter = st->iter;
+            return;
+        }
+    }
+    const double d = sqrt(d2);
+    const double inv_d = 1.0 / d;
+    double mag = 0.0, ee = 0.0, ev = 0.0;
+    if (ke) {
+        const double num = COULOMB_K * we * A.q[i] * A.q[j];
+        ee = A.dconst ? num * inv_d / A.kappa : num * inv_d * inv_d;   // num / (kappa d)
+        mag += ee * inv_d;                                              // num / (kappa d^2)
+    }
+    if (kv) {
+        const double eps = sqrt(A.eps[i] * A.eps[j]);
+        const double r = (A.R[i] + A.R[j]) * inv_d;
+        const double r2 = r * r, r6 = r2 * r2 * r2;
+        ev = wv * eps * (r6 * r6 - 2.0 * r6);
+        mag += 12.0 * wv * eps * (r6 * r6 - r6) * inv_d;
+    }
+    const double g = mag * inv_d;
+    out[0] = (T)(g * dx); out[1] = (T)(g * dy); out[2] = (T)(g * dz);
+    out[3] = (T)ee; out[4] = (T)ev;
+    (void)f64;
 }
 
 #ifndef PAIR_MINB
@@ -118,6 +178,19 @@ pair_kernel(kf_field_t f, int B, int n, const unsigned long long *__restrict__ k
     const float cut2f = (float)f.cut_pair2, tvf = (float)f.thr_vdw2, tef = (float)f.thr_elec2;
     const float band = 1e-3f;
     const float kap_inv = f.dielectric_const ? (float)(1.0 / f.kappa) : 1.0f;
+    float wf[8];
+    for (int q = 0; q < 4; ++q) {
+        wf[q] = f.uniform_weights ? (float)f.uniform_value : (float)f.w_elec[q];
+        wf[4 + q] = f.uniform_weights ? (float)f.uniform_value : (float)f.w_vdw[q];
+    }
+    SlowArgs fx64;
+    fx64.q = f.q; fx64.R = f.R; fx64.eps = f.eps;
+    fx64.kappa = f.kappa; fx64.cut2 = f.cut_pair2; fx64.te2 = f.thr_elec2; fx64.tv2 = f.thr_vdw2;
+    fx64.dconst = f.dielectric_const;
+    for (int q = 0; q < 4; ++q) {
+        fx64.wel[q] = f.uniform_weights ? f.uniform_value : f.w_elec[q];
+        fx64.wvd[q] = f.uniform_weights ? f.uniform_value : f.w_vdw[q];
+    }
 
     for (;;) {
         int item;
@@ -209,121 +282,89 @@ pair_kernel(kf_field_t f, int B, int n, const unsigned long long *__restrict__ k
                             S.list[wpos++] = (unsigned short)((lane << 5) | t);
                         }
                     }
-                    for (int q = 0; q < 3; ++q) S.acc[q][lane] = (T)0;
                     __syncwarp();
                     T fe = 0, fv = 0;
-                    for (int base = 0; base < tot; base += 32) {
-                        const int k = base + lane;
-                        const bool act = k < tot;
+                    T fx = 0, fy = 0, fz = 0;   // owner sums of this tile
+                    const int excl = incl - own;
+                    for (int base = 0; base < tot; base += RES_BATCH) {
+                      const int nbat = min(RES_BATCH, tot - base);
+                      for (int k0 = 0; k0 < nbat; k0 += 32) {
+                        const int k = base + k0 + lane;
+                        const bool act = k0 + lane < nbat;
                         const int e = act ? (int)S.list[k] : 0;
                         const int o = act ? e >> 5 : 32 + lane;   // inactive lanes: own segments
                         T out[5] = {0, 0, 0, 0, 0};
-                        long long pc = 0;
+                        int pce = 0, pcv = 0;
                         if (act) {
                             const int t = e & 31;
                             const int4 ai = I.aux[o], aj = S.J.aux[t];
                             const int i = ai.x, j = aj.x;
-                            if (i != j) {
-                                const float4 hi = I.hi[o], li = I.lo[o], hj = S.J.hi[t], lj = S.J.lo[t];
-                                const float dxf = ((hi.x - hj.x) - sx) + (li.x - lj.x);
-                                const float dyf = ((hi.y - hj.y) - sy) + (li.y - lj.y);
-                                const float dzf = ((hi.z - hj.z) - sz) + (li.z - lj.z);
-                                const float d2f = dxf * dxf + dyf * dyf + dzf * dzf;
-                                bool member = d2f <= cut2f, ke = d2f <= tef, kv = d2f <= tvf;
+                            const float4 hi = I.hi[o], li = I.lo[o], hj = S.J.hi[t], lj = S.J.lo[t];
+                            const float dxf = ((hi.x - hj.x) - sx) + (li.x - lj.x);
+                            const float dyf = ((hi.y - hj.y) - sy) + (li.y - lj.y);
+                            const float dzf = ((hi.z - hj.z) - sz) + (li.z - lj.z);
+                            const float d2f = dxf * dxf + dyf * dyf + dzf * dzf;
+                            if (i != j && d2f <= cut2f + band) {
+                                // static class window: 2-bit codes for j - i in [-32, 32)
+                                int cls = 4;
+                                if (!f.uniform_weights) {
+                                    const int off = j - i + 32;
+                                    if ((unsigned)off < 64u) {
+                                        const int4 cm = itree[o];
+                                        const unsigned wd = off < 32 ? (off < 16 ? cm.x : cm.y)
+                                                                     : (off < 48 ? cm.z : cm.w);
+                                        cls = 4 - (int)((wd >> (2 * (off & 15))) & 3u);
+                                    } else if (ai.w != 0 && aj.z != 0 && abs(ai.y - aj.y) <= 1) {
+                                        cls = slow_class(f.tparent, f.tgp, f.tggp, f.tres, f.tchain, i, j);
+                                    }
+                                }
+                                const float we = cls == 4 ? wf[3] : cls == 3 ? wf[2] : cls == 2 ? wf[1] : wf[0];
+                                const float wv = cls == 4 ? wf[7] : cls == 3 ? wf[6] : cls == 2 ? wf[5] : wf[4];
                                 const bool exact = F64 || fabsf(d2f - cut2f) <= band || fabsf(d2f - tvf) <= band ||
                                                    fabsf(d2f - tef) <= band || d2f < 1.0f;
-                                double d2 = d2f, dx = dxf, dy = dyf, dz = dzf;
                                 if (exact) {
-                                    const double4 p_i = s_pos[nb + s0 + ic + o], p_j = s_pos[nb + j0 + jb + t];
-                                    dx = xsub(p_i.x, p_j.x); dy = xsub(p_i.y, p_j.y); dz = xsub(p_i.z, p_j.z);
-                                    d2 = d2_einsum(dx, dy, dz);
-                                    member = d2 <= f.cut_pair2;
-                                    ke = d2 <= f.thr_elec2;
-                                    kv = d2 <= f.thr_vdw2;
-                                }
-                                if (member) {
-                                    pc = (long long)ke + ((long long)kv << 32);
-                                    double we, wv;
-                                    if (f.uniform_weights) {
-                                        we = wv = f.uniform_value;
-                                    } else {
-                                        // static class window: 2-bit codes for j - i in [-32, 32)
-                                        int cls = 4;
-                                        const int off = j - i + 32;
-                                        if ((unsigned)off < 64u) {
-                                            const int4 cm = itree[o];
-                                            const unsigned wd = off < 32 ? (off < 16 ? cm.x : cm.y)
-                                                                         : (off < 48 ? cm.z : cm.w);
-                                            cls = 4 - (int)((wd >> (2 * (off & 15))) & 3u);
-                                        } else if (ai.w != 0 && aj.z != 0 && abs(ai.y - aj.y) <= 1) {
-                                            cls = classify_pair(f, i, j, f.tparent[i], f.tgp[i], f.tggp[i], ai.y,
-                                                                ai.z != 0);
-                                        }
-                                        we = f.w_elec[cls - 1]; wv = f.w_vdw[cls - 1];
+                                    slow_pair<T>(F64, fx64, s_pos + nb + s0 + ic + o, s_pos + nb + j0 + jb + t, i, j,
+                                                 cls, out, &pce, &pcv, status + b);
+                                } else if (d2f <= cut2f) {
+                                    const bool ke = d2f <= tef, kv = d2f <= tvf;
+                                    pce = ke; pcv = kv;
+                                    const float4 qi = I.par[o], qj = S.J.par[t];
+                                    const float inv_r = rsqrtf(d2f);
+                                    const float inv_r2 = inv_r * inv_r;
+                                    float g = 0.f;
+                                    if (ke) {
+                                        // kappa = d: E = K w qi qj / d^2; constant: E = K w qi qj / (kappa d);
+                                        // |F| / d = E / d^2 in both cases
+                                        const float qq = (float)COULOMB_K * qi.x * qj.x * we;
+                                        const float e = f.dielectric_const ? qq * kap_inv * inv_r : qq * inv_r2;
+                                        out[3] = e;
+                                        g += e * inv_r2;
                                     }
-                                    if (F64 || d2 < 1.0) {
-                                        bool clash = false;
-                                        if (d2 < 1e-11) {
-                                            const double d = sqrt(d2);
-                                            if (d < MIN_DISTANCE) {
-                                                clash = true;
-                                                atomicMin(&status[b].dmin_bits,
-                                                          (unsigned long long)__double_as_longlong(d));
-                                                if (atomicCAS(&status[b].error, KF_ERR_NONE, KF_ERR_CLASH) == KF_ERR_NONE)
-                                                    status[b].err_iter = status[b].iter;
-                                            }
-                                        }
-                                        if (!clash) pair_fp64(f, i, j, d2, dx, dy, dz, we, wv, ke, kv, out);
-                                    } else {
-                                        const float4 qi = I.par[o], qj = S.J.par[t];
-                                        const float inv_r = rsqrtf(d2f);
-                                        const float inv_r2 = inv_r * inv_r;
-                                        float g = 0.f;
-                                        if (ke) {
-                                            // kappa = d: E = K w qi qj / d^2; constant: E = K w qi qj / (kappa d);
-                                            // |F| / d = E / d^2 in both cases
-                                            const float qq = (float)COULOMB_K * qi.x * qj.x * (float)we;
-                                            const float e = f.dielectric_const ? qq * kap_inv * inv_r : qq * inv_r2;
-                                            out[3] = e;
-                                            g += e * inv_r2;
-                                        }
-                                        if (kv) {
-                                            const float weps = (float)wv * qi.z * qj.z;
-                                            const float D = qi.y + qj.y;
-                                            const float sr = D * D * inv_r2;
-                                            const float s3 = sr * sr * sr;
-                                            const float s6 = s3 * s3;
-                                            out[4] = weps * (s6 - 2.f * s3);
-                                            g += 12.f * weps * (s6 - s3) * inv_r2;
-                                        }
-                                        out[0] = g * dxf; out[1] = g * dyf; out[2] = g * dzf;
+                                    if (kv) {
+                                        const float weps = wv * qi.z * qj.z;
+                                        const float D = qi.y + qj.y;
+                                        const float sr = D * D * inv_r2;
+                                        const float s3 = sr * sr * sr;
+                                        const float s6 = s3 * s3;
+                                        out[4] = weps * (s6 - 2.f * s3);
+                                        g += 12.f * weps * (s6 - s3) * inv_r2;
                                     }
+                                    out[0] = g * dxf; out[1] = g * dyf; out[2] = g * dzf;
                                 }
                             }
                         }
+                        const long long pc = (long long)pce + ((long long)pcv << 32);
                         // energies and counts only enter per-cell totals: the computing lane keeps them
                         fe += out[3]; fv += out[4];
                         a.cnt += pc;
-                        // forces: segmented inclusive scan by owner (segments are contiguous
-                        // lanes) on a fixed shuffle tree, so per-owner sums are deterministic
-#pragma unroll
-                        for (int d = 1; d < 32; d <<= 1) {
-                            const int ov = __shfl_up_sync(FULL, o, d);
-                            T up[3];
-#pragma unroll
-                            for (int q = 0; q < 3; ++q) up[q] = __shfl_up_sync(FULL, out[q], d);
-                            if (lane >= d && ov == o)
-#pragma unroll
-                                for (int q = 0; q < 3; ++q) out[q] += up[q];
-                        }
-                        const int on = __shfl_down_sync(FULL, o, 1);
-                        if (act && (lane == 31 || on != o))
-#pragma unroll
-                            for (int q = 0; q < 3; ++q) S.acc[q][o] += out[q];
-                        __syncwarp();
+                        if (act) { S.res[k0 + lane][0] = out[0]; S.res[k0 + lane][1] = out[1]; S.res[k0 + lane][2] = out[2]; }
+                      }
+                      __syncwarp();
+                      // each owner sums its contiguous range of the list in order (deterministic)
+                      const int lo_k = max(excl - base, 0), hi_k = min(incl - base, nbat);
+                      for (int q = lo_k; q < hi_k; ++q) { fx += S.res[q][0]; fy += S.res[q][1]; fz += S.res[q][2]; }
+                      __syncwarp();
                     }
-                    const T fx = S.acc[0][lane], fy = S.acc[1][lane], fz = S.acc[2][lane];
-                    __syncwarp();
                     a.fx += (double)fx; a.fy += (double)fy; a.fz += (double)fz;
                     a.ee += (double)fe; a.ev += (double)fv;
                 }

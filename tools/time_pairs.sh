@@ -1,9 +1,9 @@
 #!/bin/bash
-# Rebuild with a pair-kernel variant and time one eager ensemble iteration per phase.
+# Rebuild with pair-kernel occupancy variants and time the C5 ensemble step per phase.
 set -e
 for mb in "$@"; do
-  make -s -C paper_1712_05012_b200/csrc clean >/dev/null
-  make -s -C paper_1712_05012_b200/csrc EXTRA=-DPAIR_MINB=$mb -j16 >/dev/null 2>&1
-  echo "PAIR_MINB=$mb"
-  python bench.py --steps 10 --warmup 3 --no-extras | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print(d['value'], d['phase_ms_per_step'])"
+  sed -i "s/__launch_bounds__(PAIR_WARPS \* 32, SPLIT ? PAIR_MINB : [0-9])/__launch_bounds__(PAIR_WARPS * 32, SPLIT ? PAIR_MINB : $mb)/" paper_1712_05012_b200/csrc/kf_nonbonded.cu
+  make -s -C paper_1712_05012_b200/csrc -j16 >/dev/null 2>&1
+  echo "minblocks=$mb"
+  python tools/phase_times.py --config C2 --ensemble 1024 --iters 8
 done
