@@ -236,13 +236,17 @@ def _sqrt_threshold(cut: float) -> float:
 
 
 def _stencil(cell: float, reach_dist: float) -> np.ndarray:
-    """Cell offsets whose box can hold a point within reach_dist of the home box."""
-    r = int(math.ceil(reach_dist / cell))
-    rng = np.arange(-r, r + 1)
+    """The 27 offsets of a one-cell reach: own cell, the 13 lexicographically
+    positive offsets, then their negatives (a half-shell order, kept so a
+    Newton's-third-law pair kernel can take the first 14)."""
+    if cell < reach_dist:
+        raise ConfigurationError("hot-path cells must be at least one interaction reach wide")
+    rng = np.arange(-1, 2)
     ox, oy, oz = np.meshgrid(rng, rng, rng, indexing="ij")
     offs = np.stack([ox.ravel(), oy.ravel(), oz.ravel()], axis=1)
-    gap = np.maximum(np.abs(offs) - 1, 0) * cell
-    return offs[(gap * gap).sum(axis=1) <= reach_dist * reach_dist]
+    fwd = [tuple(o) for o in offs if tuple(o) > (0, 0, 0)]
+    bwd = [tuple(-np.array(o)) for o in fwd]
+    return np.array([(0, 0, 0)] + fwd + bwd, dtype=np.int64)
 
 
 def tree_classes(tree, i, j) -> np.ndarray:
