@@ -123,6 +123,8 @@ typedef struct {
     double  *theta;                 /* [B][D]                                      */
     const uint8_t *frozen;          /* [B][D]                                      */
     double  *link_T;                /* [B][L][16]: rotation (row-major 9), joint point (3), axis (3), pad */
+    double  *fk_scratch;            /* [B][ceil(n_bb/2048)][12] segment totals of the
+                                       multi-CTA backbone scan (long chains)           */
     double  *pos;                   /* [B][n][3]                                   */
     double  *forces;                /* [B][n][3]                                   */
     /* spatial hash: per trajectory an open-addressing table of H = n_buckets

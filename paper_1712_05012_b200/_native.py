@@ -54,7 +54,7 @@ class KfBatch(C.Structure):
     _fields_ = [("B", I32), ("n_buckets", I32), ("nb_cap", I32), ("record_theta", I32),
                 ("max_records", I32), ("_pad", I32)] + [
         (name, P) for name in (
-            "theta", "frozen", "link_T", "pos", "forces", "cell_key", "cell_cnt", "cell_start",
+            "theta", "frozen", "link_T", "fk_scratch", "pos", "forces", "cell_key", "cell_cnt", "cell_start",
             "occ", "occ_count", "occ_offset", "atom_slot", "atom_rank", "sorted_atom", "s_hi", "s_lo",
             "s_pos", "s_par", "s_aux", "s_tree", "cell_box", "work", "e_atom", "pair_count",
             "solv_acc", "cav_atom", "f_exp", "a_exp", "wrench", "side_tot", "bb_suffix", "tau", "energy", "status",

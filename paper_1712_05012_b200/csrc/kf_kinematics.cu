@@ -111,6 +111,125 @@ fk_scan_kernel(kf_chain_t c, const double *__restrict__ theta_all, double *__res
     }
 }
 
+// ---- long chains: the backbone scan spread over many CTAs --------------------
+// Three phases per trajectory: (1) every CTA scans a 2048-link segment of the
+// backbone in place (local transforms computed on the fly) and publishes the
+// segment total; (2) one CTA scans the segment totals; (3) every CTA applies
+// its exclusive prefix and computes the segment's axes.  Side links then
+// compose their <= 4 ancestors from the (final) backbone transform directly.
+constexpr int SEG = 2048;
+constexpr int SEG_PER = SEG / FK_THREADS;   // 8 links per thread
+
+__global__ void __launch_bounds__(FK_THREADS)
+fk_seg_scan_kernel(kf_chain_t c, const double *__restrict__ theta_all, double *__restrict__ T_all,
+                   double *__restrict__ seg_tot, int n_seg, const kf_status_t *__restrict__ status) {
+    const int b = blockIdx.y, g = blockIdx.x;
+    if (status && status[b].done) return;
+    const int L = c.n_links, D = c.n_dof, nb = c.n_bb;
+    const double *theta = theta_all + (size_t)b * D;
+    double *T = T_all + (size_t)b * L * KF_XF_STRIDE;
+    __shared__ double chunk[FK_THREADS][12];
+    const int lo = min(nb, g * SEG + (int)threadIdx.x * SEG_PER), hi = min(nb, lo + SEG_PER);
+    Xf acc = xf_identity();
+    for (int k = lo; k < hi; ++k) {
+        const int l = c.bb_order[k];
+        const Xf loc = local_transform(c.link_axis0 + 3 * l, theta[c.link_dof[l]],
+                                       c.link_body0 + 3 * c.link_parent[l]);
+        acc = xf_compose(acc, loc);
+        xf_store(T + KF_XF_STRIDE * l, acc);
+    }
+    xf_store(chunk[threadIdx.x], acc);
+    __syncthreads();
+    for (int off = 1; off < (int)blockDim.x; off <<= 1) {
+        Xf mine = xf_load(chunk[threadIdx.x]);
+        Xf r = mine;
+        if ((int)threadIdx.x >= off) r = xf_compose(xf_load(chunk[threadIdx.x - off]), mine);
+        __syncthreads();
+        xf_store(chunk[threadIdx.x], r);
+        __syncthreads();
+    }
+    if (threadIdx.x > 0 && lo < hi) {
+        const Xf pre = xf_load(chunk[threadIdx.x - 1]);
+        for (int k = lo; k < hi; ++k) {
+            double *slot = T + KF_XF_STRIDE * c.bb_order[k];
+            xf_store(slot, xf_compose(pre, xf_load(slot)));
+        }
+    }
+    if (threadIdx.x == blockDim.x - 1) xf_store(seg_tot + ((size_t)b * n_seg + g) * 12, xf_load(chunk[threadIdx.x]));
+}
+
+// exclusive prefix of the segment totals, in place (one thread per trajectory: few segments)
+__global__ void fk_seg_prefix_kernel(double *__restrict__ seg_tot, int n_seg, int B,
+                                     const kf_status_t *__restrict__ status) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= B || (status && status[b].done)) return;
+    Xf run = xf_identity();
+    for (int g = 0; g < n_seg; ++g) {
+        double *slot = seg_tot + ((size_t)b * n_seg + g) * 12;
+        const Xf tot = xf_load(slot);
+        xf_store(slot, run);
+        run = xf_compose(run, tot);
+    }
+}
+
+KF_DEV void store_axis(double *slot, const double *axis0) {
+    for (int r = 0; r < 3; ++r)
+        slot[12 + r] = slot[3 * r] * axis0[0] + slot[3 * r + 1] * axis0[1] + slot[3 * r + 2] * axis0[2];
+    slot[15] = 0.0;
+}
+
+__global__ void fk_seg_apply_kernel(kf_chain_t c, double *__restrict__ T_all, const double *__restrict__ seg_tot,
+                                    int n_seg, int B, const kf_status_t *__restrict__ status) {
+    const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int nb = c.n_bb;
+    if (gid >= (long long)B * nb) return;
+    const int b = (int)(gid / nb), k = (int)(gid % nb);
+    if (status && status[b].done) return;
+    double *T = T_all + (size_t)b * c.n_links * KF_XF_STRIDE;
+    const int l = c.bb_order[k];
+    double *slot = T + KF_XF_STRIDE * l;
+    const int g = k / SEG;
+    if (g > 0) xf_store(slot, xf_compose(xf_load(seg_tot + ((size_t)b * n_seg + g) * 12), xf_load(slot)));
+    store_axis(slot, c.link_axis0 + 3 * l);
+}
+
+// side links: compose the chain of (<= 4) side ancestors onto the backbone link
+__global__ void fk_side_kernel(kf_chain_t c, const double *__restrict__ theta_all, double *__restrict__ T_all,
+                               int B, const kf_status_t *__restrict__ status) {
+    const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int ns = c.n_side;
+    if (gid >= (long long)B * (ns + 1)) return;
+    const int b = (int)(gid / (ns + 1)), k = (int)(gid % (ns + 1));
+    if (status && status[b].done) return;
+    double *T = T_all + (size_t)b * c.n_links * KF_XF_STRIDE;
+    if (k == ns) {   // ground
+        Xf id = xf_identity();
+        xf_store(T, id);
+        for (int r = 0; r < 4; ++r) T[12 + r] = 0.0;
+        return;
+    }
+    const double *theta = theta_all + (size_t)b * c.n_dof;
+    const int l = c.side_order[k];
+    int chain_l[8];
+    int depth = 0, cur = l;
+    while (cur > 0 && depth < 8) {   // climb to the first backbone (or ground) ancestor
+        // backbone links carry dofs 0..n_bb-1 (validated on the host), side links the rest
+        const bool is_side = c.link_dof[cur] >= c.n_bb;
+        if (!is_side) break;
+        chain_l[depth++] = cur;
+        cur = c.link_parent[cur];
+    }
+    Xf acc = cur > 0 ? xf_load(T + KF_XF_STRIDE * cur) : xf_identity();
+    for (int d = depth - 1; d >= 0; --d) {
+        const int q = chain_l[d];
+        acc = xf_compose(acc, local_transform(c.link_axis0 + 3 * q, theta[c.link_dof[q]],
+                                              c.link_body0 + 3 * c.link_parent[q]));
+    }
+    double *slot = T + KF_XF_STRIDE * l;
+    xf_store(slot, acc);
+    store_axis(slot, c.link_axis0 + 3 * l);
+}
+
 // pos_a = P_l + M_l zrel_a over every (trajectory, atom)
 __global__ void fk_positions_kernel(kf_chain_t c, int B, const double *__restrict__ T_all,
                                     double *__restrict__ pos_all,
@@ -131,8 +250,24 @@ __global__ void fk_positions_kernel(kf_chain_t c, int B, const double *__restric
 }  // namespace
 
 int kf_fk_launch(const kf_chain_t *c, kf_batch_t *w, const kf_status_t *status, cudaStream_t s) {
-    fk_scan_kernel<<<w->B, FK_THREADS, 0, s>>>(*c, w->theta, w->link_T, status);
-    KF_LAUNCH_CHECK("fk_scan_kernel");
+    const int n_seg = (c->n_bb + SEG - 1) / SEG;
+    if (n_seg > 1 && w->B * n_seg <= 4 * 148 && w->fk_scratch) {
+        // long chain, few trajectories: multi-CTA backbone scan
+        fk_seg_scan_kernel<<<dim3(n_seg, w->B), FK_THREADS, 0, s>>>(*c, w->theta, w->link_T, w->fk_scratch, n_seg,
+                                                                     status);
+        KF_LAUNCH_CHECK("fk_seg_scan_kernel");
+        fk_seg_prefix_kernel<<<kf_blocks(w->B, 64), 64, 0, s>>>(w->fk_scratch, n_seg, w->B, status);
+        KF_LAUNCH_CHECK("fk_seg_prefix_kernel");
+        fk_seg_apply_kernel<<<kf_blocks((long long)w->B * c->n_bb, 256), 256, 0, s>>>(*c, w->link_T, w->fk_scratch,
+                                                                                     n_seg, w->B, status);
+        KF_LAUNCH_CHECK("fk_seg_apply_kernel");
+        fk_side_kernel<<<kf_blocks((long long)w->B * (c->n_side + 1), 256), 256, 0, s>>>(*c, w->theta, w->link_T,
+                                                                                         w->B, status);
+        KF_LAUNCH_CHECK("fk_side_kernel");
+    } else {
+        fk_scan_kernel<<<w->B, FK_THREADS, 0, s>>>(*c, w->theta, w->link_T, status);
+        KF_LAUNCH_CHECK("fk_scan_kernel");
+    }
     const long long total = (long long)w->B * c->n_atoms;
     if (total > 0) {
         fk_positions_kernel<<<kf_blocks(total, 256), 256, 0, s>>>(*c, w->B, w->link_T, w->pos, status);

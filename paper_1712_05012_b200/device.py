@@ -157,6 +157,8 @@ class DeviceChain:
             if parent[k] != prev:
                 raise ConfigurationError("backbone (phi/psi) links must form a path from ground")
             prev = k
+        if sorted(int(dof[k]) for k in bb) != list(range(len(bb))):
+            raise ConfigurationError("backbone links must carry dofs 0..2m-1 (side links after)")
         bb_set = set(bb)
         depth = np.zeros(L, np.int64)
         side = []
@@ -438,7 +440,8 @@ class Batch:
         with torch.cuda.stream(stream()):
             t = self.t = dict(
                 theta=z(B, max(D, 1)), frozen=z(B, max(D, 1), dtype=torch.uint8),
-                link_T=z(B, L, 16), pos=z(B, n, 3), forces=z(B, n, 3),
+                link_T=z(B, L, 16), fk_scratch=z(B, max(1, -(-nbb // 2048)), 12),
+                pos=z(B, n, 3), forces=z(B, n, 3),
                 cell_key=z(B, H, dtype=torch.int64), cell_cnt=z(B, H, dtype=i32),
                 cell_start=z(B, H, dtype=i32), occ=z(B, H, dtype=i32), occ_count=z(B, dtype=i32),
                 occ_offset=z(B + 1, dtype=i32), atom_slot=z(B, n, dtype=i32), atom_rank=z(B, n, dtype=i32),
