@@ -42,7 +42,7 @@ KF_DEV bool covers_shifted(double px, double py, double pz, const NbSlot &s, int
 }
 
 // Staged neighbour set of one atom (shared memory): coordinates + R_off^2,
-// an fp32 spherical-cap prefilter per neighbour, and a nearest-first order.
+// an fp32 spherical-cap prefilter per neighbour, and a largest-cap-first order.
 //
 // Cap prefilter: for a sample p = r_i + R_i q (|q| = 1) and a neighbour at
 // distance d in direction u, |p - r_j|^2 = R_i^2 + d^2 - 2 R_i d (q.u), so j can
@@ -82,7 +82,7 @@ KF_DEV void prepare_neighbors(const double *xi, double r_i, int count, double dr
             }
             S.cap[m] = cp;
             S.c2[m] = c2;
-            S.key[m] = d2;
+            S.key[m] = (double)cp.w;   // largest cap first
         } else {
             S.key[m] = INFINITY;
         }
@@ -109,56 +109,104 @@ KF_DEV void prepare_neighbors(const double *xi, double r_i, int count, double dr
 }
 
 // States + (optionally) forward-difference events of atom i's samples against
-// the staged set; returns the number of covered samples.
+// the staged set; returns this thread's count of covered samples.
+//
+// Phase A (thread per sample): the neighbours are sorted largest-cap first, so
+// most buried samples meet two coverers within the first few; a sample that
+// does within QUICK neighbours is state 2 (clamped count, no forces).  The rest
+// (exposed, critical, or slow) go to a shared list.
+// Phase B (thread per listed sample): the full scan with the clamp at 2, the
+// unique coverer, and the forward-difference events; compaction gives each
+// warp samples of similar cost.  Both phases use the reference's exact
+// coverage arithmetic, so states and forces are bit-identical.
+constexpr int QUICK = 8;
+constexpr int UND_CAP = 1024;
+
 template <bool WITH_FORCES>
 KF_DEV int enumerate_samples(const double *xi, double r_off_i, const double *samples, int N,
                              const NbSet &S, int nn, long long wi, double dr, long long *acc_nb,
                              long long *acc_i, uint8_t *counts_out, int32_t *crit_out) {
+    __shared__ int und[UND_CAP];
+    __shared__ int n_und;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const int quick = min(nn, QUICK);
     int covered = 0;
-    for (int k = threadIdx.x; k < N; k += blockDim.x) {
-        const double *q = samples + 3 * k;
-        const float qx = (float)q[0], qy = (float)q[1], qz = (float)q[2];
-        double px, py, pz;
-        sample_point(xi, r_off_i, q, px, py, pz);
-        int cnt = 0, crit = -1;
-        for (int r = 0; r < nn; ++r) {
-            const int m = S.ord[r];
-            const float4 cp = S.cap[m];
-            if (qx * cp.x + qy * cp.y + qz * cp.z < cp.w) continue;
-            if (covers(px, py, pz, S.nb[m])) {
-                crit = m;
-                if (++cnt == 2) break;
+    for (int k0 = 0; k0 < N; k0 += UND_CAP) {
+        const int kend = min(N, k0 + UND_CAP);
+        if (threadIdx.x == 0) n_und = 0;
+        __syncthreads();
+        // ---- phase A
+        for (int k = k0 + threadIdx.x; k < kend; k += blockDim.x) {
+            const double *q = samples + 3 * k;
+            const float qx = (float)q[0], qy = (float)q[1], qz = (float)q[2];
+            double px, py, pz;
+            sample_point(xi, r_off_i, q, px, py, pz);
+            int cnt = 0;
+            for (int r = 0; r < quick && cnt < 2; ++r) {
+                const int m = S.ord[r];
+                const float4 cp = S.cap[m];
+                if (qx * cp.x + qy * cp.y + qz * cp.z < cp.w) continue;
+                cnt += covers(px, py, pz, S.nb[m]);
+            }
+            if (cnt >= 2) {
+                ++covered;
+                if (counts_out) { counts_out[k] = 2; crit_out[k] = -1; }
+            } else {
+                und[atomicAdd(&n_und, 1)] = k;
             }
         }
-        covered += cnt > 0;
-        if (counts_out) {
-            counts_out[k] = (uint8_t)cnt;
-            crit_out[k] = cnt == 1 ? S.atom[crit] : -1;
-        }
-        if (WITH_FORCES && wi != 0) {
-            if (cnt == 0) {
-                for (int m = 0; m < nn; ++m) {
-                    const float4 cp = S.cap[m];
-                    if (qx * cp.x + qy * cp.y + qz * cp.z < S.c2[m]) continue;
-                    const NbSlot nbm = S.nb[m];
+        __syncthreads();
+        // ---- phase B: thread per listed sample (similar work per warp after compaction)
+        const int nu = n_und;
+        for (int u = threadIdx.x; u < nu; u += blockDim.x) {
+            const int k = und[u];
+            const double *q = samples + 3 * k;
+            const float qx = (float)q[0], qy = (float)q[1], qz = (float)q[2];
+            double px, py, pz;
+            sample_point(xi, r_off_i, q, px, py, pz);
+            int cnt = 0, crit = -1;
+            for (int r = 0; r < nn; ++r) {
+                const int m = S.ord[r];
+                const float4 cp = S.cap[m];
+                if (qx * cp.x + qy * cp.y + qz * cp.z < cp.w) continue;
+                if (covers(px, py, pz, S.nb[m])) {
+                    crit = m;
+                    if (++cnt == 2) break;
+                }
+            }
+            covered += cnt > 0;
+            if (counts_out) {
+                counts_out[k] = (uint8_t)cnt;
+                crit_out[k] = cnt == 1 ? S.atom[crit] : -1;
+            }
+            if (WITH_FORCES && wi != 0) {
+                if (cnt == 0) {
+                    // exposed: every neighbour displaced along each axis (solvation.py:224-235)
+                    for (int m = 0; m < nn; ++m) {
+                        const float4 cp = S.cap[m];
+                        if (qx * cp.x + qy * cp.y + qz * cp.z < S.c2[m]) continue;
+                        const NbSlot nbm = S.nb[m];
+                        for (int s = 0; s < 3; ++s) {
+                            if (covers_shifted(px, py, pz, nbm, s, dr)) {
+                                atomicAdd(reinterpret_cast<unsigned long long *>(&acc_nb[3 * m + s]),
+                                          (unsigned long long)wi);
+                                acc_i[s] -= wi;
+                            }
+                        }
+                    }
+                } else if (cnt == 1) {
+                    // critical: only the recorded coverer, displaced (solvation.py:236-245)
                     for (int s = 0; s < 3; ++s) {
-                        if (covers_shifted(px, py, pz, nbm, s, dr)) {
-                            atomicAdd(reinterpret_cast<unsigned long long *>(&acc_nb[3 * m + s]),
-                                      (unsigned long long)wi);
-                            acc_i[s] -= wi;
+                        if (!covers_shifted(px, py, pz, S.nb[crit], s, dr)) {
+                            acc_i[s] += wi;
+                            atomicAdd(reinterpret_cast<unsigned long long *>(&acc_nb[3 * crit + s]),
+                                      (unsigned long long)(-wi));
                         }
                     }
                 }
-            } else if (cnt == 1) {
-                for (int s = 0; s < 3; ++s) {
-                    if (!covers_shifted(px, py, pz, S.nb[crit], s, dr)) {
-                        acc_i[s] += wi;
-                        atomicAdd(reinterpret_cast<unsigned long long *>(&acc_nb[3 * crit + s]),
-                                  (unsigned long long)(-wi));
-                    }
-                }
             }
         }
+        __syncthreads();
     }
     return covered;
 }
