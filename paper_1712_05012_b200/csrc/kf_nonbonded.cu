@@ -25,6 +25,7 @@
 //   fixed order, into fp64 accumulators.
 // Both directions of each unordered pair are evaluated by their owners
 // ("full list"): no atomics on forces, run-to-run bitwise deterministic.
+#include <cstdlib>
 #include <type_traits>
 
 #include "kf_common.cuh"
@@ -33,7 +34,8 @@ namespace {
 
 constexpr double COULOMB_K = 332.06;
 constexpr double MIN_DISTANCE = 1e-6;
-constexpr int PAIR_WARPS = 4;
+constexpr int PAIR_WARPS = 4;        // warps per CTA, warp-per-cell variant
+constexpr int SPLIT_WARPS = 4;       // warps per CTA (one cell), split variant
 constexpr unsigned FULL = 0xffffffffu;
 
 struct Tile {
@@ -150,7 +152,7 @@ __device__ __noinline__ void slow_pair(bool f64, const SlowArgs &A, const double
 // (short per-cell latency: single trajectories); false: one warp per cell
 // (throughput: ensembles).
 template <bool F64, bool SPLIT>
-__global__ void __launch_bounds__(PAIR_WARPS * 32, SPLIT ? PAIR_MINB : 4)
+__global__ void __launch_bounds__((SPLIT ? SPLIT_WARPS : PAIR_WARPS) * 32, SPLIT ? 1 : 4)
 pair_kernel(kf_field_t f, int B, int n, const unsigned long long *__restrict__ keys,
             const int32_t *__restrict__ cnt, const int32_t *__restrict__ start, const int32_t *__restrict__ occ,
             const int32_t *__restrict__ occ_offset, const float4 *__restrict__ s_hi,
@@ -159,14 +161,16 @@ pair_kernel(kf_field_t f, int B, int n, const unsigned long long *__restrict__ k
             int32_t *__restrict__ work, double *__restrict__ forces, double *__restrict__ e_atom,
             long long *__restrict__ pair_count, kf_status_t *status) {
     using T = typename std::conditional<F64, double, float>::type;
-    constexpr int NI = SPLIT ? 1 : PAIR_WARPS;
+    constexpr int NW = SPLIT ? SPLIT_WARPS : PAIR_WARPS;
+    constexpr int NI = SPLIT ? 1 : NW;
     __shared__ Tile Itile[NI];               // the i-chunk (shared by the CTA's warps if SPLIT)
     __shared__ int4 itree_s[NI][32];
-    __shared__ WarpSmem<T> smem[PAIR_WARPS];
-    __shared__ double part[SPLIT ? PAIR_WARPS : 1][3][32];
-    __shared__ double epart[PAIR_WARPS][2];
-    __shared__ long long cpart[PAIR_WARPS];
-    __shared__ int item_s[PAIR_WARPS];
+    extern __shared__ __align__(16) unsigned char dyn_smem[];
+    WarpSmem<T> *smem = reinterpret_cast<WarpSmem<T> *>(dyn_smem);   // [NW]
+    __shared__ double part[SPLIT ? NW : 1][3][32];
+    __shared__ double epart[NW][2];
+    __shared__ long long cpart[NW];
+    __shared__ int item_s[NW];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     WarpSmem<T> &S = smem[warp];
     Tile &I = Itile[SPLIT ? 0 : warp];
@@ -230,20 +234,35 @@ pair_kernel(kf_field_t f, int B, int n, const unsigned long long *__restrict__ k
 
             // the 27 neighbour cells are dealt to the warps round-robin; each warp
             // keeps per-owner fp64 sums over its cells in a fixed order
-            for (int s = SPLIT ? warp : 0; s < f.n_stencil; s += SPLIT ? PAIR_WARPS : 1) {
-                const int ox = f.stencil[3 * s], oy = f.stencil[3 * s + 1], oz = f.stencil[3 * s + 2];
-                const int js = cell_probe(keys + hb, H, cx + ox, cy + oy, cz + oz);
+            // probe all neighbour cells at once (lane s <-> stencil cell s): one
+            // round of table / start / count / box loads instead of 27 serial ones
+            int p_js = -1, p_j0 = 0, p_jc = 0;
+            float4 p_lo = make_float4(0.f, 0.f, 0.f, 0.f), p_hi = p_lo;
+            if (lane < f.n_stencil) {
+                p_js = cell_probe(keys + hb, H, cx + f.stencil[3 * lane], cy + f.stencil[3 * lane + 1],
+                                  cz + f.stencil[3 * lane + 2]);
+                if (p_js >= 0) {
+                    p_j0 = start[hb + p_js]; p_jc = cnt[hb + p_js];
+                    p_lo = cell_box[2 * (hb + p_js)]; p_hi = cell_box[2 * (hb + p_js) + 1];
+                }
+            }
+            for (int s = SPLIT ? warp : 0; s < f.n_stencil; s += SPLIT ? NW : 1) {
+                const int js = __shfl_sync(FULL, p_js, s);
                 if (js < 0) continue;
+                const int ox = f.stencil[3 * s], oy = f.stencil[3 * s + 1], oz = f.stencil[3 * s + 2];
                 // i in the neighbour cell's frame; skip the cell unless some lane reaches its box
                 const float sx = (float)ox * cellf, sy = (float)oy * cellf, sz = (float)oz * cellf;
                 const float px = hi_i.x - sx, py = hi_i.y - sy, pz = hi_i.z - sz;
-                const float4 blo = cell_box[2 * (hb + js)], bhi = cell_box[2 * (hb + js) + 1];
-                const float gx = fmaxf(fmaxf(blo.x - px, px - bhi.x), 0.f);
-                const float gy = fmaxf(fmaxf(blo.y - py, py - bhi.y), 0.f);
-                const float gz = fmaxf(fmaxf(blo.z - pz, pz - bhi.z), 0.f);
+                const float blx = __shfl_sync(FULL, p_lo.x, s), bly = __shfl_sync(FULL, p_lo.y, s),
+                            blz = __shfl_sync(FULL, p_lo.z, s);
+                const float bhx = __shfl_sync(FULL, p_hi.x, s), bhy = __shfl_sync(FULL, p_hi.y, s),
+                            bhz = __shfl_sync(FULL, p_hi.z, s);
+                const float gx = fmaxf(fmaxf(blx - px, px - bhx), 0.f);
+                const float gy = fmaxf(fmaxf(bly - py, py - bhy), 0.f);
+                const float gz = fmaxf(fmaxf(blz - pz, pz - bhz), 0.f);
                 const bool need = valid && gx * gx + gy * gy + gz * gz <= pre2;
                 if (!__any_sync(FULL, need)) continue;
-                const int j0 = start[hb + js], jc = cnt[hb + js];
+                const int j0 = __shfl_sync(FULL, p_j0, s), jc = __shfl_sync(FULL, p_jc, s);
                 for (int jb = 0; jb < jc; jb += 32) {
                     const int nt = min(32, jc - jb);
                     __syncwarp();
@@ -379,7 +398,7 @@ pair_kernel(kf_field_t f, int B, int n, const unsigned long long *__restrict__ k
                 if (warp == 0 && valid) {
                     double fx = 0.0, fy = 0.0, fz = 0.0;
 #pragma unroll
-                    for (int w = 0; w < (SPLIT ? PAIR_WARPS : 1); ++w) {
+                    for (int w = 0; w < (SPLIT ? NW : 1); ++w) {
                         fx += part[w][0][lane]; fy += part[w][1][lane]; fz += part[w][2][lane];
                     }
                     const size_t o = nb + I.aux[lane].x;
@@ -409,7 +428,7 @@ pair_kernel(kf_field_t f, int B, int n, const unsigned long long *__restrict__ k
             if (threadIdx.x == 0) {
                 double te = 0.0, tv = 0.0;
                 long long tc = 0;
-                for (int w = 0; w < PAIR_WARPS; ++w) { te += epart[w][0]; tv += epart[w][1]; tc += cpart[w]; }
+                for (int w = 0; w < NW; ++w) { te += epart[w][0]; tv += epart[w][1]; tc += cpart[w]; }
                 const size_t o = nb + s_aux[nb + s0].x;
                 e_atom[2 * o] = te; e_atom[2 * o + 1] = tv;
                 pair_count[o] = tc;
@@ -470,11 +489,26 @@ int kf_pairs_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s) {
         g_pair_grid = sms * 4;
     }
     KF_CUDA(cudaMemsetAsync(w->work, 0, sizeof(int32_t), s), "memset work");
-    // one CTA per cell when the whole batch is small (latency), one warp per cell otherwise
-    const bool split = (long long)w->B * n < 200000;
+    // one CTA per cell when the whole batch is small (latency), one warp per cell otherwise;
+    // KFB200_PAIR_SPLIT_BELOW overrides the crossover (atoms per launch)
+    static long long split_below = -1;
+    if (split_below < 0) {
+        const char *env = getenv("KFB200_PAIR_SPLIT_BELOW");
+        split_below = env ? atoll(env) : 200000;
+    }
+    const bool split = (long long)w->B * n < split_below;
     auto kern = f->precision ? (split ? pair_kernel<true, true> : pair_kernel<true, false>)
                              : (split ? pair_kernel<false, true> : pair_kernel<false, false>);
-    kern<<<g_pair_grid, PAIR_WARPS * 32, 0, s>>>(
+    const int nw = split ? SPLIT_WARPS : PAIR_WARPS;
+    const size_t dyn = (size_t)nw * (f->precision ? sizeof(WarpSmem<double>) : sizeof(WarpSmem<float>));
+    static bool opted = false;
+    if (!opted) {
+        for (auto k : {pair_kernel<true, true>, pair_kernel<true, false>, pair_kernel<false, true>,
+                       pair_kernel<false, false>})
+            KF_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024), "pair smem");
+        opted = true;
+    }
+    kern<<<split ? g_pair_grid / 2 : g_pair_grid, nw * 32, dyn, s>>>(
         *f, w->B, n, w->cell_key, w->cell_cnt, w->cell_start, w->occ, w->occ_offset,
         reinterpret_cast<const float4 *>(w->s_hi), reinterpret_cast<const float4 *>(w->s_lo),
         reinterpret_cast<const double4 *>(w->s_pos), reinterpret_cast<const float4 *>(w->s_par),
