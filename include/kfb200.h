@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define KF_ABI_VERSION 1
+#define KF_ABI_VERSION 2
 
 /* ---- static chain tables (uploaded once per chain) ------------------------
  * Links are in the reference's topological order (parent < index, ground = 0),
@@ -134,7 +134,11 @@ typedef struct {
     int32_t *cell_start;            /* [B][H] first sorted index of the cell       */
     int32_t *occ;                   /* [B][H] occupied slots (first occ_count[b])  */
     int32_t *occ_count;             /* [B]                                         */
-    int32_t *occ_offset;            /* [B+1] prefix of occ_count (work items)      */
+    int32_t *occ_offset;            /* [B+1] prefix of occ_count (cells)           */
+    int32_t *chunk_pre;             /* [B][H] per occupied cell (list order): prefix
+                                       of its 32-atom i-chunks ceil(cnt/32)        */
+    int32_t *chunk_count;           /* [B] i-chunks of the trajectory              */
+    int32_t *chunk_offset;          /* [B+1] prefix of chunk_count (pair work items) */
     int32_t *atom_slot;             /* [B][n] slot of the atom's cell              */
     int32_t *atom_rank;             /* [B][n] arrival rank inside the cell         */
     int32_t *sorted_atom;           /* [B][n] atoms grouped by cell, ascending     */

@@ -78,79 +78,86 @@ __global__ void bin_insert_kernel(kf_field_t f, int B, int n, const double *__re
     atom_rank[gid] = base + rank_in;
 }
 
-// Per trajectory: exclusive scan of the occupied cells' counts in list order.
+// Block-wide exclusive scan of one int per thread (blockDim a multiple of 32).
+__device__ __forceinline__ int block_excl_scan(int v, int *wsum) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += u;
+    }
+    __syncthreads();
+    if (lane == 31) wsum[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+        int t = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int u = __shfl_up_sync(0xffffffffu, t, o);
+            if (lane >= o) t += u;
+        }
+        wsum[lane] = t;
+    }
+    __syncthreads();
+    return incl - v + (wid > 0 ? wsum[wid - 1] : 0);
+}
+
+// Per trajectory: exclusive scans, in occupied-list order, of the cells' atom
+// counts (-> cell_start, by slot) and of their 32-atom i-chunks (-> chunk_pre,
+// by list position; the pair kernel's work items are (cell, i-chunk)).
 __global__ void __launch_bounds__(1024)
 cell_scan_kernel(int H, const int32_t *__restrict__ occ, const int32_t *__restrict__ occ_count,
-                 const int32_t *__restrict__ cnt, int32_t *__restrict__ start, const kf_status_t *status) {
+                 const int32_t *__restrict__ cnt, int32_t *__restrict__ start, int32_t *__restrict__ chunk_pre,
+                 int32_t *__restrict__ chunk_count, const kf_status_t *status) {
     const int b = blockIdx.x;
     if (status[b].done) return;
     const int m = occ_count[b];
     const int32_t *ob = occ + (size_t)b * H;
     const int32_t *cb = cnt + (size_t)b * H;
     int32_t *sb = start + (size_t)b * H;
+    int32_t *pb = chunk_pre + (size_t)b * H;
     const int per = (m + blockDim.x - 1) / blockDim.x;
     const int lo = min(m, (int)threadIdx.x * per), hi = min(m, lo + per);
-    int local = 0;
-    for (int k = lo; k < hi; ++k) local += cb[ob[k]];
+    int local = 0, lchunk = 0;
+    for (int k = lo; k < hi; ++k) {
+        const int c = cb[ob[k]];
+        local += c;
+        lchunk += (c + 31) >> 5;
+    }
     __shared__ int wsum[32];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    int incl = local;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += v;
+    int run = block_excl_scan(local, wsum);
+    int crun = block_excl_scan(lchunk, wsum);
+    for (int k = lo; k < hi; ++k) {
+        const int c = cb[ob[k]];
+        sb[ob[k]] = run; run += c;
+        pb[k] = crun; crun += (c + 31) >> 5;
     }
-    if (lane == 31) wsum[wid] = incl;
-    __syncthreads();
-    if (wid == 0) {
-        int v = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int u = __shfl_up_sync(0xffffffffu, v, o);
-            if (lane >= o) v += u;
-        }
-        wsum[lane] = v;
-    }
-    __syncthreads();
-    int run = incl - local + (wid > 0 ? wsum[wid - 1] : 0);
-    for (int k = lo; k < hi; ++k) { sb[ob[k]] = run; run += cb[ob[k]]; }
+    if (threadIdx.x == blockDim.x - 1) chunk_count[b] = crun;
 }
 
-// Work-item prefix over trajectories (one item = one occupied cell).
+// Work-item prefixes over trajectories: occupied cells (bin_finalize) and
+// i-chunks (pair kernel).
 __global__ void __launch_bounds__(1024)
 occ_prefix_kernel(int B, const int32_t *__restrict__ occ_count, int32_t *__restrict__ occ_offset,
+                  const int32_t *__restrict__ chunk_count, int32_t *__restrict__ chunk_offset,
                   const kf_status_t *status) {
-    __shared__ int carry;
-    if (threadIdx.x == 0) carry = 0;
+    __shared__ int carry[2];
+    __shared__ int ws[32];
+    if (threadIdx.x == 0) carry[0] = carry[1] = 0;
     __syncthreads();
     for (int base = 0; base < B; base += blockDim.x) {
         const int b = base + threadIdx.x;
-        const int v = (b < B && !status[b].done) ? occ_count[b] : 0;
-        __shared__ int ws[32];
-        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-        int incl = v;
-        for (int o = 1; o < 32; o <<= 1) {
-            const int u = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += u;
-        }
-        if (lane == 31) ws[wid] = incl;
+        const bool live = b < B && !status[b].done;
+        const int v = live ? occ_count[b] : 0, u = live ? chunk_count[b] : 0;
+        const int ev = carry[0] + block_excl_scan(v, ws);
+        const int eu = carry[1] + block_excl_scan(u, ws);
+        if (b < B) { occ_offset[b] = ev; chunk_offset[b] = eu; }
         __syncthreads();
-        if (wid == 0) {
-            int t = lane < (int)(blockDim.x >> 5) ? ws[lane] : 0;
-            for (int o = 1; o < 32; o <<= 1) {
-                const int u = __shfl_up_sync(0xffffffffu, t, o);
-                if (lane >= o) t += u;
-            }
-            ws[lane] = t;
-        }
-        __syncthreads();
-        const int excl = carry + incl - v + (wid > 0 ? ws[wid - 1] : 0);
-        if (b < B) occ_offset[b] = excl;
-        __syncthreads();
-        if (threadIdx.x == blockDim.x - 1) carry = excl + v;
+        if (threadIdx.x == blockDim.x - 1) { carry[0] = ev + v; carry[1] = eu + u; }
         __syncthreads();
     }
-    if (threadIdx.x == 0) occ_offset[B] = carry;
+    if (threadIdx.x == 0) { occ_offset[B] = carry[0]; chunk_offset[B] = carry[1]; }
 }
 
 __global__ void bin_scatter_kernel(kf_field_t f, int B, int n, const int32_t *__restrict__ atom_slot,
@@ -258,9 +265,11 @@ int kf_bin_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s) {
     bin_insert_kernel<<<kf_blocks(total, 256), 256, 0, s>>>(*f, B, n, w->pos, w->cell_key, w->cell_cnt, w->occ,
                                                             w->occ_count, w->atom_slot, w->atom_rank, w->status);
     KF_LAUNCH_CHECK("bin_insert_kernel");
-    cell_scan_kernel<<<B, 1024, 0, s>>>(H, w->occ, w->occ_count, w->cell_cnt, w->cell_start, w->status);
+    cell_scan_kernel<<<B, 1024, 0, s>>>(H, w->occ, w->occ_count, w->cell_cnt, w->cell_start, w->chunk_pre,
+                                         w->chunk_count, w->status);
     KF_LAUNCH_CHECK("cell_scan_kernel");
-    occ_prefix_kernel<<<1, 1024, 0, s>>>(B, w->occ_count, w->occ_offset, w->status);
+    occ_prefix_kernel<<<1, 1024, 0, s>>>(B, w->occ_count, w->occ_offset, w->chunk_count, w->chunk_offset,
+                                         w->status);
     KF_LAUNCH_CHECK("occ_prefix_kernel");
     bin_scatter_kernel<<<kf_blocks(total, 256), 256, 0, s>>>(*f, B, n, w->atom_slot, w->atom_rank, w->cell_start,
                                                              w->sorted_atom, w->status);

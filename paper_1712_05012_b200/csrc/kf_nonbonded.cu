@@ -155,7 +155,8 @@ template <bool F64, bool SPLIT>
 __global__ void __launch_bounds__((SPLIT ? SPLIT_WARPS : PAIR_WARPS) * 32, SPLIT ? 1 : 4)
 pair_kernel(kf_field_t f, int B, int n, const unsigned long long *__restrict__ keys,
             const int32_t *__restrict__ cnt, const int32_t *__restrict__ start, const int32_t *__restrict__ occ,
-            const int32_t *__restrict__ occ_offset, const float4 *__restrict__ s_hi,
+            const int32_t *__restrict__ occ_count, const int32_t *__restrict__ chunk_pre,
+            const int32_t *__restrict__ chunk_offset, const float4 *__restrict__ s_hi,
             const float4 *__restrict__ s_lo, const double4 *__restrict__ s_pos, const float4 *__restrict__ s_par,
             const int4 *__restrict__ s_aux, const int4 *__restrict__ s_tree, const float4 *__restrict__ cell_box,
             int32_t *__restrict__ work, double *__restrict__ forces, double *__restrict__ e_atom,
@@ -176,7 +177,7 @@ pair_kernel(kf_field_t f, int B, int n, const unsigned long long *__restrict__ k
     Tile &I = Itile[SPLIT ? 0 : warp];
     int4 *itree = itree_s[SPLIT ? 0 : warp];
     const uint32_t H = 1u << f.hash_bits;
-    const int total = occ_offset[B];
+    const int total = chunk_offset[B];
     const float cellf = (float)f.cell;
     const float pre2 = (float)(f.cut_pair2 + 1e-2);
     const float cut2f = (float)f.cut_pair2, tvf = (float)f.thr_vdw2, tef = (float)f.thr_elec2;
@@ -209,15 +210,23 @@ pair_kernel(kf_field_t f, int B, int n, const unsigned long long *__restrict__ k
             item = __shfl_sync(FULL, item, 0);
         }
         if (item >= total) break;
-        const int b = item_owner(occ_offset, B, item);
+        // item -> (trajectory, occupied cell, 32-atom i-chunk of that cell)
+        const int b = item_owner(chunk_offset, B, item);
         const size_t hb = (size_t)b * H, nb = (size_t)b * n;
-        const int slot = occ[hb + (item - occ_offset[b])];
+        const int local = item - chunk_offset[b];
+        int klo = 0, khi = occ_count[b] - 1;          // last k with chunk_pre[k] <= local
+        while (klo < khi) {
+            const int mid = (klo + khi + 1) >> 1;
+            if (chunk_pre[hb + mid] <= local) klo = mid; else khi = mid - 1;
+        }
+        const int slot = occ[hb + klo];
+        const int ic = (local - chunk_pre[hb + klo]) << 5;
         int cx, cy, cz;
         unpack_cell((long long)keys[hb + slot], cx, cy, cz);
         const int s0 = start[hb + slot], c = cnt[hb + slot];
         double ee = 0.0, ev = 0.0;   // cell totals (per computing lane)
         long long pcount = 0;
-        for (int ic = 0; ic < c; ic += 32) {
+        {
             const int ci_n = min(32, c - ic);
             const bool valid = lane < ci_n;
             if ((!SPLIT || warp == 0) && valid) {
@@ -414,8 +423,8 @@ pair_kernel(kf_field_t f, int B, int n, const unsigned long long *__restrict__ k
                 pair_count[o] = 0;
             }
         }
-        // cell totals: fixed xor tree per warp, then warps in order, stored at the
-        // cell's lowest atom (cells are a function of the positions: deterministic)
+        // chunk totals: fixed xor tree per warp, then warps in order, stored at the
+        // chunk's first atom (chunks are a function of the positions: deterministic)
 #pragma unroll
         for (int d = 16; d > 0; d >>= 1) {
             ee += __shfl_xor_sync(FULL, ee, d);
@@ -429,14 +438,14 @@ pair_kernel(kf_field_t f, int B, int n, const unsigned long long *__restrict__ k
                 double te = 0.0, tv = 0.0;
                 long long tc = 0;
                 for (int w = 0; w < NW; ++w) { te += epart[w][0]; tv += epart[w][1]; tc += cpart[w]; }
-                const size_t o = nb + s_aux[nb + s0].x;
+                const size_t o = nb + s_aux[nb + s0 + ic].x;
                 e_atom[2 * o] = te; e_atom[2 * o + 1] = tv;
                 pair_count[o] = tc;
             }
         } else {
             __syncwarp();
             if (lane == 0) {
-                const size_t o = nb + s_aux[nb + s0].x;
+                const size_t o = nb + s_aux[nb + s0 + ic].x;
                 e_atom[2 * o] = ee; e_atom[2 * o + 1] = ev;
                 pair_count[o] = pcount;
             }
@@ -509,7 +518,7 @@ int kf_pairs_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s) {
         opted = true;
     }
     kern<<<split ? g_pair_grid / 2 : g_pair_grid, nw * 32, dyn, s>>>(
-        *f, w->B, n, w->cell_key, w->cell_cnt, w->cell_start, w->occ, w->occ_offset,
+        *f, w->B, n, w->cell_key, w->cell_cnt, w->cell_start, w->occ, w->occ_count, w->chunk_pre, w->chunk_offset,
         reinterpret_cast<const float4 *>(w->s_hi), reinterpret_cast<const float4 *>(w->s_lo),
         reinterpret_cast<const double4 *>(w->s_pos), reinterpret_cast<const float4 *>(w->s_par),
         reinterpret_cast<const int4 *>(w->s_aux), reinterpret_cast<const int4 *>(w->s_tree),
