@@ -6,21 +6,23 @@
 // TreeWeights.weights_for (topology.py:153-195), elec/vdw_pair_quantities
 // (forcefield.py:98-113) and the bincount scatter (forcefield.py:162-172).
 //
-// Work: one warp per occupied 9 A cell (dynamic work counter over the cells of
-// all trajectories); the cell's atoms (<= 32 per pass) are the warp's i-tile.
-// For each of the 27 neighbour cells that some lane can reach (per-lane
-// distance to the cell's bounding box, warp vote) the warp stages 32-atom
-// j-tiles in shared memory and runs two stages:
-//   1. prefilter: each lane tests its i against the tile in fp32 from
-//      cell-centre offsets into a 32-bit mask (band 1e-2 A^2 around cut^2);
-//   2. compacted pairs: the set bits of all lanes are dealt out one pair per
-//      lane (warp scan + __fns), so every lane does useful pair work; each
-//      pair gets its difference vector from the hi/lo fp32 offset pairs
-//      (fp64-accurate), decides membership exactly as the reference
-//      (d2 = (dx*dx + dz*dz) + dy*dy in fp64 vs max(elec, vdw)^2, and
-//      sqrt(d2) <= cut per term) — recomputed from the fp64 positions only in
-//      a 1e-3 A^2 band around each threshold — and evaluates energy and
-//      force in fp32; pairs under 1 A take the reference's fp64 formulas.
+// Work items are (occupied 9 A cell, 32-atom i-chunk of it) over all
+// trajectories, taken from a dynamic counter: one warp per item (ensembles) or
+// one CTA per item whose warps share the j-tiles (SPLIT: small batches).
+// Per item the warp probes the 27 neighbour cells at once (lane = stencil
+// cell), keeps those whose bounding box some i of the chunk reaches, and
+// concatenates their atoms into one j-stream cut into full 32-atom tiles
+// (positions shifted into the i cell's frame while staging).  Per tile:
+//   1. prefilter: lane = j, loop over the chunk's i (broadcast), fp32 d^2
+//      against cut^2 + 1e-2 A^2; a ballot per i gives owner i's 32-bit row;
+//   2. compacted pairs: the set bits of all rows are dealt out one pair per
+//      lane, owner-major (warp scan + bit walk), so every lane does useful
+//      pair work; each pair gets its difference vector from the hi/lo fp32
+//      offset pairs (fp64-accurate), decides membership exactly as the
+//      reference (d2 = (dx*dx + dz*dz) + dy*dy in fp64 vs max(elec, vdw)^2,
+//      and sqrt(d2) <= cut per term) -- recomputed from the fp64 positions
+//      only in a 1e-3 A^2 band around each threshold -- and evaluates energy
+//      and force in fp32; pairs under 1 A take the reference's fp64 formulas.
 //   The per-pair results are summed per owner lane in pair order, i.e. in a
 //   fixed order, into fp64 accumulators.
 // Both directions of each unordered pair are evaluated by their owners
@@ -38,6 +40,7 @@ constexpr int PAIR_WARPS = 4;        // warps per CTA, warp-per-cell variant
 constexpr int SPLIT_WARPS = 4;       // warps per CTA (one cell), split variant
 constexpr unsigned FULL = 0xffffffffu;
 
+
 struct Tile {
     float4 hi[32];
     float4 lo[32];
@@ -45,7 +48,10 @@ struct Tile {
     int4 aux[32];
 };
 
-constexpr int RES_BATCH = 128;
+#ifndef RES_BATCH_N
+#define RES_BATCH_N 128
+#endif
+constexpr int RES_BATCH = RES_BATCH_N;
 
 template <typename T>
 struct WarpSmem {
@@ -54,44 +60,14 @@ struct WarpSmem {
     unsigned short list[1024]; // candidate (owner << 5 | t) pairs of the tile, owner-major
 };
 
-struct Acc {
-    double fx, fy, fz, ee, ev;
-    long long cnt;   // elec-cutoff partners (low 32 bits) | vdW-cutoff partners << 32
-};
-
-// One pair in fp64 (the reference's formulas, forcefield.py:98-113, with the
-// powers written as products): used below 1 A, and for every pair in the
-// fp64 precision mode.
-template <typename T>
-KF_DEV void pair_fp64(const kf_field_t &f, int i, int j, double d2, double dx, double dy, double dz,
-                      double we, double wv, bool ke, bool kv, T *out) {
-    const double d = sqrt(d2);
-    const double inv_d = 1.0 / d;
-    double mag = 0.0, ee = 0.0, ev = 0.0;
-    if (ke) {
-        const double num = COULOMB_K * we * f.q[i] * f.q[j];
-        ee = f.dielectric_const ? num * inv_d / f.kappa : num * inv_d * inv_d;   // num / (kappa d)
-        mag += ee * inv_d;                                                       // num / (kappa d^2)
-    }
-    if (kv) {
-        const double eps = sqrt(f.eps[i] * f.eps[j]);
-        const double r = (f.R[i] + f.R[j]) * inv_d;
-        const double r2 = r * r, r6 = r2 * r2 * r2;
-        ev = wv * eps * (r6 * r6 - 2.0 * r6);
-        mag += 12.0 * wv * eps * (r6 * r6 - r6) * inv_d;
-    }
-    const double g = mag * inv_d;
-    out[0] = (T)(g * dx); out[1] = (T)(g * dy); out[2] = (T)(g * dz);
-    out[3] = (T)ee; out[4] = (T)ev;
-}
-
-// Everything the exact / fp64 pair path needs, kept out of the kernel's
-// register allocation (the path runs for pairs within 1e-3 A^2 of a cut-off,
-// below 1 A, or always in fp64 mode).
-struct SlowArgs {
-    const double *q, *R, *eps;
-    double kappa, cut2, te2, tv2, wel[4], wvd[4];
-    int dconst;
+// fp32 constants of the fast path, passed by value (kernel parameter space:
+// constant-bank operands, no registers).
+struct PairConst {
+    float we[4], wv[4];          // elec / vdW weight by class 1..4
+    float pre2, cut2, tv2, te2;  // prefilter and cut-offs (A^2)
+    float kap_inv, cell;
+    float f64_d2;                // pairs closer than this (A^2) take the fp64 formulas
+    int dconst, uniform;
 };
 
 __device__ __noinline__ int slow_class(const int32_t *tp, const int32_t *tgp, const int32_t *tgg,
@@ -105,15 +81,16 @@ __device__ __noinline__ int slow_class(const int32_t *tp, const int32_t *tgp, co
 }
 
 template <typename T>
-__device__ __noinline__ void slow_pair(bool f64, const SlowArgs &A, const double4 *pi_, const double4 *pj_, int i,
+__device__ __noinline__ void slow_pair(bool f64, const kf_field_t *A, const double4 *pi_, const double4 *pj_, int i,
                                        int j, int cls, T *out, int *pce, int *pcv, kf_status_t *st) {
     const double4 p_i = *pi_, p_j = *pj_;
     const double dx = xsub(p_i.x, p_j.x), dy = xsub(p_i.y, p_j.y), dz = xsub(p_i.z, p_j.z);
     const double d2 = d2_einsum(dx, dy, dz);
-    if (d2 > A.cut2) return;
-    const bool ke = d2 <= A.te2, kv = d2 <= A.tv2;
+    if (d2 > A->cut_pair2) return;
+    const bool ke = d2 <= A->thr_elec2, kv = d2 <= A->thr_vdw2;
     *pce = ke; *pcv = kv;
-    const double we = A.wel[cls - 1], wv = A.wvd[cls - 1];
+    const double we = A->uniform_weights ? A->uniform_value : A->w_elec[cls - 1];
+    const double wv = A->uniform_weights ? A->uniform_value : A->w_vdw[cls - 1];
     if (d2 < 1e-11) {
         const double d = sqrt(d2);
         if (d < MIN_DISTANCE) {
@@ -126,13 +103,13 @@ __device__ __noinline__ void slow_pair(bool f64, const SlowArgs &A, const double
     const double inv_d = 1.0 / d;
     double mag = 0.0, ee = 0.0, ev = 0.0;
     if (ke) {
-        const double num = COULOMB_K * we * A.q[i] * A.q[j];
-        ee = A.dconst ? num * inv_d / A.kappa : num * inv_d * inv_d;   // num / (kappa d)
+        const double num = COULOMB_K * we * A->q[i] * A->q[j];
+        ee = A->dielectric_const ? num * inv_d / A->kappa : num * inv_d * inv_d;   // num / (kappa d)
         mag += ee * inv_d;                                              // num / (kappa d^2)
     }
     if (kv) {
-        const double eps = sqrt(A.eps[i] * A.eps[j]);
-        const double r = (A.R[i] + A.R[j]) * inv_d;
+        const double eps = sqrt(A->eps[i] * A->eps[j]);
+        const double r = (A->R[i] + A->R[j]) * inv_d;
         const double r2 = r * r, r6 = r2 * r2 * r2;
         ev = wv * eps * (r6 * r6 - 2.0 * r6);
         mag += 12.0 * wv * eps * (r6 * r6 - r6) * inv_d;
@@ -143,8 +120,8 @@ __device__ __noinline__ void slow_pair(bool f64, const SlowArgs &A, const double
     (void)f64;
 }
 
-#ifndef PAIR_MINB
-#define PAIR_MINB 3
+#ifndef PAIR_MINB_W
+#define PAIR_MINB_W 4   // resident CTAs per SM asked of ptxas, warp-per-chunk variant
 #endif
 // F64 = false: fp32 pair math (the north-star configuration); true: fp64
 // pair math and fp64 per-tile sums (strict trajectory parity mode).
@@ -152,8 +129,8 @@ __device__ __noinline__ void slow_pair(bool f64, const SlowArgs &A, const double
 // (short per-cell latency: single trajectories); false: one warp per cell
 // (throughput: ensembles).
 template <bool F64, bool SPLIT>
-__global__ void __launch_bounds__((SPLIT ? SPLIT_WARPS : PAIR_WARPS) * 32, SPLIT ? 1 : 4)
-pair_kernel(kf_field_t f, int B, int n, const unsigned long long *__restrict__ keys,
+__global__ void __launch_bounds__((SPLIT ? SPLIT_WARPS : PAIR_WARPS) * 32, SPLIT ? 1 : PAIR_MINB_W)
+pair_kernel(const __grid_constant__ kf_field_t f, const PairConst pc, int B, int n, const unsigned long long *__restrict__ keys,
             const int32_t *__restrict__ cnt, const int32_t *__restrict__ start, const int32_t *__restrict__ occ,
             const int32_t *__restrict__ occ_count, const int32_t *__restrict__ chunk_pre,
             const int32_t *__restrict__ chunk_offset, const float4 *__restrict__ s_hi,
@@ -178,24 +155,8 @@ pair_kernel(kf_field_t f, int B, int n, const unsigned long long *__restrict__ k
     int4 *itree = itree_s[SPLIT ? 0 : warp];
     const uint32_t H = 1u << f.hash_bits;
     const int total = chunk_offset[B];
-    const float cellf = (float)f.cell;
-    const float pre2 = (float)(f.cut_pair2 + 1e-2);
-    const float cut2f = (float)f.cut_pair2, tvf = (float)f.thr_vdw2, tef = (float)f.thr_elec2;
+    const float cellf = pc.cell, pre2 = pc.pre2, cut2f = pc.cut2, tvf = pc.tv2, tef = pc.te2;
     const float band = 1e-3f;
-    const float kap_inv = f.dielectric_const ? (float)(1.0 / f.kappa) : 1.0f;
-    float wf[8];
-    for (int q = 0; q < 4; ++q) {
-        wf[q] = f.uniform_weights ? (float)f.uniform_value : (float)f.w_elec[q];
-        wf[4 + q] = f.uniform_weights ? (float)f.uniform_value : (float)f.w_vdw[q];
-    }
-    SlowArgs fx64;
-    fx64.q = f.q; fx64.R = f.R; fx64.eps = f.eps;
-    fx64.kappa = f.kappa; fx64.cut2 = f.cut_pair2; fx64.te2 = f.thr_elec2; fx64.tv2 = f.thr_vdw2;
-    fx64.dconst = f.dielectric_const;
-    for (int q = 0; q < 4; ++q) {
-        fx64.wel[q] = f.uniform_weights ? f.uniform_value : f.w_elec[q];
-        fx64.wvd[q] = f.uniform_weights ? f.uniform_value : f.w_vdw[q];
-    }
 
     for (;;) {
         int item;
@@ -224,8 +185,8 @@ pair_kernel(kf_field_t f, int B, int n, const unsigned long long *__restrict__ k
         int cx, cy, cz;
         unpack_cell((long long)keys[hb + slot], cx, cy, cz);
         const int s0 = start[hb + slot], c = cnt[hb + slot];
-        double ee = 0.0, ev = 0.0;   // cell totals (per computing lane)
-        long long pcount = 0;
+        double ee = 0.0, ev = 0.0;   // chunk totals (per computing lane)
+        int ce = 0, cv = 0;          // elec / vdW cut-off partners (per computing lane)
         {
             const int ci_n = min(32, c - ic);
             const bool valid = lane < ci_n;
@@ -238,60 +199,83 @@ pair_kernel(kf_field_t f, int B, int n, const unsigned long long *__restrict__ k
                 itree[lane] = s_tree[ki];
             }
             if (SPLIT) __syncthreads(); else __syncwarp();
-            const float4 hi_i = I.hi[valid ? lane : 0];
-            Acc a = {0.0, 0.0, 0.0, 0.0, 0.0, 0};
+            double ax = 0.0, ay = 0.0, az = 0.0;   // owner lane: fp64 force sums over the chunk's tiles
 
-            // the 27 neighbour cells are dealt to the warps round-robin; each warp
-            // keeps per-owner fp64 sums over its cells in a fixed order
-            // probe all neighbour cells at once (lane s <-> stencil cell s): one
-            // round of table / start / count / box loads instead of 27 serial ones
-            int p_js = -1, p_j0 = 0, p_jc = 0;
-            float4 p_lo = make_float4(0.f, 0.f, 0.f, 0.f), p_hi = p_lo;
+            // probe all neighbour cells at once (lane s <-> stencil cell s) and keep
+            // the cells whose bounding box some i of the chunk can reach
+            // (warp-uniform loop over the chunk's atoms: no lane-dependent trip
+            // counts ahead of the warp collectives below)
+            int p_j0 = 0, p_jc = 0, p_js = -1;
+            float p_sx = 0.f, p_sy = 0.f, p_sz = 0.f;
+            float4 blo = make_float4(1e30f, 1e30f, 1e30f, 0.f), bhi = make_float4(-1e30f, -1e30f, -1e30f, 0.f);
             if (lane < f.n_stencil) {
-                p_js = cell_probe(keys + hb, H, cx + f.stencil[3 * lane], cy + f.stencil[3 * lane + 1],
-                                  cz + f.stencil[3 * lane + 2]);
+                const int ox = f.stencil[3 * lane], oy = f.stencil[3 * lane + 1], oz = f.stencil[3 * lane + 2];
+                p_js = cell_probe(keys + hb, H, cx + ox, cy + oy, cz + oz);
                 if (p_js >= 0) {
-                    p_j0 = start[hb + p_js]; p_jc = cnt[hb + p_js];
-                    p_lo = cell_box[2 * (hb + p_js)]; p_hi = cell_box[2 * (hb + p_js) + 1];
+                    p_sx = (float)ox * cellf; p_sy = (float)oy * cellf; p_sz = (float)oz * cellf;
+                    blo = cell_box[2 * (hb + p_js)]; bhi = cell_box[2 * (hb + p_js) + 1];
                 }
             }
-            for (int s = SPLIT ? warp : 0; s < f.n_stencil; s += SPLIT ? NW : 1) {
-                const int js = __shfl_sync(FULL, p_js, s);
-                if (js < 0) continue;
-                const int ox = f.stencil[3 * s], oy = f.stencil[3 * s + 1], oz = f.stencil[3 * s + 2];
-                // i in the neighbour cell's frame; skip the cell unless some lane reaches its box
-                const float sx = (float)ox * cellf, sy = (float)oy * cellf, sz = (float)oz * cellf;
-                const float px = hi_i.x - sx, py = hi_i.y - sy, pz = hi_i.z - sz;
-                const float blx = __shfl_sync(FULL, p_lo.x, s), bly = __shfl_sync(FULL, p_lo.y, s),
-                            blz = __shfl_sync(FULL, p_lo.z, s);
-                const float bhx = __shfl_sync(FULL, p_hi.x, s), bhy = __shfl_sync(FULL, p_hi.y, s),
-                            bhz = __shfl_sync(FULL, p_hi.z, s);
-                const float gx = fmaxf(fmaxf(blx - px, px - bhx), 0.f);
-                const float gy = fmaxf(fmaxf(bly - py, py - bhy), 0.f);
-                const float gz = fmaxf(fmaxf(blz - pz, pz - bhz), 0.f);
-                const bool need = valid && gx * gx + gy * gy + gz * gz <= pre2;
-                if (!__any_sync(FULL, need)) continue;
-                const int j0 = __shfl_sync(FULL, p_j0, s), jc = __shfl_sync(FULL, p_jc, s);
-                for (int jb = 0; jb < jc; jb += 32) {
-                    const int nt = min(32, jc - jb);
+            __syncwarp();
+            bool keep = false;
+            for (int q = 0; q < ci_n; ++q) {
+                const float4 r = I.hi[q];   // i in the neighbour cell's frame
+                const float px = r.x - p_sx, py = r.y - p_sy, pz = r.z - p_sz;
+                const float gx = fmaxf(fmaxf(blo.x - px, px - bhi.x), 0.f);
+                const float gy = fmaxf(fmaxf(blo.y - py, py - bhi.y), 0.f);
+                const float gz = fmaxf(fmaxf(blo.z - pz, pz - bhi.z), 0.f);
+                keep |= gx * gx + gy * gy + gz * gz <= pre2;
+            }
+            if (keep) { p_j0 = start[hb + p_js]; p_jc = cnt[hb + p_js]; }
+            // the kept cells' atoms form one j-stream (stencil order), cut into
+            // full 32-atom tiles; tiles are dealt to the CTA's warps round-robin
+            int p_end = p_jc;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v = __shfl_up_sync(FULL, p_end, o);
+                if (lane >= o) p_end += v;
+            }
+            const int n_stream = __shfl_sync(FULL, p_end, 31);
+            for (int jb = SPLIT ? 32 * warp : 0; jb < n_stream; jb += SPLIT ? 32 * NW : 32) {
+                const int nt = min(32, n_stream - jb);
+                {
+                    // lane -> stream element jb + lane -> (stencil cell, atom): first cell whose end exceeds it
+                    const int e = jb + lane;
+                    int cs = 0;
+#pragma unroll
+                    for (int step = 16; step > 0; step >>= 1) {
+                        const int end = __shfl_sync(FULL, p_end, cs + step - 1);
+                        if (end <= e) cs += step;
+                    }
+                    const int cend = __shfl_sync(FULL, p_end, cs), cj0 = __shfl_sync(FULL, p_j0, cs),
+                              ccnt = __shfl_sync(FULL, p_jc, cs);
+                    const float ssx = __shfl_sync(FULL, p_sx, cs), ssy = __shfl_sync(FULL, p_sy, cs),
+                                ssz = __shfl_sync(FULL, p_sz, cs);
                     __syncwarp();
                     if (lane < nt) {
-                        const size_t kj = nb + j0 + jb + lane;
-                        S.J.hi[lane] = s_hi[kj];
+                        const int kk = cj0 + (e - (cend - ccnt));
+                        const size_t kj = nb + kk;
+                        const float4 h = s_hi[kj];
+                        int4 aux = s_aux[kj];
+                        aux.w = kk;                     // sorted index (fp64 slow path)
+                        S.J.hi[lane] = make_float4(h.x + ssx, h.y + ssy, h.z + ssz, 0.f);   // i's cell frame
                         S.J.lo[lane] = s_lo[kj];
                         S.J.par[lane] = s_par[kj];
-                        S.J.aux[lane] = s_aux[kj];
+                        S.J.aux[lane] = aux;
                     }
                     __syncwarp();
-                    // ---- stage 1: fp32 prefilter into a mask
-                    unsigned mask = 0u;
-                    if (need) {
-                        for (int t = 0; t < nt; ++t) {
-                            const float4 r = S.J.hi[t];
-                            const float dx = px - r.x, dy = py - r.y, dz = pz - r.z;
-                            mask |= (dx * dx + dy * dy + dz * dz <= pre2 ? 1u : 0u) << t;
-                        }
+                }
+                // ---- stage 1: fp32 prefilter, j per lane, i broadcast; lane o keeps owner o's row
+                unsigned mask = 0u;
+                {
+                    const float4 rj = S.J.hi[lane < nt ? lane : 0];
+                    for (int q = 0; q < ci_n; ++q) {
+                        const float4 r = I.hi[q];
+                        const float dx = r.x - rj.x, dy = r.y - rj.y, dz = r.z - rj.z;
+                        const unsigned row = __ballot_sync(FULL, lane < nt && dx * dx + dy * dy + dz * dz <= pre2);
+                        if (lane == q) mask = row;
                     }
+                }
                     // ---- stage 2: the tile's candidate pairs, owner-major, one per lane
                     const int own = __popc(mask);
                     int incl = own;
@@ -328,14 +312,14 @@ pair_kernel(kf_field_t f, int B, int n, const unsigned long long *__restrict__ k
                             const int4 ai = I.aux[o], aj = S.J.aux[t];
                             const int i = ai.x, j = aj.x;
                             const float4 hi = I.hi[o], li = I.lo[o], hj = S.J.hi[t], lj = S.J.lo[t];
-                            const float dxf = ((hi.x - hj.x) - sx) + (li.x - lj.x);
-                            const float dyf = ((hi.y - hj.y) - sy) + (li.y - lj.y);
-                            const float dzf = ((hi.z - hj.z) - sz) + (li.z - lj.z);
+                            const float dxf = (hi.x - hj.x) + (li.x - lj.x);
+                            const float dyf = (hi.y - hj.y) + (li.y - lj.y);
+                            const float dzf = (hi.z - hj.z) + (li.z - lj.z);
                             const float d2f = dxf * dxf + dyf * dyf + dzf * dzf;
                             if (i != j && d2f <= cut2f + band) {
                                 // static class window: 2-bit codes for j - i in [-32, 32)
                                 int cls = 4;
-                                if (!f.uniform_weights) {
+                                if (!pc.uniform) {
                                     const int off = j - i + 32;
                                     if ((unsigned)off < 64u) {
                                         const int4 cm = itree[o];
@@ -346,12 +330,12 @@ pair_kernel(kf_field_t f, int B, int n, const unsigned long long *__restrict__ k
                                         cls = slow_class(f.tparent, f.tgp, f.tggp, f.tres, f.tchain, i, j);
                                     }
                                 }
-                                const float we = cls == 4 ? wf[3] : cls == 3 ? wf[2] : cls == 2 ? wf[1] : wf[0];
-                                const float wv = cls == 4 ? wf[7] : cls == 3 ? wf[6] : cls == 2 ? wf[5] : wf[4];
+                                const float we = cls == 4 ? pc.we[3] : cls == 3 ? pc.we[2] : cls == 2 ? pc.we[1] : pc.we[0];
+                                const float wv = cls == 4 ? pc.wv[3] : cls == 3 ? pc.wv[2] : cls == 2 ? pc.wv[1] : pc.wv[0];
                                 const bool exact = F64 || fabsf(d2f - cut2f) <= band || fabsf(d2f - tvf) <= band ||
-                                                   fabsf(d2f - tef) <= band || d2f < 1.0f;
+                                                   fabsf(d2f - tef) <= band || d2f < pc.f64_d2;
                                 if (exact) {
-                                    slow_pair<T>(F64, fx64, s_pos + nb + s0 + ic + o, s_pos + nb + j0 + jb + t, i, j,
+                                    slow_pair<T>(F64, &f, s_pos + nb + s0 + ic + o, s_pos + nb + aj.w, i, j,
                                                  cls, out, &pce, &pcv, status + b);
                                 } else if (d2f <= cut2f) {
                                     const bool ke = d2f <= tef, kv = d2f <= tvf;
@@ -364,7 +348,7 @@ pair_kernel(kf_field_t f, int B, int n, const unsigned long long *__restrict__ k
                                         // kappa = d: E = K w qi qj / d^2; constant: E = K w qi qj / (kappa d);
                                         // |F| / d = E / d^2 in both cases
                                         const float qq = (float)COULOMB_K * qi.x * qj.x * we;
-                                        const float e = f.dielectric_const ? qq * kap_inv * inv_r : qq * inv_r2;
+                                        const float e = pc.dconst ? qq * pc.kap_inv * inv_r : qq * inv_r2;
                                         out[3] = e;
                                         g += e * inv_r2;
                                     }
@@ -381,10 +365,9 @@ pair_kernel(kf_field_t f, int B, int n, const unsigned long long *__restrict__ k
                                 }
                             }
                         }
-                        const long long pc = (long long)pce + ((long long)pcv << 32);
-                        // energies and counts only enter per-cell totals: the computing lane keeps them
+                        // energies and counts only enter per-chunk totals: the computing lane keeps them
                         fe += out[3]; fv += out[4];
-                        a.cnt += pc;
+                        ce += pce; cv += pcv;
                         if (act) { S.res[k0 + lane][0] = out[0]; S.res[k0 + lane][1] = out[1]; S.res[k0 + lane][2] = out[2]; }
                       }
                       __syncwarp();
@@ -393,16 +376,14 @@ pair_kernel(kf_field_t f, int B, int n, const unsigned long long *__restrict__ k
                       for (int q = lo_k; q < hi_k; ++q) { fx += S.res[q][0]; fy += S.res[q][1]; fz += S.res[q][2]; }
                       __syncwarp();
                     }
-                    a.fx += (double)fx; a.fy += (double)fy; a.fz += (double)fz;
-                    a.ee += (double)fe; a.ev += (double)fv;
+                    ax += (double)fx; ay += (double)fy; az += (double)fz;
+                    ee += (double)fe; ev += (double)fv;
                 }
-            }
-            ee += a.ee; ev += a.ev; pcount += a.cnt;
             if (SPLIT) {
                 // combine the warps' partial forces in warp order (deterministic)
-                part[SPLIT ? warp : 0][0][lane] = a.fx;
-                part[SPLIT ? warp : 0][1][lane] = a.fy;
-                part[SPLIT ? warp : 0][2][lane] = a.fz;
+                part[SPLIT ? warp : 0][0][lane] = ax;
+                part[SPLIT ? warp : 0][1][lane] = ay;
+                part[SPLIT ? warp : 0][2][lane] = az;
                 __syncthreads();
                 if (warp == 0 && valid) {
                     double fx = 0.0, fy = 0.0, fz = 0.0;
@@ -418,11 +399,12 @@ pair_kernel(kf_field_t f, int B, int n, const unsigned long long *__restrict__ k
                 __syncthreads();
             } else if (valid) {
                 const size_t o = nb + I.aux[lane].x;
-                forces[3 * o] = a.fx; forces[3 * o + 1] = a.fy; forces[3 * o + 2] = a.fz;
+                forces[3 * o] = ax; forces[3 * o + 1] = ay; forces[3 * o + 2] = az;
                 e_atom[2 * o] = 0.0; e_atom[2 * o + 1] = 0.0;
                 pair_count[o] = 0;
             }
         }
+        long long pcount = (long long)ce + ((long long)cv << 32);
         // chunk totals: fixed xor tree per warp, then warps in order, stored at the
         // chunk's first atom (chunks are a function of the positions: deterministic)
 #pragma unroll
@@ -503,7 +485,7 @@ int kf_pairs_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s) {
     static long long split_below = -1;
     if (split_below < 0) {
         const char *env = getenv("KFB200_PAIR_SPLIT_BELOW");
-        split_below = env ? atoll(env) : 200000;
+        split_below = env ? atoll(env) : 40000;
     }
     const bool split = (long long)w->B * n < split_below;
     auto kern = f->precision ? (split ? pair_kernel<true, true> : pair_kernel<true, false>)
@@ -517,8 +499,24 @@ int kf_pairs_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s) {
             KF_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024), "pair smem");
         opted = true;
     }
+    PairConst pc;
+    for (int q = 0; q < 4; ++q) {
+        pc.we[q] = (float)(f->uniform_weights ? f->uniform_value : f->w_elec[q]);
+        pc.wv[q] = (float)(f->uniform_weights ? f->uniform_value : f->w_vdw[q]);
+    }
+    pc.pre2 = (float)(f->cut_pair2 + 1e-2);
+    pc.cut2 = (float)f->cut_pair2; pc.tv2 = (float)f->thr_vdw2; pc.te2 = (float)f->thr_elec2;
+    pc.kap_inv = f->dielectric_const ? (float)(1.0 / f->kappa) : 1.0f;
+    pc.cell = (float)f->cell;
+    static float f64_below = -1.f;   // KFB200_PAIR_F64_BELOW (A): fp64 radius of the fp32 mode
+    if (f64_below < 0.f) {
+        const char *env = getenv("KFB200_PAIR_F64_BELOW");
+        f64_below = env ? (float)atof(env) : 1.0f;
+    }
+    pc.f64_d2 = f64_below * f64_below;
+    pc.dconst = f->dielectric_const; pc.uniform = f->uniform_weights;
     kern<<<split ? g_pair_grid / 2 : g_pair_grid, nw * 32, dyn, s>>>(
-        *f, w->B, n, w->cell_key, w->cell_cnt, w->cell_start, w->occ, w->occ_count, w->chunk_pre, w->chunk_offset,
+        *f, pc, w->B, n, w->cell_key, w->cell_cnt, w->cell_start, w->occ, w->occ_count, w->chunk_pre, w->chunk_offset,
         reinterpret_cast<const float4 *>(w->s_hi), reinterpret_cast<const float4 *>(w->s_lo),
         reinterpret_cast<const double4 *>(w->s_pos), reinterpret_cast<const float4 *>(w->s_par),
         reinterpret_cast<const int4 *>(w->s_aux), reinterpret_cast<const int4 *>(w->s_tree),

@@ -349,29 +349,56 @@ def _c1_1000():
     rmsd = np.sqrt(((p_gpu - p_ref) ** 2).sum(axis=1).mean())
     e_gpu, e_ref = E[-1].sum(), g["energies"][-1].sum()
     assert abs(e_gpu - e_ref) <= 1e-2 * abs(e_ref)
-    return rel, rmsd
+    return rel, rmsd, tr, (ch, params, w, g, step)
 
 
 def test_fold_c1_1000_iterations_fp64(fp64_pairs):
     """SURVEY.md §8(d) trajectory criterion on C1 (30 x ALA helix start, vacuum,
     K = 1000), fp64 pair mode: per record |dE| <= 1e-5 (|g_elec| + |g_vdw| +
     |g_cav|) and final RMSD <= 1e-4 A."""
-    rel, rmsd = _c1_1000()
+    rel, rmsd, _, _ = _c1_1000()
     assert rel.max() <= 1e-5 and rmsd <= 1e-4, (rel.max(), rmsd)
 
 
 def test_fold_c1_1000_iterations_fp32():
-    """Same trajectory with fp32 pair math (the default).  Per-step parity is
-    ~1e-7 and the first 200 records agree to 1e-5; from iteration ~300 the run
-    sits near a bifurcation (the fixed 0.5 degree step oscillates across the
-    minimum) and the fp32 rounding picks a neighbouring path: measured on B200,
-    max per-record deviation 1.7e-2 of the energy scale, final total energy
-    within 0.2 %.  Stated fp32 tolerance: <= 1e-5 for 200 records, <= 5e-2
-    over 1000, final energy within 1 %.  set_pair_precision("fp64") gives
+    """Same trajectory with fp32 pair math (the default).
+
+    Per-step parity is ~1e-7 (forces: median 5e-7, p99 3e-6 relative, energy
+    ~1e-7; tools/fp32_err.py).  The trajectory itself is not a smooth function
+    of that rounding: the energy is discontinuous at the 9 A / 5 A cut-offs and
+    the fixed 0.5 degree step oscillates across the minimum from iteration
+    ~300, so a 1e-7 difference can move a cut-off crossing by one iteration
+    (measured on B200: the first records above 1e-5 / 1e-4 of the energy scale
+    appear between iterations 5 and 210 depending on the kernel's rounding
+    order; max 3e-2; final energy within 0.2 %).
+
+    Stated fp32 tolerance: (a) shadowing -- from the GPU's own theta at
+    sampled iterations, the reference step (oracle) reproduces the GPU's
+    record energy to 1e-6 and its next theta to 1e-4 of the step size kappa
+    over the first 100 iterations, 2e-3 of kappa later.  The step is
+    kappa * tau / tau_max: as the helix relaxes tau_max falls far below the
+    pair forces whose fp32 rounding (~1e-7 each) it sums, so the relative
+    step error grows (measured: 1e-5 at the start, up to 6.6e-4 of kappa near
+    the minimum; 1e-7 on C2 random conformations; tools/fp32_err.py);
+    (b) whole trajectory: every record within 5e-2 of the reference's energy
+    scale and the final energy within 1 %.  set_pair_precision("fp64") gives
     4e-12 over the full 1000 (test above)."""
-    rel, rmsd = _c1_1000()
-    assert rel[:200].max() <= 1e-5
+    rel, rmsd, tr, (ch, params, w, g, step) = _c1_1000()
     assert rel.max() <= 5e-2, rel.max()
+    fld = O.OracleField(params, w)
+    frozen = np.asarray(g["frozen"], bool)
+    for k in list(range(0, 1000, 50)) + [999]:
+        th = np.asarray(tr.records[k].theta)
+        M, Pp, U, pos = O.fk(ch, th)
+        forces, e, _ = fld.evaluate(pos)
+        e_gpu = tr.records[k].energy
+        e_sum = abs(e[0]) + abs(e[1]) + abs(e[2])
+        assert abs(e_gpu.g_elec - e[0]) + abs(e_gpu.g_vdw - e[1]) <= 1e-6 * e_sum, k
+        F, T = O.wrenches(ch, pos, forces)
+        nxt, _ = O.step(O.torques(ch, U, Pp, F, T), th, frozen, step.kappa)
+        got = np.asarray(tr.records[k + 1].theta) if k + 1 < len(tr.records) else np.asarray(tr.final.theta)
+        d = np.abs((got - nxt + 180.0) % 360.0 - 180.0).max()
+        assert d <= (1e-4 if k <= 100 else 2e-3) * step.kappa, (k, d)
 
 
 def test_fold_default_stop_rule_fp64(fp64_pairs):
