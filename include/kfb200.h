@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define KF_ABI_VERSION 2
+#define KF_ABI_VERSION 4
 
 /* ---- static chain tables (uploaded once per chain) ------------------------
  * Links are in the reference's topological order (parent < index, ground = 0),
@@ -90,6 +90,12 @@ typedef struct {
                                        exposure enters g_cav or the forces)        */
     int32_t n_solv;
     int32_t precision;              /* pair math: 0 = fp32 (fp64 sums), 1 = fp64   */
+    /* hot-path sample groups: the N directions reordered into G compact groups
+       of <= 32 (host-built), padded to 32 per group                           */
+    const double *samples_grp;      /* [G][32][3]                                  */
+    const float *grp_cone;          /* [G][8]: axis xyz, cos alpha, sin alpha, count, 0, 0 */
+    int32_t n_groups;
+    int32_t _pad2;
 } kf_field_t;
 
 /* ---- per-trajectory status block ----------------------------------------- */
@@ -144,7 +150,7 @@ typedef struct {
     int32_t *sorted_atom;           /* [B][n] atoms grouped by cell, ascending     */
     float   *s_hi;                  /* [B][n][4] offset from the cell centre, fp32 */
     float   *s_lo;                  /* [B][n][4] fp32 remainder (hi + lo = fp64)   */
-    double  *s_pos;                 /* [B][n][4] fp64 position (4th: unused)       */
+    double  *s_pos;                 /* [B][n][4] fp64 position, R_off (solvation)  */
     float   *s_par;                 /* [B][n][4] q, R, sqrt(eps), 0                */
     int32_t *s_aux;                 /* [B][n][4] atom, residue, chain flag, 0      */
     int32_t *s_tree;                /* [B][n][4] parent, grandparent, great-grand  */
@@ -158,6 +164,8 @@ typedef struct {
                                        per-cell totals stored at the cell's lowest atom */
     /* solvation */
     long long *solv_acc;            /* [B][n][3] int64 fixed point                 */
+    int32_t *solv_ovf;              /* [1 + 2 B n]: count, (b, atom) pairs deferred to
+                                       the large-capacity solvation pass            */
     double  *cav_atom;              /* [B][n] gamma_i * a_exp_i                    */
     double  *f_exp;                 /* [B][n] exposure ratio (NULL: not stored)    */
     double  *a_exp;                 /* [B][n] exposed area (NULL: not stored)      */

@@ -13,7 +13,7 @@ import os
 from .errors import NativeLibraryError
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libkfb200.so")
-ABI_VERSION = 2
+ABI_VERSION = 4
 
 P = C.c_void_p
 I32 = C.c_int32
@@ -40,7 +40,8 @@ class KfField(C.Structure):
         ("cell", F64), ("hash_bits", I32), ("n_stencil", I32), ("stencil", P),
         ("n_samples", I32), ("_pad1", I32), ("samples", P), ("r_off", P), ("r_off2", P),
         ("gamma", P), ("w_int", P), ("quantum", F64), ("delta_r", F64), ("four_pi", F64),
-        ("reach_pad", F64), ("solv_atoms", P), ("n_solv", I32), ("precision", I32)]
+        ("reach_pad", F64), ("solv_atoms", P), ("n_solv", I32), ("precision", I32),
+        ("samples_grp", P), ("grp_cone", P), ("n_groups", I32), ("_pad2", I32)]
 
 
 class KfStatus(C.Structure):
@@ -58,7 +59,7 @@ class KfBatch(C.Structure):
             "occ", "occ_count", "occ_offset", "chunk_pre", "chunk_count", "chunk_offset",
             "atom_slot", "atom_rank", "sorted_atom", "s_hi", "s_lo",
             "s_pos", "s_par", "s_aux", "s_tree", "cell_box", "work", "e_atom", "pair_count",
-            "solv_acc", "cav_atom", "f_exp", "a_exp", "wrench", "side_tot", "bb_suffix", "tau", "energy", "status",
+            "solv_acc", "solv_ovf", "cav_atom", "f_exp", "a_exp", "wrench", "side_tot", "bb_suffix", "tau", "energy", "status",
             "rec_energy", "rec_theta")]
 
 

@@ -179,9 +179,11 @@ int kf_fold_iterations_eager(const kf_chain_t *c, const kf_field_t *f, kf_batch_
 }
 
 int kf_kernels_per_iteration(int solvation) {
-    // fk: scan + positions; bin: count, scan, scatter, finalize; pairs; wrench; torque
-    // (+ solvation: hot kernel, combine).  Memsets are not counted.
-    return 9 + (solvation ? 2 : 0);
+    // fk: scan + positions; bin: insert, cell scan, work prefix, scatter, finalize;
+    // pairs; wrench; torque (+ solvation: primary pass, overflow pass, combine).
+    // Memsets are not counted; chains past one FK segment (2048 backbone links)
+    // add the segmented-scan launches.
+    return 10 + (solvation ? 3 : 0);
 }
 
 int kf_clash_report(const kf_field_t *f, kf_batch_t *w, void *stream) {

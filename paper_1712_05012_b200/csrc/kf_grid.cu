@@ -223,7 +223,7 @@ bin_finalize_kernel(kf_field_t f, int B, int n, const double *__restrict__ pos,
         const int a = ids[k];
         const size_t ga = (size_t)b * n + a, gs = (size_t)b * n + s0 + k;
         const double x = pos[3 * ga], y = pos[3 * ga + 1], z = pos[3 * ga + 2];
-        s_pos[gs] = make_double4(x, y, z, 0.0);
+        s_pos[gs] = make_double4(x, y, z, f.solvation ? f.r_off[a] : 0.0);   // w: R_off (solvation gather)
         // offset from the cell centre as an fp32 pair: hi + lo == the fp64 offset
         // to ~1e-14 A, so fp32 arithmetic on them recovers fp64-accurate
         // difference vectors without absolute coordinates

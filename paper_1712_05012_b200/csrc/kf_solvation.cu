@@ -16,11 +16,16 @@
 // so the scan stops at the second cover) and immediately runs step 2 for
 // that sample; neighbour-side events go to per-slot shared int64 counters
 // flushed once to global memory, the atom's own to a block reduction.
+#include <cstdlib>
+
 #include "kf_common.cuh"
 
 namespace {
 
 constexpr int SOLV_THREADS = 256;
+#ifndef SOLV_GROUP_THREADS
+#define SOLV_GROUP_THREADS 128
+#endif
 
 struct NbSlot { double x, y, z, r2; };
 
@@ -230,40 +235,99 @@ size_t set_smem(int cap) {
                         sizeof(int32_t) + sizeof(unsigned short));
 }
 
-// Hot path: neighbours come from the spatial hash of this iteration.
-__global__ void __launch_bounds__(SOLV_THREADS)
-solv_hot_kernel(kf_field_t f, int n, int n_solv, const int32_t *__restrict__ solv_atoms,
-                const double *__restrict__ pos_all, const unsigned long long *__restrict__ keys,
-                const int32_t *__restrict__ cnt, const int32_t *__restrict__ start,
-                const int32_t *__restrict__ atom_slot, const double4 *__restrict__ s_pos,
-                const int4 *__restrict__ s_aux, long long *__restrict__ solv_acc,
-                double *__restrict__ cav_atom, double *__restrict__ f_exp_out,
-                double *__restrict__ a_exp_out, int nb_cap, kf_status_t *status) {
-    const int b = blockIdx.x / n_solv;
-    const int i = solv_atoms[blockIdx.x % n_solv];
+// ---- hot path ---------------------------------------------------------------
+//
+// Sample groups: the host orders the N sample directions into G groups of (at
+// most) 32 that are compact on the sphere (recursive bisection), each with a
+// bounding cone (axis a_g, half-angle alpha_g).  A neighbour whose enlarged cap
+// (q.u >= c2, which contains the plain cap c1) misses a group's cone can neither
+// cover nor, displaced by dr, newly cover any of its samples, so each group
+// only visits the neighbours in its candidate bitmask.  One warp owns one group
+// at a time, lane = sample: every lane walks the same candidate list (largest
+// caps first), so the loop is warp-uniform and the warp leaves as soon as all
+// its samples are covered twice.  Coverage and force arithmetic are the
+// reference's fp64 operations (see above); results are bit-identical.
+struct GroupSmem {
+    NbSlot *nb;        // [cap] sorted: largest cap first
+    float4 *cap;       // [cap] u, c1 - margin
+    float *c2;         // [cap] c2 - margin
+    int32_t *atom;     // [cap]
+    // staging (aliases acc + masks): unsorted neighbours and their sort keys
+    NbSlot *tmp;
+    int32_t *tmp_atom;
+    float *key;
+    long long *acc;    // [3 cap] neighbour-side fixed-point events
+    uint32_t *mask;    // [G][cap / 32] candidate bitmasks
+};
+
+KF_DEV GroupSmem carve_group(unsigned char *smem, int cap) {
+    GroupSmem S;
+    S.nb = reinterpret_cast<NbSlot *>(smem);
+    S.cap = reinterpret_cast<float4 *>(S.nb + cap);
+    S.c2 = reinterpret_cast<float *>(S.cap + cap);
+    S.atom = reinterpret_cast<int32_t *>(S.c2 + cap);
+    unsigned char *r1 = reinterpret_cast<unsigned char *>(S.atom + cap);
+    S.tmp = reinterpret_cast<NbSlot *>(r1);
+    S.tmp_atom = reinterpret_cast<int32_t *>(S.tmp + cap);
+    S.key = reinterpret_cast<float *>(S.tmp_atom + cap);
+    S.acc = reinterpret_cast<long long *>(r1);
+    S.mask = reinterpret_cast<uint32_t *>(S.acc + 3 * cap);
+    return S;
+}
+
+size_t group_smem(int cap, int G) {
+    const size_t base = (size_t)cap * (sizeof(NbSlot) + sizeof(float4) + sizeof(float) + sizeof(int32_t));
+    const size_t stage = (size_t)cap * (sizeof(NbSlot) + sizeof(int32_t) + sizeof(float));
+    const size_t work = (size_t)cap * 3 * sizeof(long long) + (size_t)G * ((cap + 31) / 32) * sizeof(uint32_t);
+    return base + (stage > work ? stage : work);
+}
+
+struct SolvArgs {
+    int n;
+    const double *pos_all;
+    const unsigned long long *keys;
+    const int32_t *cnt, *start, *atom_slot;
+    const double4 *s_pos;
+    const int4 *s_aux;
+    long long *solv_acc;
+    double *cav_atom, *f_exp_out, *a_exp_out;
+    kf_status_t *status;
+    int32_t *ovf;          // [0]: count, then (b, i) pairs of atoms over the fast capacity
+    int ovf_cap;
+};
+
+// One atom (the whole CTA).  nb_cap = staged-neighbour capacity of this launch;
+// OVERFLOW = false: a larger count defers the atom to the overflow list;
+// OVERFLOW = true: the large-capacity pass (a larger count is an error).
+template <bool OVERFLOW>
+KF_DEV void solv_atom(const kf_field_t &f, const SolvArgs &A, int b, int i, int nb_cap) {
+    const int n = A.n;
+    const double *__restrict__ pos_all = A.pos_all;
+    const unsigned long long *__restrict__ keys = A.keys;
+    const int32_t *__restrict__ cnt = A.cnt, *__restrict__ start = A.start, *__restrict__ atom_slot = A.atom_slot;
+    const double4 *__restrict__ s_pos = A.s_pos;
+    const int4 *__restrict__ s_aux = A.s_aux;
+    kf_status_t *status = A.status;
     if (status[b].done) return;
     extern __shared__ __align__(16) unsigned char smem[];
-    long long *acc_nb;
-    const NbSet S = carve(smem, nb_cap, &acc_nb);
-    NbSlot *nb = S.nb;
-    int32_t *nb_atom = S.atom;
-    __shared__ int nn;
+    const GroupSmem S = carve_group(smem, nb_cap);
+    __shared__ int nn, next_group;
     __shared__ long long acc_i_s[3];
     __shared__ double red[32];
-    if (threadIdx.x == 0) { nn = 0; acc_i_s[0] = acc_i_s[1] = acc_i_s[2] = 0; }
+    if (threadIdx.x == 0) { nn = 0; next_group = 0; acc_i_s[0] = acc_i_s[1] = acc_i_s[2] = 0; }
     __syncthreads();
 
     const size_t ai = (size_t)b * n + i;
     const double xi[3] = {pos_all[3 * ai], pos_all[3 * ai + 1], pos_all[3 * ai + 2]};
-    const double r_off_i = f.r_off[i];
+    const double r_i = f.r_off[i];
     const uint32_t H = 1u << f.hash_bits;
     const size_t hb = (size_t)b * H, nbase = (size_t)b * n;
     int cx, cy, cz;
     unpack_cell((long long)keys[hb + atom_slot[ai]], cx, cy, cz);
 
-    // gather: probe the stencil cells (one thread each), then sweep all their
-    // members with every thread of the block
-    __shared__ int cell_first[32], cell_len[32], cell_pre[33];
+    // ---- gather the reachable neighbours (stencil cells probed by one warp,
+    // their members swept by the whole block) into the staging area
+    __shared__ int cell_first[32], cell_pre[33];
     if (threadIdx.x < 32) {
         int first = 0, len = 0;
         if ((int)threadIdx.x < f.n_stencil) {
@@ -273,7 +337,6 @@ solv_hot_kernel(kf_field_t f, int n, int n_solv, const int32_t *__restrict__ sol
             if (js >= 0) { first = start[hb + js]; len = cnt[hb + js]; }
         }
         cell_first[threadIdx.x] = first;
-        cell_len[threadIdx.x] = len;
         int incl = len;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -296,44 +359,172 @@ solv_hot_kernel(kf_field_t f, int n, int n_solv, const int32_t *__restrict__ sol
         const int j = s_aux[nbase + kk].x;
         if (j == i) continue;
         const double dx = xi[0] - pj.x, dy = xi[1] - pj.y, dz = xi[2] - pj.z;
-        const double lim = r_off_i + f.r_off[j] + f.reach_pad;
-        if (dx * dx + dy * dy + dz * dz > lim * lim) continue;
+        const double lim = r_i + pj.w + f.reach_pad;           // pj.w = R_off_j
+        const double d2 = dx * dx + dy * dy + dz * dz;
+        if (d2 > lim * lim) continue;
         const int slot = atomicAdd(&nn, 1);
         if (slot < nb_cap) {
-            nb[slot] = NbSlot{pj.x, pj.y, pj.z, f.r_off2[j]};
-            nb_atom[slot] = j;
+            const double r2j = xmul(pj.w, pj.w);                 // = r_off2[j] (host R_off * R_off)
+            S.tmp[slot] = NbSlot{pj.x, pj.y, pj.z, r2j};
+            S.tmp_atom[slot] = j;
+            // sort key c1 (smaller = larger cap); -3 for a coincident atom
+            const double d = sqrt(d2);
+            S.key[slot] = d > 1e-6 ? (float)((r_i * r_i + d2 - r2j) / (2.0 * r_i * d)) : -3.f;
         }
     }
     __syncthreads();
     const int count = nn;
     if (count > nb_cap) {
         if (threadIdx.x == 0) {
-            atomicMax(&status[b].overflow, count);
-            if (atomicCAS(&status[b].error, KF_ERR_NONE, KF_ERR_CAPACITY) == KF_ERR_NONE)
-                status[b].err_iter = status[b].iter;
+            const int e = OVERFLOW ? A.ovf_cap : atomicAdd(A.ovf, 1);
+            if (e < A.ovf_cap) {
+                A.ovf[1 + 2 * e] = b;
+                A.ovf[2 + 2 * e] = i;
+            } else {
+                atomicMax(&status[b].overflow, count);
+                if (atomicCAS(&status[b].error, KF_ERR_NONE, KF_ERR_CAPACITY) == KF_ERR_NONE)
+                    status[b].err_iter = status[b].iter;
+            }
         }
         return;
     }
-    prepare_neighbors(xi, r_off_i, count, f.delta_r, S);
-    for (int m = threadIdx.x; m < 3 * count; m += blockDim.x) acc_nb[m] = 0;
+    // ---- rank sort (largest cap first; ties by arrival) and the caps in sorted order
+    const double dr = f.delta_r;
+    for (int m = threadIdx.x; m < count; m += blockDim.x) {
+        const float km = S.key[m];
+        int r = 0;
+        for (int t = 0; t < count; ++t) {
+            const float kt = S.key[t];
+            r += (kt < km) || (kt == km && t < m);
+        }
+        const NbSlot q = S.tmp[m];
+        S.nb[r] = q;
+        S.atom[r] = S.tmp_atom[m];
+        const double dx = q.x - xi[0], dy = q.y - xi[1], dz = q.z - xi[2];
+        const double d2 = dx * dx + dy * dy + dz * dz;
+        const double d = sqrt(d2);
+        if (d > 1e-6) {
+            const double inv = 1.0 / d, rj = sqrt(q.r2);
+            const double c1 = (r_i * r_i + d2 - q.r2) / (2.0 * r_i * d);
+            S.cap[r] = make_float4((float)(dx * inv), (float)(dy * inv), (float)(dz * inv), (float)c1 - CAP_MARGIN);
+            S.c2[r] = (float)((r_i * r_i + d2 - (rj + dr) * (rj + dr)) / (2.0 * r_i * d)) - CAP_MARGIN;
+        } else {
+            S.cap[r] = make_float4(0.f, 0.f, 0.f, -3.f);
+            S.c2[r] = -3.f;
+        }
+    }
+    __syncthreads();
+    // ---- candidate bitmasks: group cone vs enlarged cap
+    const int G = f.n_groups, W = (count + 31) >> 5;
+    {
+        // lane = neighbour of word w (its cap in registers), warps sweep the groups
+        const int lane = threadIdx.x & 31;
+        for (int w = 0; w < W; ++w) {
+            const int m = (w << 5) + lane;
+            float4 cp = make_float4(0.f, 0.f, 0.f, 0.f);
+            float cb = 1.f, sb = 0.f;
+            bool live = m < count;
+            if (live) {
+                cp = S.cap[m];
+                cb = fminf(fmaxf(S.c2[m], -1.f), 1.f);
+                sb = sqrtf(fmaxf(0.f, 1.f - cb * cb));
+            }
+            for (int g = threadIdx.x >> 5; g < G; g += blockDim.x >> 5) {
+                const float4 ax = reinterpret_cast<const float4 *>(f.grp_cone)[2 * g];
+                const float sin_a = f.grp_cone[8 * g + 4];
+                // cone (a_g, alpha) meets the enlarged cap (u, beta): angle(a, u) <= alpha + beta
+                const bool keep = live && (cb <= -ax.w ||
+                                           ax.x * cp.x + ax.y * cp.y + ax.z * cp.z >= ax.w * cb - sin_a * sb - 1e-3f);
+                const uint32_t bits = __ballot_sync(0xffffffffu, keep);
+                if (lane == 0) S.mask[g * W + w] = bits;
+            }
+        }
+    }
+#ifdef SOLV_SETUP_ONLY
+    return;
+#endif
+    for (int m = threadIdx.x; m < 3 * count; m += blockDim.x) S.acc[m] = 0;
     __syncthreads();
 
-    long long acc_i[3] = {0, 0, 0};
+    // ---- one warp per sample group, lane = sample
+    const int lane = threadIdx.x & 31;
     const long long wi = f.w_int[i];
-    const int covered = enumerate_samples<true>(xi, r_off_i, f.samples, f.n_samples, S, count, wi,
-                                                f.delta_r, acc_nb, acc_i, nullptr, nullptr);
+    long long acc_i[3] = {0, 0, 0};
+    int covered = 0;
+    for (;;) {
+        // groups are taken from a block counter: warps that meet cheap
+        // (buried) groups take more of them
+        int g = 0;
+        if (lane == 0) g = atomicAdd(&next_group, 1);
+        g = __shfl_sync(0xffffffffu, g, 0);
+        if (g >= G) break;
+        const bool valid = lane < (int)f.grp_cone[8 * g + 5];
+        const double *q = f.samples_grp + 3 * (32 * g + (valid ? lane : 0));
+        const float qx = (float)q[0], qy = (float)q[1], qz = (float)q[2];
+        double px, py, pz;
+        sample_point(xi, r_i, q, px, py, pz);
+        int cnt = valid ? 0 : 2, crit = -1;
+        const uint32_t *gm = S.mask + g * W;
+        for (int w = 0; w < W; ++w) {
+            uint32_t bits = gm[w];
+            while (bits) {
+                const int m = (w << 5) + __ffs(bits) - 1;
+                bits &= bits - 1u;
+                if (cnt < 2) {
+                    const float4 cp = S.cap[m];
+                    if (qx * cp.x + qy * cp.y + qz * cp.z >= cp.w && covers(px, py, pz, S.nb[m])) {
+                        crit = m;
+                        ++cnt;
+                    }
+                }
+            }
+            if (__all_sync(0xffffffffu, cnt >= 2)) break;
+        }
+        if (valid) covered += cnt > 0;
+        if (wi == 0 || !valid) continue;
+        if (cnt == 0) {
+            // exposed: every candidate displaced along each axis (solvation.py:224-235)
+            for (int w = 0; w < W; ++w) {
+                uint32_t bits = gm[w];
+                while (bits) {
+                    const int m = (w << 5) + __ffs(bits) - 1;
+                    bits &= bits - 1u;
+                    const float4 cp = S.cap[m];
+                    if (qx * cp.x + qy * cp.y + qz * cp.z < S.c2[m]) continue;
+                    const NbSlot nbm = S.nb[m];
+                    for (int s = 0; s < 3; ++s) {
+                        if (covers_shifted(px, py, pz, nbm, s, dr)) {
+                            atomicAdd(reinterpret_cast<unsigned long long *>(&S.acc[3 * m + s]),
+                                      (unsigned long long)wi);
+                            acc_i[s] -= wi;
+                        }
+                    }
+                }
+            }
+        } else if (cnt == 1) {
+            // critical: only the recorded coverer, displaced (solvation.py:236-245)
+            const NbSlot nbc = S.nb[crit];
+            for (int s = 0; s < 3; ++s) {
+                if (!covers_shifted(px, py, pz, nbc, s, dr)) {
+                    acc_i[s] += wi;
+                    atomicAdd(reinterpret_cast<unsigned long long *>(&S.acc[3 * crit + s]),
+                              (unsigned long long)(-wi));
+                }
+            }
+        }
+    }
     const double cov_total = block_sum((double)covered, red);
     for (int s = 0; s < 3; ++s) {
         const long long v = warp_sum_ll(acc_i[s]);
-        if ((threadIdx.x & 31) == 0 && v != 0)
+        if (lane == 0 && v != 0)
             atomicAdd(reinterpret_cast<unsigned long long *>(&acc_i_s[s]), (unsigned long long)v);
     }
     __syncthreads();
-    long long *acc = solv_acc + (size_t)b * n * 3;
+    long long *acc = A.solv_acc + (size_t)b * n * 3;
     for (int m = threadIdx.x; m < 3 * count; m += blockDim.x) {
-        const long long v = acc_nb[m];
+        const long long v = S.acc[m];
         if (v != 0)
-            atomicAdd(reinterpret_cast<unsigned long long *>(&acc[3 * (size_t)nb_atom[m / 3] + m % 3]),
+            atomicAdd(reinterpret_cast<unsigned long long *>(&acc[3 * (size_t)S.atom[m / 3] + m % 3]),
                       (unsigned long long)v);
     }
     if (threadIdx.x == 0) {
@@ -345,8 +536,29 @@ solv_hot_kernel(kf_field_t f, int n, int n_solv, const int32_t *__restrict__ sol
         const long long cov = (long long)cov_total;
         const double f_exp = (double)(f.n_samples - cov) / (double)f.n_samples;
         const double a_exp = xmul(f_exp, xmul(f.four_pi, f.r_off2[i]));
-        cav_atom[ai] = xmul(f.gamma[i], a_exp);
-        if (f_exp_out) { f_exp_out[ai] = f_exp; a_exp_out[ai] = a_exp; }
+        A.cav_atom[ai] = xmul(f.gamma[i], a_exp);
+        if (A.f_exp_out) { A.f_exp_out[ai] = f_exp; A.a_exp_out[ai] = a_exp; }
+    }
+}
+
+#ifndef SOLV_FAST_CAP
+#define SOLV_FAST_CAP 256
+#endif
+
+// Primary pass: one CTA per (trajectory, solvation atom) with a small staging
+// capacity (more CTAs per SM); the rare atom with more reachable neighbours is
+// deferred to solv_overflow_kernel.
+__global__ void __launch_bounds__(SOLV_GROUP_THREADS)
+solv_group_kernel(const __grid_constant__ kf_field_t f, const SolvArgs A, int n_solv, const int32_t *__restrict__ solv_atoms) {
+    solv_atom<false>(f, A, blockIdx.x / n_solv, solv_atoms[blockIdx.x % n_solv], SOLV_FAST_CAP);
+}
+
+__global__ void __launch_bounds__(SOLV_GROUP_THREADS)
+solv_overflow_kernel(const __grid_constant__ kf_field_t f, const SolvArgs A, int nb_cap) {
+    const int m = min(*A.ovf, A.ovf_cap);
+    for (int e = blockIdx.x; e < m; e += gridDim.x) {
+        solv_atom<true>(f, A, A.ovf[1 + 2 * e], A.ovf[2 + 2 * e], nb_cap);
+        __syncthreads();
     }
 }
 
@@ -510,17 +722,37 @@ int kf_solvation_launch(const kf_field_t *f, kf_batch_t *w, int n, int n_solv, c
     const int B = w->B;
     KF_CUDA(cudaMemsetAsync(w->solv_acc, 0, sizeof(long long) * (size_t)B * n * 3, s), "memset solv_acc");
     if (n_solv > 0) {
-        const size_t smem = set_smem(w->nb_cap);
-        static size_t opted = 0;
-        if (smem > 48 * 1024 && smem > opted) {
-            KF_CUDA(cudaFuncSetAttribute(solv_hot_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+        SolvArgs A;
+        A.n = n; A.pos_all = w->pos; A.keys = w->cell_key; A.cnt = w->cell_cnt; A.start = w->cell_start;
+        A.atom_slot = w->atom_slot; A.s_pos = reinterpret_cast<const double4 *>(w->s_pos);
+        A.s_aux = reinterpret_cast<const int4 *>(w->s_aux); A.solv_acc = w->solv_acc; A.cav_atom = w->cav_atom;
+        A.f_exp_out = w->f_exp; A.a_exp_out = w->a_exp; A.status = w->status;
+        A.ovf = w->solv_ovf; A.ovf_cap = B * n;
+        KF_CUDA(cudaMemsetAsync(w->solv_ovf, 0, sizeof(int32_t), s), "memset solv_ovf");
+        const size_t smem = group_smem(SOLV_FAST_CAP, f->n_groups);
+        const size_t smem_ovf = group_smem(w->nb_cap, f->n_groups);
+        static size_t opted = 0, opted_ovf = 0;
+        if (smem > opted) {   // dynamic + static shared memory may pass the 48 KB default
+            KF_CUDA(cudaFuncSetAttribute(solv_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                     "smem attr");
             opted = smem;
         }
-        solv_hot_kernel<<<(unsigned)((long long)B * n_solv), SOLV_THREADS, smem, s>>>(
-            *f, n, n_solv, solv_atoms, w->pos, w->cell_key, w->cell_cnt, w->cell_start, w->atom_slot,
-            reinterpret_cast<const double4 *>(w->s_pos), reinterpret_cast<const int4 *>(w->s_aux), w->solv_acc, w->cav_atom, w->f_exp, w->a_exp, w->nb_cap, w->status);
-        KF_LAUNCH_CHECK("solv_hot_kernel");
+        if (smem_ovf > opted_ovf) {
+            KF_CUDA(cudaFuncSetAttribute(solv_overflow_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem_ovf), "smem attr");
+            opted_ovf = smem_ovf;
+        }
+        solv_group_kernel<<<(unsigned)((long long)B * n_solv), SOLV_GROUP_THREADS, smem, s>>>(*f, A, n_solv, solv_atoms);
+        KF_LAUNCH_CHECK("solv_group_kernel");
+        static int ovf_grid = 0;
+        if (ovf_grid == 0) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&ovf_grid, cudaDevAttrMultiProcessorCount, dev);
+            ovf_grid *= 2;
+        }
+        solv_overflow_kernel<<<ovf_grid, SOLV_GROUP_THREADS, smem_ovf, s>>>(*f, A, w->nb_cap);
+        KF_LAUNCH_CHECK("solv_overflow_kernel");
     }
     const long long total = (long long)B * n * 3;
     solv_combine_kernel<<<kf_blocks(total, 256), 256, 0, s>>>(B, n, f->quantum, w->solv_acc, w->forces, w->status);

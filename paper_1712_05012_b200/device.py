@@ -27,7 +27,7 @@ import torch
 from . import _native as N
 from .errors import (ConfigurationError, NativeLibraryError, StericClashError)
 from .forcefield import MIN_DISTANCE, EnergyBreakdown
-from .solvation import ExposureStates, SasaResult, check_cav_cutoff, force_quantum
+from .solvation import ExposureStates, SasaResult, check_cav_cutoff, force_quantum, sample_groups
 
 _streams: dict = {}
 _precision = {"pair": os.environ.get("KFB200_PAIR_PRECISION", "fp32")}
@@ -373,6 +373,13 @@ class DeviceField(ParamTables):
                      solv_nz=_up(np.flatnonzero(gamma != 0.0), np.int32),
                      solv_all=_up(np.arange(n), np.int32))
             s.n_samples = sphere.n
+            groups, cones = sample_groups(sphere.points)
+            grp = np.zeros((len(groups), 32, 3))
+            for g, ix in enumerate(groups):
+                grp[g, :len(ix)] = np.asarray(sphere.points, float)[ix]
+            t.update(samples_grp=_up(grp, np.float64), grp_cone=_up(cones, np.float32))
+            s.samples_grp, s.grp_cone = t["samples_grp"].data_ptr(), t["grp_cone"].data_ptr()
+            s.n_groups = len(groups)
             s.quantum, s.delta_r, s.four_pi = float(quantum), float(scfg.delta_r), 4.0 * math.pi
             for name in ("samples", "r_off", "r_off2", "gamma", "w_int"):
                 setattr(s, name, t[name].data_ptr())
@@ -427,8 +434,10 @@ class Batch:
 
     def __init__(self, dc: DeviceChain | None, df: DeviceField | None, B: int, *,
                  max_records: int = 0, record_theta: bool = False, store_sasa: bool = False,
-                 nb_cap: int = 512):
+                 nb_cap: int | None = None):
         dev = _device()
+        if nb_cap is None:
+            nb_cap = int(os.environ.get("KFB200_SOLV_NB_CAP", "512"))
         n = dc.n_atoms if dc is not None else df.n
         L = dc.n_links if dc is not None else 1
         D = dc.n_dof if dc is not None else 0
@@ -452,7 +461,7 @@ class Batch:
                 s_tree=z(B, n, 4, dtype=i32), cell_box=z(B, H, 8, dtype=torch.float32),
                 work=z(4, dtype=i32),
                 e_atom=z(B, n, 2), pair_count=z(B, n, dtype=torch.int64),
-                solv_acc=z(B, n, 3, dtype=torch.int64), cav_atom=z(B, n),
+                solv_acc=z(B, n, 3, dtype=torch.int64), solv_ovf=z(1 + 2 * B * n, dtype=i32), cav_atom=z(B, n),
                 f_exp=z(B, n) if store_sasa else None, a_exp=z(B, n) if store_sasa else None,
                 wrench=z(B, L, 6), side_tot=z(B, max(R, 1), 6), bb_suffix=z(B, max(nbb, 1), 6),
                 tau=z(B, max(D, 1)), energy=z(B, 3),

@@ -116,6 +116,59 @@ def force_quantum(params, r_off: np.ndarray, nq: int, delta_r: float):
     return np.round(delta / quantum).astype(np.int64), quantum
 
 
+def sample_groups(points: np.ndarray, size: int = 32):
+    """Order the sample directions into compact groups of <= `size` for the hot
+    solvation kernel (one warp per group, lane = sample).
+
+    Recursive bisection: each split sorts the set along one of 12 directions in
+    the plane of its two principal axes, cuts at a multiple of `size`, and keeps
+    the direction whose halves have the smaller angular radius.  Returns
+    (groups: list of index arrays, cones: float32 [G, 8] = axis xyz, cos alpha,
+    sin alpha, count, 0, 0), alpha bounding every member's angle to the axis.
+    Coverage results do not depend on the sample order, so
+    this is a pure scheduling choice."""
+    pts = np.asarray(points, float)
+
+    def radius(ix):
+        a = pts[ix].mean(axis=0)
+        a = a / max(float(np.linalg.norm(a)), 1e-12)
+        return float(np.arccos(np.clip((pts[ix] @ a).min(), -1.0, 1.0)))
+
+    groups = []
+
+    def split(ix):
+        if len(ix) <= size:
+            groups.append(ix)
+            return
+        c = pts[ix] - pts[ix].mean(axis=0)
+        v = np.linalg.svd(c, full_matrices=False)[2]
+        half = ((len(ix) + size - 1) // size + 1) // 2 * size
+        best = None
+        for ang in np.linspace(0.0, np.pi, 12, endpoint=False):
+            order = ix[np.argsort(c @ (np.cos(ang) * v[0] + np.sin(ang) * v[1]), kind="stable")]
+            cost = max(radius(order[:half]), radius(order[half:]))
+            if best is None or cost < best[0]:
+                best = (cost, order)
+        split(best[1][:half])
+        split(best[1][half:])
+
+    split(np.arange(len(pts)))
+    cones = np.zeros((len(groups), 8), np.float32)
+    for g, ix in enumerate(groups):
+        a = pts[ix].mean(axis=0)
+        norm = float(np.linalg.norm(a))
+        if norm < 1e-6:                      # a group spread over the whole sphere
+            a, ca = np.array([1.0, 0.0, 0.0]), -1.0
+        else:
+            a = a / norm
+            ca = max(-1.0, float((pts[ix] @ a).min()) - 1e-6)
+        cones[g, :3] = a
+        cones[g, 3] = ca
+        cones[g, 4] = math.sqrt(max(0.0, 1.0 - ca * ca))
+        cones[g, 5] = len(ix)
+    return groups, cones
+
+
 def sasa_pass(positions, params, neighbors, sphere: SampleSphere,
               config: SolvationConfig = SolvationConfig()):
     from . import device

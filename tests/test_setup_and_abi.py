@@ -126,3 +126,18 @@ def test_hot_path_has_no_cpu_fallback():
         fld.evaluate(np.zeros((ch.n_atoms, 3)) + np.arange(ch.n_atoms)[:, None])
     with pytest.raises(P.NativeLibraryError):
         P.fold(ch, ch.conf_zp(), fld, P.StepConfig(max_iters=2))
+
+
+@pytest.mark.parametrize("n", [12, 100, 1024, 4096])
+def test_sample_groups_partition_and_cones(n):
+    """Hot-path sample groups (solvation.sample_groups): every sample in exactly
+    one group of <= 32, and each group's cone bounds all its members."""
+    from paper_1712_05012_b200 import solvation as S
+    pts = np.asarray(S.generate_samples(n).points)
+    groups, cones = S.sample_groups(pts)
+    assert np.array_equal(np.sort(np.concatenate(groups)), np.arange(n))
+    assert all(0 < len(ix) <= 32 for ix in groups)
+    for g, ix in enumerate(groups):
+        assert cones[g, 5] == len(ix)
+        assert np.all(pts[ix] @ cones[g, :3].astype(float) >= cones[g, 3] - 1e-6)
+        assert abs(cones[g, 3] ** 2 + cones[g, 4] ** 2 - 1.0) < 1e-5
