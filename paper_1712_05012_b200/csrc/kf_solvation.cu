@@ -258,9 +258,10 @@ struct GroupSmem {
     float *key;
     long long *acc;    // [3 cap] neighbour-side fixed-point events
     uint32_t *mask;    // [G][cap / 32] candidate bitmasks
+    uint32_t *full;    // [G][cap / 32] neighbours covering every sample of the group
 };
 
-KF_DEV GroupSmem carve_group(unsigned char *smem, int cap) {
+KF_DEV GroupSmem carve_group(unsigned char *smem, int cap, int G) {
     GroupSmem S;
     S.nb = reinterpret_cast<NbSlot *>(smem);
     S.cap = reinterpret_cast<float4 *>(S.nb + cap);
@@ -272,13 +273,14 @@ KF_DEV GroupSmem carve_group(unsigned char *smem, int cap) {
     S.key = reinterpret_cast<float *>(S.tmp_atom + cap);
     S.acc = reinterpret_cast<long long *>(r1);
     S.mask = reinterpret_cast<uint32_t *>(S.acc + 3 * cap);
+    S.full = S.mask + (size_t)G * ((cap + 31) / 32);
     return S;
 }
 
 size_t group_smem(int cap, int G) {
     const size_t base = (size_t)cap * (sizeof(NbSlot) + sizeof(float4) + sizeof(float) + sizeof(int32_t));
     const size_t stage = (size_t)cap * (sizeof(NbSlot) + sizeof(int32_t) + sizeof(float));
-    const size_t work = (size_t)cap * 3 * sizeof(long long) + (size_t)G * ((cap + 31) / 32) * sizeof(uint32_t);
+    const size_t work = (size_t)cap * 3 * sizeof(long long) + 2 * (size_t)G * ((cap + 31) / 32) * sizeof(uint32_t);
     return base + (stage > work ? stage : work);
 }
 
@@ -310,7 +312,7 @@ KF_DEV void solv_atom(const kf_field_t &f, const SolvArgs &A, int b, int i, int 
     kf_status_t *status = A.status;
     if (status[b].done) return;
     extern __shared__ __align__(16) unsigned char smem[];
-    const GroupSmem S = carve_group(smem, nb_cap);
+    const GroupSmem S = carve_group(smem, nb_cap, f.n_groups);
     __shared__ int nn, next_group;
     __shared__ long long acc_i_s[3];
     __shared__ double red[32];
@@ -348,28 +350,44 @@ KF_DEV void solv_atom(const kf_field_t &f, const SolvArgs &A, int b, int i, int 
     }
     __syncthreads();
     const int cand = cell_pre[32];
-    for (int c = threadIdx.x; c < cand; c += blockDim.x) {
-        int lo = 0, hi = 32;
-        while (hi - lo > 1) {
-            const int mid = (lo + hi) >> 1;
-            if (cell_pre[mid] <= c) lo = mid; else hi = mid;
+    constexpr int GATHER_UNROLL = 4;   // candidates in flight per thread (independent loads)
+    const float r_i_f = (float)r_i;
+    for (int c0 = threadIdx.x; c0 < cand; c0 += GATHER_UNROLL * blockDim.x) {
+        double4 pjs[GATHER_UNROLL];
+        int js[GATHER_UNROLL];
+#pragma unroll
+        for (int u = 0; u < GATHER_UNROLL; ++u) {
+            const int c = c0 + u * blockDim.x;
+            js[u] = -1;
+            if (c < cand) {
+                int lo = 0, hi = 32;
+                while (hi - lo > 1) {
+                    const int mid = (lo + hi) >> 1;
+                    if (cell_pre[mid] <= c) lo = mid; else hi = mid;
+                }
+                const int kk = cell_first[lo] + (c - cell_pre[lo]);
+                pjs[u] = s_pos[nbase + kk];
+                js[u] = s_aux[nbase + kk].x;
+            }
         }
-        const int kk = cell_first[lo] + (c - cell_pre[lo]);
-        const double4 pj = s_pos[nbase + kk];
-        const int j = s_aux[nbase + kk].x;
-        if (j == i) continue;
-        const double dx = xi[0] - pj.x, dy = xi[1] - pj.y, dz = xi[2] - pj.z;
-        const double lim = r_i + pj.w + f.reach_pad;           // pj.w = R_off_j
-        const double d2 = dx * dx + dy * dy + dz * dz;
-        if (d2 > lim * lim) continue;
-        const int slot = atomicAdd(&nn, 1);
-        if (slot < nb_cap) {
-            const double r2j = xmul(pj.w, pj.w);                 // = r_off2[j] (host R_off * R_off)
-            S.tmp[slot] = NbSlot{pj.x, pj.y, pj.z, r2j};
-            S.tmp_atom[slot] = j;
-            // sort key c1 (smaller = larger cap); -3 for a coincident atom
-            const double d = sqrt(d2);
-            S.key[slot] = d > 1e-6 ? (float)((r_i * r_i + d2 - r2j) / (2.0 * r_i * d)) : -3.f;
+#pragma unroll
+        for (int u = 0; u < GATHER_UNROLL; ++u) {
+            const int j = js[u];
+            if (j < 0 || j == i) continue;
+            const double4 pj = pjs[u];
+            const double dx = xi[0] - pj.x, dy = xi[1] - pj.y, dz = xi[2] - pj.z;
+            const double lim = r_i + pj.w + f.reach_pad;           // pj.w = R_off_j
+            const double d2 = dx * dx + dy * dy + dz * dz;
+            if (d2 > lim * lim) continue;
+            const int slot = atomicAdd(&nn, 1);
+            if (slot < nb_cap) {
+                const double r2j = xmul(pj.w, pj.w);                 // = r_off2[j] (host R_off * R_off)
+                S.tmp[slot] = NbSlot{pj.x, pj.y, pj.z, r2j};
+                S.tmp_atom[slot] = j;
+                // sort key c1 (smaller = larger cap, fp32: ordering only); -3 for a coincident atom
+                const float d2f = (float)d2, df = sqrtf(d2f);
+                S.key[slot] = d2f > 1e-12f ? (r_i_f * r_i_f + d2f - (float)r2j) / (2.f * r_i_f * df) : -3.f;
+            }
         }
     }
     __syncthreads();
@@ -390,6 +408,7 @@ KF_DEV void solv_atom(const kf_field_t &f, const SolvArgs &A, int b, int i, int 
     }
     // ---- rank sort (largest cap first; ties by arrival) and the caps in sorted order
     const double dr = f.delta_r;
+    const float drf = (float)dr;
     for (int m = threadIdx.x; m < count; m += blockDim.x) {
         const float km = S.key[m];
         int r = 0;
@@ -400,14 +419,14 @@ KF_DEV void solv_atom(const kf_field_t &f, const SolvArgs &A, int b, int i, int 
         const NbSlot q = S.tmp[m];
         S.nb[r] = q;
         S.atom[r] = S.tmp_atom[m];
-        const double dx = q.x - xi[0], dy = q.y - xi[1], dz = q.z - xi[2];
-        const double d2 = dx * dx + dy * dy + dz * dz;
-        const double d = sqrt(d2);
-        if (d > 1e-6) {
-            const double inv = 1.0 / d, rj = sqrt(q.r2);
-            const double c1 = (r_i * r_i + d2 - q.r2) / (2.0 * r_i * d);
-            S.cap[r] = make_float4((float)(dx * inv), (float)(dy * inv), (float)(dz * inv), (float)c1 - CAP_MARGIN);
-            S.c2[r] = (float)((r_i * r_i + d2 - (rj + dr) * (rj + dr)) / (2.0 * r_i * d)) - CAP_MARGIN;
+        // caps in fp32: prefilters with a 1e-3 margin (fp32 error here ~1e-6)
+        const float dx = (float)(q.x - xi[0]), dy = (float)(q.y - xi[1]), dz = (float)(q.z - xi[2]);
+        const float d2 = dx * dx + dy * dy + dz * dz;
+        if (d2 > 1e-12f) {
+            const float d = sqrtf(d2), inv = 1.f / d, r2j = (float)q.r2, rj = sqrtf(r2j);
+            const float ri2 = r_i_f * r_i_f, den = 1.f / (2.f * r_i_f * d);
+            S.cap[r] = make_float4(dx * inv, dy * inv, dz * inv, (ri2 + d2 - r2j) * den - CAP_MARGIN);
+            S.c2[r] = (ri2 + d2 - (rj + drf) * (rj + drf)) * den - CAP_MARGIN;
         } else {
             S.cap[r] = make_float4(0.f, 0.f, 0.f, -3.f);
             S.c2[r] = -3.f;
@@ -422,21 +441,30 @@ KF_DEV void solv_atom(const kf_field_t &f, const SolvArgs &A, int b, int i, int 
         for (int w = 0; w < W; ++w) {
             const int m = (w << 5) + lane;
             float4 cp = make_float4(0.f, 0.f, 0.f, 0.f);
-            float cb = 1.f, sb = 0.f;
+            float cb = 1.f, sb = 0.f, cf = 2.f, sf = 0.f;
             bool live = m < count;
             if (live) {
                 cp = S.cap[m];
                 cb = fminf(fmaxf(S.c2[m], -1.f), 1.f);
                 sb = sqrtf(fmaxf(0.f, 1.f - cb * cb));
+                // full cover: the plain cap tightened by 1e-3 (cap.w is c1 - 1e-3)
+                if (cp.w > -2.f) {
+                    cf = cp.w + 2e-3f;
+                    sf = sqrtf(fmaxf(0.f, 1.f - cf * cf));
+                }
             }
             for (int g = threadIdx.x >> 5; g < G; g += blockDim.x >> 5) {
                 const float4 ax = reinterpret_cast<const float4 *>(f.grp_cone)[2 * g];
                 const float sin_a = f.grp_cone[8 * g + 4];
+                const float dot = ax.x * cp.x + ax.y * cp.y + ax.z * cp.z;
                 // cone (a_g, alpha) meets the enlarged cap (u, beta): angle(a, u) <= alpha + beta
-                const bool keep = live && (cb <= -ax.w ||
-                                           ax.x * cp.x + ax.y * cp.y + ax.z * cp.z >= ax.w * cb - sin_a * sb - 1e-3f);
+                const bool keep = live && (cb <= -ax.w || dot >= ax.w * cb - sin_a * sb - 1e-3f);
+                // cone inside the tightened plain cap (beta1 > alpha, angle(a, u) <= beta1 - alpha):
+                // every sample of the group is covered by m, exactly (margins >> rounding)
+                const bool full = live && cf < ax.w && dot >= ax.w * cf + sin_a * sf + 1e-3f;
                 const uint32_t bits = __ballot_sync(0xffffffffu, keep);
-                if (lane == 0) S.mask[g * W + w] = bits;
+                const uint32_t fbits = __ballot_sync(0xffffffffu, full);
+                if (lane == 0) { S.mask[g * W + w] = bits; S.full[g * W + w] = fbits; }
             }
         }
     }
@@ -463,10 +491,21 @@ KF_DEV void solv_atom(const kf_field_t &f, const SolvArgs &A, int b, int i, int 
         const float qx = (float)q[0], qy = (float)q[1], qz = (float)q[2];
         double px, py, pz;
         sample_point(xi, r_i, q, px, py, pz);
-        int cnt = valid ? 0 : 2, crit = -1;
-        const uint32_t *gm = S.mask + g * W;
+        const uint32_t *gm = S.mask + g * W, *gf = S.full + g * W;
+        // neighbours covering the whole group: two of them settle every sample
+        int nfull = 0, f0 = -1;
         for (int w = 0; w < W; ++w) {
-            uint32_t bits = gm[w];
+            const uint32_t fb = gf[w];
+            if (fb && f0 < 0) f0 = (w << 5) + __ffs(fb) - 1;
+            nfull += __popc(fb);
+        }
+        if (nfull >= 2) {
+            if (valid) ++covered;
+            continue;
+        }
+        int cnt = valid ? nfull : 2, crit = nfull == 1 ? f0 : -1;
+        for (int w = 0; w < W; ++w) {
+            uint32_t bits = gm[w] & ~gf[w];
             while (bits) {
                 const int m = (w << 5) + __ffs(bits) - 1;
                 bits &= bits - 1u;
