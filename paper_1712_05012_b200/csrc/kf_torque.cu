@@ -58,6 +58,62 @@ __global__ void wrench_kernel(kf_chain_t c, int B, const double *__restrict__ po
     o[0] = F0; o[1] = F1; o[2] = F2; o[3] = T0; o[4] = T1; o[5] = T2;
 }
 
+// Steps 5-6 of a fold iteration (all threads of the CTA): energies and
+// record, stop tests (kcm.py:325-350), theta record, compliance step.
+KF_DEV void finish_iteration(const kf_chain_t &c, const kf_batch_t &w, const kf_step_t &step, int b,
+                             const double *tau, double tmax, double ge, double gv, double gc, double sp,
+                             double sp5, int *stop_reason) {
+    const int D = c.n_dof;
+    kf_status_t *st = w.status + b;
+    const uint8_t *frozen = w.frozen + (size_t)b * D;
+    double *th = w.theta + (size_t)b * D;
+    // 5. record + stop tests (thread 0), theta copy (all)
+    const int it = st->iter;
+    if (threadIdx.x == 0) {
+        double *e = w.energy + 3 * (size_t)b;
+        e[0] = ge; e[1] = gv; e[2] = gc;
+        st->n_pairs = (long long)(0.5 * sp);
+        st->n_pairs_vdw = (long long)(0.5 * sp5);
+        int reason = KF_REASON_NONE;
+        if (it < w.max_records) {
+            double *rec = w.rec_energy + ((size_t)b * w.max_records + it) * 4;
+            rec[0] = ge; rec[1] = gv; rec[2] = gc; rec[3] = tmax;
+        }
+        if (it == 0) st->tau0 = tmax;
+        const double tau0 = st->tau0;
+        if (tmax == 0.0) reason = KF_REASON_TORQUE_FREE;
+        else if (step.torque_tol > 0 && tmax < step.torque_tol) reason = KF_REASON_TORQUE_TOL;
+        else if (step.torque_tol_rel > 0 && tmax < step.torque_tol_rel * tau0) reason = KF_REASON_TORQUE_TOL_REL;
+        else if (step.energy_window && it >= step.energy_window && it < w.max_records) {
+            const double *r0 = w.rec_energy + ((size_t)b * w.max_records + it) * 4;
+            const double *r1 = w.rec_energy + ((size_t)b * w.max_records + it - step.energy_window) * 4;
+            const double g0 = (r0[0] + r0[1]) + r0[2], g1 = (r1[0] + r1[1]) + r1[2];
+            if (fabs(g0 - g1) < step.energy_tol) reason = KF_REASON_PLATEAU;
+        }
+        *stop_reason = reason;
+    }
+    if (w.record_theta && it < w.max_records) {
+        double *rt = w.rec_theta + ((size_t)b * w.max_records + it) * D;
+        for (int d = threadIdx.x; d < D; d += blockDim.x) rt[d] = th[d];
+    }
+    __syncthreads();
+    const int reason = *stop_reason;
+
+    // 6. compliance step: theta' = mod(mod(theta + kappa*tau/tau_max)) on free joints
+    if (reason == KF_REASON_NONE) {
+        for (int d = threadIdx.x; d < D; d += blockDim.x) {
+            const double delta = frozen[d] ? 0.0 : __ddiv_rn(xmul(step.kappa, tau[d]), tmax);
+            th[d] = np_mod360(np_mod360(xadd(th[d], delta)));
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        st->iter = it + 1;
+        if (reason != KF_REASON_NONE) { st->done = 1; st->reason = reason; }
+        else if (it + 1 >= step.max_iters) { st->done = 1; st->reason = KF_REASON_MAX_ITERS; }
+    }
+}
+
 struct TorqueArgs {
     const double *link_T;      // [B][L][KF_XF_STRIDE]
     const double *wrench;      // [B][L][6]
@@ -168,55 +224,151 @@ torque_step_kernel(kf_chain_t c, kf_field_t f, TorqueArgs ta, kf_batch_t w, kf_s
         }
         return;
     }
-    double *th = w.theta + (size_t)b * D;
+    finish_iteration(c, w, step, b, tau, tmax, ge, gv, gc, sp, sp5, &stop_reason);
+}
 
-    // 5. record + stop tests (thread 0), theta copy (all)
-    const int it = st->iter;
-    if (threadIdx.x == 0) {
-        double *e = w.energy + 3 * (size_t)b;
-        e[0] = ge; e[1] = gv; e[2] = gc;
-        st->n_pairs = (long long)(0.5 * sp);
-        st->n_pairs_vdw = (long long)(0.5 * sp5);
-        int reason = KF_REASON_NONE;
-        if (it < w.max_records) {
-            double *rec = w.rec_energy + ((size_t)b * w.max_records + it) * 4;
-            rec[0] = ge; rec[1] = gv; rec[2] = gc; rec[3] = tmax;
-        }
-        if (it == 0) st->tau0 = tmax;
-        if (mode == 1) {
-            const double tau0 = st->tau0;
-            if (tmax == 0.0) reason = KF_REASON_TORQUE_FREE;
-            else if (step.torque_tol > 0 && tmax < step.torque_tol) reason = KF_REASON_TORQUE_TOL;
-            else if (step.torque_tol_rel > 0 && tmax < step.torque_tol_rel * tau0) reason = KF_REASON_TORQUE_TOL_REL;
-            else if (step.energy_window && it >= step.energy_window && it < w.max_records) {
-                const double *r0 = w.rec_energy + ((size_t)b * w.max_records + it) * 4;
-                const double *r1 = w.rec_energy + ((size_t)b * w.max_records + it - step.energy_window) * 4;
-                const double g0 = (r0[0] + r0[1]) + r0[2], g1 = (r1[0] + r1[1]) + r1[2];
-                if (fabs(g0 - g1) < step.energy_tol) reason = KF_REASON_PLATEAU;
+// ---- long chains: the same iteration over several CTAs per trajectory ------
+//
+// The backbone is cut into segments of TQ_SEG dofs (one CTA each).  Pass 1:
+// each CTA runs the side chains attached in its segment and the segment-local
+// blocked suffix scan; segment totals go to scratch.  Pass 2: each CTA adds the
+// totals of the later segments, projects its backbone torques and reduces a
+// partial tau_max and a slice of the energy sums.  Pass 3 (one CTA per
+// trajectory) combines the partials in segment order and finishes the
+// iteration.  scratch = fk_scratch ([B][n_seg][12]: segment total 6 |
+// partials 6), free once forward kinematics has run.
+constexpr int TQ_SEG = 2048;
+
+__global__ void __launch_bounds__(TQ_THREADS)
+torque_seg_kernel(kf_chain_t c, TorqueArgs ta, kf_batch_t w, int n_seg) {
+    const int g = blockIdx.x, b = blockIdx.y;
+    const kf_status_t *st = w.status + b;
+    if (st->done || st->error) return;
+    __shared__ double chunk[TQ_THREADS][6];
+    __shared__ double red[32];
+    const int L = c.n_links, D = c.n_dof, nb = c.n_bb;
+    const double *T = ta.link_T + (size_t)b * L * KF_XF_STRIDE;
+    const double *Wr = ta.wrench + (size_t)b * L * 6;
+    double *suf = ta.bb_suffix + (size_t)b * nb * 6;
+    double *tau = ta.tau + (size_t)b * D;
+    const uint8_t *frozen = w.frozen + (size_t)b * D;
+    const int k0 = g * TQ_SEG, k1 = min(nb, k0 + TQ_SEG);
+    const int per = (k1 - k0 + blockDim.x - 1) / blockDim.x;
+    const int lo = min(k1, k0 + (int)threadIdx.x * per), hi = min(k1, lo + per);
+    W6 acc = w6_zero();
+    double tmax = 0.0;
+    for (int k = hi - 1; k >= lo; --k) {
+        w6_add(acc, w6_load(Wr + 6 * c.bb_by_dof[k]));
+        const int r = c.bb_side_res[k];
+        if (r >= 0) {   // the residue's side chain: plain suffix in chi order (kcm.py:209-225)
+            W6 agg = w6_zero();
+            for (int e = c.chi_res_off[r + 1] - 1; e >= c.chi_res_off[r]; --e) {
+                const int l = c.chi_links[e];
+                w6_add(agg, w6_load(Wr + 6 * l));
+                const int d = c.link_dof[l];
+                const double t = project(T + KF_XF_STRIDE * l, agg);
+                tau[d] = t;
+                if (!frozen[d]) tmax = fmax(tmax, fabs(t));
             }
+            w6_add(acc, agg);
         }
-        stop_reason = reason;
+        w6_store(suf + 6 * k, acc);
     }
-    if (w.record_theta && it < w.max_records) {
-        double *rt = w.rec_theta + ((size_t)b * w.max_records + it) * D;
-        for (int d = threadIdx.x; d < D; d += blockDim.x) rt[d] = th[d];
-    }
+    for (int q = 0; q < 3; ++q) { chunk[threadIdx.x][q] = acc.f[q]; chunk[threadIdx.x][3 + q] = acc.t[q]; }
     __syncthreads();
-    const int reason = stop_reason;
-
-    // 6. compliance step: theta' = mod(mod(theta + kappa*tau/tau_max)) on free joints
-    if (reason == KF_REASON_NONE) {
-        for (int d = threadIdx.x; d < D; d += blockDim.x) {
-            const double delta = frozen[d] ? 0.0 : __ddiv_rn(xmul(step.kappa, tau[d]), tmax);
-            th[d] = np_mod360(np_mod360(xadd(th[d], delta)));
+    for (int off = 1; off < (int)blockDim.x; off <<= 1) {
+        double v[6];
+        for (int q = 0; q < 6; ++q) v[q] = chunk[threadIdx.x][q];
+        if (threadIdx.x + off < blockDim.x)
+            for (int q = 0; q < 6; ++q) v[q] += chunk[threadIdx.x + off][q];
+        __syncthreads();
+        for (int q = 0; q < 6; ++q) chunk[threadIdx.x][q] = v[q];
+        __syncthreads();
+    }
+    if (threadIdx.x + 1 < blockDim.x) {
+        const W6 later = w6_load(chunk[threadIdx.x + 1]);
+        for (int k = lo; k < hi; ++k) {
+            W6 s6 = w6_load(suf + 6 * k);
+            w6_add(s6, later);
+            w6_store(suf + 6 * k, s6);
         }
     }
-    __syncthreads();
+    tmax = block_max(tmax, red);
+    double *sc = w.fk_scratch + ((size_t)b * n_seg + g) * 12;
     if (threadIdx.x == 0) {
-        st->iter = it + 1;
-        if (reason != KF_REASON_NONE) { st->done = 1; st->reason = reason; }
-        else if (it + 1 >= step.max_iters) { st->done = 1; st->reason = KF_REASON_MAX_ITERS; }
+        w6_store(sc, w6_load(chunk[0]));
+        sc[6] = tmax;
     }
+}
+
+__global__ void __launch_bounds__(TQ_THREADS)
+torque_seg_project_kernel(kf_chain_t c, kf_field_t f, TorqueArgs ta, kf_batch_t w, int n_seg) {
+    const int g = blockIdx.x, b = blockIdx.y;
+    const kf_status_t *st = w.status + b;
+    if (st->done || st->error) return;
+    __shared__ double red[32];
+    const int L = c.n_links, D = c.n_dof, nb = c.n_bb, n = c.n_atoms;
+    const double *T = ta.link_T + (size_t)b * L * KF_XF_STRIDE;
+    const double *suf = ta.bb_suffix + (size_t)b * nb * 6;
+    double *tau = ta.tau + (size_t)b * D;
+    const uint8_t *frozen = w.frozen + (size_t)b * D;
+    double *sc = w.fk_scratch + (size_t)b * n_seg * 12;
+    W6 later = w6_zero();
+    for (int h = n_seg - 1; h > g; --h) w6_add(later, w6_load(sc + 12 * h));
+    const int k0 = g * TQ_SEG, k1 = min(nb, k0 + TQ_SEG);
+    double tmax = 0.0;
+    for (int k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
+        const int l = c.bb_by_dof[k];
+        W6 s6 = w6_load(suf + 6 * k);
+        w6_add(s6, later);
+        const int d = c.link_dof[l];
+        const double t = project(T + KF_XF_STRIDE * l, s6);
+        tau[d] = t;
+        if (!frozen[d]) tmax = fmax(tmax, fabs(t));
+    }
+    tmax = block_max(tmax, red);
+    // this CTA's slice of the energy sums
+    const int a0 = (int)((long long)n * g / n_seg), a1 = (int)((long long)n * (g + 1) / n_seg);
+    const double *ea = w.e_atom + (size_t)b * n * 2;
+    double se = 0.0, sv = 0.0, scv = 0.0, sp = 0.0, sp5 = 0.0;
+    for (int a = a0 + threadIdx.x; a < a1; a += blockDim.x) {
+        se += ea[2 * a]; sv += ea[2 * a + 1];
+        if (f.solvation) scv += w.cav_atom[(size_t)b * n + a];
+        const long long pc = w.pair_count[(size_t)b * n + a];
+        sp += (double)(pc & 0xffffffffLL);
+        sp5 += (double)(pc >> 32);
+    }
+    se = block_sum(se, red);
+    sv = block_sum(sv, red);
+    scv = block_sum(scv, red);
+    sp = block_sum(sp, red);
+    sp5 = block_sum(sp5, red);
+    if (threadIdx.x == 0) {
+        double *p = sc + 12 * g + 6;
+        p[0] = fmax(p[0], tmax);   // p[0]: side-chain max from pass 1
+        p[1] = se; p[2] = sv; p[3] = scv; p[4] = sp; p[5] = sp5;
+    }
+}
+
+__global__ void __launch_bounds__(TQ_THREADS)
+torque_seg_finish_kernel(kf_chain_t c, TorqueArgs ta, kf_batch_t w, kf_step_t step, int n_seg) {
+    const int b = blockIdx.x;
+    kf_status_t *st = w.status + b;
+    if (st->done) return;
+    if (st->error) {   // domain error this iteration: freeze, no record, no step
+        if (threadIdx.x == 0) st->done = 1;
+        return;
+    }
+    __shared__ int stop_reason;
+    const double *sc = w.fk_scratch + (size_t)b * n_seg * 12;
+    double tmax = 0.0, se = 0.0, sv = 0.0, scv = 0.0, sp = 0.0, sp5 = 0.0;
+    for (int g = 0; g < n_seg; ++g) {   // fixed order: deterministic
+        const double *p = sc + 12 * g + 6;
+        tmax = fmax(tmax, p[0]);
+        se += p[1]; sv += p[2]; scv += p[3]; sp += p[4]; sp5 += p[5];
+    }
+    finish_iteration(c, w, step, b, ta.tau + (size_t)b * c.n_dof, tmax, 0.5 * se, 0.5 * sv, scv, sp, sp5,
+                     &stop_reason);
 }
 
 // kcm_step for the API (B = 1): deltas and theta' (kcm.py:264-274).
@@ -253,6 +405,16 @@ int kf_torque_launch(const kf_chain_t *c, const kf_field_t *f, kf_batch_t *w, co
     if (step) st = *step;
     kf_field_t fz{};
     if (f) fz = *f;
+    const int n_seg = (c->n_bb + TQ_SEG - 1) / TQ_SEG;
+    if (mode == 1 && n_seg > 1 && w->B * n_seg <= 4 * 148 && w->fk_scratch && bb_suffix) {
+        torque_seg_kernel<<<dim3(n_seg, w->B), TQ_THREADS, 0, s>>>(*c, ta, *w, n_seg);
+        KF_LAUNCH_CHECK("torque_seg_kernel");
+        torque_seg_project_kernel<<<dim3(n_seg, w->B), TQ_THREADS, 0, s>>>(*c, fz, ta, *w, n_seg);
+        KF_LAUNCH_CHECK("torque_seg_project_kernel");
+        torque_seg_finish_kernel<<<w->B, TQ_THREADS, 0, s>>>(*c, ta, *w, st, n_seg);
+        KF_LAUNCH_CHECK("torque_seg_finish_kernel");
+        return 0;
+    }
     torque_step_kernel<<<w->B, TQ_THREADS, 0, s>>>(*c, fz, ta, *w, st, mode);
     KF_LAUNCH_CHECK("torque_step_kernel");
     return 0;

@@ -463,3 +463,27 @@ def test_scans_match_single_point():
     theta[ch.dof_psi(1)] = grid.axes[1][4] + 180.0
     e = P.single_point(ch, P.Conformation(theta, conf.frozen, 2), fld)
     assert grid.g_total[2, 4] == pytest.approx(e.g_total, rel=1e-12)
+
+
+def test_fold_long_chain_multi_cta_path(fp64_pairs):
+    """Chains past one 2048-dof backbone segment take the multi-CTA FK and
+    torque passes (kf_kinematics.cu fk_seg_*, kf_torque.cu torque_seg_*).
+    1100 random A/C/S residues (2200 backbone dofs, 2 segments), fp64 pair
+    math, 4 iterations vs the oracle: energies and tau_max to 1e-9, theta to
+    1e-9 degrees."""
+    P = _P()
+    seq = [str(x) for x in np.random.default_rng(5).choice(["ALA", "CYS", "SER"], 1100)]
+    ch, params, w, fld = make_system(seq)
+    rng = np.random.default_rng(6)
+    conf = ch.conf_from_backbone(rng.uniform(-90, 90, len(seq)), rng.uniform(-90, 90, len(seq)))
+    step = P.StepConfig(max_iters=4, torque_tol_rel=0.0, energy_window=0)
+    tr = P.fold(ch, conf, fld, step)
+    ref = O.fold(ch, conf.theta, conf.frozen, O.OracleField(params, w), kappa=0.5, max_iters=4,
+                 torque_tol_rel=0.0, energy_window=0)
+    E = np.array([[r.energy.g_elec, r.energy.g_vdw, r.energy.g_cav] for r in tr.records])
+    scale = np.abs(ref["energies"]).sum(1)
+    assert np.all(np.abs(E - ref["energies"]).sum(1) <= 1e-9 * scale)
+    tm = np.array([r.tau_max for r in tr.records])
+    assert np.all(np.abs(tm - ref["tau_max"]) <= 1e-9 * ref["tau_max"])
+    d = np.abs((np.asarray(tr.final.theta) - ref["final"] + 180.0) % 360.0 - 180.0).max()
+    assert d <= 1e-9, d
