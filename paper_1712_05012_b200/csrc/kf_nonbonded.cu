@@ -120,8 +120,70 @@ __device__ __noinline__ void slow_pair(bool f64, const kf_field_t *A, const doub
     (void)f64;
 }
 
+// One ordered pair (owner i, partner j) of the fast path: difference vector
+// from the hi/lo fp32 offsets, the reference's membership tests, the static
+// class window, and fp32 energy/force -- with the exact fp64 recomputation in
+// the 1e-3 A^2 threshold bands and below f64_d2 (always, in fp64 mode).
+// out = force on i (x, y, z), elec and vdW energy.  Shared by both kernels.
+template <bool F64, typename T>
+KF_DEV void pair_eval(const kf_field_t &f, const PairConst &pc, float4 hi, float4 li, float4 qi, int4 ai, int4 cm,
+                      float4 hj, float4 lj, float4 qj, int4 aj, const double4 *pos_i, const double4 *pos_j,
+                      kf_status_t *st, T out[5], int &pce, int &pcv) {
+    const float cut2f = pc.cut2, tvf = pc.tv2, tef = pc.te2;
+    const float band = 1e-3f;
+    const int i = ai.x, j = aj.x;
+    const float dxf = (hi.x - hj.x) + (li.x - lj.x);
+    const float dyf = (hi.y - hj.y) + (li.y - lj.y);
+    const float dzf = (hi.z - hj.z) + (li.z - lj.z);
+    const float d2f = dxf * dxf + dyf * dyf + dzf * dzf;
+    if (i == j || d2f > cut2f + band) return;
+    // static class window: 2-bit codes for j - i in [-32, 32)
+    int cls = 4;
+    if (!pc.uniform) {
+        const int off = j - i + 32;
+        if ((unsigned)off < 64u) {
+            const unsigned wd = off < 32 ? (off < 16 ? cm.x : cm.y) : (off < 48 ? cm.z : cm.w);
+            cls = 4 - (int)((wd >> (2 * (off & 15))) & 3u);
+        } else if (ai.w != 0 && aj.z != 0 && abs(ai.y - aj.y) <= 1) {
+            cls = slow_class(f.tparent, f.tgp, f.tggp, f.tres, f.tchain, i, j);
+        }
+    }
+    const float we = cls == 4 ? pc.we[3] : cls == 3 ? pc.we[2] : cls == 2 ? pc.we[1] : pc.we[0];
+    const float wv = cls == 4 ? pc.wv[3] : cls == 3 ? pc.wv[2] : cls == 2 ? pc.wv[1] : pc.wv[0];
+    const bool exact = F64 || fabsf(d2f - cut2f) <= band || fabsf(d2f - tvf) <= band ||
+                       fabsf(d2f - tef) <= band || d2f < pc.f64_d2;
+    if (exact) {
+        slow_pair<T>(F64, &f, pos_i, pos_j, i, j, cls, out, &pce, &pcv, st);
+        return;
+    }
+    if (d2f > cut2f) return;
+    const bool ke = d2f <= tef, kv = d2f <= tvf;
+    pce = ke; pcv = kv;
+    const float inv_r = rsqrtf(d2f);
+    const float inv_r2 = inv_r * inv_r;
+    float g = 0.f;
+    if (ke) {
+        // kappa = d: E = K w qi qj / d^2; constant: E = K w qi qj / (kappa d);
+        // |F| / d = E / d^2 in both cases
+        const float qq = (float)COULOMB_K * qi.x * qj.x * we;
+        const float e = pc.dconst ? qq * pc.kap_inv * inv_r : qq * inv_r2;
+        out[3] = e;
+        g += e * inv_r2;
+    }
+    if (kv) {
+        const float weps = wv * qi.z * qj.z;
+        const float D = qi.y + qj.y;
+        const float sr = D * D * inv_r2;
+        const float s3 = sr * sr * sr;
+        const float s6 = s3 * s3;
+        out[4] = weps * (s6 - 2.f * s3);
+        g += 12.f * weps * (s6 - s3) * inv_r2;
+    }
+    out[0] = g * dxf; out[1] = g * dyf; out[2] = g * dzf;
+}
+
 #ifndef PAIR_MINB_W
-#define PAIR_MINB_W 4   // resident CTAs per SM asked of ptxas, warp-per-chunk variant
+#define PAIR_MINB_W 5   // resident CTAs per SM asked of ptxas, warp-per-chunk variant
 #endif
 // F64 = false: fp32 pair math (the north-star configuration); true: fp64
 // pair math and fp64 per-tile sums (strict trajectory parity mode).
@@ -310,60 +372,9 @@ pair_kernel(const __grid_constant__ kf_field_t f, const PairConst pc, int B, int
                         if (act) {
                             const int t = e & 31;
                             const int4 ai = I.aux[o], aj = S.J.aux[t];
-                            const int i = ai.x, j = aj.x;
                             const float4 hi = I.hi[o], li = I.lo[o], hj = S.J.hi[t], lj = S.J.lo[t];
-                            const float dxf = (hi.x - hj.x) + (li.x - lj.x);
-                            const float dyf = (hi.y - hj.y) + (li.y - lj.y);
-                            const float dzf = (hi.z - hj.z) + (li.z - lj.z);
-                            const float d2f = dxf * dxf + dyf * dyf + dzf * dzf;
-                            if (i != j && d2f <= cut2f + band) {
-                                // static class window: 2-bit codes for j - i in [-32, 32)
-                                int cls = 4;
-                                if (!pc.uniform) {
-                                    const int off = j - i + 32;
-                                    if ((unsigned)off < 64u) {
-                                        const int4 cm = itree[o];
-                                        const unsigned wd = off < 32 ? (off < 16 ? cm.x : cm.y)
-                                                                     : (off < 48 ? cm.z : cm.w);
-                                        cls = 4 - (int)((wd >> (2 * (off & 15))) & 3u);
-                                    } else if (ai.w != 0 && aj.z != 0 && abs(ai.y - aj.y) <= 1) {
-                                        cls = slow_class(f.tparent, f.tgp, f.tggp, f.tres, f.tchain, i, j);
-                                    }
-                                }
-                                const float we = cls == 4 ? pc.we[3] : cls == 3 ? pc.we[2] : cls == 2 ? pc.we[1] : pc.we[0];
-                                const float wv = cls == 4 ? pc.wv[3] : cls == 3 ? pc.wv[2] : cls == 2 ? pc.wv[1] : pc.wv[0];
-                                const bool exact = F64 || fabsf(d2f - cut2f) <= band || fabsf(d2f - tvf) <= band ||
-                                                   fabsf(d2f - tef) <= band || d2f < pc.f64_d2;
-                                if (exact) {
-                                    slow_pair<T>(F64, &f, s_pos + nb + s0 + ic + o, s_pos + nb + aj.w, i, j,
-                                                 cls, out, &pce, &pcv, status + b);
-                                } else if (d2f <= cut2f) {
-                                    const bool ke = d2f <= tef, kv = d2f <= tvf;
-                                    pce = ke; pcv = kv;
-                                    const float4 qi = I.par[o], qj = S.J.par[t];
-                                    const float inv_r = rsqrtf(d2f);
-                                    const float inv_r2 = inv_r * inv_r;
-                                    float g = 0.f;
-                                    if (ke) {
-                                        // kappa = d: E = K w qi qj / d^2; constant: E = K w qi qj / (kappa d);
-                                        // |F| / d = E / d^2 in both cases
-                                        const float qq = (float)COULOMB_K * qi.x * qj.x * we;
-                                        const float e = pc.dconst ? qq * pc.kap_inv * inv_r : qq * inv_r2;
-                                        out[3] = e;
-                                        g += e * inv_r2;
-                                    }
-                                    if (kv) {
-                                        const float weps = wv * qi.z * qj.z;
-                                        const float D = qi.y + qj.y;
-                                        const float sr = D * D * inv_r2;
-                                        const float s3 = sr * sr * sr;
-                                        const float s6 = s3 * s3;
-                                        out[4] = weps * (s6 - 2.f * s3);
-                                        g += 12.f * weps * (s6 - s3) * inv_r2;
-                                    }
-                                    out[0] = g * dxf; out[1] = g * dyf; out[2] = g * dzf;
-                                }
-                            }
+                            pair_eval<F64, T>(f, pc, hi, li, I.par[o], ai, itree[o], hj, lj, S.J.par[t], aj,
+                                              s_pos + nb + s0 + ic + o, s_pos + nb + aj.w, status + b, out, pce, pcv);
                         }
                         // energies and counts only enter per-chunk totals: the computing lane keeps them
                         fe += out[3]; fv += out[4];
@@ -435,6 +446,235 @@ pair_kernel(const __grid_constant__ kf_field_t f, const PairConst pc, int B, int
     }
 }
 
+// ---- dense variant --------------------------------------------------------
+//
+// Same work items, probes and j-stream as pair_kernel, but no compaction: lane
+// = owner i (its data in registers), the j-tile is broadcast from shared
+// memory.  Chunks of <= 16 (<= 8) atoms are duplicated across 2 (4) lane
+// groups that take alternating j, so more lanes work; the groups' fp64 sums are
+// combined by a fixed xor tree at the end of the item.  Each lane sums its
+// own pairs in j order: deterministic, no per-pair shared-memory traffic.
+template <bool F64, bool SPLIT>
+__global__ void __launch_bounds__((SPLIT ? SPLIT_WARPS : PAIR_WARPS) * 32, SPLIT ? 1 : PAIR_MINB_W)
+pair_dense_kernel(const __grid_constant__ kf_field_t f, const PairConst pc, int B, int n,
+                  const unsigned long long *__restrict__ keys, const int32_t *__restrict__ cnt,
+                  const int32_t *__restrict__ start, const int32_t *__restrict__ occ,
+                  const int32_t *__restrict__ occ_count, const int32_t *__restrict__ chunk_pre,
+                  const int32_t *__restrict__ chunk_offset, const float4 *__restrict__ s_hi,
+                  const float4 *__restrict__ s_lo, const double4 *__restrict__ s_pos,
+                  const float4 *__restrict__ s_par, const int4 *__restrict__ s_aux, const int4 *__restrict__ s_tree,
+                  const float4 *__restrict__ cell_box, int32_t *__restrict__ work, double *__restrict__ forces,
+                  double *__restrict__ e_atom, long long *__restrict__ pair_count, kf_status_t *status) {
+    using T = typename std::conditional<F64, double, float>::type;
+    constexpr int NW = SPLIT ? SPLIT_WARPS : PAIR_WARPS;
+    __shared__ Tile Jt[NW];
+    __shared__ float4 ihi_s[SPLIT ? 1 : NW][32];   // the chunk's hi offsets (probe / box test)
+    __shared__ double part[SPLIT ? NW : 1][3][32];
+    __shared__ double epart[NW][2];
+    __shared__ long long cpart[NW];
+    __shared__ int item_s[1];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    Tile &J = Jt[warp];
+    float4 *ihi = ihi_s[SPLIT ? 0 : warp];
+    const uint32_t H = 1u << f.hash_bits;
+    const int total = chunk_offset[B];
+    const float cellf = pc.cell, pre2 = pc.pre2;
+
+    for (;;) {
+        int item;
+        if (SPLIT) {
+            __syncthreads();
+            if (threadIdx.x == 0) item_s[0] = atomicAdd(work, 1);
+            __syncthreads();
+            item = item_s[0];
+        } else {
+            item = 0;
+            if (lane == 0) item = atomicAdd(work, 1);
+            item = __shfl_sync(FULL, item, 0);
+        }
+        if (item >= total) break;
+        // item -> (trajectory, occupied cell, 32-atom i-chunk of that cell)
+        const int b = item_owner(chunk_offset, B, item);
+        const size_t hb = (size_t)b * H, nb = (size_t)b * n;
+        const int local = item - chunk_offset[b];
+        int klo = 0, khi = occ_count[b] - 1;          // last k with chunk_pre[k] <= local
+        while (klo < khi) {
+            const int mid = (klo + khi + 1) >> 1;
+            if (chunk_pre[hb + mid] <= local) klo = mid; else khi = mid - 1;
+        }
+        const int slot = occ[hb + klo];
+        const int ic = (local - chunk_pre[hb + klo]) << 5;
+        int cx, cy, cz;
+        unpack_cell((long long)keys[hb + slot], cx, cy, cz);
+        const int s0 = start[hb + slot], c = cnt[hb + slot];
+        const int ci_n = min(32, c - ic);
+        // lane -> (owner slot, j phase): chunks of <= 16 / <= 8 atoms use 2 / 4 phases
+        const int nph = ci_n > 16 ? 1 : ci_n > 8 ? 2 : 4;
+        const int wi = 32 / nph, oi = lane % wi, ph = lane / wi;
+        const bool own = oi < ci_n;
+        const size_t ki = nb + s0 + ic + (own ? oi : 0);
+        const float4 hi = s_hi[ki], li = s_lo[ki], qi = s_par[ki];
+        const int4 ai = s_aux[ki], cm = s_tree[ki];
+        if ((!SPLIT || warp == 0) && lane < ci_n) ihi[lane] = s_hi[nb + s0 + ic + lane];
+        if (SPLIT) __syncthreads(); else __syncwarp();
+
+        // probe the 27 neighbour cells (lane = stencil cell), keep those whose box
+        // some i reaches (warp-uniform loop over the chunk's atoms)
+        int p_j0 = 0, p_jc = 0, p_js = -1;
+        float p_sx = 0.f, p_sy = 0.f, p_sz = 0.f;
+        float4 blo = make_float4(1e30f, 1e30f, 1e30f, 0.f), bhi = make_float4(-1e30f, -1e30f, -1e30f, 0.f);
+        if (lane < f.n_stencil) {
+            const int ox = f.stencil[3 * lane], oy = f.stencil[3 * lane + 1], oz = f.stencil[3 * lane + 2];
+            p_js = cell_probe(keys + hb, H, cx + ox, cy + oy, cz + oz);
+            if (p_js >= 0) {
+                p_sx = (float)ox * cellf; p_sy = (float)oy * cellf; p_sz = (float)oz * cellf;
+                blo = cell_box[2 * (hb + p_js)]; bhi = cell_box[2 * (hb + p_js) + 1];
+            }
+        }
+        __syncwarp();
+        bool keep = false;
+        for (int q = 0; q < ci_n; ++q) {
+            const float4 r = ihi[q];
+            const float px = r.x - p_sx, py = r.y - p_sy, pz = r.z - p_sz;
+            const float gx = fmaxf(fmaxf(blo.x - px, px - bhi.x), 0.f);
+            const float gy = fmaxf(fmaxf(blo.y - py, py - bhi.y), 0.f);
+            const float gz = fmaxf(fmaxf(blo.z - pz, pz - bhi.z), 0.f);
+            keep |= gx * gx + gy * gy + gz * gz <= pre2;
+        }
+        if (keep) { p_j0 = start[hb + p_js]; p_jc = cnt[hb + p_js]; }
+        int p_end = p_jc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(FULL, p_end, o);
+            if (lane >= o) p_end += v;
+        }
+        const int n_stream = __shfl_sync(FULL, p_end, 31);
+
+        double ax = 0.0, ay = 0.0, az = 0.0, ee = 0.0, ev = 0.0;
+        int ce = 0, cv = 0;
+        for (int jb = SPLIT ? 32 * warp : 0; jb < n_stream; jb += SPLIT ? 32 * NW : 32) {
+            const int nt = min(32, n_stream - jb);
+            {
+                const int e = jb + lane;
+                int cs = 0;
+#pragma unroll
+                for (int step = 16; step > 0; step >>= 1) {
+                    const int end = __shfl_sync(FULL, p_end, cs + step - 1);
+                    if (end <= e) cs += step;
+                }
+                const int cend = __shfl_sync(FULL, p_end, cs), cj0 = __shfl_sync(FULL, p_j0, cs),
+                          ccnt = __shfl_sync(FULL, p_jc, cs);
+                const float ssx = __shfl_sync(FULL, p_sx, cs), ssy = __shfl_sync(FULL, p_sy, cs),
+                            ssz = __shfl_sync(FULL, p_sz, cs);
+                __syncwarp();
+                if (lane < nt) {
+                    const int kk = cj0 + (e - (cend - ccnt));
+                    const size_t kj = nb + kk;
+                    const float4 h = s_hi[kj];
+                    int4 aux = s_aux[kj];
+                    aux.w = kk;                     // sorted index (fp64 slow path)
+                    J.hi[lane] = make_float4(h.x + ssx, h.y + ssy, h.z + ssz, 0.f);   // i's cell frame
+                    J.lo[lane] = s_lo[kj];
+                    J.par[lane] = s_par[kj];
+                    J.aux[lane] = aux;
+                }
+                __syncwarp();
+            }
+            T fx = 0, fy = 0, fz = 0, fe = 0, fv = 0;
+            if (own) {
+#ifdef PAIR_DENSE_POP
+                // prefilter the lane's j into a mask, then pop its set bits: the
+                // pair body runs max(popcount) times per warp, not nt / nph
+                unsigned mask = 0u;
+                for (int t = ph; t < nt; t += nph) {
+                    const float4 hj = J.hi[t];
+                    const float dx = hi.x - hj.x, dy = hi.y - hj.y, dz = hi.z - hj.z;
+                    mask |= (dx * dx + dy * dy + dz * dz <= pre2 ? 1u : 0u) << t;
+                }
+                while (mask) {
+                    const int t = __ffs(mask) - 1;
+                    mask &= mask - 1u;
+                    const float4 hj = J.hi[t];
+#else
+                for (int t = ph; t < nt; t += nph) {
+                    const float4 hj = J.hi[t];
+                    const float dx = hi.x - hj.x, dy = hi.y - hj.y, dz = hi.z - hj.z;
+                    if (dx * dx + dy * dy + dz * dz > pre2) continue;
+#endif
+                    T out[5] = {0, 0, 0, 0, 0};
+                    int pce = 0, pcv = 0;
+                    const int4 aj = J.aux[t];
+                    pair_eval<F64, T>(f, pc, hi, li, qi, ai, cm, hj, J.lo[t], J.par[t], aj, s_pos + ki,
+                                      s_pos + nb + aj.w, status + b, out, pce, pcv);
+                    fx += out[0]; fy += out[1]; fz += out[2]; fe += out[3]; fv += out[4];
+                    ce += pce; cv += pcv;
+                }
+            }
+            ax += (double)fx; ay += (double)fy; az += (double)fz;
+            ee += (double)fe; ev += (double)fv;
+            __syncwarp();
+        }
+        // combine the j phases of each owner (fixed xor tree: both partners get the same sum)
+        for (int m = wi; m < 32; m <<= 1) {
+            ax += __shfl_xor_sync(FULL, ax, m);
+            ay += __shfl_xor_sync(FULL, ay, m);
+            az += __shfl_xor_sync(FULL, az, m);
+        }
+        if (SPLIT) {
+            // combine the warps' partial forces in warp order (deterministic)
+            part[SPLIT ? warp : 0][0][lane] = ax;
+            part[SPLIT ? warp : 0][1][lane] = ay;
+            part[SPLIT ? warp : 0][2][lane] = az;
+            __syncthreads();
+            if (warp == 0 && own && ph == 0) {
+                double sx = 0.0, sy = 0.0, sz = 0.0;
+#pragma unroll
+                for (int w = 0; w < (SPLIT ? NW : 1); ++w) {
+                    sx += part[w][0][lane]; sy += part[w][1][lane]; sz += part[w][2][lane];
+                }
+                const size_t o = nb + ai.x;
+                forces[3 * o] = sx; forces[3 * o + 1] = sy; forces[3 * o + 2] = sz;
+                e_atom[2 * o] = 0.0; e_atom[2 * o + 1] = 0.0;
+                pair_count[o] = 0;
+            }
+            __syncthreads();
+        } else if (own && ph == 0) {
+            const size_t o = nb + ai.x;
+            forces[3 * o] = ax; forces[3 * o + 1] = ay; forces[3 * o + 2] = az;
+            e_atom[2 * o] = 0.0; e_atom[2 * o + 1] = 0.0;
+            pair_count[o] = 0;
+        }
+        long long pcount = (long long)ce + ((long long)cv << 32);
+        // chunk totals: fixed xor tree per warp, then warps in order, stored at the
+        // chunk's first atom (chunks are a function of the positions: deterministic)
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+            ee += __shfl_xor_sync(FULL, ee, d);
+            ev += __shfl_xor_sync(FULL, ev, d);
+            pcount += __shfl_xor_sync(FULL, pcount, d);
+        }
+        if (SPLIT) {
+            if (lane == 0) { epart[warp][0] = ee; epart[warp][1] = ev; cpart[warp] = pcount; }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                double te = 0.0, tv = 0.0;
+                long long tc = 0;
+                for (int w = 0; w < NW; ++w) { te += epart[w][0]; tv += epart[w][1]; tc += cpart[w]; }
+                const size_t o = nb + s_aux[nb + s0 + ic].x;
+                e_atom[2 * o] = te; e_atom[2 * o + 1] = tv;
+                pair_count[o] = tc;
+            }
+        } else {
+            __syncwarp();
+            if (lane == 0) {
+                const size_t o = nb + s_aux[nb + s0 + ic].x;
+                e_atom[2 * o] = ee; e_atom[2 * o + 1] = ev;
+                pair_count[o] = pcount;
+            }
+        }
+    }
+}
+
 // On error only: smallest (i, j), i < j, among pairs at the minimum distance.
 __global__ void clash_report_kernel(kf_field_t f, int B, int n, const unsigned long long *__restrict__ keys,
                                     const int32_t *__restrict__ cnt, const int32_t *__restrict__ start,
@@ -468,16 +708,30 @@ __global__ void clash_report_kernel(kf_field_t f, int B, int n, const unsigned l
     }
 }
 
-int g_pair_grid = 0;
+int g_sms = 0;
+
+// Persistent grid: every CTA the SMs can hold (occupancy API), per kernel.
+template <typename K>
+int resident_grid(K kern, int threads, size_t dyn) {
+    struct Entry { const void *k; size_t dyn; int grid; };
+    static Entry cache[16];
+    static int n_cache = 0;
+    for (int e = 0; e < n_cache; ++e)
+        if (cache[e].k == (const void *)kern && cache[e].dyn == dyn) return cache[e].grid;
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, dyn);
+    const int grid = g_sms * (per_sm > 0 ? per_sm : 1);
+    if (n_cache < 16) cache[n_cache++] = Entry{(const void *)kern, dyn, grid};
+    return grid;
+}
 
 }  // namespace
 
 int kf_pairs_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s) {
-    if (g_pair_grid == 0) {
-        int dev = 0, sms = 148;
+    if (g_sms == 0) {
+        int dev = 0;
         cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        g_pair_grid = sms * 4;
+        cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
     }
     KF_CUDA(cudaMemsetAsync(w->work, 0, sizeof(int32_t), s), "memset work");
     // one CTA per cell when the whole batch is small (latency), one warp per cell otherwise;
@@ -488,10 +742,18 @@ int kf_pairs_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s) {
         split_below = env ? atoll(env) : 40000;
     }
     const bool split = (long long)w->B * n < split_below;
-    auto kern = f->precision ? (split ? pair_kernel<true, true> : pair_kernel<true, false>)
-                             : (split ? pair_kernel<false, true> : pair_kernel<false, false>);
+    static int variant = -1;   // KFB200_PAIR_KERNEL: 1 = compacted list, 2 = dense lanes
+    if (variant < 0) {
+        const char *env = getenv("KFB200_PAIR_KERNEL");
+        variant = env ? atoi(env) : 2;
+    }
+    auto kern = variant == 2
+                    ? (f->precision ? (split ? pair_dense_kernel<true, true> : pair_dense_kernel<true, false>)
+                                    : (split ? pair_dense_kernel<false, true> : pair_dense_kernel<false, false>))
+                    : (f->precision ? (split ? pair_kernel<true, true> : pair_kernel<true, false>)
+                                    : (split ? pair_kernel<false, true> : pair_kernel<false, false>));
     const int nw = split ? SPLIT_WARPS : PAIR_WARPS;
-    const size_t dyn = (size_t)nw * (f->precision ? sizeof(WarpSmem<double>) : sizeof(WarpSmem<float>));
+    const size_t dyn = variant == 2 ? 0 : (size_t)nw * (f->precision ? sizeof(WarpSmem<double>) : sizeof(WarpSmem<float>));
     static bool opted = false;
     if (!opted) {
         for (auto k : {pair_kernel<true, true>, pair_kernel<true, false>, pair_kernel<false, true>,
@@ -515,7 +777,7 @@ int kf_pairs_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s) {
     }
     pc.f64_d2 = f64_below * f64_below;
     pc.dconst = f->dielectric_const; pc.uniform = f->uniform_weights;
-    kern<<<split ? g_pair_grid / 2 : g_pair_grid, nw * 32, dyn, s>>>(
+    kern<<<resident_grid(kern, nw * 32, dyn), nw * 32, dyn, s>>>(
         *f, pc, w->B, n, w->cell_key, w->cell_cnt, w->cell_start, w->occ, w->occ_count, w->chunk_pre, w->chunk_offset,
         reinterpret_cast<const float4 *>(w->s_hi), reinterpret_cast<const float4 *>(w->s_lo),
         reinterpret_cast<const double4 *>(w->s_pos), reinterpret_cast<const float4 *>(w->s_par),
