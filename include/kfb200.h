@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define KF_ABI_VERSION 4
+#define KF_ABI_VERSION 5
 
 /* ---- static chain tables (uploaded once per chain) ------------------------
  * Links are in the reference's topological order (parent < index, ground = 0),
@@ -96,6 +96,9 @@ typedef struct {
     const float *grp_cone;          /* [G][8]: axis xyz, cos alpha, sin alpha, count, 0, 0 */
     int32_t n_groups;
     int32_t _pad2;
+    /* per-atom records gathered by binning (one 16-byte load each)            */
+    const float *atom_par;          /* [n][4]: q, R, sqrt(eps), 0 (fp32)           */
+    const int32_t *atom_aux;        /* [n][4]: atom, residue, chain flag, class_slow (0 if uniform) */
 } kf_field_t;
 
 /* ---- per-trajectory status block ----------------------------------------- */

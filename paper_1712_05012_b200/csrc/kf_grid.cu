@@ -18,6 +18,8 @@
 //   finalize per occupied cell: members sorted by atom index (deterministic
 //            visit order) and the cell-ordered SoA the pair kernel stages:
 //            fp32 offset from the cell centre, fp64 position, params, aux ints
+#include <algorithm>
+
 #include "kf_common.cuh"
 
 namespace {
@@ -179,7 +181,7 @@ constexpr int FIN_WARPS = 4;
 constexpr int FIN_CAP = 1024;
 
 __global__ void __launch_bounds__(FIN_WARPS * 32)
-bin_finalize_kernel(kf_field_t f, int B, int n, const double *__restrict__ pos,
+bin_finalize_kernel(const __grid_constant__ kf_field_t f, int B, int n, const double *__restrict__ pos,
                     const unsigned long long *__restrict__ keys, const int32_t *__restrict__ occ,
                     const int32_t *__restrict__ occ_offset, const int32_t *__restrict__ cnt,
                     const int32_t *__restrict__ start, int32_t *__restrict__ sorted_atom,
@@ -189,8 +191,9 @@ bin_finalize_kernel(kf_field_t f, int B, int n, const double *__restrict__ pos,
                     float4 *__restrict__ cell_box, const kf_status_t *status) {
     __shared__ int buf[FIN_WARPS][FIN_CAP];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int item = blockIdx.x * FIN_WARPS + warp;
-    if (item >= occ_offset[B]) return;
+    const int total = occ_offset[B];
+    // persistent: warps stride over the occupied cells of all trajectories
+    for (int item = blockIdx.x * FIN_WARPS + warp; item < total; item += gridDim.x * FIN_WARPS) {
     const int b = item_owner(occ_offset, B, item);
     const size_t H = (size_t)1 << f.hash_bits;
     const int slot = occ[b * H + (item - occ_offset[b])];
@@ -237,9 +240,8 @@ bin_finalize_kernel(kf_field_t f, int B, int n, const double *__restrict__ pos,
         }
         s_hi[gs] = make_float4(h[0], h[1], h[2], 0.f);
         s_lo[gs] = make_float4(l[0], l[1], l[2], 0.f);
-        s_par[gs] = make_float4(f.q32[a], f.R32[a], f.seps32[a], 0.f);
-        s_aux[gs] = make_int4(a, tree ? f.tres[a] : 0, tree ? (int)f.tchain[a] : 0,
-                              tree ? (int)f.class_slow[a] : 0);
+        s_par[gs] = reinterpret_cast<const float4 *>(f.atom_par)[a];
+        s_aux[gs] = reinterpret_cast<const int4 *>(f.atom_aux)[a];
         s_tree[gs] = tree ? reinterpret_cast<const int4 *>(f.class_map)[a] : make_int4(0, 0, 0, 0);
     }
 #pragma unroll
@@ -251,6 +253,8 @@ bin_finalize_kernel(kf_field_t f, int B, int n, const double *__restrict__ pos,
     if (lane == 0) {
         cell_box[2 * (b * H + slot)] = make_float4(bl[0], bl[1], bl[2], 0.f);
         cell_box[2 * (b * H + slot) + 1] = make_float4(bh[0], bh[1], bh[2], 0.f);
+    }
+    __syncwarp();
     }
 }
 
@@ -274,7 +278,15 @@ int kf_bin_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s) {
     bin_scatter_kernel<<<kf_blocks(total, 256), 256, 0, s>>>(*f, B, n, w->atom_slot, w->atom_rank, w->cell_start,
                                                              w->sorted_atom, w->status);
     KF_LAUNCH_CHECK("bin_scatter_kernel");
-    bin_finalize_kernel<<<kf_blocks(total, FIN_WARPS), FIN_WARPS * 32, 0, s>>>(
+    static int fin_grid = 0;
+    if (fin_grid == 0) {
+        int dev = 0, sms = 148, per_sm = 1;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bin_finalize_kernel, FIN_WARPS * 32, 0);
+        fin_grid = sms * (per_sm > 0 ? per_sm : 1);
+    }
+    bin_finalize_kernel<<<(unsigned)std::min<long long>(fin_grid, kf_blocks(total, FIN_WARPS)), FIN_WARPS * 32, 0, s>>>(
         *f, B, n, w->pos, w->cell_key, w->occ, w->occ_offset, w->cell_cnt, w->cell_start, w->sorted_atom,
         reinterpret_cast<float4 *>(w->s_hi), reinterpret_cast<float4 *>(w->s_lo),
         reinterpret_cast<double4 *>(w->s_pos), reinterpret_cast<float4 *>(w->s_par),

@@ -317,13 +317,20 @@ class ParamTables:
                                 q=_up(q, np.float64), R=_up(R, np.float64), eps=_up(eps, np.float64))
         s = self.struct = N.KfField()
         s.n_atoms = n
+        par = np.zeros((n, 4), f32)
+        par[:, 0], par[:, 1], par[:, 2] = q, R, np.sqrt(eps)
+        aux = np.zeros((n, 4), np.int32)
+        aux[:, 0] = np.arange(n)
         if hasattr(weights, "tree") and hasattr(weights, "table"):
+            aux[:, 1] = np.asarray(weights.tree.residue_of)
+            aux[:, 2] = np.asarray(weights.tree.chain_mask).astype(np.int32)
             tree = weights.tree
             cmap, slow = class_window(tree)
             t.update(tparent=_up(tree.parent, np.int32), tgp=_up(tree.grandparent, np.int32),
                      tggp=_up(tree.greatgrand, np.int32), tres=_up(tree.residue_of, np.int32),
                      tchain=_up(tree.chain_mask, np.uint8), class_map=_up(cmap, np.int32),
                      class_slow=_up(slow, np.uint8))
+            aux[:, 3] = slow.astype(np.int32)
             s.uniform_weights = 0
             for k, v in enumerate(np.asarray(weights.table.elec_by_class())[1:5]):
                 s.w_elec[k] = float(v)
@@ -336,6 +343,7 @@ class ParamTables:
             raise ConfigurationError(
                 f"unsupported pair-weight provider {type(weights).__name__}: "
                 "use TreeWeights or UniformWeights")
+        t.update(atom_par=_up(par, f32), atom_aux=_up(aux, np.int32))
         if dielectric is not None:
             s.dielectric_const = 1 if dielectric.mode == "constant" else 0
             s.kappa = float(dielectric.kappa)
