@@ -246,8 +246,9 @@ void kf_graph_cache_clear(void);
  * StericClashError message (forcefield.py:84-88).  Run only on error. */
 int kf_clash_report(const kf_field_t *f, kf_batch_t *w, void *stream);
 
-/* Kernel launches enqueued per loop iteration (bench bookkeeping). */
-int kf_kernels_per_iteration(int solvation);
+/* Kernel launches this library has enqueued so far (host counter; a captured
+ * CUDA graph replays the launches counted while it was captured). */
+unsigned long long kf_launch_counter(void);
 /* Issue-rate microbenchmark of this GPU: kind 0 = FP32 FFMA, 1 = FP64 DFMA.
  * Writes FLOP/s (FMA = 2 FLOP) measured with events on `stream` to *out. */
 int kf_peak_flops(int kind, double *out, void *stream);

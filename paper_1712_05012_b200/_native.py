@@ -109,7 +109,7 @@ _PROTOS = {
                            P, P, P, P, P]),
     "kf_fixed_to_f64": (I32, [P, C.c_int64, F64, P, P]),
     "kf_bin": (I32, [P, P, P]),
-    "kf_kernels_per_iteration": (I32, [C.c_int]),
+    "kf_launch_counter": (C.c_ulonglong, []),
     "kf_peak_flops": (I32, [C.c_int, P, P]),
     "kf_pairs": (I32, [P, P, P]),
     "kf_solvation_forces": (I32, [P, C.c_int, P, P, P, P, C.c_int, P, P, P, P, F64, F64,

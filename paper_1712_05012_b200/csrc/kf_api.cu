@@ -66,6 +66,10 @@ int enqueue_iteration(const kf_chain_t *c, const kf_field_t *f, kf_batch_t *w, c
 }
 }  // namespace
 
+static unsigned long long g_launches = 0;
+void kf_count_launch() { ++g_launches; }
+unsigned long long kf_launches_so_far() { return g_launches; }
+
 void kf_set_error(const char *where, cudaError_t e) {
     g_last_error = std::string(where) + ": " + cudaGetErrorString(e);
 }
@@ -178,13 +182,7 @@ int kf_fold_iterations_eager(const kf_chain_t *c, const kf_field_t *f, kf_batch_
     return 0;
 }
 
-int kf_kernels_per_iteration(int solvation) {
-    // fk: scan + positions; bin: insert, cell scan, work prefix, scatter, finalize;
-    // pairs; wrench; torque (+ solvation: primary pass, overflow pass, combine).
-    // Memsets are not counted; chains past one FK segment (2048 backbone links)
-    // add the segmented-scan launches.
-    return 10 + (solvation ? 3 : 0);
-}
+unsigned long long kf_launch_counter(void) { return kf_launches_so_far(); }
 
 int kf_clash_report(const kf_field_t *f, kf_batch_t *w, void *stream) {
     return kf_clash_report_launch(f, w, f->n_atoms, (cudaStream_t)stream);

@@ -184,8 +184,12 @@ KF_DEV double block_max(double v, double *scratch) {
 
 // ---- error plumbing (host) ---------------------------------------------------
 void kf_set_error(const char *where, cudaError_t e);
+// Every kernel launch of the library goes through this check, which also
+// counts it (kf_launch_counter: the bench's gpu_launches).
+void kf_count_launch();
 #define KF_LAUNCH_CHECK(where)                                   \
     do {                                                         \
+        kf_count_launch();                                       \
         cudaError_t _e = cudaGetLastError();                     \
         if (_e != cudaSuccess) { kf_set_error(where, _e); return 1; } \
     } while (0)

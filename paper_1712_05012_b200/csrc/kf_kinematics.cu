@@ -111,6 +111,99 @@ fk_scan_kernel(kf_chain_t c, const double *__restrict__ theta_all, double *__res
     }
 }
 
+// ---- short chains: the whole iteration's FK in shared memory ----------------
+// Same operations and association as fk_scan_kernel, but the link transforms
+// live in shared memory (12 doubles each) until the final write of T (with
+// the joint axes) and of the atom positions, which this kernel also computes:
+// one global write per link and per atom instead of several read-modify-writes.
+constexpr int FKS_THREADS = 128;
+constexpr int FKS_STRIDE = 12;
+
+__global__ void __launch_bounds__(FKS_THREADS)
+fk_smem_kernel(const __grid_constant__ kf_chain_t c, const double *__restrict__ theta_all,
+               double *__restrict__ T_all, double *__restrict__ pos_all, const kf_status_t *__restrict__ status) {
+    const int b = blockIdx.x;
+    if (status && status[b].done) return;
+    extern __shared__ __align__(16) double S[];     // [L][12]
+    __shared__ double chunk[FKS_THREADS][12];
+    const int L = c.n_links, D = c.n_dof, n = c.n_atoms;
+    const double *theta = theta_all + (size_t)b * D;
+
+    for (int l = threadIdx.x; l < L; l += blockDim.x) {
+        Xf a;
+        if (l == 0 || c.link_dof[l] < 0) {
+            a = xf_identity();
+        } else {
+            const int p = c.link_parent[l];
+            a = local_transform(c.link_axis0 + 3 * l, theta[c.link_dof[l]], c.link_body0 + 3 * p);
+        }
+        xf_store(S + FKS_STRIDE * l, a);
+    }
+    __syncthreads();
+
+    const int nb = c.n_bb;
+    const int per = (nb + blockDim.x - 1) / blockDim.x;
+    const int lo = min(nb, (int)threadIdx.x * per), hi = min(nb, lo + per);
+    Xf acc = xf_identity();
+    for (int k = lo; k < hi; ++k) {
+        double *slot = S + FKS_STRIDE * c.bb_order[k];
+        acc = xf_compose(acc, xf_load(slot));
+        xf_store(slot, acc);
+    }
+    xf_store(chunk[threadIdx.x], acc);
+    __syncthreads();
+    for (int off = 1; off < (int)blockDim.x; off <<= 1) {
+        Xf mine = xf_load(chunk[threadIdx.x]);
+        Xf r = mine;
+        if ((int)threadIdx.x >= off) r = xf_compose(xf_load(chunk[threadIdx.x - off]), mine);
+        __syncthreads();
+        xf_store(chunk[threadIdx.x], r);
+        __syncthreads();
+    }
+    if (threadIdx.x > 0 && lo < hi) {
+        const Xf pre = xf_load(chunk[threadIdx.x - 1]);
+        for (int k = lo; k < hi; ++k) {
+            double *slot = S + FKS_STRIDE * c.bb_order[k];
+            xf_store(slot, xf_compose(pre, xf_load(slot)));
+        }
+    }
+    __syncthreads();
+    for (int d = 0; d < c.side_depth; ++d) {
+        for (int k = c.side_depth_off[d] + threadIdx.x; k < c.side_depth_off[d + 1]; k += blockDim.x) {
+            const int l = c.side_order[k];
+            double *slot = S + FKS_STRIDE * l;
+            xf_store(slot, xf_compose(xf_load(S + FKS_STRIDE * c.link_parent[l]), xf_load(slot)));
+        }
+        __syncthreads();
+    }
+    // T with the current joint axes U_l = M_l axis0_l (chain.py:257); ground keeps 0
+    double *T = T_all + (size_t)b * L * KF_XF_STRIDE;
+    for (int e = threadIdx.x; e < L * KF_XF_STRIDE; e += blockDim.x) {
+        const int l = e / KF_XF_STRIDE, q = e - l * KF_XF_STRIDE;
+        const double *src = S + FKS_STRIDE * l;
+        double v;
+        if (q < 12) {
+            v = src[q];
+        } else if (q < 15 && l != 0 && c.link_dof[l] >= 0) {
+            const int r = q - 12;
+            const double *a = c.link_axis0 + 3 * l;
+            v = src[3 * r] * a[0] + src[3 * r + 1] * a[1] + src[3 * r + 2] * a[2];
+        } else {
+            v = 0.0;
+        }
+        T[e] = v;
+    }
+    // positions pos_a = P_l + M_l zrel_a (fk_positions_kernel's arithmetic)
+    double *pos = pos_all + (size_t)b * n * 3;
+    for (int a = threadIdx.x; a < n; a += blockDim.x) {
+        const double *t = S + FKS_STRIDE * c.atom_link[a];
+        const double zx = c.atom_zrel[3 * a], zy = c.atom_zrel[3 * a + 1], zz = c.atom_zrel[3 * a + 2];
+        pos[3 * a] = t[9] + (t[0] * zx + t[1] * zy + t[2] * zz);
+        pos[3 * a + 1] = t[10] + (t[3] * zx + t[4] * zy + t[5] * zz);
+        pos[3 * a + 2] = t[11] + (t[6] * zx + t[7] * zy + t[8] * zz);
+    }
+}
+
 // ---- long chains: the backbone scan spread over many CTAs --------------------
 // Three phases per trajectory: (1) every CTA scans a 2048-link segment of the
 // backbone in place (local transforms computed on the fly) and publishes the
@@ -265,6 +358,18 @@ int kf_fk_launch(const kf_chain_t *c, kf_batch_t *w, const kf_status_t *status, 
                                                                                          w->B, status);
         KF_LAUNCH_CHECK("fk_side_kernel");
     } else {
+        const size_t smem = (size_t)c->n_links * FKS_STRIDE * sizeof(double);
+        if (n_seg <= 1 && smem <= 110 * 1024) {
+            static size_t opted = 0;
+            if (smem > opted) {
+                KF_CUDA(cudaFuncSetAttribute(fk_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                        "fk smem");
+                opted = smem;
+            }
+            fk_smem_kernel<<<w->B, FKS_THREADS, smem, s>>>(*c, w->theta, w->link_T, w->pos, status);
+            KF_LAUNCH_CHECK("fk_smem_kernel");
+            return 0;
+        }
         fk_scan_kernel<<<w->B, FK_THREADS, 0, s>>>(*c, w->theta, w->link_T, status);
         KF_LAUNCH_CHECK("fk_scan_kernel");
     }
