@@ -360,12 +360,19 @@ def main():
             dist.destroy_process_group()
         return
     peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
-    traffic = None
+    # the dominant kernel of this run (kf_nonbonded.cu picks dense lanes for fp32
+    # pair math, the compacted list for fp64) and its DRAM traffic per launch from
+    # the committed `ncu --set full` capture of the same workload, if there is one
+    kernel = "pair_kernel<1,0>" if P.pair_precision() == "fp64" else "pair_dense_kernel<0,0>"
+    traffic, traffic_src = None, None
     prof_path = os.path.join(ROOT, "profiles", "pair_kernel_traffic.json")
     if os.path.exists(prof_path):
         try:
-            traffic = json.load(open(prof_path)).get("bytes_per_launch")
-        except (OSError, ValueError):
+            for rec in json.load(open(prof_path)):
+                if rec.get("kernel") == kernel and rec.get("workload") == workload_name(args) \
+                        and rec.get("ensemble") == B:
+                    traffic, traffic_src = rec.get("bytes_per_launch"), rec.get("source")
+        except (OSError, ValueError, AttributeError):
             traffic = None
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
@@ -378,9 +385,9 @@ def main():
         "pair_interactions_per_s": pairs_per_step * K / (ms_max * 1e-3),
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "api": "paper_1712_05012_b200.fold_ensemble (host numpy in, host Trajectory data out)"},
-        "roofline": {"kernel": "pair_kernel (K3)", "bound": "fp32", "achieved": achieved,
+        "roofline": {"kernel": kernel + " (K3)", "bound": "fp32", "achieved": achieved,
                      "peak": peak32 / 1e12, "unit": "TFLOP/s", "frac": achieved / (peak32 / 1e12),
-                     "traffic": traffic,
+                     "traffic": traffic, "traffic_source": traffic_src,
                      "work": f"25*P9 + 17*P5 FLOP per trajectory (SURVEY.md §8(d)); P9={p9}, P5={p5} "
                              f"on this rank's {B} trajectories",
                      "peak_source": "kf_peak_flops FFMA microbenchmark, this GPU, this run",

@@ -742,11 +742,15 @@ int kf_pairs_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s) {
         split_below = env ? atoll(env) : 40000;
     }
     const bool split = (long long)w->B * n < split_below;
-    static int variant = -1;   // KFB200_PAIR_KERNEL: 1 = compacted list, 2 = dense lanes
-    if (variant < 0) {
+    // KFB200_PAIR_KERNEL: 1 = compacted pair list, 2 = dense lanes.  Default:
+    // dense for fp32 pair math, compacted for fp64 (its pair body is long
+    // enough that full lanes pay for the compaction)
+    static int env_variant = -1;
+    if (env_variant < 0) {
         const char *env = getenv("KFB200_PAIR_KERNEL");
-        variant = env ? atoi(env) : 2;
+        env_variant = env ? atoi(env) : 0;
     }
+    const int variant = env_variant ? env_variant : (f->precision ? 1 : 2);
     auto kern = variant == 2
                     ? (f->precision ? (split ? pair_dense_kernel<true, true> : pair_dense_kernel<true, false>)
                                     : (split ? pair_dense_kernel<false, true> : pair_dense_kernel<false, false>))
