@@ -129,15 +129,32 @@ fk_smem_kernel(const __grid_constant__ kf_chain_t c, const double *__restrict__ 
     const int L = c.n_links, D = c.n_dof, n = c.n_atoms;
     const double *theta = theta_all + (size_t)b * D;
 
-    for (int l = threadIdx.x; l < L; l += blockDim.x) {
-        Xf a;
-        if (l == 0 || c.link_dof[l] < 0) {
-            a = xf_identity();
-        } else {
-            const int p = c.link_parent[l];
-            a = local_transform(c.link_axis0 + 3 * l, theta[c.link_dof[l]], c.link_body0 + 3 * p);
+    {
+        // local transforms; the chain tables and angles of U links per thread are
+        // loaded ahead of the math (latency of one round, not U)
+        const int32_t *__restrict__ link_dof = c.link_dof;
+        const int32_t *__restrict__ link_parent = c.link_parent;
+        constexpr int U = 4;
+        for (int l0 = threadIdx.x; l0 < L; l0 += U * blockDim.x) {
+            int dof[U], par[U];
+            double th[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int l = l0 + u * blockDim.x;
+                dof[u] = (l < L && l != 0) ? link_dof[l] : -1;
+                par[u] = (l < L && l != 0) ? link_parent[l] : 0;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) th[u] = dof[u] >= 0 ? theta[dof[u]] : 0.0;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int l = l0 + u * blockDim.x;
+                if (l >= L) break;
+                const Xf a = dof[u] < 0 ? xf_identity()
+                                        : local_transform(c.link_axis0 + 3 * l, th[u], c.link_body0 + 3 * par[u]);
+                xf_store(S + FKS_STRIDE * l, a);
+            }
         }
-        xf_store(S + FKS_STRIDE * l, a);
     }
     __syncthreads();
 
@@ -177,30 +194,48 @@ fk_smem_kernel(const __grid_constant__ kf_chain_t c, const double *__restrict__ 
         __syncthreads();
     }
     // T with the current joint axes U_l = M_l axis0_l (chain.py:257); ground keeps 0
-    double *T = T_all + (size_t)b * L * KF_XF_STRIDE;
-    for (int e = threadIdx.x; e < L * KF_XF_STRIDE; e += blockDim.x) {
-        const int l = e / KF_XF_STRIDE, q = e - l * KF_XF_STRIDE;
+    double *__restrict__ T = T_all + (size_t)b * L * KF_XF_STRIDE;
+    const int32_t *__restrict__ link_dof = c.link_dof;
+    const double *__restrict__ axis0 = c.link_axis0;
+    for (int l = threadIdx.x; l < L; l += blockDim.x) {
         const double *src = S + FKS_STRIDE * l;
-        double v;
-        if (q < 12) {
-            v = src[q];
-        } else if (q < 15 && l != 0 && c.link_dof[l] >= 0) {
-            const int r = q - 12;
-            const double *a = c.link_axis0 + 3 * l;
-            v = src[3 * r] * a[0] + src[3 * r + 1] * a[1] + src[3 * r + 2] * a[2];
-        } else {
-            v = 0.0;
-        }
-        T[e] = v;
+        double *dst = T + (size_t)KF_XF_STRIDE * l;
+        const bool joint = l != 0 && link_dof[l] >= 0;
+        const double a0 = axis0[3 * l], a1 = axis0[3 * l + 1], a2 = axis0[3 * l + 2];
+        double v[KF_XF_STRIDE];
+#pragma unroll
+        for (int q = 0; q < 12; ++q) v[q] = src[q];
+#pragma unroll
+        for (int r = 0; r < 3; ++r) v[12 + r] = joint ? src[3 * r] * a0 + src[3 * r + 1] * a1 + src[3 * r + 2] * a2 : 0.0;
+        v[15] = 0.0;
+        double2 *d2 = reinterpret_cast<double2 *>(dst);
+#pragma unroll
+        for (int q = 0; q < KF_XF_STRIDE / 2; ++q) d2[q] = make_double2(v[2 * q], v[2 * q + 1]);
     }
-    // positions pos_a = P_l + M_l zrel_a (fk_positions_kernel's arithmetic)
-    double *pos = pos_all + (size_t)b * n * 3;
-    for (int a = threadIdx.x; a < n; a += blockDim.x) {
-        const double *t = S + FKS_STRIDE * c.atom_link[a];
-        const double zx = c.atom_zrel[3 * a], zy = c.atom_zrel[3 * a + 1], zz = c.atom_zrel[3 * a + 2];
-        pos[3 * a] = t[9] + (t[0] * zx + t[1] * zy + t[2] * zz);
-        pos[3 * a + 1] = t[10] + (t[3] * zx + t[4] * zy + t[5] * zz);
-        pos[3 * a + 2] = t[11] + (t[6] * zx + t[7] * zy + t[8] * zz);
+    // positions pos_a = P_l + M_l zrel_a (fk_positions_kernel's arithmetic);
+    // the chain tables are loaded ahead of the stores (no aliasing with pos)
+    double *__restrict__ pos = pos_all + (size_t)b * n * 3;
+    const int32_t *__restrict__ atom_link = c.atom_link;
+    const double *__restrict__ zrel = c.atom_zrel;
+    constexpr int U = 4;
+    for (int a0 = threadIdx.x; a0 < n; a0 += U * blockDim.x) {
+        int lk[U];
+        double z[U][3];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int a = a0 + u * blockDim.x;
+            lk[u] = a < n ? atom_link[a] : 0;
+            for (int q = 0; q < 3; ++q) z[u][q] = a < n ? zrel[3 * a + q] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int a = a0 + u * blockDim.x;
+            if (a >= n) break;
+            const double *t = S + FKS_STRIDE * lk[u];
+            pos[3 * a] = t[9] + (t[0] * z[u][0] + t[1] * z[u][1] + t[2] * z[u][2]);
+            pos[3 * a + 1] = t[10] + (t[3] * z[u][0] + t[4] * z[u][1] + t[5] * z[u][2]);
+            pos[3 * a + 2] = t[11] + (t[6] * z[u][0] + t[7] * z[u][1] + t[8] * z[u][2]);
+        }
     }
 }
 
