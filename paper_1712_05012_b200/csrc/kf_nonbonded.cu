@@ -68,6 +68,7 @@ struct PairConst {
     float kap_inv, cell;
     float f64_d2;                // pairs closer than this (A^2) take the fp64 formulas
     int dconst, uniform;
+    int te_is_cut;               // elec threshold within 1e-6 A^2 of the pair cut-off
 };
 
 __device__ __noinline__ int slow_class(const int32_t *tp, const int32_t *tgp, const int32_t *tgg,
@@ -148,10 +149,16 @@ KF_DEV void pair_eval(const kf_field_t &f, const PairConst &pc, float4 hi, float
             cls = slow_class(f.tparent, f.tgp, f.tggp, f.tres, f.tchain, i, j);
         }
     }
+#ifdef PAIR_SEL_WEIGHTS
     const float we = cls == 4 ? pc.we[3] : cls == 3 ? pc.we[2] : cls == 2 ? pc.we[1] : pc.we[0];
     const float wv = cls == 4 ? pc.wv[3] : cls == 3 ? pc.wv[2] : cls == 2 ? pc.wv[1] : pc.wv[0];
+#else
+    const float we = pc.we[cls - 1], wv = pc.wv[cls - 1];   // constant-bank loads, indexed
+#endif
+    // exact recomputation near a threshold: |d2 - t| <= band for t in {cut, te, tv}
+    // (te == cut to ~1e-14 for the default cut-offs: pc.te_is_cut folds the test)
     const bool exact = F64 || fabsf(d2f - cut2f) <= band || fabsf(d2f - tvf) <= band ||
-                       fabsf(d2f - tef) <= band || d2f < pc.f64_d2;
+                       (!pc.te_is_cut && fabsf(d2f - tef) <= band) || d2f < pc.f64_d2;
     if (exact) {
         slow_pair<T>(F64, &f, pos_i, pos_j, i, j, cls, out, &pce, &pcv, st);
         return;
@@ -192,7 +199,7 @@ KF_DEV void pair_eval(const kf_field_t &f, const PairConst &pc, float4 hi, float
 // (throughput: ensembles).
 template <bool F64, bool SPLIT>
 __global__ void __launch_bounds__((SPLIT ? SPLIT_WARPS : PAIR_WARPS) * 32, SPLIT ? 1 : PAIR_MINB_W)
-pair_kernel(const __grid_constant__ kf_field_t f, const PairConst pc, int B, int n, const unsigned long long *__restrict__ keys,
+pair_kernel(const __grid_constant__ kf_field_t f, const __grid_constant__ PairConst pc, int B, int n, const unsigned long long *__restrict__ keys,
             const int32_t *__restrict__ cnt, const int32_t *__restrict__ start, const int32_t *__restrict__ occ,
             const int32_t *__restrict__ occ_count, const int32_t *__restrict__ chunk_pre,
             const int32_t *__restrict__ chunk_offset, const float4 *__restrict__ s_hi,
@@ -456,7 +463,7 @@ pair_kernel(const __grid_constant__ kf_field_t f, const PairConst pc, int B, int
 // own pairs in j order: deterministic, no per-pair shared-memory traffic.
 template <bool F64, bool SPLIT>
 __global__ void __launch_bounds__((SPLIT ? SPLIT_WARPS : PAIR_WARPS) * 32, SPLIT ? 1 : PAIR_MINB_W)
-pair_dense_kernel(const __grid_constant__ kf_field_t f, const PairConst pc, int B, int n,
+pair_dense_kernel(const __grid_constant__ kf_field_t f, const __grid_constant__ PairConst pc, int B, int n,
                   const unsigned long long *__restrict__ keys, const int32_t *__restrict__ cnt,
                   const int32_t *__restrict__ start, const int32_t *__restrict__ occ,
                   const int32_t *__restrict__ occ_count, const int32_t *__restrict__ chunk_pre,
@@ -781,6 +788,7 @@ int kf_pairs_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s) {
     }
     pc.f64_d2 = f64_below * f64_below;
     pc.dconst = f->dielectric_const; pc.uniform = f->uniform_weights;
+    pc.te_is_cut = fabs(f->thr_elec2 - f->cut_pair2) < 1e-6 ? 1 : 0;
     kern<<<resident_grid(kern, nw * 32, dyn), nw * 32, dyn, s>>>(
         *f, pc, w->B, n, w->cell_key, w->cell_cnt, w->cell_start, w->occ, w->occ_count, w->chunk_pre, w->chunk_offset,
         reinterpret_cast<const float4 *>(w->s_hi), reinterpret_cast<const float4 *>(w->s_lo),
