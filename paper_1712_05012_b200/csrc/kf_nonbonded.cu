@@ -515,8 +515,8 @@ pair_dense_kernel(const __grid_constant__ kf_field_t f, const __grid_constant__ 
         unpack_cell((long long)keys[hb + slot], cx, cy, cz);
         const int s0 = start[hb + slot], c = cnt[hb + slot];
         const int ci_n = min(32, c - ic);
-        // lane -> (owner slot, j phase): chunks of <= 16 / <= 8 atoms use 2 / 4 phases
-        const int nph = ci_n > 16 ? 1 : ci_n > 8 ? 2 : 4;
+        // lane -> (owner slot, j phase): chunks of <= 16 / 8 / 4 / 2 atoms use 2 / 4 / 8 / 16 phases
+        const int nph = ci_n > 16 ? 1 : ci_n > 8 ? 2 : ci_n > 4 ? 4 : ci_n > 2 ? 8 : 16;
         const int wi = 32 / nph, oi = lane % wi, ph = lane / wi;
         const bool own = oi < ci_n;
         const size_t ki = nb + s0 + ic + (own ? oi : 0);
