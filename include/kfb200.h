@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define KF_ABI_VERSION 5
+#define KF_ABI_VERSION 6
 
 /* ---- static chain tables (uploaded once per chain) ------------------------
  * Links are in the reference's topological order (parent < index, ground = 0),
@@ -128,7 +128,7 @@ typedef struct {
     int32_t nb_cap;                 /* solvation neighbour capacity per atom       */
     int32_t record_theta;           /* store theta per iteration                   */
     int32_t max_records;            /* record ring capacity (iterations)           */
-    int32_t _pad;
+    int32_t pair_chunk;             /* atoms per pair-kernel work item: 4/8/16/32, 0 = auto */
     double  *theta;                 /* [B][D]                                      */
     const uint8_t *frozen;          /* [B][D]                                      */
     double  *link_T;                /* [B][L][16]: rotation (row-major 9), joint point (3), axis (3), pad */

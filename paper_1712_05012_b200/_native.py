@@ -13,7 +13,7 @@ import os
 from .errors import NativeLibraryError
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libkfb200.so")
-ABI_VERSION = 5
+ABI_VERSION = 6
 
 P = C.c_void_p
 I32 = C.c_int32
@@ -54,7 +54,7 @@ class KfStatus(C.Structure):
 
 class KfBatch(C.Structure):
     _fields_ = [("B", I32), ("n_buckets", I32), ("nb_cap", I32), ("record_theta", I32),
-                ("max_records", I32), ("_pad", I32)] + [
+                ("max_records", I32), ("pair_chunk", I32)] + [
         (name, P) for name in (
             "theta", "frozen", "link_T", "fk_scratch", "pos", "forces", "cell_key", "cell_cnt", "cell_start",
             "occ", "occ_count", "occ_offset", "chunk_pre", "chunk_count", "chunk_offset",

@@ -41,6 +41,21 @@ KF_DEV double np_mod360(double a) {
 // ---- rigid transforms: [M row-major 3x3 | p], x -> M x + p ----------------
 // link_T rows are KF_XF_STRIDE doubles: M (9), joint point P (3), axis U (3), pad
 #define KF_XF_STRIDE 16
+// Pair-kernel work items: occupied cells cut into i-chunks of at most `chunk`
+// atoms (a power of two <= 32).  Small chunks keep the dense kernel's lanes busy
+// (a chunk of c atoms runs 32 / c j-phases); large ones amortise the per-item
+// neighbour staging over more atoms.  Measured optimum on B200 (C2 chains):
+// 4 below 4k atoms per launch, 8 below 1M, 16 above; the fp64 pair mode (the
+// compacted kernel, lane = one of 32 owners) keeps 32.  kf_batch_t.pair_chunk
+// overrides (0 = this rule).  Part of the work decomposition, so results are
+// bitwise reproducible for a given (B, n) but not across chunk sizes.
+inline int kf_pair_chunk(int B, int n, int requested, int precision) {
+    if (requested == 4 || requested == 8 || requested == 16 || requested == 32) return requested;
+    if (precision) return 32;
+    const long long atoms = (long long)B * n;
+    return atoms < 4000 ? 4 : atoms < 1000000 ? 8 : 16;
+}
+
 struct Xf { double m[9]; double p[3]; };
 
 KF_DEV Xf xf_identity() {

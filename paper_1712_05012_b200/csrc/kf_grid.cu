@@ -109,7 +109,7 @@ __device__ __forceinline__ int block_excl_scan(int v, int *wsum) {
 // counts (-> cell_start, by slot) and of their 32-atom i-chunks (-> chunk_pre,
 // by list position; the pair kernel's work items are (cell, i-chunk)).
 __global__ void __launch_bounds__(1024)
-cell_scan_kernel(int H, const int32_t *__restrict__ occ, const int32_t *__restrict__ occ_count,
+cell_scan_kernel(int H, int chunk, const int32_t *__restrict__ occ, const int32_t *__restrict__ occ_count,
                  const int32_t *__restrict__ cnt, int32_t *__restrict__ start, int32_t *__restrict__ chunk_pre,
                  int32_t *__restrict__ chunk_count, const kf_status_t *status) {
     const int b = blockIdx.x;
@@ -125,7 +125,7 @@ cell_scan_kernel(int H, const int32_t *__restrict__ occ, const int32_t *__restri
     for (int k = lo; k < hi; ++k) {
         const int c = cb[ob[k]];
         local += c;
-        lchunk += (c + 31) >> 5;
+        lchunk += (c + chunk - 1) / chunk;
     }
     __shared__ int wsum[32];
     int run = block_excl_scan(local, wsum);
@@ -133,7 +133,7 @@ cell_scan_kernel(int H, const int32_t *__restrict__ occ, const int32_t *__restri
     for (int k = lo; k < hi; ++k) {
         const int c = cb[ob[k]];
         sb[ob[k]] = run; run += c;
-        pb[k] = crun; crun += (c + 31) >> 5;
+        pb[k] = crun; crun += (c + chunk - 1) / chunk;
     }
     if (threadIdx.x == blockDim.x - 1) chunk_count[b] = crun;
 }
@@ -269,7 +269,7 @@ int kf_bin_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s) {
     bin_insert_kernel<<<kf_blocks(total, 256), 256, 0, s>>>(*f, B, n, w->pos, w->cell_key, w->cell_cnt, w->occ,
                                                             w->occ_count, w->atom_slot, w->atom_rank, w->status);
     KF_LAUNCH_CHECK("bin_insert_kernel");
-    cell_scan_kernel<<<B, 1024, 0, s>>>(H, w->occ, w->occ_count, w->cell_cnt, w->cell_start, w->chunk_pre,
+    cell_scan_kernel<<<B, 1024, 0, s>>>(H, kf_pair_chunk(B, n, w->pair_chunk, f->precision), w->occ, w->occ_count, w->cell_cnt, w->cell_start, w->chunk_pre,
                                          w->chunk_count, w->status);
     KF_LAUNCH_CHECK("cell_scan_kernel");
     occ_prefix_kernel<<<1, 1024, 0, s>>>(B, w->occ_count, w->occ_offset, w->chunk_count, w->chunk_offset,

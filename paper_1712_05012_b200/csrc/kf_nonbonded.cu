@@ -199,7 +199,7 @@ KF_DEV void pair_eval(const kf_field_t &f, const PairConst &pc, float4 hi, float
 // (throughput: ensembles).
 template <bool F64, bool SPLIT>
 __global__ void __launch_bounds__((SPLIT ? SPLIT_WARPS : PAIR_WARPS) * 32, SPLIT ? 1 : PAIR_MINB_W)
-pair_kernel(const __grid_constant__ kf_field_t f, const __grid_constant__ PairConst pc, int B, int n, const unsigned long long *__restrict__ keys,
+pair_kernel(const __grid_constant__ kf_field_t f, const __grid_constant__ PairConst pc, int B, int n, int chunk, const unsigned long long *__restrict__ keys,
             const int32_t *__restrict__ cnt, const int32_t *__restrict__ start, const int32_t *__restrict__ occ,
             const int32_t *__restrict__ occ_count, const int32_t *__restrict__ chunk_pre,
             const int32_t *__restrict__ chunk_offset, const float4 *__restrict__ s_hi,
@@ -250,14 +250,14 @@ pair_kernel(const __grid_constant__ kf_field_t f, const __grid_constant__ PairCo
             if (chunk_pre[hb + mid] <= local) klo = mid; else khi = mid - 1;
         }
         const int slot = occ[hb + klo];
-        const int ic = (local - chunk_pre[hb + klo]) << 5;
+        const int ic = (local - chunk_pre[hb + klo]) * chunk;
         int cx, cy, cz;
         unpack_cell((long long)keys[hb + slot], cx, cy, cz);
         const int s0 = start[hb + slot], c = cnt[hb + slot];
         double ee = 0.0, ev = 0.0;   // chunk totals (per computing lane)
         int ce = 0, cv = 0;          // elec / vdW cut-off partners (per computing lane)
         {
-            const int ci_n = min(32, c - ic);
+            const int ci_n = min(chunk, c - ic);
             const bool valid = lane < ci_n;
             if ((!SPLIT || warp == 0) && valid) {
                 const size_t ki = nb + s0 + ic + lane;
@@ -463,7 +463,7 @@ pair_kernel(const __grid_constant__ kf_field_t f, const __grid_constant__ PairCo
 // own pairs in j order: deterministic, no per-pair shared-memory traffic.
 template <bool F64, bool SPLIT>
 __global__ void __launch_bounds__((SPLIT ? SPLIT_WARPS : PAIR_WARPS) * 32, SPLIT ? 1 : PAIR_MINB_W)
-pair_dense_kernel(const __grid_constant__ kf_field_t f, const __grid_constant__ PairConst pc, int B, int n,
+pair_dense_kernel(const __grid_constant__ kf_field_t f, const __grid_constant__ PairConst pc, int B, int n, int chunk,
                   const unsigned long long *__restrict__ keys, const int32_t *__restrict__ cnt,
                   const int32_t *__restrict__ start, const int32_t *__restrict__ occ,
                   const int32_t *__restrict__ occ_count, const int32_t *__restrict__ chunk_pre,
@@ -510,11 +510,11 @@ pair_dense_kernel(const __grid_constant__ kf_field_t f, const __grid_constant__ 
             if (chunk_pre[hb + mid] <= local) klo = mid; else khi = mid - 1;
         }
         const int slot = occ[hb + klo];
-        const int ic = (local - chunk_pre[hb + klo]) << 5;
+        const int ic = (local - chunk_pre[hb + klo]) * chunk;
         int cx, cy, cz;
         unpack_cell((long long)keys[hb + slot], cx, cy, cz);
         const int s0 = start[hb + slot], c = cnt[hb + slot];
-        const int ci_n = min(32, c - ic);
+        const int ci_n = min(chunk, c - ic);
         // lane -> (owner slot, j phase): chunks of <= 16 / 8 / 4 / 2 atoms use 2 / 4 / 8 / 16 phases
         const int nph = ci_n > 16 ? 1 : ci_n > 8 ? 2 : ci_n > 4 ? 4 : ci_n > 2 ? 8 : 16;
         const int wi = 32 / nph, oi = lane % wi, ph = lane / wi;
@@ -790,7 +790,7 @@ int kf_pairs_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s) {
     pc.dconst = f->dielectric_const; pc.uniform = f->uniform_weights;
     pc.te_is_cut = fabs(f->thr_elec2 - f->cut_pair2) < 1e-6 ? 1 : 0;
     kern<<<resident_grid(kern, nw * 32, dyn), nw * 32, dyn, s>>>(
-        *f, pc, w->B, n, w->cell_key, w->cell_cnt, w->cell_start, w->occ, w->occ_count, w->chunk_pre, w->chunk_offset,
+        *f, pc, w->B, n, kf_pair_chunk(w->B, n, w->pair_chunk, f->precision), w->cell_key, w->cell_cnt, w->cell_start, w->occ, w->occ_count, w->chunk_pre, w->chunk_offset,
         reinterpret_cast<const float4 *>(w->s_hi), reinterpret_cast<const float4 *>(w->s_lo),
         reinterpret_cast<const double4 *>(w->s_pos), reinterpret_cast<const float4 *>(w->s_par),
         reinterpret_cast<const int4 *>(w->s_aux), reinterpret_cast<const int4 *>(w->s_tree),
