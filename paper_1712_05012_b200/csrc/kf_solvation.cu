@@ -313,10 +313,9 @@ KF_DEV void solv_atom(const kf_field_t &f, const SolvArgs &A, int b, int i, int 
     if (status[b].done) return;
     extern __shared__ __align__(16) unsigned char smem[];
     const GroupSmem S = carve_group(smem, nb_cap, f.n_groups);
-    __shared__ int nn, next_group;
+    __shared__ int nn, next_group, covered_s;
     __shared__ long long acc_i_s[3];
-    __shared__ double red[32];
-    if (threadIdx.x == 0) { nn = 0; next_group = 0; acc_i_s[0] = acc_i_s[1] = acc_i_s[2] = 0; }
+    if (threadIdx.x == 0) { nn = 0; next_group = 0; covered_s = 0; acc_i_s[0] = acc_i_s[1] = acc_i_s[2] = 0; }
     __syncthreads();
 
     const size_t ai = (size_t)b * n + i;
@@ -552,12 +551,12 @@ KF_DEV void solv_atom(const kf_field_t &f, const SolvArgs &A, int b, int i, int 
             }
         }
     }
-    const double cov_total = block_sum((double)covered, red);
-    for (int s = 0; s < 3; ++s) {
-        const long long v = warp_sum_ll(acc_i[s]);
-        if (lane == 0 && v != 0)
-            atomicAdd(reinterpret_cast<unsigned long long *>(&acc_i_s[s]), (unsigned long long)v);
-    }
+    // integer totals: order-free shared atomics (no block-wide reduction tree)
+    const int wcov = __reduce_add_sync(0xffffffffu, covered);
+    if (lane == 0 && wcov) atomicAdd(&covered_s, wcov);
+    for (int s = 0; s < 3; ++s)
+        if (acc_i[s] != 0)
+            atomicAdd(reinterpret_cast<unsigned long long *>(&acc_i_s[s]), (unsigned long long)acc_i[s]);
     __syncthreads();
     long long *acc = A.solv_acc + (size_t)b * n * 3;
     for (int m = threadIdx.x; m < 3 * count; m += blockDim.x) {
@@ -572,7 +571,7 @@ KF_DEV void solv_atom(const kf_field_t &f, const SolvArgs &A, int b, int i, int 
                 atomicAdd(reinterpret_cast<unsigned long long *>(&acc[3 * (size_t)i + s]),
                           (unsigned long long)acc_i_s[s]);
         // f_exp = (N - covered) / N; a_exp = f_exp * (4 pi R_off^2); term = gamma * a_exp
-        const long long cov = (long long)cov_total;
+        const long long cov = covered_s;
         const double f_exp = (double)(f.n_samples - cov) / (double)f.n_samples;
         const double a_exp = xmul(f_exp, xmul(f.four_pi, f.r_off2[i]));
         A.cav_atom[ai] = xmul(f.gamma[i], a_exp);
