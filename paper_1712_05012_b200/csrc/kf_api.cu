@@ -30,7 +30,7 @@ int kf_wrench_launch(const kf_chain_t *c, int B, const double *pos, const double
                      const kf_status_t *status, cudaStream_t s);
 int kf_torque_launch(const kf_chain_t *c, const kf_field_t *f, kf_batch_t *w, const double *link_T,
                      const double *wrench, double *side_tot, double *bb_suffix, double *tau,
-                     const kf_step_t *step, int mode, cudaStream_t s);
+                     const kf_step_t *step, int mode, cudaStream_t s, int fuse_wrench = 0);
 int kf_kcm_step_launch(const double *tau, const double *theta, const uint8_t *frozen, int D, double kappa,
                        double *theta_out, double *deltas, cudaStream_t s);
 
@@ -60,8 +60,8 @@ int enqueue_iteration(const kf_chain_t *c, const kf_field_t *f, kf_batch_t *w, c
     if (kf_bin_launch(f, w, n, s)) return 1;
     if (kf_pairs_launch(f, w, n, s)) return 1;
     if (f->solvation && kf_solvation_launch(f, w, n, f->n_solv, f->solv_atoms, s)) return 1;
-    if (kf_wrench_launch(c, w->B, w->pos, w->forces, w->wrench, w->status, s)) return 1;
-    if (kf_torque_launch(c, f, w, w->link_T, w->wrench, w->side_tot, w->bb_suffix, w->tau, st, 1, s)) return 1;
+    // wrenches (fused into the torque CTA when they fit in shared memory) + torques + step
+    if (kf_torque_launch(c, f, w, w->link_T, w->wrench, w->side_tot, w->bb_suffix, w->tau, st, 1, s, 1)) return 1;
     return 0;
 }
 }  // namespace
@@ -123,9 +123,9 @@ int kf_energy_reduce(const kf_field_t *f, kf_batch_t *w, int n, void *stream) {
 int kf_torques_step(const kf_chain_t *c, const kf_field_t *f, kf_batch_t *w, const kf_step_t *step,
                     void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
-    if (kf_wrench_launch(c, w->B, w->pos, w->forces, w->wrench, w->status, s)) return 1;
+    if (!step && kf_wrench_launch(c, w->B, w->pos, w->forces, w->wrench, w->status, s)) return 1;
     return kf_torque_launch(c, f, w, w->link_T, w->wrench, w->side_tot, w->bb_suffix, w->tau, step,
-                            step ? 1 : 0, s);
+                            step ? 1 : 0, s, step ? 1 : 0);
 }
 
 static int fold_graph(const kf_chain_t *c, const kf_field_t *f, kf_batch_t *w, const kf_step_t *step,

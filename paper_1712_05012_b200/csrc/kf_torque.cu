@@ -34,16 +34,9 @@ KF_DEV double project(const double *X, const W6 &w) {
 
 // F_l = sum F_a, T_l = sum r_a x F_a over the link's atoms in ascending order
 // (np.cross + np.bincount, kcm.py:181-187): exact same roundings.
-__global__ void wrench_kernel(kf_chain_t c, int B, const double *__restrict__ pos_all,
-                              const double *__restrict__ f_all, double *__restrict__ wrench_all,
-                              const kf_status_t *status) {
-    const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    const int L = c.n_links, n = c.n_atoms;
-    if (gid >= (long long)B * L) return;
-    const int b = (int)(gid / L), l = (int)(gid % L);
-    if (status && (status[b].done || status[b].error)) return;
-    const double *pos = pos_all + (size_t)b * n * 3;
-    const double *frc = f_all + (size_t)b * n * 3;
+// One link's wrench: F = sum F_a, T = sum r_a x F_a over its atoms in ascending
+// order (np.cross + np.bincount, kcm.py:181-187): exact same roundings.
+KF_DEV void link_wrench(const kf_chain_t &c, int l, const double *pos, const double *frc, double *o) {
     double F0 = 0.0, F1 = 0.0, F2 = 0.0, T0 = 0.0, T1 = 0.0, T2 = 0.0;
     for (int e = c.link_atom_off[l]; e < c.link_atom_off[l + 1]; ++e) {
         const int a = c.link_atoms[e];
@@ -54,8 +47,18 @@ __global__ void wrench_kernel(kf_chain_t c, int B, const double *__restrict__ po
         T1 = xadd(T1, xsub(xmul(r2, g0), xmul(r0, g2)));
         T2 = xadd(T2, xsub(xmul(r0, g1), xmul(r1, g0)));
     }
-    double *o = wrench_all + 6 * gid;
     o[0] = F0; o[1] = F1; o[2] = F2; o[3] = T0; o[4] = T1; o[5] = T2;
+}
+
+__global__ void wrench_kernel(kf_chain_t c, int B, const double *__restrict__ pos_all,
+                              const double *__restrict__ f_all, double *__restrict__ wrench_all,
+                              const kf_status_t *status) {
+    const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int L = c.n_links, n = c.n_atoms;
+    if (gid >= (long long)B * L) return;
+    const int b = (int)(gid / L), l = (int)(gid % L);
+    if (status && (status[b].done || status[b].error)) return;
+    link_wrench(c, l, pos_all + (size_t)b * n * 3, f_all + (size_t)b * n * 3, wrench_all + 6 * gid);
 }
 
 // Steps 5-6 of a fold iteration (all threads of the CTA): energies and
@@ -125,7 +128,8 @@ struct TorqueArgs {
 // One CTA per trajectory.  mode: 0 = torques only (API), 1 = fold iteration,
 // 2 = energy reduction only (Field.evaluate)
 __global__ void __launch_bounds__(TQ_THREADS)
-torque_step_kernel(kf_chain_t c, kf_field_t f, TorqueArgs ta, kf_batch_t w, kf_step_t step, int mode) {
+torque_step_kernel(kf_chain_t c, kf_field_t f, TorqueArgs ta, kf_batch_t w, kf_step_t step, int mode,
+                   int fuse_wrench) {
     const int b = blockIdx.x;
     kf_status_t *st = w.status ? w.status + b : nullptr;
     if (st && st->done) return;
@@ -139,6 +143,14 @@ torque_step_kernel(kf_chain_t c, kf_field_t f, TorqueArgs ta, kf_batch_t w, kf_s
     const int L = c.n_links, D = c.n_dof, R = c.n_res, nb = c.n_bb;
     const double *T = ta.link_T + (size_t)b * L * KF_XF_STRIDE;
     const double *Wr = ta.wrench + (size_t)b * L * 6;
+    if (fuse_wrench) {   // wrenches of this iteration straight into shared memory
+        extern __shared__ __align__(16) double wsm[];   // [L][6]
+        const int n = c.n_atoms;
+        for (int l = threadIdx.x; l < L; l += blockDim.x)
+            link_wrench(c, l, w.pos + (size_t)b * n * 3, w.forces + (size_t)b * n * 3, wsm + 6 * l);
+        __syncthreads();
+        Wr = wsm;
+    }
     double *side = ta.side_tot + (size_t)b * R * 6;
     double *suf = ta.bb_suffix + (size_t)b * nb * 6;
     double *tau = ta.tau + (size_t)b * D;
@@ -399,7 +411,7 @@ int kf_wrench_launch(const kf_chain_t *c, int B, const double *pos, const double
 
 int kf_torque_launch(const kf_chain_t *c, const kf_field_t *f, kf_batch_t *w, const double *link_T,
                      const double *wrench, double *side_tot, double *bb_suffix, double *tau,
-                     const kf_step_t *step, int mode, cudaStream_t s) {
+                     const kf_step_t *step, int mode, cudaStream_t s, int fuse_wrench) {
     TorqueArgs ta{link_T, wrench, side_tot, bb_suffix, tau};
     kf_step_t st{};
     if (step) st = *step;
@@ -407,6 +419,8 @@ int kf_torque_launch(const kf_chain_t *c, const kf_field_t *f, kf_batch_t *w, co
     if (f) fz = *f;
     const int n_seg = (c->n_bb + TQ_SEG - 1) / TQ_SEG;
     if (mode == 1 && n_seg > 1 && w->B * n_seg <= 4 * 148 && w->fk_scratch && bb_suffix) {
+        if (fuse_wrench &&
+            kf_wrench_launch(c, w->B, w->pos, w->forces, const_cast<double *>(wrench), w->status, s)) return 1;
         torque_seg_kernel<<<dim3(n_seg, w->B), TQ_THREADS, 0, s>>>(*c, ta, *w, n_seg);
         KF_LAUNCH_CHECK("torque_seg_kernel");
         torque_seg_project_kernel<<<dim3(n_seg, w->B), TQ_THREADS, 0, s>>>(*c, fz, ta, *w, n_seg);
@@ -415,7 +429,22 @@ int kf_torque_launch(const kf_chain_t *c, const kf_field_t *f, kf_batch_t *w, co
         KF_LAUNCH_CHECK("torque_seg_finish_kernel");
         return 0;
     }
-    torque_step_kernel<<<w->B, TQ_THREADS, 0, s>>>(*c, fz, ta, *w, st, mode);
+    // a fold iteration computes its own wrenches (pos, forces of this batch) in
+    // shared memory when they fit; otherwise the separate wrench pass
+    const size_t wsm = (size_t)c->n_links * 6 * sizeof(double);
+    const bool fuse = fuse_wrench && wsm <= 96 * 1024;
+    if (fuse_wrench && !fuse) {
+        if (kf_wrench_launch(c, w->B, w->pos, w->forces, const_cast<double *>(wrench), w->status, s)) return 1;
+    }
+    if (fuse) {
+        static size_t opted = 0;
+        if (wsm > opted) {
+            KF_CUDA(cudaFuncSetAttribute(torque_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm),
+                    "torque smem");
+            opted = wsm;
+        }
+    }
+    torque_step_kernel<<<w->B, TQ_THREADS, fuse ? wsm : 0, s>>>(*c, fz, ta, *w, st, mode, fuse ? 1 : 0);
     KF_LAUNCH_CHECK("torque_step_kernel");
     return 0;
 }
