@@ -180,32 +180,23 @@ __global__ void bin_scatter_kernel(kf_field_t f, int B, int n, const int32_t *__
 constexpr int FIN_WARPS = 4;
 constexpr int FIN_CAP = 1024;
 
-__global__ void __launch_bounds__(FIN_WARPS * 32)
-bin_finalize_kernel(const __grid_constant__ kf_field_t f, int B, int n, const double *__restrict__ pos,
-                    const unsigned long long *__restrict__ keys, const int32_t *__restrict__ occ,
-                    const int32_t *__restrict__ occ_offset, const int32_t *__restrict__ cnt,
-                    const int32_t *__restrict__ start, int32_t *__restrict__ sorted_atom,
-                    float4 *__restrict__ s_hi, float4 *__restrict__ s_lo,
-                    double4 *__restrict__ s_pos, float4 *__restrict__ s_par,
-                    int4 *__restrict__ s_aux, int4 *__restrict__ s_tree,
-                    float4 *__restrict__ cell_box, const kf_status_t *status) {
-    __shared__ int buf[FIN_WARPS][FIN_CAP];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int total = occ_offset[B];
-    // persistent: warps stride over the occupied cells of all trajectories
-    for (int item = blockIdx.x * FIN_WARPS + warp; item < total; item += gridDim.x * FIN_WARPS) {
-    const int b = item_owner(occ_offset, B, item);
-    const size_t H = (size_t)1 << f.hash_bits;
-    const int slot = occ[b * H + (item - occ_offset[b])];
+// One occupied cell, one warp: rank sort of its members by atom index, then the
+// cell-ordered SoA and the members' bounding box.  buf: FIN_CAP ints of this warp.
+KF_DEV void finalize_cell(const kf_field_t &f, int b, int n, size_t H, int slot, int lane, int *buf, int cap,
+                          const double *__restrict__ pos, const unsigned long long *__restrict__ keys,
+                          const int32_t *__restrict__ cnt, const int32_t *__restrict__ start,
+                          int32_t *__restrict__ sorted_atom, float4 *__restrict__ s_hi, float4 *__restrict__ s_lo,
+                          double4 *__restrict__ s_pos, float4 *__restrict__ s_par, int4 *__restrict__ s_aux,
+                          int4 *__restrict__ s_tree, float4 *__restrict__ cell_box) {
     const int s0 = start[b * H + slot], c = cnt[b * H + slot];
     int32_t *ids = sorted_atom + (size_t)b * n + s0;
-    if (c <= FIN_CAP) {
-        for (int k = lane; k < c; k += 32) buf[warp][k] = ids[k];
+    if (c <= cap) {
+        for (int k = lane; k < c; k += 32) buf[k] = ids[k];
         __syncwarp();
         for (int k = lane; k < c; k += 32) {
-            const int v = buf[warp][k];
+            const int v = buf[k];
             int rank = 0;
-            for (int m = 0; m < c; ++m) rank += buf[warp][m] < v;
+            for (int m = 0; m < c; ++m) rank += buf[m] < v;
             ids[rank] = v;
         }
     } else if (lane == 0) {   // pathological cell: serial insertion sort
@@ -254,14 +245,173 @@ bin_finalize_kernel(const __grid_constant__ kf_field_t f, int B, int n, const do
         cell_box[2 * (b * H + slot)] = make_float4(bl[0], bl[1], bl[2], 0.f);
         cell_box[2 * (b * H + slot) + 1] = make_float4(bh[0], bh[1], bh[2], 0.f);
     }
-    __syncwarp();
+}
+
+__global__ void __launch_bounds__(FIN_WARPS * 32)
+bin_finalize_kernel(const __grid_constant__ kf_field_t f, int B, int n, const double *__restrict__ pos,
+                    const unsigned long long *__restrict__ keys, const int32_t *__restrict__ occ,
+                    const int32_t *__restrict__ occ_offset, const int32_t *__restrict__ cnt,
+                    const int32_t *__restrict__ start, int32_t *__restrict__ sorted_atom,
+                    float4 *__restrict__ s_hi, float4 *__restrict__ s_lo,
+                    double4 *__restrict__ s_pos, float4 *__restrict__ s_par,
+                    int4 *__restrict__ s_aux, int4 *__restrict__ s_tree,
+                    float4 *__restrict__ cell_box, const kf_status_t *status) {
+    __shared__ int buf[FIN_WARPS][FIN_CAP];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int total = occ_offset[B];
+    const size_t H = (size_t)1 << f.hash_bits;
+    // persistent: warps stride over the occupied cells of all trajectories
+    for (int item = blockIdx.x * FIN_WARPS + warp; item < total; item += gridDim.x * FIN_WARPS) {
+        const int b = item_owner(occ_offset, B, item);
+        const int slot = occ[b * H + (item - occ_offset[b])];
+        finalize_cell(f, b, n, H, slot, lane, buf[warp], FIN_CAP, pos, keys, cnt, start, sorted_atom, s_hi, s_lo, s_pos,
+                      s_par, s_aux, s_tree, cell_box);
+        __syncwarp();
     }
+}
+
+// ---- small trajectories: the whole binning of one trajectory in one CTA -------
+// Same table, scans, scatter and finalize as the kernel pipeline above, with
+// block barriers in place of kernel boundaries and the table cleared by its own
+// CTA (no memsets).  The last CTA to finish (ticket in work[2]) builds the
+// work-item prefixes over trajectories from the published counts.
+constexpr int BF_THREADS = 512;
+#ifndef BF_MAX_ATOMS
+#define BF_MAX_ATOMS 8192   // per-trajectory atoms below which binning runs fused
+#endif
+constexpr int BF_WARPS = BF_THREADS / 32;
+constexpr int BF_CAP = 512;   // per-warp rank-sort buffer (larger cells: serial insertion sort)
+
+__global__ void __launch_bounds__(BF_THREADS)
+bin_fused_kernel(const __grid_constant__ kf_field_t f, int B, int n, int chunk, const double *__restrict__ pos,
+                 unsigned long long *__restrict__ keys, int32_t *__restrict__ cnt, int32_t *__restrict__ start,
+                 int32_t *__restrict__ occ, int32_t *__restrict__ occ_count, int32_t *__restrict__ chunk_pre,
+                 int32_t *__restrict__ chunk_count, int32_t *__restrict__ occ_offset,
+                 int32_t *__restrict__ chunk_offset, int32_t *__restrict__ atom_slot,
+                 int32_t *__restrict__ atom_rank, int32_t *__restrict__ sorted_atom, float4 *__restrict__ s_hi,
+                 float4 *__restrict__ s_lo, double4 *__restrict__ s_pos, float4 *__restrict__ s_par,
+                 int4 *__restrict__ s_aux, int4 *__restrict__ s_tree, float4 *__restrict__ cell_box,
+                 int32_t *__restrict__ ticket, kf_status_t *status) {
+    __shared__ int m_s, last_s, carry_s[2];
+    __shared__ int wsum[32];
+    __shared__ int buf[BF_WARPS][BF_CAP];
+    const int b = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const size_t H = (size_t)1 << f.hash_bits;
+    if (!status[b].done) {
+        unsigned long long *tk = keys + b * H;
+        int32_t *tc = cnt + b * H, *ts = start + b * H, *to = occ + b * H, *tp = chunk_pre + b * H;
+        for (size_t q = threadIdx.x; q < H; q += blockDim.x) { tk[q] = EMPTY; tc[q] = 0; }
+        if (threadIdx.x == 0) m_s = 0;
+        __syncthreads();
+        // insert: cell key per atom, CAS into the table, warp-aggregated counts
+        const double inv = 1.0 / f.cell;
+        for (int a0 = 0; a0 < n; a0 += blockDim.x) {
+            const int a = a0 + threadIdx.x;
+            if (a < n) {
+                const size_t ga = (size_t)b * n + a;
+                const double x = pos[3 * ga], y = pos[3 * ga + 1], z = pos[3 * ga + 2];
+                int cx = 0, cy = 0, cz = 0;
+                if (!(isfinite(x) && isfinite(y) && isfinite(z))) {
+                    if (atomicCAS(&status[b].error, KF_ERR_NONE, KF_ERR_NONFINITE) == KF_ERR_NONE)
+                        status[b].err_iter = status[b].iter;
+                } else {
+                    cx = cell_coord(x, inv); cy = cell_coord(y, inv); cz = cell_coord(z, inv);
+                }
+                const unsigned long long key = (unsigned long long)pack_cell(cx, cy, cz);
+                uint32_t slot = cell_hash(cx, cy, cz, (uint32_t)H - 1);
+                const unsigned active = __activemask();
+                const unsigned same = __match_any_sync(active, key);
+                const int leader = __ffs(same) - 1;
+                if (lane == leader) {
+                    for (;;) {
+                        const unsigned long long prev = atomicCAS(&tk[slot], EMPTY, key);
+                        if (prev == EMPTY) { to[atomicAdd(&m_s, 1)] = (int32_t)slot; break; }
+                        if (prev == key) break;
+                        slot = (slot + 1) & ((uint32_t)H - 1);
+                    }
+                }
+                slot = __shfl_sync(same, slot, leader);
+                const int rank_in = __popc(same & ((1u << lane) - 1u));
+                int base = 0;
+                if (lane == leader) base = atomicAdd(&tc[slot], __popc(same));
+                base = __shfl_sync(same, base, leader);
+                atom_slot[ga] = (int32_t)slot;
+                atom_rank[ga] = base + rank_in;
+            }
+        }
+        __syncthreads();
+        // exclusive scans of atom counts and i-chunks over the occupied list
+        const int m = m_s;
+        const int per = (m + blockDim.x - 1) / blockDim.x;
+        const int lo = min(m, (int)threadIdx.x * per), hi = min(m, lo + per);
+        int local = 0, lchunk = 0;
+        for (int k = lo; k < hi; ++k) {
+            const int c = tc[to[k]];
+            local += c;
+            lchunk += (c + chunk - 1) / chunk;
+        }
+        int run = block_excl_scan(local, wsum);
+        int crun = block_excl_scan(lchunk, wsum);
+        for (int k = lo; k < hi; ++k) {
+            const int c = tc[to[k]];
+            ts[to[k]] = run; run += c;
+            tp[k] = crun; crun += (c + chunk - 1) / chunk;
+        }
+        if (threadIdx.x == blockDim.x - 1) { occ_count[b] = m; chunk_count[b] = crun; }
+        __syncthreads();
+        // scatter, then one warp per cell
+        for (int a = threadIdx.x; a < n; a += blockDim.x) {
+            const size_t ga = (size_t)b * n + a;
+            sorted_atom[(size_t)b * n + ts[atom_slot[ga]] + atom_rank[ga]] = a;
+        }
+        __syncthreads();
+        for (int k = warp; k < m; k += BF_WARPS) {
+            finalize_cell(f, b, n, H, to[k], lane, buf[warp], BF_CAP, pos, keys, cnt, start, sorted_atom, s_hi, s_lo, s_pos,
+                          s_par, s_aux, s_tree, cell_box);
+            __syncwarp();
+        }
+    }
+    // the last CTA: work-item prefixes over trajectories (live ones only)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last_s = atomicAdd(ticket, 1) == B - 1;
+    }
+    __syncthreads();
+    if (!last_s) return;
+    __threadfence();
+    if (threadIdx.x == 0) carry_s[0] = carry_s[1] = 0;
+    __syncthreads();
+    for (int base = 0; base < B; base += blockDim.x) {
+        const int bb = base + threadIdx.x;
+        const bool live = bb < B && !status[bb].done;
+        const int v = live ? __ldcg(&occ_count[bb]) : 0, u = live ? __ldcg(&chunk_count[bb]) : 0;
+        const int ev = carry_s[0] + block_excl_scan(v, wsum);
+        const int eu = carry_s[1] + block_excl_scan(u, wsum);
+        if (bb < B) { occ_offset[bb] = ev; chunk_offset[bb] = eu; }
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) { carry_s[0] = ev + v; carry_s[1] = eu + u; }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) { occ_offset[B] = carry_s[0]; chunk_offset[B] = carry_s[1]; *ticket = 0; }
 }
 
 }  // namespace
 
 int kf_bin_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s) {
     const int B = w->B, H = 1 << f->hash_bits;
+    if (n <= BF_MAX_ATOMS) {   // one CTA per trajectory does the whole binning
+        bin_fused_kernel<<<B, BF_THREADS, 0, s>>>(
+            *f, B, n, kf_pair_chunk(B, n, w->pair_chunk, f->precision), w->pos, w->cell_key, w->cell_cnt,
+            w->cell_start, w->occ, w->occ_count, w->chunk_pre, w->chunk_count, w->occ_offset, w->chunk_offset,
+            w->atom_slot, w->atom_rank, w->sorted_atom, reinterpret_cast<float4 *>(w->s_hi),
+            reinterpret_cast<float4 *>(w->s_lo), reinterpret_cast<double4 *>(w->s_pos),
+            reinterpret_cast<float4 *>(w->s_par), reinterpret_cast<int4 *>(w->s_aux),
+            reinterpret_cast<int4 *>(w->s_tree), reinterpret_cast<float4 *>(w->cell_box), w->work + 2, w->status);
+        KF_LAUNCH_CHECK("bin_fused_kernel");
+        return 0;
+    }
     KF_CUDA(cudaMemsetAsync(w->cell_key, 0xFF, sizeof(unsigned long long) * (size_t)B * H, s), "memset keys");
     KF_CUDA(cudaMemsetAsync(w->cell_cnt, 0, sizeof(int32_t) * (size_t)B * H, s), "memset cnt");
     KF_CUDA(cudaMemsetAsync(w->occ_count, 0, sizeof(int32_t) * (size_t)B, s), "memset occ");
