@@ -579,17 +579,18 @@ KF_DEV void solv_atom(const kf_field_t &f, const SolvArgs &A, int b, int i, int 
     }
 }
 
-#ifndef SOLV_FAST_CAP
-#define SOLV_FAST_CAP 256
-#endif
-
 // Primary pass: one CTA per (trajectory, solvation atom) with a small staging
-// capacity (more CTAs per SM); the rare atom with more reachable neighbours is
-// deferred to solv_overflow_kernel.
-__global__ void __launch_bounds__(SOLV_GROUP_THREADS)
+// capacity CAP (more CTAs per SM); the rare atom with more reachable neighbours
+// is deferred to solv_overflow_kernel.  Two builds: ensembles (many small CTAs
+// resident, CAP 144) and single chains (CAP 256: denser chains overflow less).
+template <int CAP, int MINB>
+__global__ void __launch_bounds__(SOLV_GROUP_THREADS, MINB)
 solv_group_kernel(const __grid_constant__ kf_field_t f, const SolvArgs A, int n_solv, const int32_t *__restrict__ solv_atoms) {
-    solv_atom<false>(f, A, blockIdx.x / n_solv, solv_atoms[blockIdx.x % n_solv], SOLV_FAST_CAP);
+    solv_atom<false>(f, A, blockIdx.x / n_solv, solv_atoms[blockIdx.x % n_solv], CAP);
 }
+constexpr int SOLV_CAP_ENSEMBLE = 144, SOLV_MINB_ENSEMBLE = 16;
+constexpr int SOLV_CAP_SINGLE = 256, SOLV_MINB_SINGLE = 8;
+constexpr int SOLV_ENSEMBLE_MIN_B = 16;
 
 __global__ void __launch_bounds__(SOLV_GROUP_THREADS)
 solv_overflow_kernel(const __grid_constant__ kf_field_t f, const SolvArgs A, int nb_cap) {
@@ -767,20 +768,23 @@ int kf_solvation_launch(const kf_field_t *f, kf_batch_t *w, int n, int n_solv, c
         A.f_exp_out = w->f_exp; A.a_exp_out = w->a_exp; A.status = w->status;
         A.ovf = w->solv_ovf; A.ovf_cap = B * n;
         KF_CUDA(cudaMemsetAsync(w->solv_ovf, 0, sizeof(int32_t), s), "memset solv_ovf");
-        const size_t smem = group_smem(SOLV_FAST_CAP, f->n_groups);
+        const bool ens = B >= SOLV_ENSEMBLE_MIN_B;
+        const int cap = ens ? SOLV_CAP_ENSEMBLE : SOLV_CAP_SINGLE;
+        auto kern = ens ? solv_group_kernel<SOLV_CAP_ENSEMBLE, SOLV_MINB_ENSEMBLE>
+                        : solv_group_kernel<SOLV_CAP_SINGLE, SOLV_MINB_SINGLE>;
+        const size_t smem = group_smem(cap, f->n_groups);
         const size_t smem_ovf = group_smem(w->nb_cap, f->n_groups);
-        static size_t opted = 0, opted_ovf = 0;
-        if (smem > opted) {   // dynamic + static shared memory may pass the 48 KB default
-            KF_CUDA(cudaFuncSetAttribute(solv_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-                    "smem attr");
-            opted = smem;
+        static size_t opted[2] = {0, 0}, opted_ovf = 0;
+        if (smem > opted[ens]) {   // dynamic + static shared memory may pass the 48 KB default
+            KF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
+            opted[ens] = smem;
         }
         if (smem_ovf > opted_ovf) {
             KF_CUDA(cudaFuncSetAttribute(solv_overflow_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem_ovf), "smem attr");
             opted_ovf = smem_ovf;
         }
-        solv_group_kernel<<<(unsigned)((long long)B * n_solv), SOLV_GROUP_THREADS, smem, s>>>(*f, A, n_solv, solv_atoms);
+        kern<<<(unsigned)((long long)B * n_solv), SOLV_GROUP_THREADS, smem, s>>>(*f, A, n_solv, solv_atoms);
         KF_LAUNCH_CHECK("solv_group_kernel");
         static int ovf_grid = 0;
         if (ovf_grid == 0) {
