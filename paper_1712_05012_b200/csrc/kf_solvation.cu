@@ -23,6 +23,9 @@
 namespace {
 
 constexpr int SOLV_THREADS = 256;
+#ifndef SOLV_VOTE
+#define SOLV_VOTE 4   // candidates between warp votes on "all samples covered twice"
+#endif
 #ifndef SOLV_GROUP_THREADS
 #define SOLV_GROUP_THREADS 128
 #endif
@@ -503,8 +506,12 @@ KF_DEV void solv_atom(const kf_field_t &f, const SolvArgs &A, int b, int i, int 
             continue;
         }
         int cnt = valid ? nfull : 2, crit = nfull == 1 ? f0 : -1;
+        // candidates largest cap first; the warp leaves as soon as every sample is
+        // covered twice (vote every SOLV_VOTE candidates)
+        int since_vote = 0;
         for (int w = 0; w < W; ++w) {
             uint32_t bits = gm[w] & ~gf[w];
+            bool all_done = false;
             while (bits) {
                 const int m = (w << 5) + __ffs(bits) - 1;
                 bits &= bits - 1u;
@@ -515,8 +522,12 @@ KF_DEV void solv_atom(const kf_field_t &f, const SolvArgs &A, int b, int i, int 
                         ++cnt;
                     }
                 }
+                if (++since_vote == SOLV_VOTE) {
+                    since_vote = 0;
+                    if (__all_sync(0xffffffffu, cnt >= 2)) { all_done = true; break; }
+                }
             }
-            if (__all_sync(0xffffffffu, cnt >= 2)) break;
+            if (all_done || __all_sync(0xffffffffu, cnt >= 2)) break;
         }
         if (valid) covered += cnt > 0;
         if (wi == 0 || !valid) continue;
