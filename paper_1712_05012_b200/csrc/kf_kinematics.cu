@@ -240,13 +240,16 @@ fk_smem_kernel(const __grid_constant__ kf_chain_t c, const double *__restrict__ 
 }
 
 // ---- long chains: the backbone scan spread over many CTAs --------------------
-// Three phases per trajectory: (1) every CTA scans a 2048-link segment of the
+// Three phases per trajectory: (1) every CTA scans a SEG-link segment of the
 // backbone in place (local transforms computed on the fly) and publishes the
 // segment total; (2) one CTA scans the segment totals; (3) every CTA applies
 // its exclusive prefix and computes the segment's axes.  Side links then
 // compose their <= 4 ancestors from the (final) backbone transform directly.
-constexpr int SEG = 2048;
-constexpr int SEG_PER = SEG / FK_THREADS;   // 8 links per thread
+#ifndef FK_SEG
+#define FK_SEG 512
+#endif
+constexpr int SEG = FK_SEG;                 // kf_common: KF_BB_SEG (scratch rows)
+constexpr int SEG_PER = SEG / FK_THREADS;   // links per thread
 
 __global__ void __launch_bounds__(FK_THREADS)
 fk_seg_scan_kernel(kf_chain_t c, const double *__restrict__ theta_all, double *__restrict__ T_all,
@@ -287,17 +290,25 @@ fk_seg_scan_kernel(kf_chain_t c, const double *__restrict__ theta_all, double *_
 }
 
 // exclusive prefix of the segment totals, in place (one thread per trajectory: few segments)
+// Exclusive prefix of the segment totals, one CTA per trajectory (thread =
+// segment): Hillis-Steele over the compositions in shared memory.
 __global__ void fk_seg_prefix_kernel(double *__restrict__ seg_tot, int n_seg, int B,
                                      const kf_status_t *__restrict__ status) {
-    const int b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= B || (status && status[b].done)) return;
-    Xf run = xf_identity();
-    for (int g = 0; g < n_seg; ++g) {
-        double *slot = seg_tot + ((size_t)b * n_seg + g) * 12;
-        const Xf tot = xf_load(slot);
-        xf_store(slot, run);
-        run = xf_compose(run, tot);
+    const int b = blockIdx.x, g = threadIdx.x;
+    if (status && status[b].done) return;
+    extern __shared__ double pre[];   // [blockDim][12]
+    double *slot = seg_tot + ((size_t)b * n_seg + g) * 12;
+    const Xf mine = g < n_seg ? xf_load(slot) : xf_identity();
+    xf_store(pre + 12 * g, mine);
+    __syncthreads();
+    for (int off = 1; off < (int)blockDim.x; off <<= 1) {
+        Xf r = xf_load(pre + 12 * g);
+        if (g >= off) r = xf_compose(xf_load(pre + 12 * (g - off)), r);
+        __syncthreads();
+        xf_store(pre + 12 * g, r);
+        __syncthreads();
     }
+    if (g < n_seg) xf_store(slot, g > 0 ? xf_load(pre + 12 * (g - 1)) : xf_identity());
 }
 
 KF_DEV void store_axis(double *slot, const double *axis0) {
@@ -379,12 +390,25 @@ __global__ void fk_positions_kernel(kf_chain_t c, int B, const double *__restric
 
 int kf_fk_launch(const kf_chain_t *c, kf_batch_t *w, const kf_status_t *status, cudaStream_t s) {
     const int n_seg = (c->n_bb + SEG - 1) / SEG;
+    const size_t smem = (size_t)c->n_links * FKS_STRIDE * sizeof(double);
+    if (smem <= 110 * 1024) {   // whole chain in one CTA's shared memory
+        static size_t opted = 0;
+        if (smem > opted) {
+            KF_CUDA(cudaFuncSetAttribute(fk_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                    "fk smem");
+            opted = smem;
+        }
+        fk_smem_kernel<<<w->B, FKS_THREADS, smem, s>>>(*c, w->theta, w->link_T, w->pos, status);
+        KF_LAUNCH_CHECK("fk_smem_kernel");
+        return 0;
+    }
     if (n_seg > 1 && w->B * n_seg <= 4 * 148 && w->fk_scratch) {
         // long chain, few trajectories: multi-CTA backbone scan
         fk_seg_scan_kernel<<<dim3(n_seg, w->B), FK_THREADS, 0, s>>>(*c, w->theta, w->link_T, w->fk_scratch, n_seg,
                                                                      status);
         KF_LAUNCH_CHECK("fk_seg_scan_kernel");
-        fk_seg_prefix_kernel<<<kf_blocks(w->B, 64), 64, 0, s>>>(w->fk_scratch, n_seg, w->B, status);
+        const int pt = (n_seg + 31) / 32 * 32;
+        fk_seg_prefix_kernel<<<w->B, pt, (size_t)pt * 12 * sizeof(double), s>>>(w->fk_scratch, n_seg, w->B, status);
         KF_LAUNCH_CHECK("fk_seg_prefix_kernel");
         fk_seg_apply_kernel<<<kf_blocks((long long)w->B * c->n_bb, 256), 256, 0, s>>>(*c, w->link_T, w->fk_scratch,
                                                                                      n_seg, w->B, status);
@@ -393,18 +417,6 @@ int kf_fk_launch(const kf_chain_t *c, kf_batch_t *w, const kf_status_t *status, 
                                                                                          w->B, status);
         KF_LAUNCH_CHECK("fk_side_kernel");
     } else {
-        const size_t smem = (size_t)c->n_links * FKS_STRIDE * sizeof(double);
-        if (n_seg <= 1 && smem <= 110 * 1024) {
-            static size_t opted = 0;
-            if (smem > opted) {
-                KF_CUDA(cudaFuncSetAttribute(fk_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-                        "fk smem");
-                opted = smem;
-            }
-            fk_smem_kernel<<<w->B, FKS_THREADS, smem, s>>>(*c, w->theta, w->link_T, w->pos, status);
-            KF_LAUNCH_CHECK("fk_smem_kernel");
-            return 0;
-        }
         fk_scan_kernel<<<w->B, FK_THREADS, 0, s>>>(*c, w->theta, w->link_T, status);
         KF_LAUNCH_CHECK("fk_scan_kernel");
     }

@@ -61,60 +61,70 @@ __global__ void wrench_kernel(kf_chain_t c, int B, const double *__restrict__ po
     link_wrench(c, l, pos_all + (size_t)b * n * 3, f_all + (size_t)b * n * 3, wrench_all + 6 * gid);
 }
 
-// Steps 5-6 of a fold iteration (all threads of the CTA): energies and
-// record, stop tests (kcm.py:325-350), theta record, compliance step.
-KF_DEV void finish_iteration(const kf_chain_t &c, const kf_batch_t &w, const kf_step_t &step, int b,
-                             const double *tau, double tmax, double ge, double gv, double gc, double sp,
-                             double sp5, int *stop_reason) {
-    const int D = c.n_dof;
+// Step 5 of a fold iteration (thread 0): energies, record, stop tests
+// (kcm.py:325-350).  Returns the stop reason (KF_REASON_NONE: step).
+KF_DEV int decide_iteration(const kf_batch_t &w, const kf_step_t &step, int b, int it, double tmax, double ge,
+                            double gv, double gc, double sp, double sp5) {
     kf_status_t *st = w.status + b;
+    double *e = w.energy + 3 * (size_t)b;
+    e[0] = ge; e[1] = gv; e[2] = gc;
+    st->n_pairs = (long long)(0.5 * sp);
+    st->n_pairs_vdw = (long long)(0.5 * sp5);
+    if (it < w.max_records) {
+        double *rec = w.rec_energy + ((size_t)b * w.max_records + it) * 4;
+        rec[0] = ge; rec[1] = gv; rec[2] = gc; rec[3] = tmax;
+    }
+    if (it == 0) st->tau0 = tmax;
+    const double tau0 = st->tau0;
+    int reason = KF_REASON_NONE;
+    if (tmax == 0.0) reason = KF_REASON_TORQUE_FREE;
+    else if (step.torque_tol > 0 && tmax < step.torque_tol) reason = KF_REASON_TORQUE_TOL;
+    else if (step.torque_tol_rel > 0 && tmax < step.torque_tol_rel * tau0) reason = KF_REASON_TORQUE_TOL_REL;
+    else if (step.energy_window && it >= step.energy_window && it < w.max_records) {
+        const double *r0 = w.rec_energy + ((size_t)b * w.max_records + it) * 4;
+        const double *r1 = w.rec_energy + ((size_t)b * w.max_records + it - step.energy_window) * 4;
+        const double g0 = (r0[0] + r0[1]) + r0[2], g1 = (r1[0] + r1[1]) + r1[2];
+        if (fabs(g0 - g1) < step.energy_tol) reason = KF_REASON_PLATEAU;
+    }
+    return reason;
+}
+
+// Step 6 over dofs [d0, d1) (the calling threads): theta record, then the
+// compliance step theta' = mod(mod(theta + kappa*tau/tau_max)) on free joints.
+KF_DEV void step_dofs(const kf_batch_t &w, const kf_step_t &step, int b, int D, int it, int reason,
+                      const double *tau, double tmax, int d0, int d1, int tid, int nthreads) {
     const uint8_t *frozen = w.frozen + (size_t)b * D;
     double *th = w.theta + (size_t)b * D;
-    // 5. record + stop tests (thread 0), theta copy (all)
-    const int it = st->iter;
-    if (threadIdx.x == 0) {
-        double *e = w.energy + 3 * (size_t)b;
-        e[0] = ge; e[1] = gv; e[2] = gc;
-        st->n_pairs = (long long)(0.5 * sp);
-        st->n_pairs_vdw = (long long)(0.5 * sp5);
-        int reason = KF_REASON_NONE;
-        if (it < w.max_records) {
-            double *rec = w.rec_energy + ((size_t)b * w.max_records + it) * 4;
-            rec[0] = ge; rec[1] = gv; rec[2] = gc; rec[3] = tmax;
-        }
-        if (it == 0) st->tau0 = tmax;
-        const double tau0 = st->tau0;
-        if (tmax == 0.0) reason = KF_REASON_TORQUE_FREE;
-        else if (step.torque_tol > 0 && tmax < step.torque_tol) reason = KF_REASON_TORQUE_TOL;
-        else if (step.torque_tol_rel > 0 && tmax < step.torque_tol_rel * tau0) reason = KF_REASON_TORQUE_TOL_REL;
-        else if (step.energy_window && it >= step.energy_window && it < w.max_records) {
-            const double *r0 = w.rec_energy + ((size_t)b * w.max_records + it) * 4;
-            const double *r1 = w.rec_energy + ((size_t)b * w.max_records + it - step.energy_window) * 4;
-            const double g0 = (r0[0] + r0[1]) + r0[2], g1 = (r1[0] + r1[1]) + r1[2];
-            if (fabs(g0 - g1) < step.energy_tol) reason = KF_REASON_PLATEAU;
-        }
-        *stop_reason = reason;
-    }
     if (w.record_theta && it < w.max_records) {
         double *rt = w.rec_theta + ((size_t)b * w.max_records + it) * D;
-        for (int d = threadIdx.x; d < D; d += blockDim.x) rt[d] = th[d];
+        for (int d = d0 + tid; d < d1; d += nthreads) rt[d] = th[d];
     }
-    __syncthreads();
-    const int reason = *stop_reason;
-
-    // 6. compliance step: theta' = mod(mod(theta + kappa*tau/tau_max)) on free joints
-    if (reason == KF_REASON_NONE) {
-        for (int d = threadIdx.x; d < D; d += blockDim.x) {
+    if (reason == KF_REASON_NONE)
+        for (int d = d0 + tid; d < d1; d += nthreads) {
             const double delta = frozen[d] ? 0.0 : __ddiv_rn(xmul(step.kappa, tau[d]), tmax);
             th[d] = np_mod360(np_mod360(xadd(th[d], delta)));
         }
-    }
+}
+
+// Iteration counter and stop flags after the step (thread 0).
+KF_DEV void close_iteration(kf_status_t *st, const kf_step_t &step, int it, int reason) {
+    st->iter = it + 1;
+    if (reason != KF_REASON_NONE) { st->done = 1; st->reason = reason; }
+    else if (it + 1 >= step.max_iters) { st->done = 1; st->reason = KF_REASON_MAX_ITERS; }
+}
+
+// Steps 5-6 of a fold iteration by one CTA.
+KF_DEV void finish_iteration(const kf_chain_t &c, const kf_batch_t &w, const kf_step_t &step, int b,
+                             const double *tau, double tmax, double ge, double gv, double gc, double sp,
+                             double sp5, int *stop_reason) {
+    kf_status_t *st = w.status + b;
+    const int it = st->iter;
+    if (threadIdx.x == 0) *stop_reason = decide_iteration(w, step, b, it, tmax, ge, gv, gc, sp, sp5);
     __syncthreads();
-    if (threadIdx.x == 0) {
-        st->iter = it + 1;
-        if (reason != KF_REASON_NONE) { st->done = 1; st->reason = reason; }
-        else if (it + 1 >= step.max_iters) { st->done = 1; st->reason = KF_REASON_MAX_ITERS; }
-    }
+    const int reason = *stop_reason;
+    step_dofs(w, step, b, c.n_dof, it, reason, tau, tmax, 0, c.n_dof, threadIdx.x, blockDim.x);
+    __syncthreads();
+    if (threadIdx.x == 0) close_iteration(st, step, it, reason);
 }
 
 struct TorqueArgs {
@@ -249,7 +259,10 @@ torque_step_kernel(kf_chain_t c, kf_field_t f, TorqueArgs ta, kf_batch_t w, kf_s
 // trajectory) combines the partials in segment order and finishes the
 // iteration.  scratch = fk_scratch ([B][n_seg][12]: segment total 6 |
 // partials 6), free once forward kinematics has run.
-constexpr int TQ_SEG = 2048;
+#ifndef TQ_SEG_N
+#define TQ_SEG_N 512
+#endif
+constexpr int TQ_SEG = TQ_SEG_N;   // <= the FK segment (they share fk_scratch rows)
 
 __global__ void __launch_bounds__(TQ_THREADS)
 torque_seg_kernel(kf_chain_t c, TorqueArgs ta, kf_batch_t w, int n_seg) {
@@ -366,21 +379,39 @@ __global__ void __launch_bounds__(TQ_THREADS)
 torque_seg_finish_kernel(kf_chain_t c, TorqueArgs ta, kf_batch_t w, kf_step_t step, int n_seg) {
     const int b = blockIdx.x;
     kf_status_t *st = w.status + b;
-    if (st->done) return;
-    if (st->error) {   // domain error this iteration: freeze, no record, no step
-        if (threadIdx.x == 0) st->done = 1;
+    double *sc = w.fk_scratch + (size_t)b * n_seg * 12;
+    // decision for the step pass in sc[0][0..2]: (reason, tau_max, iteration); -1 = no record, no step
+    if (st->done || st->error) {
+        if (threadIdx.x == 0) {
+            if (!st->done) st->done = 1;   // domain error this iteration: freeze
+            sc[0] = -1.0;
+        }
         return;
     }
-    __shared__ int stop_reason;
-    const double *sc = w.fk_scratch + (size_t)b * n_seg * 12;
+    if (threadIdx.x != 0) return;
     double tmax = 0.0, se = 0.0, sv = 0.0, scv = 0.0, sp = 0.0, sp5 = 0.0;
     for (int g = 0; g < n_seg; ++g) {   // fixed order: deterministic
         const double *p = sc + 12 * g + 6;
         tmax = fmax(tmax, p[0]);
         se += p[1]; sv += p[2]; scv += p[3]; sp += p[4]; sp5 += p[5];
     }
-    finish_iteration(c, w, step, b, ta.tau + (size_t)b * c.n_dof, tmax, 0.5 * se, 0.5 * sv, scv, sp, sp5,
-                     &stop_reason);
+    const int it = st->iter;
+    const int reason = decide_iteration(w, step, b, it, tmax, 0.5 * se, 0.5 * sv, scv, sp, sp5);
+    sc[0] = (double)reason; sc[1] = tmax; sc[2] = (double)it;
+    close_iteration(st, step, it, reason);
+}
+
+// Theta records and the compliance step, dof ranges spread over n_seg CTAs.
+__global__ void __launch_bounds__(TQ_THREADS)
+torque_seg_step_kernel(kf_chain_t c, TorqueArgs ta, kf_batch_t w, kf_step_t step, int n_seg) {
+    const int g = blockIdx.x, b = blockIdx.y;
+    const double *sc = w.fk_scratch + (size_t)b * n_seg * 12;
+    const double code = sc[0];
+    if (code < 0.0) return;
+    const int D = c.n_dof;
+    const int d0 = (int)((long long)D * g / n_seg), d1 = (int)((long long)D * (g + 1) / n_seg);
+    step_dofs(w, step, b, D, (int)sc[2], (int)code, ta.tau + (size_t)b * D, sc[1], d0, d1, threadIdx.x,
+              blockDim.x);
 }
 
 // kcm_step for the API (B = 1): deltas and theta' (kcm.py:264-274).
@@ -425,8 +456,10 @@ int kf_torque_launch(const kf_chain_t *c, const kf_field_t *f, kf_batch_t *w, co
         KF_LAUNCH_CHECK("torque_seg_kernel");
         torque_seg_project_kernel<<<dim3(n_seg, w->B), TQ_THREADS, 0, s>>>(*c, fz, ta, *w, n_seg);
         KF_LAUNCH_CHECK("torque_seg_project_kernel");
-        torque_seg_finish_kernel<<<w->B, TQ_THREADS, 0, s>>>(*c, ta, *w, st, n_seg);
+        torque_seg_finish_kernel<<<w->B, 32, 0, s>>>(*c, ta, *w, st, n_seg);
         KF_LAUNCH_CHECK("torque_seg_finish_kernel");
+        torque_seg_step_kernel<<<dim3(n_seg, w->B), TQ_THREADS, 0, s>>>(*c, ta, *w, st, n_seg);
+        KF_LAUNCH_CHECK("torque_seg_step_kernel");
         return 0;
     }
     // a fold iteration computes its own wrenches (pos, forces of this batch) in

@@ -457,7 +457,7 @@ class Batch:
         with torch.cuda.stream(stream()):
             t = self.t = dict(
                 theta=z(B, max(D, 1)), frozen=z(B, max(D, 1), dtype=torch.uint8),
-                link_T=z(B, L, 16), fk_scratch=z(B, max(1, -(-nbb // 2048)), 12),
+                link_T=z(B, L, 16), fk_scratch=z(B, max(1, -(-nbb // 256)), 12),   # >= ceil(n_bb / segment) rows
                 pos=z(B, n, 3), forces=z(B, n, 3),
                 cell_key=z(B, H, dtype=torch.int64), cell_cnt=z(B, H, dtype=i32),
                 cell_start=z(B, H, dtype=i32), occ=z(B, H, dtype=i32), occ_count=z(B, dtype=i32),
