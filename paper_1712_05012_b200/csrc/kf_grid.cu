@@ -401,7 +401,7 @@ bin_fused_kernel(const __grid_constant__ kf_field_t f, int B, int n, int chunk, 
 
 int kf_bin_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s) {
     const int B = w->B, H = 1 << f->hash_bits;
-    if (n <= BF_MAX_ATOMS) {   // one CTA per trajectory does the whole binning
+    if (n <= BF_MAX_ATOMS && B >= 32) {   // ensembles: one CTA per trajectory does the whole binning
         bin_fused_kernel<<<B, BF_THREADS, 0, s>>>(
             *f, B, n, kf_pair_chunk(B, n, w->pair_chunk, f->precision), w->pos, w->cell_key, w->cell_cnt,
             w->cell_start, w->occ, w->occ_count, w->chunk_pre, w->chunk_count, w->occ_offset, w->chunk_offset,
