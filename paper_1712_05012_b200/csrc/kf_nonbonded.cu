@@ -589,25 +589,10 @@ pair_dense_kernel(const __grid_constant__ kf_field_t f, const __grid_constant__ 
             }
             T fx = 0, fy = 0, fz = 0, fe = 0, fv = 0;
             if (own) {
-#ifdef PAIR_DENSE_POP
-                // prefilter the lane's j into a mask, then pop its set bits: the
-                // pair body runs max(popcount) times per warp, not nt / nph
-                unsigned mask = 0u;
-                for (int t = ph; t < nt; t += nph) {
-                    const float4 hj = J.hi[t];
-                    const float dx = hi.x - hj.x, dy = hi.y - hj.y, dz = hi.z - hj.z;
-                    mask |= (dx * dx + dy * dy + dz * dz <= pre2 ? 1u : 0u) << t;
-                }
-                while (mask) {
-                    const int t = __ffs(mask) - 1;
-                    mask &= mask - 1u;
-                    const float4 hj = J.hi[t];
-#else
                 for (int t = ph; t < nt; t += nph) {
                     const float4 hj = J.hi[t];
                     const float dx = hi.x - hj.x, dy = hi.y - hj.y, dz = hi.z - hj.z;
                     if (dx * dx + dy * dy + dz * dz > pre2) continue;
-#endif
                     T out[5] = {0, 0, 0, 0, 0};
                     int pce = 0, pcv = 0;
                     const int4 aj = J.aux[t];
