@@ -20,6 +20,13 @@
 
 #include "kf_common.cuh"
 
+#ifdef SOLV_STATS
+__device__ unsigned long long g_solv_stats[8];
+#define SSTAT(k, v) atomicAdd(&g_solv_stats[k], (unsigned long long)(v))
+#else
+#define SSTAT(k, v)
+#endif
+
 namespace {
 
 constexpr int SOLV_THREADS = 256;
@@ -501,10 +508,13 @@ KF_DEV void solv_atom(const kf_field_t &f, const SolvArgs &A, int b, int i, int 
             if (fb && f0 < 0) f0 = (w << 5) + __ffs(fb) - 1;
             nfull += __popc(fb);
         }
+        if (lane == 0) { SSTAT(0, 1); SSTAT(7, W); }
         if (nfull >= 2) {
+            if (lane == 0) SSTAT(1, 1);
             if (valid) ++covered;
             continue;
         }
+        if (lane == 0 && nfull == 1) SSTAT(2, 1);
         int cnt = valid ? nfull : 2, crit = nfull == 1 ? f0 : -1;
         // candidates largest cap first; the warp leaves as soon as every sample is
         // covered twice (vote every SOLV_VOTE candidates)
@@ -515,6 +525,7 @@ KF_DEV void solv_atom(const kf_field_t &f, const SolvArgs &A, int b, int i, int 
             while (bits) {
                 const int m = (w << 5) + __ffs(bits) - 1;
                 bits &= bits - 1u;
+                if (lane == 0) SSTAT(3, 1);
                 if (cnt < 2) {
                     const float4 cp = S.cap[m];
                     if (qx * cp.x + qy * cp.y + qz * cp.z >= cp.w && covers(px, py, pz, S.nb[m])) {
@@ -530,6 +541,10 @@ KF_DEV void solv_atom(const kf_field_t &f, const SolvArgs &A, int b, int i, int 
             if (all_done || __all_sync(0xffffffffu, cnt >= 2)) break;
         }
         if (valid) covered += cnt > 0;
+#ifdef SOLV_STATS
+        { const unsigned ex = __ballot_sync(0xffffffffu, valid && cnt == 0), cr = __ballot_sync(0xffffffffu, valid && cnt == 1);
+          if (lane == 0) { SSTAT(4, __popc(ex)); SSTAT(5, __popc(cr)); if (ex) SSTAT(6, 1); } }
+#endif
         if (wi == 0 || !valid) continue;
         if (cnt == 0) {
             // exposed: every candidate displaced along each axis (solvation.py:224-235)
@@ -851,3 +866,10 @@ int kf_solv_forces_api_launch(const double *pos, int n, const double *r_off, con
     KF_LAUNCH_CHECK("solv_forces_api_kernel");
     return 0;
 }
+
+#ifdef SOLV_STATS
+extern "C" int kf_debug_solv_stats(unsigned long long *out) {
+    cudaDeviceSynchronize();
+    return (int)cudaMemcpyFromSymbol(out, g_solv_stats, sizeof(unsigned long long) * 8);
+}
+#endif
