@@ -306,6 +306,7 @@ struct SolvArgs {
     kf_status_t *status;
     int32_t *ovf;          // [0]: count, then (b, i) pairs of atoms over the fast capacity
     int ovf_cap;
+    int fast_cap;          // primary-pass capacity (<= the build's CAP; tests lower it)
 };
 
 // One atom (the whole CTA).  nb_cap = staged-neighbour capacity of this launch;
@@ -612,7 +613,7 @@ KF_DEV void solv_atom(const kf_field_t &f, const SolvArgs &A, int b, int i, int 
 template <int CAP, int MINB>
 __global__ void __launch_bounds__(SOLV_GROUP_THREADS, MINB)
 solv_group_kernel(const __grid_constant__ kf_field_t f, const SolvArgs A, int n_solv, const int32_t *__restrict__ solv_atoms) {
-    solv_atom<false>(f, A, blockIdx.x / n_solv, solv_atoms[blockIdx.x % n_solv], CAP);
+    solv_atom<false>(f, A, blockIdx.x / n_solv, solv_atoms[blockIdx.x % n_solv], min(CAP, A.fast_cap));
 }
 constexpr int SOLV_CAP_ENSEMBLE = 144, SOLV_MINB_ENSEMBLE = 16;
 constexpr int SOLV_CAP_SINGLE = 256, SOLV_MINB_SINGLE = 8;
@@ -793,6 +794,12 @@ int kf_solvation_launch(const kf_field_t *f, kf_batch_t *w, int n, int n_solv, c
         A.s_aux = reinterpret_cast<const int4 *>(w->s_aux); A.solv_acc = w->solv_acc; A.cav_atom = w->cav_atom;
         A.f_exp_out = w->f_exp; A.a_exp_out = w->a_exp; A.status = w->status;
         A.ovf = w->solv_ovf; A.ovf_cap = B * n;
+        static int fast_cap_env = -1;   // KFB200_SOLV_FAST_CAP: lower the primary capacity (tests)
+        if (fast_cap_env < 0) {
+            const char *env = getenv("KFB200_SOLV_FAST_CAP");
+            fast_cap_env = env ? atoi(env) : 1 << 30;
+        }
+        A.fast_cap = fast_cap_env;
         KF_CUDA(cudaMemsetAsync(w->solv_ovf, 0, sizeof(int32_t), s), "memset solv_ovf");
         const bool ens = B >= SOLV_ENSEMBLE_MIN_B;
         const int cap = ens ? SOLV_CAP_ENSEMBLE : SOLV_CAP_SINGLE;

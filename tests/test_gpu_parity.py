@@ -487,3 +487,43 @@ def test_fold_long_chain_multi_cta_path(fp64_pairs):
     assert np.all(np.abs(tm - ref["tau_max"]) <= 1e-9 * ref["tau_max"])
     d = np.abs((np.asarray(tr.final.theta) - ref["final"] + 180.0) % 360.0 - 180.0).max()
     assert d <= 1e-9, d
+
+
+_OVERFLOW_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, 'tests'); sys.path.insert(0, '.')
+from conftest import golden, make_system
+import paper_1712_05012_b200 as P
+from dataclasses import replace
+g = golden("mixed_water")
+ch, params, w, _ = make_system(g["seq"], solvation=True)
+null = replace(params, q=np.zeros(ch.n_atoms), eps=np.zeros(ch.n_atoms))
+res = P.Field(null, w, P.FieldConfig(solvation=True)).evaluate(g["positions"])
+assert np.array_equal(res.forces, g["solv_forces"])
+assert np.array_equal(res.sasa.f_exp, g["sasa_f_exp"])
+ch, params, w, fld = make_system(g["seq"], solvation=True)
+conf = P.Conformation(g["theta"], np.zeros(ch.n_dof, bool), ch.n_residues)
+step = P.StepConfig(max_iters=3, torque_tol_rel=0.0, energy_window=0)
+ens = P.fold_ensemble(ch, [conf] * 16, fld, step)          # ensemble build of the solvation pass
+one = P.fold(ch, conf, fld, step)
+E = np.array([[r.energy.g_elec, r.energy.g_vdw, r.energy.g_cav] for r in one.records])
+for b in range(16):
+    assert np.allclose(ens.energies[b, :3, :3], E, rtol=1e-12, atol=1e-12), b
+print("ok")
+"""
+
+
+def test_solvation_overflow_pass_bitexact():
+    """Atoms with more reachable neighbours than the primary pass stages go to
+    solv_overflow_kernel.  With the primary capacity forced to 4
+    (KFB200_SOLV_FAST_CAP, read once per process, hence the subprocess) nearly
+    every atom takes that path: forces and exposures stay bit-exact, and the
+    ensemble build agrees with single folds."""
+    import os
+    import subprocess
+    import sys
+    from conftest import ROOT
+    env = dict(os.environ, KFB200_SOLV_FAST_CAP="4")
+    out = subprocess.run([sys.executable, "-c", _OVERFLOW_SCRIPT], cwd=ROOT, env=env, capture_output=True,
+                         text=True, timeout=600)
+    assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-3000:]
