@@ -360,6 +360,27 @@ def main():
             dist.destroy_process_group()
         return
     peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    hbm_peak = json.load(open(peaks_path)).get("hbm_gbs") if os.path.exists(peaks_path) else None
+    # HBM rooflines of the byte-bound phases (north star: binning, scans, kinematics):
+    # algorithmic bytes per trajectory (SURVEY.md §8(d) formulas) x B / phase time
+    n_at, L = ch.n_atoms, len(ch.links)
+    H = 1 << int(np.ceil(np.log2(max(2 * n_at, 2))))
+    phase_bytes = {
+        # theta in; link transforms (16 f64) and positions out
+        "fk": 8 * D + 128 * L + 24 * n_at,
+        # positions in; hash table (key 8 + count/start/occ/chunk 4x4 + box 32) and the
+        # cell-ordered SoA (hi/lo/par/aux/tree 5x16 + fp64 position 32) + slot/rank/sorted out
+        "bin": 24 * n_at + H * (8 + 16 + 32) + n_at * (5 * 16 + 32 + 12),
+        # transforms, positions, forces, per-atom energies/counts in; tau, theta out
+        "torque": 128 * L + 48 * n_at + 24 * n_at + 16 * D,
+    }
+    phase_roofline = {}
+    for ph, by in phase_bytes.items():
+        t = acc.get(ph, 0.0)
+        if t > 0 and hbm_peak:
+            gbs = by * B / (t * 1e-3) / 1e9
+            phase_roofline[ph] = {"bound": "hbm", "bytes_per_launch": by * B, "achieved": gbs, "peak": hbm_peak,
+                                  "unit": "GB/s", "frac": gbs / hbm_peak}
     # the dominant kernel of this run (kf_nonbonded.cu picks dense lanes for fp32
     # pair math, the compacted list for fp64) and its DRAM traffic per launch from
     # the committed `ncu --set full` capture of the same workload, if there is one
@@ -394,11 +415,12 @@ def main():
                      "fp64_peak_tflops": peak64 / 1e12,
                      "kernel_share_of_step": pair_ms / step_ms_eager},
         "phase_ms_per_step": acc,
+        "phase_rooflines": phase_roofline,
         "gpu_launches": launches,
         "clocks": clk,
         "cpu_baseline": cpu,
         "single_trajectory": extras or None,
-        "hbm_peak_gbs": json.load(open(peaks_path)).get("hbm_gbs") if os.path.exists(peaks_path) else None,
+        "hbm_peak_gbs": hbm_peak,
     }
     print(json.dumps(line), flush=True)
     if world > 1:
