@@ -160,7 +160,13 @@ KF_DEV void pair_eval(const kf_field_t &f, const PairConst &pc, float4 hi, float
     const bool exact = F64 || fabsf(d2f - cut2f) <= band || fabsf(d2f - tvf) <= band ||
                        (!pc.te_is_cut && fabsf(d2f - tef) <= band) || d2f < pc.f64_d2;
     if (exact) {
-        slow_pair<T>(F64, &f, pos_i, pos_j, i, j, cls, out, &pce, &pcv, st);
+        // the outlined path writes through pointers: give it its own stack
+        // temporaries so out / pce / pcv stay in registers on the fast path
+        T so[5] = {0, 0, 0, 0, 0};
+        int sce = 0, scv = 0;
+        slow_pair<T>(F64, &f, pos_i, pos_j, i, j, cls, so, &sce, &scv, st);
+        out[0] = so[0]; out[1] = so[1]; out[2] = so[2]; out[3] = so[3]; out[4] = so[4];
+        pce = sce; pcv = scv;
         return;
     }
     if (d2f > cut2f) return;
