@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define KF_ABI_VERSION 6
+#define KF_ABI_VERSION 7
 
 /* ---- static chain tables (uploaded once per chain) ------------------------
  * Links are in the reference's topological order (parent < index, ground = 0),
@@ -99,6 +99,7 @@ typedef struct {
     /* per-atom records gathered by binning (one 16-byte load each)            */
     const float *atom_par;          /* [n][4]: q, R, sqrt(eps), 0 (fp32)           */
     const int32_t *atom_aux;        /* [n][4]: atom, residue, chain flag, class_slow (0 if uniform) */
+    double r_off_max;               /* max R_off over atoms (solvation cell pruning) */
 } kf_field_t;
 
 /* ---- per-trajectory status block ----------------------------------------- */

@@ -13,7 +13,7 @@ import os
 from .errors import NativeLibraryError
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libkfb200.so")
-ABI_VERSION = 6
+ABI_VERSION = 7
 
 P = C.c_void_p
 I32 = C.c_int32
@@ -42,7 +42,7 @@ class KfField(C.Structure):
         ("gamma", P), ("w_int", P), ("quantum", F64), ("delta_r", F64), ("four_pi", F64),
         ("reach_pad", F64), ("solv_atoms", P), ("n_solv", I32), ("precision", I32),
         ("samples_grp", P), ("grp_cone", P), ("n_groups", I32), ("_pad2", I32),
-        ("atom_par", P), ("atom_aux", P)]
+        ("atom_par", P), ("atom_aux", P), ("r_off_max", F64)]
 
 
 class KfStatus(C.Structure):

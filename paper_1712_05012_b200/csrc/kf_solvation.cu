@@ -301,6 +301,7 @@ struct SolvArgs {
     const int32_t *cnt, *start, *atom_slot;
     const double4 *s_pos;
     const int4 *s_aux;
+    const float4 *cell_box;   // [B][H][2] members' box (fp32 offsets from the cell centre)
     long long *solv_acc;
     double *cav_atom, *f_exp_out, *a_exp_out;
     kf_status_t *status;
@@ -346,7 +347,19 @@ KF_DEV void solv_atom(const kf_field_t &f, const SolvArgs &A, int b, int i, int 
             const int s = threadIdx.x;
             const int js = cell_probe(keys + hb, H, cx + f.stencil[3 * s], cy + f.stencil[3 * s + 1],
                                       cz + f.stencil[3 * s + 2]);
-            if (js >= 0) { first = start[hb + js]; len = cnt[hb + js]; }
+            if (js >= 0) {
+                // skip the cell unless its members' box is within R_off_i + max R_off + pad
+                const int nx = cx + f.stencil[3 * s], ny = cy + f.stencil[3 * s + 1], nz = cz + f.stencil[3 * s + 2];
+                const float px = (float)(xi[0] - ((double)nx + 0.5) * f.cell);
+                const float py = (float)(xi[1] - ((double)ny + 0.5) * f.cell);
+                const float pz = (float)(xi[2] - ((double)nz + 0.5) * f.cell);
+                const float4 lo = A.cell_box[2 * (hb + js)], hi = A.cell_box[2 * (hb + js) + 1];
+                const float gx = fmaxf(fmaxf(lo.x - px, px - hi.x), 0.f);
+                const float gy = fmaxf(fmaxf(lo.y - py, py - hi.y), 0.f);
+                const float gz = fmaxf(fmaxf(lo.z - pz, pz - hi.z), 0.f);
+                const float reach = (float)(r_i + f.r_off_max + f.reach_pad) + 1e-3f;
+                if (gx * gx + gy * gy + gz * gz <= reach * reach) { first = start[hb + js]; len = cnt[hb + js]; }
+            }
         }
         cell_first[threadIdx.x] = first;
         int incl = len;
@@ -796,6 +809,7 @@ int kf_solvation_launch(const kf_field_t *f, kf_batch_t *w, int n, int n_solv, c
         A.n = n; A.pos_all = w->pos; A.keys = w->cell_key; A.cnt = w->cell_cnt; A.start = w->cell_start;
         A.atom_slot = w->atom_slot; A.s_pos = reinterpret_cast<const double4 *>(w->s_pos);
         A.s_aux = reinterpret_cast<const int4 *>(w->s_aux); A.solv_acc = w->solv_acc; A.cav_atom = w->cav_atom;
+        A.cell_box = reinterpret_cast<const float4 *>(w->cell_box);
         A.f_exp_out = w->f_exp; A.a_exp_out = w->a_exp; A.status = w->status;
         A.ovf = w->solv_ovf; A.ovf_cap = B * n;
         static int fast_cap_env = -1;   // KFB200_SOLV_FAST_CAP: lower the primary capacity (tests)

@@ -374,6 +374,7 @@ class DeviceField(ParamTables):
             w_int, quantum = force_quantum(fld.params, r_off, sphere.n, scfg.delta_r)
             gamma = np.asarray(fld.params.gamma, float)
             s.reach_pad = scfg.delta_r + 1e-3
+            s.r_off_max = float(np.max(r_off)) if len(r_off) else 0.0
             reach = max(reach, 2.0 * float(np.max(r_off)) + s.reach_pad)
             t.update(samples=_up(sphere.points, np.float64), r_off=_up(r_off, np.float64),
                      r_off2=_up(r_off2, np.float64), gamma=_up(gamma, np.float64),
