@@ -149,12 +149,7 @@ KF_DEV void pair_eval(const kf_field_t &f, const PairConst &pc, float4 hi, float
             cls = slow_class(f.tparent, f.tgp, f.tggp, f.tres, f.tchain, i, j);
         }
     }
-#ifdef PAIR_SEL_WEIGHTS
-    const float we = cls == 4 ? pc.we[3] : cls == 3 ? pc.we[2] : cls == 2 ? pc.we[1] : pc.we[0];
-    const float wv = cls == 4 ? pc.wv[3] : cls == 3 ? pc.wv[2] : cls == 2 ? pc.wv[1] : pc.wv[0];
-#else
     const float we = pc.we[cls - 1], wv = pc.wv[cls - 1];   // constant-bank loads, indexed
-#endif
     // exact recomputation near a threshold: |d2 - t| <= band for t in {cut, te, tv}
     // (te == cut to ~1e-14 for the default cut-offs: pc.te_is_cut folds the test)
     const bool exact = F64 || fabsf(d2f - cut2f) <= band || fabsf(d2f - tvf) <= band ||

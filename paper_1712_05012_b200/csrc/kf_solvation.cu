@@ -491,9 +491,6 @@ KF_DEV void solv_atom(const kf_field_t &f, const SolvArgs &A, int b, int i, int 
             }
         }
     }
-#ifdef SOLV_SETUP_ONLY
-    return;
-#endif
     for (int m = threadIdx.x; m < 3 * count; m += blockDim.x) S.acc[m] = 0;
     __syncthreads();
 
