@@ -632,6 +632,9 @@ solv_group_kernel(const __grid_constant__ kf_field_t f, const SolvArgs A, int n_
 constexpr int SOLV_CAP_ENSEMBLE = 144, SOLV_MINB_ENSEMBLE = SOLV_MINB_ENS;
 constexpr int SOLV_CAP_SINGLE = 256, SOLV_MINB_SINGLE = 8;
 constexpr int SOLV_ENSEMBLE_MIN_B = 16;
+#ifndef OVF_BLOCKS_PER_SM
+#define OVF_BLOCKS_PER_SM 4   // resident CTAs per SM of the overflow pass (49 KB of staging each)
+#endif
 
 __global__ void __launch_bounds__(SOLV_GROUP_THREADS)
 solv_overflow_kernel(const __grid_constant__ kf_field_t f, const SolvArgs A, int nb_cap) {
@@ -839,7 +842,7 @@ int kf_solvation_launch(const kf_field_t *f, kf_batch_t *w, int n, int n_solv, c
             int dev = 0;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&ovf_grid, cudaDevAttrMultiProcessorCount, dev);
-            ovf_grid *= 2;
+            ovf_grid *= OVF_BLOCKS_PER_SM;
         }
         solv_overflow_kernel<<<ovf_grid, SOLV_GROUP_THREADS, smem_ovf, s>>>(*f, A, w->nb_cap);
         KF_LAUNCH_CHECK("solv_overflow_kernel");
