@@ -81,6 +81,11 @@ class Clocks:
             self.fh = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
                                           "-lms", "100"], stdout=self.fh, stderr=subprocess.DEVNULL)
+            # nvidia-smi takes a moment to start: wait for its first line so that even a
+            # short timed region is sampled
+            t_end = time.time() + 5.0
+            while time.time() < t_end and os.path.getsize(self.path) == 0 and self.proc.poll() is None:
+                time.sleep(0.02)
         except (OSError, FileNotFoundError):
             self.proc = None
 
@@ -104,8 +109,15 @@ class Clocks:
             for nm, v in zip(names, f[5:9]):
                 if v.lower() == "active":
                     reasons.add(nm)
-        if not sm:
-            return None
+        if not sm:   # no sample in the window: one query right after it
+            try:
+                q = subprocess.run(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                    f"--id={self.idx}"], capture_output=True, text=True, timeout=30).stdout
+                f = [x.strip() for x in q.strip().splitlines()[0].split(",")]
+                sm, mx = [float(f[1])], float(f[2])
+                reasons = {nm for nm, v in zip(names, f[5:9]) if v.lower() == "active"}
+            except (OSError, ValueError, IndexError, subprocess.SubprocessError):
+                return None
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
                 "samples": len(sm)}
 
