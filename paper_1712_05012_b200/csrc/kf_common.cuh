@@ -1,5 +1,6 @@
 // Shared device helpers for the kfb200 kernels (sm_100a).
 #pragma once
+#include <cstdlib>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <math.h>
@@ -50,6 +51,12 @@ KF_DEV double np_mod360(double a) {
 // overrides (0 = this rule).  Part of the work decomposition, so results are
 // bitwise reproducible for a given (B, n) but not across chunk sizes.
 inline int kf_pair_chunk(int B, int n, int requested, int precision) {
+    static int env_chunk = -1;   // KFB200_PAIR_CHUNK: process-wide override (measurements)
+    if (env_chunk < 0) {
+        const char *e = getenv("KFB200_PAIR_CHUNK");
+        env_chunk = e ? atoi(e) : 0;
+    }
+    if (!requested) requested = env_chunk;
     if (requested == 4 || requested == 8 || requested == 16 || requested == 32) return requested;
     if (precision) return 32;
     const long long atoms = (long long)B * n;
