@@ -137,14 +137,15 @@ struct TorqueArgs {
 
 // One CTA per trajectory.  mode: 0 = torques only (API), 1 = fold iteration,
 // 2 = energy reduction only (Field.evaluate)
-__global__ void __launch_bounds__(TQ_THREADS)
+template <int NT>
+__global__ void __launch_bounds__(NT)
 torque_step_kernel(kf_chain_t c, kf_field_t f, TorqueArgs ta, kf_batch_t w, kf_step_t step, int mode,
                    int fuse_wrench) {
     const int b = blockIdx.x;
     kf_status_t *st = w.status ? w.status + b : nullptr;
     if (st && st->done) return;
     __shared__ double red[32];
-    __shared__ double chunk[TQ_THREADS][6];
+    __shared__ double chunk[NT][6];
     __shared__ int stop_reason;
     if (st && st->error) {   // domain error this iteration: freeze, no record, no step
         if (threadIdx.x == 0) st->done = 1;
@@ -469,15 +470,18 @@ int kf_torque_launch(const kf_chain_t *c, const kf_field_t *f, kf_batch_t *w, co
     if (fuse_wrench && !fuse) {
         if (kf_wrench_launch(c, w->B, w->pos, w->forces, const_cast<double *>(wrench), w->status, s)) return 1;
     }
+    // one CTA per trajectory: 512 threads for a lone chain (its latency is the
+    // iteration's), 256 for ensembles (more trajectories per SM)
+    const bool wide = w->B < 64;
+    auto kern = wide ? torque_step_kernel<TQ_THREADS> : torque_step_kernel<TQ_THREADS / 2>;
     if (fuse) {
-        static size_t opted = 0;
-        if (wsm > opted) {
-            KF_CUDA(cudaFuncSetAttribute(torque_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm),
-                    "torque smem");
-            opted = wsm;
+        static size_t opted[2] = {0, 0};
+        if (wsm > opted[wide]) {
+            KF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm), "torque smem");
+            opted[wide] = wsm;
         }
     }
-    torque_step_kernel<<<w->B, TQ_THREADS, fuse ? wsm : 0, s>>>(*c, fz, ta, *w, st, mode, fuse ? 1 : 0);
+    kern<<<w->B, wide ? TQ_THREADS : TQ_THREADS / 2, fuse ? wsm : 0, s>>>(*c, fz, ta, *w, st, mode, fuse ? 1 : 0);
     KF_LAUNCH_CHECK("torque_step_kernel");
     return 0;
 }
