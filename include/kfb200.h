@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define KF_ABI_VERSION 7
+#define KF_ABI_VERSION 8
 
 /* ---- static chain tables (uploaded once per chain) ------------------------
  * Links are in the reference's topological order (parent < index, ground = 0),
@@ -170,6 +170,9 @@ typedef struct {
     long long *solv_acc;            /* [B][n][3] int64 fixed point                 */
     int32_t *solv_ovf;              /* [1 + 2 B n]: count, (b, atom) pairs deferred to
                                        the large-capacity solvation pass            */
+    long long *pair_fj;             /* [B][n][6] half-list j-side forces, fixed point
+                                       (lo xyz in 2^-28, hi xyz in 2^12); kept zero
+                                       between launches; NULL: full-list kernel     */
     double  *cav_atom;              /* [B][n] gamma_i * a_exp_i                    */
     double  *f_exp;                 /* [B][n] exposure ratio (NULL: not stored)    */
     double  *a_exp;                 /* [B][n] exposed area (NULL: not stored)      */

@@ -13,7 +13,7 @@ import os
 from .errors import NativeLibraryError
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libkfb200.so")
-ABI_VERSION = 7
+ABI_VERSION = 8
 
 P = C.c_void_p
 I32 = C.c_int32
@@ -60,7 +60,7 @@ class KfBatch(C.Structure):
             "occ", "occ_count", "occ_offset", "chunk_pre", "chunk_count", "chunk_offset",
             "atom_slot", "atom_rank", "sorted_atom", "s_hi", "s_lo",
             "s_pos", "s_par", "s_aux", "s_tree", "cell_box", "work", "e_atom", "pair_count",
-            "solv_acc", "solv_ovf", "cav_atom", "f_exp", "a_exp", "wrench", "side_tot", "bb_suffix", "tau", "energy", "status",
+            "solv_acc", "solv_ovf", "pair_fj", "cav_atom", "f_exp", "a_exp", "wrench", "side_tot", "bb_suffix", "tau", "energy", "status",
             "rec_energy", "rec_theta")]
 
 

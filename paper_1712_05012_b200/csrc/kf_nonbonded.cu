@@ -36,6 +36,10 @@ namespace {
 
 constexpr double COULOMB_K = 332.06;
 constexpr double MIN_DISTANCE = 1e-6;
+// two-level fixed point of the half-list kernel's j-side forces: hi in units of
+// 2^12, lo (the exact remainder, |r| <= 2^11) in units of 2^-28
+constexpr double FJ_HI = 4096.0, FJ_HI_INV = 1.0 / 4096.0;
+constexpr double FJ_LO = 1.0 / 268435456.0, FJ_LO_INV = 268435456.0;
 constexpr int PAIR_WARPS = 4;        // warps per CTA, warp-per-cell variant
 constexpr int SPLIT_WARPS = 4;       // warps per CTA (one cell), split variant
 constexpr unsigned FULL = 0xffffffffu;
@@ -462,7 +466,7 @@ pair_kernel(const __grid_constant__ kf_field_t f, const __grid_constant__ PairCo
 // groups that take alternating j, so more lanes work; the groups' fp64 sums are
 // combined by a fixed xor tree at the end of the item.  Each lane sums its
 // own pairs in j order: deterministic, no per-pair shared-memory traffic.
-template <bool F64, bool SPLIT>
+template <bool F64, bool SPLIT, bool HALF>
 __global__ void __launch_bounds__((SPLIT ? SPLIT_WARPS : PAIR_WARPS) * 32, SPLIT ? 1 : PAIR_MINB_W)
 pair_dense_kernel(const __grid_constant__ kf_field_t f, const __grid_constant__ PairConst pc, int B, int n, int chunk,
                   const unsigned long long *__restrict__ keys, const int32_t *__restrict__ cnt,
@@ -472,10 +476,12 @@ pair_dense_kernel(const __grid_constant__ kf_field_t f, const __grid_constant__ 
                   const float4 *__restrict__ s_lo, const double4 *__restrict__ s_pos,
                   const float4 *__restrict__ s_par, const int4 *__restrict__ s_aux, const int4 *__restrict__ s_tree,
                   const float4 *__restrict__ cell_box, int32_t *__restrict__ work, double *__restrict__ forces,
-                  double *__restrict__ e_atom, long long *__restrict__ pair_count, kf_status_t *status) {
+                  double *__restrict__ e_atom, long long *__restrict__ pair_count, kf_status_t *status,
+                  long long *__restrict__ fj_fixed) {
     using T = typename std::conditional<F64, double, float>::type;
     constexpr int NW = SPLIT ? SPLIT_WARPS : PAIR_WARPS;
     __shared__ Tile Jt[NW];
+    __shared__ float Jf_s[HALF ? NW : 1][32][3];    // HALF: this tile's forces on its j atoms
     __shared__ float4 ihi_s[SPLIT ? 1 : NW][32];   // the chunk's hi offsets (probe / box test)
     __shared__ double part[SPLIT ? NW : 1][3][32];
     __shared__ double epart[NW][2];
@@ -531,7 +537,8 @@ pair_dense_kernel(const __grid_constant__ kf_field_t f, const __grid_constant__ 
         int p_j0 = 0, p_jc = 0, p_js = -1;
         float p_sx = 0.f, p_sy = 0.f, p_sz = 0.f;
         float4 blo = make_float4(1e30f, 1e30f, 1e30f, 0.f), bhi = make_float4(-1e30f, -1e30f, -1e30f, 0.f);
-        if (lane < f.n_stencil) {
+        // HALF: own cell + the 13 forward cells (stencil order, device.py _stencil)
+        if (lane < (HALF ? min(14, f.n_stencil) : f.n_stencil)) {
             const int ox = f.stencil[3 * lane], oy = f.stencil[3 * lane + 1], oz = f.stencil[3 * lane + 2];
             p_js = cell_probe(keys + hb, H, cx + ox, cy + oy, cz + oz);
             if (p_js >= 0) {
@@ -586,10 +593,58 @@ pair_dense_kernel(const __grid_constant__ kf_field_t f, const __grid_constant__ 
                     J.par[lane] = s_par[kj];
                     J.aux[lane] = aux;
                 }
+                if (HALF) { Jf_s[warp][lane][0] = 0.f; Jf_s[warp][lane][1] = 0.f; Jf_s[warp][lane][2] = 0.f; }
                 __syncwarp();
             }
             T fx = 0, fy = 0, fz = 0, fe = 0, fv = 0;
-            if (own) {
+            if (HALF) {
+                // each unordered pair once: own cell j after i (sorted order), forward
+                // cells all; the force on j (-f) is summed over the phase group's lanes
+                // (fixed xor tree) and stored for this tile (each t visited once)
+                const int n_it = (nt + nph - 1) / nph;
+                const int i_pos = ic + oi;              // i's position in its cell
+                for (int kt = 0; kt < n_it; ++kt) {
+                    const int t = ph + kt * nph;
+                    const bool live = own && t < nt && (jb + t >= c || jb + t > i_pos);
+                    const float4 hj = J.hi[t < nt ? t : 0];
+                    const float dx = hi.x - hj.x, dy = hi.y - hj.y, dz = hi.z - hj.z;
+                    const bool pass = live && dx * dx + dy * dy + dz * dz <= pre2;
+                    if (!__any_sync(FULL, pass)) continue;
+                    T out[5] = {0, 0, 0, 0, 0};
+                    int pce = 0, pcv = 0;
+                    if (pass) {
+                        const int4 aj = J.aux[t];
+                        pair_eval<F64, T>(f, pc, hi, li, qi, ai, cm, hj, J.lo[t], J.par[t], aj, s_pos + ki,
+                                          s_pos + nb + aj.w, status + b, out, pce, pcv);
+                    }
+                    fx += out[0]; fy += out[1]; fz += out[2]; fe += out[3]; fv += out[4];
+                    ce += pce; cv += pcv;
+                    float jx = (float)-out[0], jy = (float)-out[1], jz = (float)-out[2];
+                    for (int m = wi >> 1; m > 0; m >>= 1) {
+                        jx += __shfl_xor_sync(FULL, jx, m);
+                        jy += __shfl_xor_sync(FULL, jy, m);
+                        jz += __shfl_xor_sync(FULL, jz, m);
+                    }
+                    if (oi == 0 && t < nt) { Jf_s[warp][t][0] = jx; Jf_s[warp][t][1] = jy; Jf_s[warp][t][2] = jz; }
+                }
+                __syncwarp();
+                // flush: the tile's j forces into the trajectory's two-level fixed point
+                // (integer atomics: order-free, so the result is schedule-independent)
+                if (lane < nt) {
+                    const double v[3] = {(double)Jf_s[warp][lane][0], (double)Jf_s[warp][lane][1],
+                                         (double)Jf_s[warp][lane][2]};
+                    long long *dst = fj_fixed + 6 * (nb + J.aux[lane].x);
+                    for (int q = 0; q < 3; ++q) {
+                        if (v[q] == 0.0) continue;
+                        const long long hi_u = __double2ll_rn(v[q] * FJ_HI_INV);     // units of 2^12
+                        const double rem = v[q] - (double)hi_u * FJ_HI;            // exact, |rem| <= 2^11
+                        const long long lo_u = __double2ll_rn(rem * FJ_LO_INV);     // units of 2^-28
+                        if (lo_u) atomicAdd(reinterpret_cast<unsigned long long *>(dst + q), (unsigned long long)lo_u);
+                        if (hi_u) atomicAdd(reinterpret_cast<unsigned long long *>(dst + 3 + q),
+                                            (unsigned long long)hi_u);
+                    }
+                }
+            } else if (own) {
                 for (int t = ph; t < nt; t += nph) {
                     const float4 hj = J.hi[t];
                     const float dx = hi.x - hj.x, dy = hi.y - hj.y, dz = hi.z - hj.z;
@@ -637,6 +692,7 @@ pair_dense_kernel(const __grid_constant__ kf_field_t f, const __grid_constant__ 
             e_atom[2 * o] = 0.0; e_atom[2 * o + 1] = 0.0;
             pair_count[o] = 0;
         }
+        if (HALF) { ee *= 2.0; ev *= 2.0; ce *= 2; cv *= 2; }   // pairs counted once: the reductions halve
         long long pcount = (long long)ce + ((long long)cv << 32);
         // chunk totals: fixed xor tree per warp, then warps in order, stored at the
         // chunk's first atom (chunks are a function of the positions: deterministic)
@@ -665,6 +721,23 @@ pair_dense_kernel(const __grid_constant__ kf_field_t f, const __grid_constant__ 
                 pair_count[o] = pcount;
             }
         }
+    }
+}
+
+// forces += the half-list kernel's j-side fixed point, which is then cleared
+// (thread = one force component: coalesced over the [B][n][3] forces)
+__global__ void fj_combine_kernel(int B, int n, long long *__restrict__ fj, double *__restrict__ forces,
+                                  const kf_status_t *status) {
+    const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid >= 3LL * B * n) return;
+    const long long a = gid / 3;
+    const int q = (int)(gid - 3 * a);
+    if (status[a / n].done) return;
+    long long *p = fj + 6 * a;
+    const long long lo = p[q], hi = p[3 + q];
+    if (lo || hi) {
+        forces[gid] += (double)hi * FJ_HI + (double)lo * FJ_LO;
+        p[q] = 0; p[3 + q] = 0;
     }
 }
 
@@ -735,22 +808,22 @@ int kf_pairs_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s) {
         split_below = env ? atoll(env) : 40000;
     }
     const bool split = (long long)w->B * n < split_below;
-    // KFB200_PAIR_KERNEL: 1 = compacted pair list, 2 = dense lanes.  Default:
-    // dense for fp32 pair math, compacted for fp64 (its pair body is long
-    // enough that full lanes pay for the compaction)
+    // KFB200_PAIR_KERNEL: 1 = compacted pair list, 2 = dense lanes (full list),
+    // 3 = dense lanes, half list (Newton's third law; j-side forces in integer
+    // fixed point).  Default: half list for fp32 pair math on ensembles, full list
+    // for small launches, compacted for fp64 (its pair body is long enough that
+    // full lanes pay for the compaction).
     static int env_variant = -1;
     if (env_variant < 0) {
         const char *env = getenv("KFB200_PAIR_KERNEL");
         env_variant = env ? atoi(env) : 0;
     }
-    const int variant = env_variant ? env_variant : (f->precision ? 1 : 2);
-    auto kern = variant == 2
-                    ? (f->precision ? (split ? pair_dense_kernel<true, true> : pair_dense_kernel<true, false>)
-                                    : (split ? pair_dense_kernel<false, true> : pair_dense_kernel<false, false>))
-                    : (f->precision ? (split ? pair_kernel<true, true> : pair_kernel<true, false>)
-                                    : (split ? pair_kernel<false, true> : pair_kernel<false, false>));
+    // (the half list wins for ensembles; a lone chain's latency-bound CTA-per-item
+    // pass does better on the full list without the fixed-point pass)
+    int variant = env_variant ? env_variant : (f->precision ? 1 : split ? 2 : 3);
+    if (variant == 3 && (f->precision || !w->pair_fj)) variant = f->precision ? 1 : 2;
     const int nw = split ? SPLIT_WARPS : PAIR_WARPS;
-    const size_t dyn = variant == 2 ? 0 : (size_t)nw * (f->precision ? sizeof(WarpSmem<double>) : sizeof(WarpSmem<float>));
+    const int chunk = kf_pair_chunk(w->B, n, w->pair_chunk, f->precision);
     static bool opted = false;
     if (!opted) {
         for (auto k : {pair_kernel<true, true>, pair_kernel<true, false>, pair_kernel<false, true>,
@@ -775,13 +848,30 @@ int kf_pairs_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s) {
     pc.f64_d2 = f64_below * f64_below;
     pc.dconst = f->dielectric_const; pc.uniform = f->uniform_weights;
     pc.te_is_cut = fabs(f->thr_elec2 - f->cut_pair2) < 1e-6 ? 1 : 0;
-    kern<<<resident_grid(kern, nw * 32, dyn), nw * 32, dyn, s>>>(
-        *f, pc, w->B, n, kf_pair_chunk(w->B, n, w->pair_chunk, f->precision), w->cell_key, w->cell_cnt, w->cell_start, w->occ, w->occ_count, w->chunk_pre, w->chunk_offset,
-        reinterpret_cast<const float4 *>(w->s_hi), reinterpret_cast<const float4 *>(w->s_lo),
-        reinterpret_cast<const double4 *>(w->s_pos), reinterpret_cast<const float4 *>(w->s_par),
-        reinterpret_cast<const int4 *>(w->s_aux), reinterpret_cast<const int4 *>(w->s_tree),
-        reinterpret_cast<const float4 *>(w->cell_box), w->work, w->forces, w->e_atom, w->pair_count,
-        w->status);
+#define KF_PAIR_ARGS                                                                                          \
+    *f, pc, w->B, n, chunk, w->cell_key, w->cell_cnt, w->cell_start, w->occ, w->occ_count, w->chunk_pre,       \
+        w->chunk_offset, reinterpret_cast<const float4 *>(w->s_hi), reinterpret_cast<const float4 *>(w->s_lo), \
+        reinterpret_cast<const double4 *>(w->s_pos), reinterpret_cast<const float4 *>(w->s_par),              \
+        reinterpret_cast<const int4 *>(w->s_aux), reinterpret_cast<const int4 *>(w->s_tree),                  \
+        reinterpret_cast<const float4 *>(w->cell_box), w->work, w->forces, w->e_atom, w->pair_count, w->status
+    if (variant == 1) {
+        const size_t dyn = (size_t)nw * (f->precision ? sizeof(WarpSmem<double>) : sizeof(WarpSmem<float>));
+        auto kern = f->precision ? (split ? pair_kernel<true, true> : pair_kernel<true, false>)
+                                 : (split ? pair_kernel<false, true> : pair_kernel<false, false>);
+        kern<<<resident_grid(kern, nw * 32, dyn), nw * 32, dyn, s>>>(KF_PAIR_ARGS);
+    } else {
+        const bool half = variant == 3;
+        auto kern = half ? (split ? pair_dense_kernel<false, true, true> : pair_dense_kernel<false, false, true>)
+                         : f->precision ? (split ? pair_dense_kernel<true, true, false> : pair_dense_kernel<true, false, false>)
+                                        : (split ? pair_dense_kernel<false, true, false> : pair_dense_kernel<false, false, false>);
+        kern<<<resident_grid(kern, nw * 32, 0), nw * 32, 0, s>>>(KF_PAIR_ARGS, w->pair_fj);
+        if (half) {
+            KF_LAUNCH_CHECK("pair_kernel");
+            const long long total = 3LL * w->B * n;
+            fj_combine_kernel<<<kf_blocks(total, 256), 256, 0, s>>>(w->B, n, w->pair_fj, w->forces, w->status);
+        }
+    }
+#undef KF_PAIR_ARGS
     KF_LAUNCH_CHECK("pair_kernel");
     return 0;
 }

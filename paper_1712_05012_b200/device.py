@@ -470,7 +470,8 @@ class Batch:
                 s_tree=z(B, n, 4, dtype=i32), cell_box=z(B, H, 8, dtype=torch.float32),
                 work=z(4, dtype=i32),
                 e_atom=z(B, n, 2), pair_count=z(B, n, dtype=torch.int64),
-                solv_acc=z(B, n, 3, dtype=torch.int64), solv_ovf=z(1 + 2 * B * n, dtype=i32), cav_atom=z(B, n),
+                solv_acc=z(B, n, 3, dtype=torch.int64), solv_ovf=z(1 + 2 * B * n, dtype=i32),
+                pair_fj=z(B, n, 6, dtype=torch.int64), cav_atom=z(B, n),
                 f_exp=z(B, n) if store_sasa else None, a_exp=z(B, n) if store_sasa else None,
                 wrench=z(B, L, 6), side_tot=z(B, max(R, 1), 6), bb_suffix=z(B, max(nbb, 1), 6),
                 tau=z(B, max(D, 1)), energy=z(B, 3),
