@@ -393,10 +393,11 @@ def main():
             gbs = by * B / (t * 1e-3) / 1e9
             phase_roofline[ph] = {"bound": "hbm", "bytes_per_launch": by * B, "achieved": gbs, "peak": hbm_peak,
                                   "unit": "GB/s", "frac": gbs / hbm_peak}
-    # the dominant kernel of this run (kf_nonbonded.cu picks dense lanes for fp32
-    # pair math, the compacted list for fp64) and its DRAM traffic per launch from
+    # the dominant kernel of this run (kf_nonbonded.cu: half-list dense lanes for
+    # fp32 ensembles, the compacted list for fp64) and its DRAM traffic per launch from
     # the committed `ncu --set full` capture of the same workload, if there is one
-    kernel = "pair_kernel<1,0>" if P.pair_precision() == "fp64" else "pair_dense_kernel<0,0>"
+    kernel = "pair_kernel<1,0>" if P.pair_precision() == "fp64" else \
+        ("pair_dense_kernel<0,0,1>" if B * ch.n_atoms >= 40000 else "pair_dense_kernel<0,1,0>")
     traffic, traffic_src = None, None
     prof_path = os.path.join(ROOT, "profiles", "pair_kernel_traffic.json")
     if os.path.exists(prof_path):
