@@ -170,8 +170,8 @@ typedef struct {
     long long *solv_acc;            /* [B][n][3] int64 fixed point                 */
     int32_t *solv_ovf;              /* [1 + 2 B n]: count, (b, atom) pairs deferred to
                                        the large-capacity solvation pass            */
-    long long *pair_fj;             /* [B][n][6] half-list j-side forces, fixed point
-                                       (lo xyz in 2^-28, hi xyz in 2^12); kept zero
+    long long *pair_fj;             /* [2][B][n][3] half-list j-side forces, fixed point
+                                       (lo plane in 2^-28, hi plane in 2^12); kept zero
                                        between launches; NULL: full-list kernel     */
     double  *cav_atom;              /* [B][n] gamma_i * a_exp_i                    */
     double  *f_exp;                 /* [B][n] exposure ratio (NULL: not stored)    */

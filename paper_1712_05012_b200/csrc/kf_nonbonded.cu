@@ -478,6 +478,7 @@ pair_dense_kernel(const __grid_constant__ kf_field_t f, const __grid_constant__ 
                   const float4 *__restrict__ cell_box, int32_t *__restrict__ work, double *__restrict__ forces,
                   double *__restrict__ e_atom, long long *__restrict__ pair_count, kf_status_t *status,
                   long long *__restrict__ fj_fixed) {
+    const long long fj_plane = 3LL * B * n;
     using T = typename std::conditional<F64, double, float>::type;
     constexpr int NW = SPLIT ? SPLIT_WARPS : PAIR_WARPS;
     __shared__ Tile Jt[NW];
@@ -633,14 +634,15 @@ pair_dense_kernel(const __grid_constant__ kf_field_t f, const __grid_constant__ 
                 if (lane < nt) {
                     const double v[3] = {(double)Jf_s[warp][lane][0], (double)Jf_s[warp][lane][1],
                                          (double)Jf_s[warp][lane][2]};
-                    long long *dst = fj_fixed + 6 * (nb + J.aux[lane].x);
+                    // planes: lo [B n 3] then hi [B n 3] (the hi plane is rarely touched)
+                    long long *dst = fj_fixed + 3 * (nb + J.aux[lane].x);
                     for (int q = 0; q < 3; ++q) {
                         if (v[q] == 0.0) continue;
                         const long long hi_u = __double2ll_rn(v[q] * FJ_HI_INV);     // units of 2^12
                         const double rem = v[q] - (double)hi_u * FJ_HI;            // exact, |rem| <= 2^11
                         const long long lo_u = __double2ll_rn(rem * FJ_LO_INV);     // units of 2^-28
                         if (lo_u) atomicAdd(reinterpret_cast<unsigned long long *>(dst + q), (unsigned long long)lo_u);
-                        if (hi_u) atomicAdd(reinterpret_cast<unsigned long long *>(dst + 3 + q),
+                        if (hi_u) atomicAdd(reinterpret_cast<unsigned long long *>(dst + fj_plane + q),
                                             (unsigned long long)hi_u);
                     }
                 }
@@ -733,11 +735,12 @@ __global__ void fj_combine_kernel(int B, int n, long long *__restrict__ fj, doub
     const long long a = gid / 3;
     const int q = (int)(gid - 3 * a);
     if (status[a / n].done) return;
-    long long *p = fj + 6 * a;
-    const long long lo = p[q], hi = p[3 + q];
+    long long *p = fj + 3 * a;
+    const long long plane = 3LL * B * n;
+    const long long lo = p[q], hi = p[plane + q];
     if (lo || hi) {
         forces[gid] += (double)hi * FJ_HI + (double)lo * FJ_LO;
-        p[q] = 0; p[3 + q] = 0;
+        p[q] = 0; p[plane + q] = 0;
     }
 }
 
