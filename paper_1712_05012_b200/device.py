@@ -488,6 +488,9 @@ class Batch:
 
     def reset_status(self):
         self.t["status"].zero_()
+        # a trajectory stopped by a device error leaves its half-list fixed-point
+        # j forces uncleared (the wrench pass that folds them in does not run)
+        self.t["pair_fj"].zero_()
 
     def status(self):
         raw = self.t["status"].cpu().numpy().tobytes()
