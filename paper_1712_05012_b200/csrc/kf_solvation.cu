@@ -507,10 +507,6 @@ KF_DEV void solv_atom(const kf_field_t &f, const SolvArgs &A, int b, int i, int 
         g = __shfl_sync(0xffffffffu, g, 0);
         if (g >= G) break;
         const bool valid = lane < (int)f.grp_cone[8 * g + 5];
-        const double *q = f.samples_grp + 3 * (32 * g + (valid ? lane : 0));
-        const float qx = (float)q[0], qy = (float)q[1], qz = (float)q[2];
-        double px, py, pz;
-        sample_point(xi, r_i, q, px, py, pz);
         const uint32_t *gm = S.mask + g * W, *gf = S.full + g * W;
         // neighbours covering the whole group: two of them settle every sample
         int nfull = 0, f0 = -1;
@@ -526,6 +522,11 @@ KF_DEV void solv_atom(const kf_field_t &f, const SolvArgs &A, int b, int i, int 
             continue;
         }
         if (lane == 0 && nfull == 1) SSTAT(2, 1);
+        // unsettled group: this lane's sample point
+        const double *q = f.samples_grp + 3 * (32 * g + (valid ? lane : 0));
+        const float qx = (float)q[0], qy = (float)q[1], qz = (float)q[2];
+        double px, py, pz;
+        sample_point(xi, r_i, q, px, py, pz);
         int cnt = valid ? nfull : 2, crit = nfull == 1 ? f0 : -1;
         // candidates largest cap first; the warp leaves as soon as every sample is
         // covered twice (vote every SOLV_VOTE candidates)
