@@ -30,6 +30,7 @@ __device__ unsigned long long g_solv_stats[8];
 namespace {
 
 constexpr int SOLV_THREADS = 256;
+constexpr int SOLV_MAX_GROUPS = 128;   // sample groups tracked in shared memory (N <= 4096)
 #ifndef SOLV_VOTE
 #define SOLV_VOTE 4   // candidates between warp votes on "all samples covered twice"
 #endif
@@ -327,7 +328,9 @@ KF_DEV void solv_atom(const kf_field_t &f, const SolvArgs &A, int b, int i, int 
     const GroupSmem S = carve_group(smem, nb_cap, f.n_groups);
     __shared__ int nn, next_group, covered_s;
     __shared__ long long acc_i_s[3];
+    __shared__ int gfull_s[SOLV_MAX_GROUPS];   // full coverers per sample group
     if (threadIdx.x == 0) { nn = 0; next_group = 0; covered_s = 0; acc_i_s[0] = acc_i_s[1] = acc_i_s[2] = 0; }
+    for (int q = threadIdx.x; q < SOLV_MAX_GROUPS; q += blockDim.x) gfull_s[q] = 0;
     __syncthreads();
 
     const size_t ai = (size_t)b * n + i;
@@ -487,12 +490,30 @@ KF_DEV void solv_atom(const kf_field_t &f, const SolvArgs &A, int b, int i, int 
                 const bool full = live && cf < ax.w && dot >= ax.w * cf + sin_a * sf + 1e-3f;
                 const uint32_t bits = __ballot_sync(0xffffffffu, keep);
                 const uint32_t fbits = __ballot_sync(0xffffffffu, full);
-                if (lane == 0) { S.mask[g * W + w] = bits; S.full[g * W + w] = fbits; }
+                if (lane == 0) {
+                    S.mask[g * W + w] = bits; S.full[g * W + w] = fbits;
+                    if (fbits && g < SOLV_MAX_GROUPS) atomicAdd(&gfull_s[g], __popc(fbits));
+                }
             }
         }
     }
     for (int m = threadIdx.x; m < 3 * count; m += blockDim.x) S.acc[m] = 0;
     __syncthreads();
+    // groups with two full coverers are settled (every sample covered twice, no
+    // events): their samples are counted here and only the open groups are listed
+    // for the warps (list order is free: groups are independent, totals integer)
+    __shared__ int glist_s[SOLV_MAX_GROUPS];
+    __shared__ int n_open_s;
+    const bool use_list = G <= SOLV_MAX_GROUPS;
+    if (threadIdx.x == 0) n_open_s = 0;
+    __syncthreads();
+    if (use_list)
+        for (int t = threadIdx.x; t < G; t += blockDim.x) {
+            if (gfull_s[t] >= 2) atomicAdd(&covered_s, (int)f.grp_cone[8 * t + 5]);
+            else glist_s[atomicAdd(&n_open_s, 1)] = t;
+        }
+    __syncthreads();
+    const int n_open = use_list ? n_open_s : G;
 
     // ---- one warp per sample group, lane = sample
     const int lane = threadIdx.x & 31;
@@ -502,10 +523,11 @@ KF_DEV void solv_atom(const kf_field_t &f, const SolvArgs &A, int b, int i, int 
     for (;;) {
         // groups are taken from a block counter: warps that meet cheap
         // (buried) groups take more of them
-        int g = 0;
-        if (lane == 0) g = atomicAdd(&next_group, 1);
-        g = __shfl_sync(0xffffffffu, g, 0);
-        if (g >= G) break;
+        int k = 0;
+        if (lane == 0) k = atomicAdd(&next_group, 1);
+        k = __shfl_sync(0xffffffffu, k, 0);
+        if (k >= n_open) break;
+        const int g = use_list ? glist_s[k] : k;
         const bool valid = lane < (int)f.grp_cone[8 * g + 5];
         const uint32_t *gm = S.mask + g * W, *gf = S.full + g * W;
         // neighbours covering the whole group: two of them settle every sample
