@@ -482,7 +482,9 @@ pair_dense_kernel(const __grid_constant__ kf_field_t f, const __grid_constant__ 
     using T = typename std::conditional<F64, double, float>::type;
     constexpr int NW = SPLIT ? SPLIT_WARPS : PAIR_WARPS;
     __shared__ Tile Jt[NW];
-    __shared__ float Jf_s[HALF ? NW : 1][32][3];    // HALF: this tile's forces on its j atoms
+    // HALF: per lane, its contribution to each j of the tile ([x|y|z][t][owner slot],
+    // chunks of <= 16 atoms); summed per j in owner order at the end of the tile
+    __shared__ __align__(16) float Jc_s[HALF ? NW : 1][3][32][16];
     __shared__ float4 ihi_s[SPLIT ? 1 : NW][32];   // the chunk's hi offsets (probe / box test)
     __shared__ double part[SPLIT ? NW : 1][3][32];
     __shared__ double epart[NW][2];
@@ -594,7 +596,11 @@ pair_dense_kernel(const __grid_constant__ kf_field_t f, const __grid_constant__ 
                     J.par[lane] = s_par[kj];
                     J.aux[lane] = aux;
                 }
-                if (HALF) { Jf_s[warp][lane][0] = 0.f; Jf_s[warp][lane][1] = 0.f; Jf_s[warp][lane][2] = 0.f; }
+                if (HALF) {
+                    float4 *z = reinterpret_cast<float4 *>(&Jc_s[warp][0][0][0]);
+#pragma unroll
+                    for (int q = 0; q < 3 * 32 * 16 / 4 / 32; ++q) z[lane + 32 * q] = make_float4(0.f, 0.f, 0.f, 0.f);
+                }
                 __syncwarp();
             }
             T fx = 0, fy = 0, fz = 0, fe = 0, fv = 0;
@@ -620,20 +626,27 @@ pair_dense_kernel(const __grid_constant__ kf_field_t f, const __grid_constant__ 
                     }
                     fx += out[0]; fy += out[1]; fz += out[2]; fe += out[3]; fv += out[4];
                     ce += pce; cv += pcv;
-                    float jx = (float)-out[0], jy = (float)-out[1], jz = (float)-out[2];
-                    for (int m = wi >> 1; m > 0; m >>= 1) {
-                        jx += __shfl_xor_sync(FULL, jx, m);
-                        jy += __shfl_xor_sync(FULL, jy, m);
-                        jz += __shfl_xor_sync(FULL, jz, m);
+                    if (pass) {   // this lane's -f on j = t (slot [t][oi]: one writer per tile)
+                        Jc_s[warp][0][t][oi] = (float)-out[0];
+                        Jc_s[warp][1][t][oi] = (float)-out[1];
+                        Jc_s[warp][2][t][oi] = (float)-out[2];
                     }
-                    if (oi == 0 && t < nt) { Jf_s[warp][t][0] = jx; Jf_s[warp][t][1] = jy; Jf_s[warp][t][2] = jz; }
                 }
                 __syncwarp();
                 // flush: the tile's j forces into the trajectory's two-level fixed point
                 // (integer atomics: order-free, so the result is schedule-independent)
                 if (lane < nt) {
-                    const double v[3] = {(double)Jf_s[warp][lane][0], (double)Jf_s[warp][lane][1],
-                                         (double)Jf_s[warp][lane][2]};
+                    double v[3];
+#pragma unroll
+                    for (int q = 0; q < 3; ++q) {   // owner slots in order: deterministic
+                        const float4 *r = reinterpret_cast<const float4 *>(&Jc_s[warp][q][lane][0]);
+                        float acc = 0.f;
+                        for (int o4 = 0; o4 < (wi + 3) / 4; ++o4) {
+                            const float4 c4 = r[o4];
+                            acc += c4.x; acc += c4.y; acc += c4.z; acc += c4.w;
+                        }
+                        v[q] = (double)acc;
+                    }
                     // planes: lo [B n 3] then hi [B n 3] (the hi plane is rarely touched)
                     long long *dst = fj_fixed + 3 * (nb + J.aux[lane].x);
                     for (int q = 0; q < 3; ++q) {
@@ -824,9 +837,10 @@ int kf_pairs_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s) {
     // (the half list wins for ensembles; a lone chain's latency-bound CTA-per-item
     // pass does better on the full list without the fixed-point pass)
     int variant = env_variant ? env_variant : (f->precision ? 1 : split ? 2 : 3);
-    if (variant == 3 && (f->precision || !w->pair_fj)) variant = f->precision ? 1 : 2;
-    const int nw = split ? SPLIT_WARPS : PAIR_WARPS;
     const int chunk = kf_pair_chunk(w->B, n, w->pair_chunk, f->precision);
+    // the half list needs its fixed-point buffer and chunks of <= 16 atoms
+    if (variant == 3 && (f->precision || !w->pair_fj || chunk > 16)) variant = f->precision ? 1 : 2;
+    const int nw = split ? SPLIT_WARPS : PAIR_WARPS;
     static bool opted = false;
     if (!opted) {
         for (auto k : {pair_kernel<true, true>, pair_kernel<true, false>, pair_kernel<false, true>,
