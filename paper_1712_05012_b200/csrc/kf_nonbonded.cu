@@ -171,7 +171,10 @@ KF_DEV void pair_eval(const kf_field_t &f, const PairConst &pc, float4 hi, float
     if (d2f > cut2f) return;
     const bool ke = d2f <= tef, kv = d2f <= tvf;
     pce = ke; pcv = kv;
-    const float inv_r = rsqrtf(d2f);
+    // MUFU.RSQ without the subnormal fix-up rsqrtf carries: d2f >= f64_d2 > 0
+    // here (closer pairs took the exact path), so the result is the same
+    float inv_r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(inv_r) : "f"(d2f));
     const float inv_r2 = inv_r * inv_r;
     float g = 0.f;
     if (ke) {
@@ -606,8 +609,7 @@ pair_dense_kernel(const __grid_constant__ kf_field_t f, const __grid_constant__ 
             T fx = 0, fy = 0, fz = 0, fe = 0, fv = 0;
             if (HALF) {
                 // each unordered pair once: own cell j after i (sorted order), forward
-                // cells all; the force on j (-f) is summed over the phase group's lanes
-                // (fixed xor tree) and stored for this tile (each t visited once)
+                // cells all; the force on j (-f) is kept per (j, owner) for this tile
                 const int n_it = (nt + nph - 1) / nph;
                 const int i_pos = ic + oi;              // i's position in its cell
                 for (int kt = 0; kt < n_it; ++kt) {
@@ -659,15 +661,24 @@ pair_dense_kernel(const __grid_constant__ kf_field_t f, const __grid_constant__ 
                                             (unsigned long long)hi_u);
                     }
                 }
-            } else if (own) {
-                for (int t = ph; t < nt; t += nph) {
-                    const float4 hj = J.hi[t];
-                    const float dx = hi.x - hj.x, dy = hi.y - hj.y, dz = hi.z - hj.z;
-                    if (dx * dx + dy * dy + dz * dz > pre2) continue;
+            } else {
+                // this lane's prefilter hits over the tile (bit kt: j = ph + kt * nph), then
+                // each lane walks its own hits in ascending order: the warp runs
+                // max-over-lanes iterations, not one per j that any lane meets
+                unsigned hits = 0;
+                if (own)
+                    for (int t = ph, kt = 0; t < nt; t += nph, ++kt) {
+                        const float4 hj = J.hi[t];
+                        const float dx = hi.x - hj.x, dy = hi.y - hj.y, dz = hi.z - hj.z;
+                        if (dx * dx + dy * dy + dz * dz <= pre2) hits |= 1u << kt;
+                    }
+                while (hits) {
+                    const int t = ph + (__ffs(hits) - 1) * nph;
+                    hits &= hits - 1;
                     T out[5] = {0, 0, 0, 0, 0};
                     int pce = 0, pcv = 0;
                     const int4 aj = J.aux[t];
-                    pair_eval<F64, T>(f, pc, hi, li, qi, ai, cm, hj, J.lo[t], J.par[t], aj, s_pos + ki,
+                    pair_eval<F64, T>(f, pc, hi, li, qi, ai, cm, J.hi[t], J.lo[t], J.par[t], aj, s_pos + ki,
                                       s_pos + nb + aj.w, status + b, out, pce, pcv);
                     fx += out[0]; fy += out[1]; fz += out[2]; fe += out[3]; fv += out[4];
                     ce += pce; cv += pcv;
