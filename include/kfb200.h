@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define KF_ABI_VERSION 8
+#define KF_ABI_VERSION 9
 
 /* ---- static chain tables (uploaded once per chain) ------------------------
  * Links are in the reference's topological order (parent < index, ground = 0),
@@ -95,7 +95,8 @@ typedef struct {
     const double *samples_grp;      /* [G][32][3]                                  */
     const float *grp_cone;          /* [G][8]: axis xyz, cos alpha, sin alpha, count, 0, 0 */
     int32_t n_groups;
-    int32_t _pad2;
+    int32_t flat;                   /* 1: FieldConfig(use_hash=False): one all-atom cell
+                                       (quadratic candidates, kcm.py:153-162), n_stencil 1 */
     /* per-atom records gathered by binning (one 16-byte load each)            */
     const float *atom_par;          /* [n][4]: q, R, sqrt(eps), 0 (fp32)           */
     const int32_t *atom_aux;        /* [n][4]: atom, residue, chain flag, class_slow (0 if uniform) */
@@ -120,7 +121,8 @@ typedef struct {
 
 enum { KF_REASON_NONE = 0, KF_REASON_MAX_ITERS = 1, KF_REASON_TORQUE_FREE = 2,
        KF_REASON_TORQUE_TOL = 3, KF_REASON_TORQUE_TOL_REL = 4, KF_REASON_PLATEAU = 5 };
-enum { KF_ERR_NONE = 0, KF_ERR_CLASH = 1, KF_ERR_NONFINITE = 2, KF_ERR_CAPACITY = 3 };
+enum { KF_ERR_NONE = 0, KF_ERR_CLASH = 1, KF_ERR_NONFINITE = 2, KF_ERR_CAPACITY = 3,
+       KF_ERR_EXTENT = 4 /* flat layout: an atom beyond 2048 A of the centroid cell */ };
 
 /* ---- batch workspace (B trajectories, caller-allocated) ------------------ */
 typedef struct {

@@ -34,4 +34,4 @@ from .spatial import (Cutoffs, GridConfig, HashGrid, NeighborTable, build_grid,
                       build_neighbor_table, filtered_lists, filtered_pairs)
 from .topology import (BondTree, InteractionClass, TreeWeights, UniformWeights,
                        WeightTable, build_tree, classify)
-from .runlog import RunLog, fold_batch, write_manifest, write_pdb
+from .runlog import RunLog, bench_table, fold_batch, write_manifest, write_pdb

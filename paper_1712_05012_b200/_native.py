@@ -13,7 +13,7 @@ import os
 from .errors import NativeLibraryError
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libkfb200.so")
-ABI_VERSION = 8
+ABI_VERSION = 9
 
 P = C.c_void_p
 I32 = C.c_int32
@@ -41,7 +41,7 @@ class KfField(C.Structure):
         ("n_samples", I32), ("_pad1", I32), ("samples", P), ("r_off", P), ("r_off2", P),
         ("gamma", P), ("w_int", P), ("quantum", F64), ("delta_r", F64), ("four_pi", F64),
         ("reach_pad", F64), ("solv_atoms", P), ("n_solv", I32), ("precision", I32),
-        ("samples_grp", P), ("grp_cone", P), ("n_groups", I32), ("_pad2", I32),
+        ("samples_grp", P), ("grp_cone", P), ("n_groups", I32), ("flat", I32),
         ("atom_par", P), ("atom_aux", P), ("r_off_max", F64)]
 
 
@@ -71,7 +71,7 @@ class KfStep(C.Structure):
 
 REASONS = {1: "max_iters", 2: "torque-free", 3: "torque tolerance",
            4: "torque tolerance (relative)", 5: "energy plateau"}
-ERR_CLASH, ERR_NONFINITE, ERR_CAPACITY = 1, 2, 3
+ERR_CLASH, ERR_NONFINITE, ERR_CAPACITY, ERR_EXTENT = 1, 2, 3, 4
 
 # every exported symbol of include/kfb200.h with its argument types
 _PROTOS = {

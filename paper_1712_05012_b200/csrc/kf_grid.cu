@@ -270,6 +270,35 @@ bin_finalize_kernel(const __grid_constant__ kf_field_t f, int B, int n, const do
     }
 }
 
+// The last CTA of a per-trajectory binning kernel (ticket in work[2]) builds the
+// work-item prefixes over trajectories (live ones only) from the published counts.
+KF_DEV void publish_prefixes(int B, const int32_t *occ_count, const int32_t *chunk_count, int32_t *occ_offset,
+                             int32_t *chunk_offset, int32_t *ticket, const kf_status_t *status, int *wsum) {
+    __shared__ int last_s, carry_s[2];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last_s = atomicAdd(ticket, 1) == B - 1;
+    }
+    __syncthreads();
+    if (!last_s) return;
+    __threadfence();
+    if (threadIdx.x == 0) carry_s[0] = carry_s[1] = 0;
+    __syncthreads();
+    for (int base = 0; base < B; base += blockDim.x) {
+        const int bb = base + threadIdx.x;
+        const bool live = bb < B && !status[bb].done;
+        const int v = live ? __ldcg(&occ_count[bb]) : 0, u = live ? __ldcg(&chunk_count[bb]) : 0;
+        const int ev = carry_s[0] + block_excl_scan(v, wsum);
+        const int eu = carry_s[1] + block_excl_scan(u, wsum);
+        if (bb < B) { occ_offset[bb] = ev; chunk_offset[bb] = eu; }
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) { carry_s[0] = ev + v; carry_s[1] = eu + u; }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) { occ_offset[B] = carry_s[0]; chunk_offset[B] = carry_s[1]; *ticket = 0; }
+}
+
 // ---- small trajectories: the whole binning of one trajectory in one CTA -------
 // Same table, scans, scatter and finalize as the kernel pipeline above, with
 // block barriers in place of kernel boundaries and the table cleared by its own
@@ -292,7 +321,7 @@ bin_fused_kernel(const __grid_constant__ kf_field_t f, int B, int n, int chunk, 
                  float4 *__restrict__ s_lo, double4 *__restrict__ s_pos, float4 *__restrict__ s_par,
                  int4 *__restrict__ s_aux, int4 *__restrict__ s_tree, float4 *__restrict__ cell_box,
                  int32_t *__restrict__ ticket, kf_status_t *status) {
-    __shared__ int m_s, last_s, carry_s[2];
+    __shared__ int m_s;
     __shared__ int wsum[32];
     __shared__ int buf[BF_WARPS][BF_CAP];
     const int b = blockIdx.x;
@@ -372,35 +401,145 @@ bin_fused_kernel(const __grid_constant__ kf_field_t f, int B, int n, int chunk, 
             __syncwarp();
         }
     }
-    // the last CTA: work-item prefixes over trajectories (live ones only)
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        last_s = atomicAdd(ticket, 1) == B - 1;
-    }
-    __syncthreads();
-    if (!last_s) return;
-    __threadfence();
-    if (threadIdx.x == 0) carry_s[0] = carry_s[1] = 0;
-    __syncthreads();
-    for (int base = 0; base < B; base += blockDim.x) {
-        const int bb = base + threadIdx.x;
-        const bool live = bb < B && !status[bb].done;
-        const int v = live ? __ldcg(&occ_count[bb]) : 0, u = live ? __ldcg(&chunk_count[bb]) : 0;
-        const int ev = carry_s[0] + block_excl_scan(v, wsum);
-        const int eu = carry_s[1] + block_excl_scan(u, wsum);
-        if (bb < B) { occ_offset[bb] = ev; chunk_offset[bb] = eu; }
+    publish_prefixes(B, occ_count, chunk_count, occ_offset, chunk_offset, ticket, status, wsum);
+}
+
+
+// ---- FieldConfig(use_hash=False): the quadratic all-pairs layout ---------------
+// Reference: Field._neighbor_table -> _brute_table (kcm.py:94-102, :153-162):
+// every pair is a candidate, no hashing.  Here: ONE cell holding every atom in
+// index order (identity permutation, no sort), centred on the trajectory's
+// centroid, with the one-cell stencil {0,0,0} (host side), so the same pair and
+// solvation kernels sweep all n^2 / 2 candidates.  The fp32 hi offsets must stay
+// within FLAT_MAX_OFFSET of the centre for the 1e-2 A^2 prefilter margin
+// (ulp(2048) = 1.2e-4 A -> |d(d^2)| < 8e-3 A^2 at the 9 A cut-off); beyond it the
+// trajectory stops with KF_ERR_EXTENT.  One CTA per trajectory.
+constexpr int FL_THREADS = 512;
+constexpr double FLAT_MAX_OFFSET = 2048.0;
+
+__global__ void __launch_bounds__(FL_THREADS)
+bin_flat_kernel(const __grid_constant__ kf_field_t f, int B, int n, int chunk, const double *__restrict__ pos,
+                unsigned long long *__restrict__ keys, int32_t *__restrict__ cnt, int32_t *__restrict__ start,
+                int32_t *__restrict__ occ, int32_t *__restrict__ occ_count, int32_t *__restrict__ chunk_pre,
+                int32_t *__restrict__ chunk_count, int32_t *__restrict__ occ_offset,
+                int32_t *__restrict__ chunk_offset, int32_t *__restrict__ atom_slot,
+                int32_t *__restrict__ atom_rank, int32_t *__restrict__ sorted_atom, float4 *__restrict__ s_hi,
+                float4 *__restrict__ s_lo, double4 *__restrict__ s_pos, float4 *__restrict__ s_par,
+                int4 *__restrict__ s_aux, int4 *__restrict__ s_tree, float4 *__restrict__ cell_box,
+                int32_t *__restrict__ ticket, kf_status_t *status) {
+    constexpr int NWF = FL_THREADS / 32;
+    __shared__ double red_s[NWF][3];
+    __shared__ float box_s[NWF][6];
+    __shared__ int slot_s, cell_s[3];
+    __shared__ int wsum[32];
+    const int b = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const size_t H = (size_t)1 << f.hash_bits;
+    if (!status[b].done) {
+        const double *pb = pos + (size_t)b * n * 3;
+        // centroid of the finite coordinates (fixed reduction order)
+        double sx = 0.0, sy = 0.0, sz = 0.0;
+        int bad = 0;
+        for (int a = threadIdx.x; a < n; a += blockDim.x) {
+            const double x = pb[3 * a], y = pb[3 * a + 1], z = pb[3 * a + 2];
+            if (isfinite(x) && isfinite(y) && isfinite(z)) { sx += x; sy += y; sz += z; } else bad = 1;
+        }
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+            sx += __shfl_xor_sync(0xffffffffu, sx, d);
+            sy += __shfl_xor_sync(0xffffffffu, sy, d);
+            sz += __shfl_xor_sync(0xffffffffu, sz, d);
+        }
+        if (lane == 0) { red_s[warp][0] = sx; red_s[warp][1] = sy; red_s[warp][2] = sz; }
+        bad = __syncthreads_or(bad);
+        if (bad && threadIdx.x == 0 && atomicCAS(&status[b].error, KF_ERR_NONE, KF_ERR_NONFINITE) == KF_ERR_NONE)
+            status[b].err_iter = status[b].iter;
+        unsigned long long *tk = keys + b * H;
+        int32_t *tc = cnt + b * H;
+        for (size_t q = threadIdx.x; q < H; q += blockDim.x) { tk[q] = EMPTY; tc[q] = 0; }
         __syncthreads();
-        if (threadIdx.x == blockDim.x - 1) { carry_s[0] = ev + v; carry_s[1] = eu + u; }
+        if (threadIdx.x == 0) {
+            double c[3] = {0.0, 0.0, 0.0};
+            for (int w = 0; w < NWF; ++w)
+                for (int q = 0; q < 3; ++q) c[q] += red_s[w][q];
+            const double inv = 1.0 / f.cell;
+            const int cx = cell_coord(c[0] / n, inv), cy = cell_coord(c[1] / n, inv), cz = cell_coord(c[2] / n, inv);
+            const uint32_t slot = cell_hash(cx, cy, cz, (uint32_t)H - 1);
+            tk[slot] = (unsigned long long)pack_cell(cx, cy, cz);
+            tc[slot] = n;
+            start[b * H + slot] = 0;
+            occ[b * H] = (int32_t)slot;
+            chunk_pre[b * H] = 0;
+            occ_count[b] = 1;
+            chunk_count[b] = (n + chunk - 1) / chunk;
+            slot_s = (int)slot; cell_s[0] = cx; cell_s[1] = cy; cell_s[2] = cz;
+        }
         __syncthreads();
+        const int slot = slot_s;
+        const double ctr[3] = {((double)cell_s[0] + 0.5) * f.cell, ((double)cell_s[1] + 0.5) * f.cell,
+                               ((double)cell_s[2] + 0.5) * f.cell};
+        const bool tree = !f.uniform_weights;
+        float bl[3] = {INFINITY, INFINITY, INFINITY}, bh[3] = {-INFINITY, -INFINITY, -INFINITY};
+        int far = 0;
+        for (int a = threadIdx.x; a < n; a += blockDim.x) {
+            const size_t g = (size_t)b * n + a;
+            const double x = pb[3 * a], y = pb[3 * a + 1], z = pb[3 * a + 2];
+            atom_slot[g] = slot; atom_rank[g] = a; sorted_atom[g] = a;
+            s_pos[g] = make_double4(x, y, z, f.solvation ? f.r_off[a] : 0.0);
+            const double r[3] = {x - ctr[0], y - ctr[1], z - ctr[2]};
+            float h[3], l[3];
+            for (int q = 0; q < 3; ++q) {
+                h[q] = (float)r[q];
+                l[q] = (float)(r[q] - (double)h[q]);
+                bl[q] = fminf(bl[q], h[q]);
+                bh[q] = fmaxf(bh[q], h[q]);
+                far |= !(fabs(r[q]) <= FLAT_MAX_OFFSET);
+            }
+            s_hi[g] = make_float4(h[0], h[1], h[2], 0.f);
+            s_lo[g] = make_float4(l[0], l[1], l[2], 0.f);
+            s_par[g] = reinterpret_cast<const float4 *>(f.atom_par)[a];
+            s_aux[g] = reinterpret_cast<const int4 *>(f.atom_aux)[a];
+            s_tree[g] = tree ? reinterpret_cast<const int4 *>(f.class_map)[a] : make_int4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1)
+            for (int q = 0; q < 3; ++q) {
+                bl[q] = fminf(bl[q], __shfl_xor_sync(0xffffffffu, bl[q], d));
+                bh[q] = fmaxf(bh[q], __shfl_xor_sync(0xffffffffu, bh[q], d));
+            }
+        if (lane == 0)
+            for (int q = 0; q < 3; ++q) { box_s[warp][q] = bl[q]; box_s[warp][3 + q] = bh[q]; }
+        far = __syncthreads_or(far);
+        if (threadIdx.x == 0) {
+            for (int w = 1; w < NWF; ++w)
+                for (int q = 0; q < 3; ++q) {
+                    box_s[0][q] = fminf(box_s[0][q], box_s[w][q]);
+                    box_s[0][3 + q] = fmaxf(box_s[0][3 + q], box_s[w][3 + q]);
+                }
+            cell_box[2 * (b * H + slot)] = make_float4(box_s[0][0], box_s[0][1], box_s[0][2], 0.f);
+            cell_box[2 * (b * H + slot) + 1] = make_float4(box_s[0][3], box_s[0][4], box_s[0][5], 0.f);
+            if (far && !bad && atomicCAS(&status[b].error, KF_ERR_NONE, KF_ERR_EXTENT) == KF_ERR_NONE)
+                status[b].err_iter = status[b].iter;
+        }
     }
-    if (threadIdx.x == 0) { occ_offset[B] = carry_s[0]; chunk_offset[B] = carry_s[1]; *ticket = 0; }
+    publish_prefixes(B, occ_count, chunk_count, occ_offset, chunk_offset, ticket, status, wsum);
 }
 
 }  // namespace
 
 int kf_bin_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s) {
     const int B = w->B, H = 1 << f->hash_bits;
+    if (f->flat) {   // FieldConfig(use_hash=False)
+        bin_flat_kernel<<<B, FL_THREADS, 0, s>>>(
+            *f, B, n, kf_pair_chunk(B, n, w->pair_chunk, f->precision), w->pos, w->cell_key, w->cell_cnt,
+            w->cell_start, w->occ, w->occ_count, w->chunk_pre, w->chunk_count, w->occ_offset, w->chunk_offset,
+            w->atom_slot, w->atom_rank, w->sorted_atom, reinterpret_cast<float4 *>(w->s_hi),
+            reinterpret_cast<float4 *>(w->s_lo), reinterpret_cast<double4 *>(w->s_pos),
+            reinterpret_cast<float4 *>(w->s_par), reinterpret_cast<int4 *>(w->s_aux),
+            reinterpret_cast<int4 *>(w->s_tree), reinterpret_cast<float4 *>(w->cell_box), w->work + 2, w->status);
+        KF_LAUNCH_CHECK("bin_flat_kernel");
+        return 0;
+    }
     if (n <= BF_MAX_ATOMS && B >= 32) {   // ensembles: one CTA per trajectory does the whole binning
         bin_fused_kernel<<<B, BF_THREADS, 0, s>>>(
             *f, B, n, kf_pair_chunk(B, n, w->pair_chunk, f->precision), w->pos, w->cell_key, w->cell_cnt,

@@ -395,7 +395,9 @@ class DeviceField(ParamTables):
             self.n_solv_nz = int(np.count_nonzero(gamma != 0.0))
         reach *= 1.0 + 1e-9
         s.cell = reach              # one cell per reach: the 27-cell stencil
-        sten = _stencil(s.cell, reach)
+        # use_hash=False (kcm.py:94-102): one all-atom cell, every pair a candidate
+        s.flat = 0 if cfg.use_hash else 1
+        sten = _stencil(s.cell, reach) if cfg.use_hash else np.zeros((1, 3), np.int64)
         t["stencil"] = _up(sten, np.int32)
         s.stencil = t["stencil"].data_ptr()
         s.n_stencil = len(sten)
@@ -511,6 +513,9 @@ def _raise_status(st, df: DeviceField | None, batch: Batch, prefix: str = "", b:
         raise StericClashError(f"{prefix}atoms {i} and {j} closer than {MIN_DISTANCE} A (d={d:.3e})")
     if st.error == N.ERR_NONFINITE:
         raise ConfigurationError(f"{prefix}non-finite coordinates cannot be hashed")
+    if st.error == N.ERR_EXTENT:
+        raise ConfigurationError(f"{prefix}use_hash=False: an atom lies more than 2048 A from the structure's "
+                                 "centroid cell (fp32 offset range of the all-pairs layout)")
     if st.error == N.ERR_CAPACITY:
         raise NativeLibraryError(f"{prefix}solvation neighbour capacity exceeded "
                                  f"({st.overflow} > {batch.struct.nb_cap})")

@@ -179,3 +179,53 @@ def fold_batch(chain, confs, fld, step, out, *, manifest: dict | None = None, ve
     if manifest is not None:
         write_manifest(out, manifest)
     return trajs
+
+
+BENCH_COLUMNS = ["m", "atoms", "t_hash_build", "t_force_hashed", "t_force_brute", "t_solvation"]
+
+
+def bench_table(sizes, out, *, water: bool = False, samples: int = 1024, repeat: int = 3,
+                gamma_set: str = "sharp", params_path=None, verbose: bool = False) -> list:
+    """``kinefold bench`` (cli.py:245-286): poly-ALA chains of ``sizes``
+    residues at the zero-point conformation, one ``Field.evaluate`` with the
+    hash grid and one with ``use_hash=False`` (the quadratic path) per repeat,
+    best-of-``repeat`` phase times (device-event seconds here).  Writes
+    ``out/bench.csv`` (the reference's columns and 6-decimal format) and
+    ``out/manifest.json``; returns the rows."""
+    import dataclasses
+
+    from . import __version__
+    from .chain import build_chain, forward_kinematics
+    from .kcm import Field, FieldConfig
+    from .params import load_params
+    from .solvation import SolvationConfig
+    from .topology import TreeWeights, build_tree
+    out = Path(out)
+    out.mkdir(parents=True, exist_ok=True)
+    ps = load_params(params_path)
+    rows = []
+    for m in [int(s) for s in sizes]:
+        chain = build_chain(["ALA"] * m)
+        weights = TreeWeights(build_tree(chain), ps.weights)
+        base = FieldConfig(solvation=bool(water), solvation_cfg=SolvationConfig(samples=samples))
+        params = ps.resolve(chain, gamma_set)
+        fld_h = Field(params, weights, base)
+        fld_b = Field(params, weights, dataclasses.replace(base, use_hash=False))
+        pos = forward_kinematics(chain, chain.conf_zp())
+        t_hash = t_force_h = t_force_b = t_solv = float("inf")
+        for _ in range(max(1, int(repeat))):
+            r = fld_h.evaluate(pos)
+            t_hash = min(t_hash, r.timings["hash"])
+            t_force_h = min(t_force_h, r.timings["force"])
+            t_solv = min(t_solv, r.timings["solvation"])
+            rb = fld_b.evaluate(pos)
+            # the quadratic mode's layout pass is force work (cli.py:272-273)
+            t_force_b = min(t_force_b, rb.timings["force"] + rb.timings["hash"])
+        rows.append([m, chain.n_atoms, t_hash, t_force_h, t_force_b, t_solv])
+        if verbose:
+            print(f"{m:6d} {chain.n_atoms:7d} {t_hash:10.5f} {t_force_h:11.5f} {t_force_b:11.5f} {t_solv:10.5f}")
+    _csv(out / "bench.csv", [BENCH_COLUMNS] + [[r[0], r[1]] + [f"{x:.6f}" for x in r[2:]] for r in rows])
+    write_manifest(out, {"version": __version__, "command": "bench",
+                         "arguments": {"sizes": ",".join(str(s) for s in sizes), "water": bool(water),
+                                       "samples": samples, "repeat": repeat, "gamma_set": gamma_set}})
+    return rows

@@ -529,3 +529,82 @@ def test_solvation_overflow_pass_bitexact():
     out = subprocess.run([sys.executable, "-c", _OVERFLOW_SCRIPT], cwd=ROOT, env=env, capture_output=True,
                          text=True, timeout=600)
     assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-3000:]
+
+
+# ---- FieldConfig(use_hash=False): the quadratic all-pairs path (kcm.py:94-102, :153-162)
+
+def _flat(fld):
+    from dataclasses import replace
+    P = _P()
+    return P.Field(fld.params, fld.weights, replace(fld.config, use_hash=False))
+
+
+@pytest.mark.parametrize("name", ["c1_helix", "c2_random"])
+def test_use_hash_false_evaluate_matches_reference(name):
+    """The brute-force table gives the same pair set as the hash grid (the
+    reference's grid independence), so the same force/energy bars hold."""
+    g = golden(name)
+    ch, params, w, fld = make_system(g["seq"])
+    res = _flat(fld).evaluate(g["positions"])
+    _, _, extra = O.OracleField(params, w).evaluate(g["positions"])
+    scale = pair_scale(params, w, g["positions"], extra["i"], extra["j"], extra["d"])
+    err = np.linalg.norm(res.forces - g["forces"], axis=1)
+    assert np.all(err <= FORCE_TOL * np.maximum(scale, 1e-300)), (err / scale).max()
+    e = np.array([res.energy.g_elec, res.energy.g_vdw, res.energy.g_cav])
+    assert np.all(np.abs(e - g["energies"]) <= 1e-6 * np.abs(g["energies"]) + 1e-9)
+
+
+def test_use_hash_false_solvation_bitexact():
+    from dataclasses import replace
+    P = _P()
+    g = golden("mixed_water")
+    ch, params, w, _ = make_system(g["seq"], solvation=True)
+    null = replace(params, q=np.zeros(ch.n_atoms), eps=np.zeros(ch.n_atoms))
+    fld = P.Field(null, w, P.FieldConfig(solvation=True, use_hash=False))
+    res = fld.evaluate(g["positions"])
+    assert np.array_equal(res.forces, g["solv_forces"])
+    assert np.array_equal(res.sasa.f_exp, g["sasa_f_exp"])
+    assert res.energy.g_cav == pytest.approx(float(g["sasa_g_cav"]), rel=1e-13, abs=1e-12)
+
+
+@pytest.mark.parametrize("name,solv", [("fold_vacuum", False), ("fold_water", True)])
+def test_use_hash_false_fold_matches_reference(name, solv):
+    P = _P()
+    g, step = _traj(name)
+    ch, params, w, fld = make_system(g["seq"], solvation=solv)
+    conf = P.Conformation(g["theta0"], g["frozen"], ch.n_residues)
+    tr = P.fold(ch, conf, _flat(fld), step)
+    assert tr.iterations == len(g["energies"]) and tr.reason == str(g["reason"])
+    E = np.array([[r.energy.g_elec, r.energy.g_vdw, r.energy.g_cav] for r in tr.records])
+    scale = np.abs(g["energies"]).sum(axis=1)
+    assert np.all(np.abs(E - g["energies"]).sum(axis=1) <= 1e-5 * scale)
+
+
+def test_use_hash_false_ensemble_half_list():
+    """Ensembles take the half-list kernel; with one all-atom cell it sweeps each
+    unordered pair once.  The first record (the start conformations, before the
+    fp32 summation order can steer these clash-laden random starts apart) meets
+    the pair bar against the hashed ensemble; the pair counts are equal."""
+    P = _P()
+    ch, params, w, fld = make_system(["ALA", "SER", "CYS"] * 6)
+    rng = np.random.default_rng(5)
+    confs = [ch.conf_from_backbone(rng.uniform(-90, 90, ch.n_residues), rng.uniform(-90, 90, ch.n_residues))
+             for _ in range(256)]   # B * n >= 40k: the warp-per-item half-list kernel
+    st = P.StepConfig(max_iters=1, torque_tol_rel=0.0, energy_window=0)
+    a = P.fold_ensemble(ch, confs, fld, st)
+    b = P.fold_ensemble(ch, confs, _flat(fld), st)
+    ea, eb = a.energies[:, 0, :3], b.energies[:, 0, :3]
+    assert np.all(np.abs(ea - eb).sum(axis=1) <= 1e-6 * np.abs(ea).sum(axis=1))
+    assert np.abs(b.theta - a.theta).max() <= 1e-4 * st.kappa
+    if a.n_pairs is not None:
+        assert np.array_equal(a.n_pairs, b.n_pairs)
+
+
+def test_use_hash_false_extent_guard():
+    from paper_1712_05012_b200.errors import ConfigurationError
+    g = golden("c1_helix")
+    _, _, _, fld = make_system(g["seq"])
+    pos = np.array(g["positions"], float)
+    pos[0] += 5000.0
+    with pytest.raises(ConfigurationError, match="use_hash=False"):
+        _flat(fld).evaluate(pos)

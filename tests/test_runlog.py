@@ -111,3 +111,21 @@ def test_fold_batch_matches_reference_cli(tmp_path):
             (["snap_000000.pdb", "snap_000010.pdb", "snap_000020.pdb"] if run == 0
              else ["snap_000000.pdb", "snap_000010.pdb"])
     _pdb_close(tmp_path / "run_0000" / "snap_000010.pdb", os.path.join(GOLD, "run_0000", "snap_000010.pdb"))
+
+
+@pytest.mark.gpu
+def test_bench_table_rows_and_trend(tmp_path):
+    """``kinefold bench`` (test_cli.py:97-106): header + one row per size, and
+    at the largest size the hashed force pass beats the quadratic one."""
+    import json
+
+    import paper_1712_05012_b200 as P
+    out = tmp_path / "b"
+    P.bench_table([20, 40, 80], out, repeat=2)
+    with open(out / "bench.csv", newline="") as fh:
+        rows = list(csv.reader(fh))
+    assert rows[0] == ["m", "atoms", "t_hash_build", "t_force_hashed", "t_force_brute", "t_solvation"]
+    assert len(rows) == 4 and [r[0] for r in rows[1:]] == ["20", "40", "80"]
+    assert all(len(v.split(".")[1]) == 6 for r in rows[1:] for v in r[2:])
+    assert float(rows[-1][3]) <= float(rows[-1][4])
+    assert json.loads((out / "manifest.json").read_text())["command"] == "bench"
