@@ -398,16 +398,30 @@ def main():
     # the committed `ncu --set full` capture of the same workload, if there is one
     kernel = "pair_kernel<1,0>" if P.pair_precision() == "fp64" else \
         ("pair_dense_kernel<0,0,1>" if B * ch.n_atoms >= 40000 else "pair_dense_kernel<0,1,0>")
-    traffic, traffic_src = None, None
+    traffic, traffic_src, prof = None, None, {}
     prof_path = os.path.join(ROOT, "profiles", "pair_kernel_traffic.json")
     if os.path.exists(prof_path):
         try:
             for rec in json.load(open(prof_path)):
                 if rec.get("kernel") == kernel and rec.get("workload") == workload_name(args) \
                         and rec.get("ensemble") == B:
-                    traffic, traffic_src = rec.get("bytes_per_launch"), rec.get("source")
+                    traffic, traffic_src, prof = rec.get("bytes_per_launch"), rec.get("source"), rec
         except (OSError, ValueError, AttributeError):
             traffic = None
+    # shared-memory bandwidth of the pair kernel (north star): the capture's shared
+    # wavefronts per launch (128 B each) over the live-measured launch time, against
+    # the nominal 32 banks x 4 B per clock per SM at the clock seen under load
+    smem = None
+    wf = prof.get("smem_wavefronts_per_launch")
+    if wf and pair_ms > 0:
+        mhz = (clk or {}).get("sm_mhz") or 1965.0
+        sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
+        smem_peak = 128.0 * sm_count * mhz * 1e6 / 1e9
+        smem_gbs = wf * 128.0 / (pair_ms * 1e-3) / 1e9
+        smem = {"achieved": smem_gbs, "peak": smem_peak, "unit": "GB/s", "frac": smem_gbs / smem_peak,
+                "wavefronts_per_launch": wf, "fma_pipe_pct_of_active": prof.get("fma_pipe_pct"),
+                "issue_active_pct": prof.get("issue_active_pct"),
+                "peak_source": f"nominal 128 B/clk/SM x {sm_count} SMs at {mhz:.0f} MHz"}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
@@ -426,7 +440,8 @@ def main():
                              f"on this rank's {B} trajectories",
                      "peak_source": "kf_peak_flops FFMA microbenchmark, this GPU, this run",
                      "fp64_peak_tflops": peak64 / 1e12,
-                     "kernel_share_of_step": pair_ms / step_ms_eager},
+                     "kernel_share_of_step": pair_ms / step_ms_eager,
+                     "smem": smem},
         "phase_ms_per_step": acc,
         "phase_rooflines": phase_roofline,
         "gpu_launches": launches,
