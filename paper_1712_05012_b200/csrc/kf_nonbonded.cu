@@ -64,6 +64,10 @@ struct WarpSmem {
     unsigned short list[1024]; // candidate (owner << 5 | t) pairs of the tile, owner-major
 };
 
+#ifndef EXACT_BITWISE
+#define EXACT_BITWISE 1   // exact-band membership test without short-circuit branches
+#endif
+
 // fp32 constants of the fast path, passed by value (kernel parameter space:
 // constant-bank operands, no registers).
 struct PairConst {
@@ -156,8 +160,14 @@ KF_DEV void pair_eval(const kf_field_t &f, const PairConst &pc, float4 hi, float
     const float we = pc.we[cls - 1], wv = pc.wv[cls - 1];   // constant-bank loads, indexed
     // exact recomputation near a threshold: |d2 - t| <= band for t in {cut, te, tv}
     // (te == cut to ~1e-14 for the default cut-offs: pc.te_is_cut folds the test)
+#if EXACT_BITWISE
+    // non-short-circuit: predicated compares instead of a branch per threshold
+    const bool exact = F64 || ((fabsf(d2f - cut2f) <= band) | (fabsf(d2f - tvf) <= band) |
+                               (!pc.te_is_cut & (fabsf(d2f - tef) <= band)) | (d2f < pc.f64_d2));
+#else
     const bool exact = F64 || fabsf(d2f - cut2f) <= band || fabsf(d2f - tvf) <= band ||
                        (!pc.te_is_cut && fabsf(d2f - tef) <= band) || d2f < pc.f64_d2;
+#endif
     if (exact) {
         // the outlined path writes through pointers: give it its own stack
         // temporaries so out / pce / pcv stay in registers on the fast path
@@ -168,7 +178,7 @@ KF_DEV void pair_eval(const kf_field_t &f, const PairConst &pc, float4 hi, float
         pce = sce; pcv = scv;
         return;
     }
-    if (d2f > cut2f) return;
+    // (here d2f < cut2f - band: nearer the cut-off went exact, beyond it returned above)
     const bool ke = d2f <= tef, kv = d2f <= tvf;
     pce = ke; pcv = kv;
     // MUFU.RSQ without the subnormal fix-up rsqrtf carries: d2f >= f64_d2 > 0
@@ -176,24 +186,22 @@ KF_DEV void pair_eval(const kf_field_t &f, const PairConst &pc, float4 hi, float
     float inv_r;
     asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(inv_r) : "f"(d2f));
     const float inv_r2 = inv_r * inv_r;
-    float g = 0.f;
-    if (ke) {
-        // kappa = d: E = K w qi qj / d^2; constant: E = K w qi qj / (kappa d);
-        // |F| / d = E / d^2 in both cases
-        const float qq = (float)COULOMB_K * qi.x * qj.x * we;
-        const float e = pc.dconst ? qq * pc.kap_inv * inv_r : qq * inv_r2;
-        out[3] = e;
-        g += e * inv_r2;
-    }
-    if (kv) {
-        const float weps = wv * qi.z * qj.z;
-        const float D = qi.y + qj.y;
-        const float sr = D * D * inv_r2;
-        const float s3 = sr * sr * sr;
-        const float s6 = s3 * s3;
-        out[4] = weps * (s6 - 2.f * s3);
-        g += 12.f * weps * (s6 - s3) * inv_r2;
-    }
+    // both terms evaluated and selected (no divergent branches; same values)
+    // kappa = d: E = K w qi qj / d^2; constant: E = K w qi qj / (kappa d);
+    // |F| / d = E / d^2 in both cases
+    const float qq = (float)COULOMB_K * qi.x * qj.x * we;
+    const float e = pc.dconst ? qq * pc.kap_inv * inv_r : qq * inv_r2;
+    const float weps = wv * qi.z * qj.z;
+    const float D = qi.y + qj.y;
+    const float sr = D * D * inv_r2;
+    const float s3 = sr * sr * sr;
+    const float s6 = s3 * s3;
+    out[3] = ke ? e : 0.f;
+    out[4] = kv ? weps * (s6 - 2.f * s3) : 0.f;
+    // g = e / d^2, then + 12 w eps (s6 - s3) / d^2 as one FFMA (the rounding of the
+    // branchy form: fp32 trajectories are chaotic, keep their rounding stable)
+    float g = ke ? e * inv_r2 : 0.f;
+    g = kv ? __fmaf_rn(12.f * weps * (s6 - s3), inv_r2, g) : g;
     out[0] = g * dxf; out[1] = g * dyf; out[2] = g * dzf;
 }
 
@@ -614,7 +622,9 @@ pair_dense_kernel(const __grid_constant__ kf_field_t f, const __grid_constant__ 
                 const int i_pos = ic + oi;              // i's position in its cell
                 for (int kt = 0; kt < n_it; ++kt) {
                     const int t = ph + kt * nph;
-                    const bool live = own && t < nt && (jb + t >= c || jb + t > i_pos);
+                    // own-cell atoms lead the stream (stream positions < c, i_pos < c), so
+                    // "j after i in the own cell, or j in a forward cell" is one compare
+                    const bool live = own && t < nt && jb + t > i_pos;
                     const float4 hj = J.hi[t < nt ? t : 0];
                     const float dx = hi.x - hj.x, dy = hi.y - hj.y, dz = hi.z - hj.z;
                     const bool pass = live && dx * dx + dy * dy + dz * dz <= pre2;
@@ -628,10 +638,11 @@ pair_dense_kernel(const __grid_constant__ kf_field_t f, const __grid_constant__ 
                     }
                     fx += out[0]; fy += out[1]; fz += out[2]; fe += out[3]; fv += out[4];
                     ce += pce; cv += pcv;
-                    if (pass) {   // this lane's -f on j = t (slot [t][oi]: one writer per tile)
-                        Jc_s[warp][0][t][oi] = (float)-out[0];
-                        Jc_s[warp][1][t][oi] = (float)-out[1];
-                        Jc_s[warp][2][t][oi] = (float)-out[2];
+                    if (pass) {   // this lane's f on i for j = t (slot [t][oi]: one writer per
+                        // tile); the flush subtracts, so j receives -f
+                        Jc_s[warp][0][t][oi] = (float)out[0];
+                        Jc_s[warp][1][t][oi] = (float)out[1];
+                        Jc_s[warp][2][t][oi] = (float)out[2];
                     }
                 }
                 __syncwarp();
@@ -645,7 +656,7 @@ pair_dense_kernel(const __grid_constant__ kf_field_t f, const __grid_constant__ 
                         float acc = 0.f;
                         for (int o4 = 0; o4 < (wi + 3) / 4; ++o4) {
                             const float4 c4 = r[o4];
-                            acc += c4.x; acc += c4.y; acc += c4.z; acc += c4.w;
+                            acc -= c4.x; acc -= c4.y; acc -= c4.z; acc -= c4.w;   // (-a) + (-b) == -a - b
                         }
                         v[q] = (double)acc;
                     }
