@@ -111,9 +111,15 @@ __device__ __forceinline__ int block_excl_scan(int v, int *wsum) {
 __global__ void __launch_bounds__(1024)
 cell_scan_kernel(int H, int chunk, const int32_t *__restrict__ occ, const int32_t *__restrict__ occ_count,
                  const int32_t *__restrict__ cnt, int32_t *__restrict__ start, int32_t *__restrict__ chunk_pre,
-                 int32_t *__restrict__ chunk_count, const kf_status_t *status) {
+                 int32_t *__restrict__ chunk_count, const kf_status_t *status, int32_t *__restrict__ occ_offset,
+                 int32_t *__restrict__ chunk_offset) {
+    // occ_offset / chunk_offset non-null (one trajectory): the work prefixes are
+    // written here and occ_prefix_kernel is skipped
     const int b = blockIdx.x;
-    if (status[b].done) return;
+    if (status[b].done) {
+        if (occ_offset && threadIdx.x == 0) { occ_offset[0] = occ_offset[1] = 0; chunk_offset[0] = chunk_offset[1] = 0; }
+        return;
+    }
     const int m = occ_count[b];
     const int32_t *ob = occ + (size_t)b * H;
     const int32_t *cb = cnt + (size_t)b * H;
@@ -135,7 +141,22 @@ cell_scan_kernel(int H, int chunk, const int32_t *__restrict__ occ, const int32_
         sb[ob[k]] = run; run += c;
         pb[k] = crun; crun += (c + chunk - 1) / chunk;
     }
-    if (threadIdx.x == blockDim.x - 1) chunk_count[b] = crun;
+    if (threadIdx.x == blockDim.x - 1) {
+        chunk_count[b] = crun;
+        if (occ_offset) { occ_offset[0] = 0; occ_offset[1] = m; chunk_offset[0] = 0; chunk_offset[1] = crun; }
+    }
+}
+
+// The per-launch hash-table reset (keys empty, counts and occupied counts zero):
+// one kernel node instead of three memsets.
+__global__ void bin_clear_kernel(long long n_tab, int B, unsigned long long *__restrict__ keys,
+                                 int32_t *__restrict__ cnt, int32_t *__restrict__ occ_count) {
+    for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < n_tab;
+         q += (long long)gridDim.x * blockDim.x) {
+        keys[q] = EMPTY;
+        cnt[q] = 0;
+        if (q < B) occ_count[q] = 0;
+    }
 }
 
 // Work-item prefixes over trajectories: occupied cells (bin_finalize) and
@@ -551,19 +572,23 @@ int kf_bin_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s) {
         KF_LAUNCH_CHECK("bin_fused_kernel");
         return 0;
     }
-    KF_CUDA(cudaMemsetAsync(w->cell_key, 0xFF, sizeof(unsigned long long) * (size_t)B * H, s), "memset keys");
-    KF_CUDA(cudaMemsetAsync(w->cell_cnt, 0, sizeof(int32_t) * (size_t)B * H, s), "memset cnt");
-    KF_CUDA(cudaMemsetAsync(w->occ_count, 0, sizeof(int32_t) * (size_t)B, s), "memset occ");
+    const long long n_tab = (long long)B * H;
+    bin_clear_kernel<<<(unsigned)std::min<long long>(kf_blocks(n_tab, 256), 4 * 148), 256, 0, s>>>(
+        n_tab, B, w->cell_key, w->cell_cnt, w->occ_count);
+    KF_LAUNCH_CHECK("bin_clear_kernel");
     const long long total = (long long)B * n;
     bin_insert_kernel<<<kf_blocks(total, 256), 256, 0, s>>>(*f, B, n, w->pos, w->cell_key, w->cell_cnt, w->occ,
                                                             w->occ_count, w->atom_slot, w->atom_rank, w->status);
     KF_LAUNCH_CHECK("bin_insert_kernel");
-    cell_scan_kernel<<<B, 1024, 0, s>>>(H, kf_pair_chunk(B, n, w->pair_chunk, f->precision), w->occ, w->occ_count, w->cell_cnt, w->cell_start, w->chunk_pre,
-                                         w->chunk_count, w->status);
+    cell_scan_kernel<<<B, 1024, 0, s>>>(H, kf_pair_chunk(B, n, w->pair_chunk, f->precision), w->occ, w->occ_count,
+                                         w->cell_cnt, w->cell_start, w->chunk_pre, w->chunk_count, w->status,
+                                         B == 1 ? w->occ_offset : nullptr, B == 1 ? w->chunk_offset : nullptr);
     KF_LAUNCH_CHECK("cell_scan_kernel");
-    occ_prefix_kernel<<<1, 1024, 0, s>>>(B, w->occ_count, w->occ_offset, w->chunk_count, w->chunk_offset,
-                                         w->status);
-    KF_LAUNCH_CHECK("occ_prefix_kernel");
+    if (B > 1) {
+        occ_prefix_kernel<<<1, 1024, 0, s>>>(B, w->occ_count, w->occ_offset, w->chunk_count, w->chunk_offset,
+                                             w->status);
+        KF_LAUNCH_CHECK("occ_prefix_kernel");
+    }
     bin_scatter_kernel<<<kf_blocks(total, 256), 256, 0, s>>>(*f, B, n, w->atom_slot, w->atom_rank, w->cell_start,
                                                              w->sorted_atom, w->status);
     KF_LAUNCH_CHECK("bin_scatter_kernel");
