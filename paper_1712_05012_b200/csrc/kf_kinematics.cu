@@ -124,10 +124,16 @@ fk_smem_kernel(const __grid_constant__ kf_chain_t c, const double *__restrict__ 
                double *__restrict__ T_all, double *__restrict__ pos_all, const kf_status_t *__restrict__ status) {
     const int b = blockIdx.x;
     if (status && status[b].done) return;
-    extern __shared__ __align__(16) double S[];     // [L][12]
+    extern __shared__ __align__(16) double S[];     // [L][12], then the int tables below
     __shared__ double chunk[FKS_THREADS][12];
-    const int L = c.n_links, D = c.n_dof, n = c.n_atoms;
+    const int L = c.n_links, D = c.n_dof, n = c.n_atoms, nb = c.n_bb, ns = c.n_side;
     const double *theta = theta_all + (size_t)b * D;
+    // the chain tables the serial phases walk, staged once (one global round trip
+    // instead of one per dependent step): parent, dof, backbone order, side order
+    int *sh_par = reinterpret_cast<int *>(S + FKS_STRIDE * L), *sh_dof = sh_par + L, *sh_bb = sh_dof + L,
+        *sh_side = sh_bb + nb;
+    for (int k = threadIdx.x; k < nb; k += blockDim.x) sh_bb[k] = c.bb_order[k];
+    for (int k = threadIdx.x; k < ns; k += blockDim.x) sh_side[k] = c.side_order[k];
 
     {
         // local transforms; the chain tables and angles of U links per thread are
@@ -143,6 +149,7 @@ fk_smem_kernel(const __grid_constant__ kf_chain_t c, const double *__restrict__ 
                 const int l = l0 + u * blockDim.x;
                 dof[u] = (l < L && l != 0) ? link_dof[l] : -1;
                 par[u] = (l < L && l != 0) ? link_parent[l] : 0;
+                if (l < L) { sh_dof[l] = dof[u]; sh_par[l] = par[u]; }
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) th[u] = dof[u] >= 0 ? theta[dof[u]] : 0.0;
@@ -158,12 +165,11 @@ fk_smem_kernel(const __grid_constant__ kf_chain_t c, const double *__restrict__ 
     }
     __syncthreads();
 
-    const int nb = c.n_bb;
     const int per = (nb + blockDim.x - 1) / blockDim.x;
     const int lo = min(nb, (int)threadIdx.x * per), hi = min(nb, lo + per);
     Xf acc = xf_identity();
     for (int k = lo; k < hi; ++k) {
-        double *slot = S + FKS_STRIDE * c.bb_order[k];
+        double *slot = S + FKS_STRIDE * sh_bb[k];
         acc = xf_compose(acc, xf_load(slot));
         xf_store(slot, acc);
     }
@@ -180,16 +186,16 @@ fk_smem_kernel(const __grid_constant__ kf_chain_t c, const double *__restrict__ 
     if (threadIdx.x > 0 && lo < hi) {
         const Xf pre = xf_load(chunk[threadIdx.x - 1]);
         for (int k = lo; k < hi; ++k) {
-            double *slot = S + FKS_STRIDE * c.bb_order[k];
+            double *slot = S + FKS_STRIDE * sh_bb[k];
             xf_store(slot, xf_compose(pre, xf_load(slot)));
         }
     }
     __syncthreads();
     for (int d = 0; d < c.side_depth; ++d) {
         for (int k = c.side_depth_off[d] + threadIdx.x; k < c.side_depth_off[d + 1]; k += blockDim.x) {
-            const int l = c.side_order[k];
+            const int l = sh_side[k];
             double *slot = S + FKS_STRIDE * l;
-            xf_store(slot, xf_compose(xf_load(S + FKS_STRIDE * c.link_parent[l]), xf_load(slot)));
+            xf_store(slot, xf_compose(xf_load(S + FKS_STRIDE * sh_par[l]), xf_load(slot)));
         }
         __syncthreads();
     }
@@ -200,7 +206,7 @@ fk_smem_kernel(const __grid_constant__ kf_chain_t c, const double *__restrict__ 
     for (int l = threadIdx.x; l < L; l += blockDim.x) {
         const double *src = S + FKS_STRIDE * l;
         double *dst = T + (size_t)KF_XF_STRIDE * l;
-        const bool joint = l != 0 && link_dof[l] >= 0;
+        const bool joint = l != 0 && sh_dof[l] >= 0;
         const double a0 = axis0[3 * l], a1 = axis0[3 * l + 1], a2 = axis0[3 * l + 2];
         double v[KF_XF_STRIDE];
 #pragma unroll
@@ -390,8 +396,9 @@ __global__ void fk_positions_kernel(kf_chain_t c, int B, const double *__restric
 
 int kf_fk_launch(const kf_chain_t *c, kf_batch_t *w, const kf_status_t *status, cudaStream_t s) {
     const int n_seg = (c->n_bb + SEG - 1) / SEG;
-    const size_t smem = (size_t)c->n_links * FKS_STRIDE * sizeof(double);
-    if (smem <= 110 * 1024) {   // whole chain in one CTA's shared memory
+    const size_t smem = (size_t)c->n_links * FKS_STRIDE * sizeof(double) +
+                        sizeof(int32_t) * (2 * (size_t)c->n_links + c->n_bb + c->n_side);
+    if (smem <= 110 * 1024) {   // whole chain (transforms + walk tables) in one CTA's shared memory
         static size_t opted = 0;
         if (smem > opted) {
             KF_CUDA(cudaFuncSetAttribute(fk_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
