@@ -422,6 +422,19 @@ def main():
                 "wavefronts_per_launch": wf, "fma_pipe_pct_of_active": prof.get("fma_pipe_pct"),
                 "issue_active_pct": prof.get("issue_active_pct"),
                 "peak_source": f"nominal 128 B/clk/SM x {sm_count} SMs at {mhz:.0f} MHz"}
+    # instruction issue (the kernel's actual bound): the capture's warp-instructions per
+    # launch over the live launch time, against 4 schedulers x 1 warp-instruction/clk per SM
+    issue = None
+    wi = prof.get("warp_instructions_per_launch")
+    if wi and pair_ms > 0:
+        mhz = (clk or {}).get("sm_mhz") or 1965.0
+        sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
+        ipk = 4.0 * sm_count * mhz * 1e6 / 1e9
+        got = wi / (pair_ms * 1e-3) / 1e9
+        issue = {"achieved": got, "peak": ipk, "unit": "G warp-instructions/s", "frac": got / ipk,
+                 "warp_instructions_per_launch": wi,
+                 "per_pair": wi / max(1.0, float(p9)),
+                 "peak_source": f"4 issue slots/clk/SM x {sm_count} SMs at {mhz:.0f} MHz"}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
@@ -441,7 +454,7 @@ def main():
                      "peak_source": "kf_peak_flops FFMA microbenchmark, this GPU, this run",
                      "fp64_peak_tflops": peak64 / 1e12,
                      "kernel_share_of_step": pair_ms / step_ms_eager,
-                     "smem": smem},
+                     "smem": smem, "issue": issue},
         "phase_ms_per_step": acc,
         "phase_rooflines": phase_roofline,
         "gpu_launches": launches,
