@@ -337,7 +337,7 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_extras:
         # single-trajectory C2 / C3 on one GPU (graph-replayed), and CPU legs
-        for cfg in ("C2", "C3"):
+        for cfg in ("C2", "C3", "C4"):   # C4: ~100k atoms (GPU only; the CPU port needs ~20 s/iteration)
             c_ch, c_p, c_w, c_f = workloads.system(cfg, solvation=args.water)
             r1 = DV.EnsembleRunner(c_ch, c_f, 1, P.StepConfig(max_iters=W + K, torque_tol_rel=0.0,
                                                             energy_window=0), chunk=16)
