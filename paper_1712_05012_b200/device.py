@@ -498,6 +498,18 @@ class Batch:
         raw = self.t["status"].cpu().numpy().tobytes()
         return (N.KfStatus * self.B).from_buffer_copy(raw)
 
+    def status_array(self) -> np.ndarray:
+        """The status block as a numpy structured array (one D2H copy)."""
+        return np.frombuffer(self.t["status"].cpu().numpy().tobytes(), np.dtype(N.KfStatus))
+
+    def status_snapshots(self):
+        """Two pinned host copies of the status block with their events (the
+        fold loop's pipelined stop test)."""
+        if getattr(self, "_snaps", None) is None:
+            self._snaps = [(torch.empty_like(self.t["status"], device="cpu").pin_memory(),
+                            torch.cuda.Event()) for _ in range(2)]
+        return self._snaps
+
 
 # --------------------------------------------------------------------------
 # errors from the device status block
@@ -608,8 +620,14 @@ def _step_struct(step) -> N.KfStep:
     return s
 
 
+_STATUS_DTYPE = np.dtype(N.KfStatus)
+
+
 def _run_loop(dc, df, b, step, chunk: int, on_first=None):
-    """Replay graph chunks until every trajectory reports done."""
+    """Replay graph chunks until every trajectory reports done.  The stop test
+    is pipelined: chunk k+1 is enqueued before the host reads chunk k's status
+    (an async copy into pinned memory), so the GPU never idles on the poll; a
+    chunk enqueued after the last trajectory stopped is a no-op on device."""
     lib = N.lib()
     cs, fs, bs, ss = N.ref(dc.struct), N.ref(df.struct_for(False)), N.ref(b.struct), N.ref(_step_struct(step))
     s = stream()
@@ -619,13 +637,23 @@ def _run_loop(dc, df, b, step, chunk: int, on_first=None):
         done_iters = 1
         if all(x.done for x in b.status()):
             done_iters = step.max_iters
+    snaps = b.status_snapshots()
+    pending, turn = None, 0
     while done_iters < step.max_iters:
         k = min(chunk, step.max_iters - done_iters)
         N.check(lib.kf_fold_iterations(cs, fs, bs, ss, k, _sp()), "kf_fold_iterations")
         done_iters += k
-        sts = b.status()
-        if all(x.done for x in sts):
+        if done_iters >= step.max_iters:
             break
+        host, ev = snaps[turn]
+        host.copy_(b.t["status"], non_blocking=True)
+        ev.record(s)
+        if pending is not None:
+            p_host, p_ev = pending
+            p_ev.synchronize()
+            if np.frombuffer(p_host.numpy().tobytes(), _STATUS_DTYPE)["done"].all():
+                break
+        pending, turn = snaps[turn], 1 - turn
     s.synchronize()
 
 
@@ -731,13 +759,34 @@ class EnsembleRunner:
                            record_theta=record_theta)
         self.fld = fld
 
+    def _pinned(self):
+        if getattr(self, "_pin", None) is None:
+            D = self.dc.n_dof
+            self._pin = (torch.empty((self.B, D), dtype=torch.float64).pin_memory(),
+                         torch.empty((self.B, D), dtype=torch.uint8).pin_memory())
+        return self._pin
+
     def load(self, thetas, frozen):
+        """Host conformations in: staged in pinned memory, copied asynchronously."""
         b, D = self.batch, self.dc.n_dof
-        with torch.cuda.stream(stream()):
+        pin_t, pin_f = self._pinned()
+        s = stream()
+        s.synchronize()   # the previous run's copies out of the pinned buffers are done
+        if isinstance(thetas, (list, tuple)):
+            np.stack(thetas, out=pin_t.numpy(), casting="same_kind")
+            fz = pin_f.numpy()
+            if all(getattr(f, "dtype", None) == np.bool_ for f in frozen):
+                np.stack(frozen, out=fz.view(np.bool_))
+            else:
+                np.stack([np.asarray(f, np.uint8) for f in frozen], out=fz)
+        else:
+            pin_t.numpy()[...] = np.asarray(thetas, float)
+            pin_f.numpy()[...] = np.asarray(frozen, np.uint8)
+        with torch.cuda.stream(s):
             b.reset_status()
             _prep_clash_key(b)
-            b.t["theta"][:, :D].copy_(torch.as_tensor(np.asarray(thetas, float)))
-            b.t["frozen"][:, :D].copy_(torch.as_tensor(np.asarray(frozen, np.uint8)))
+            b.t["theta"][:, :D].copy_(pin_t, non_blocking=True)
+            b.t["frozen"][:, :D].copy_(pin_f, non_blocking=True)
 
     def load_device(self, theta_dev):
         """theta already on the device ([B, D] float64)."""
@@ -777,20 +826,22 @@ class EnsembleRunner:
     def result(self) -> EnsembleResult:
         b, D = self.batch, self.dc.n_dof
         with torch.cuda.stream(stream()):
-            sts = b.status()
-            for k, st in enumerate(sts):
-                if st.error:
-                    _raise_status(st, self.df, b, prefix=f"trajectory {k}: aborted at iteration "
-                                  f"{st.err_iter}: ", b=k)
-            iters = np.array([st.iter for st in sts])
+            sa = b.status_array()
+            bad = np.flatnonzero(sa["error"])
+            if len(bad):
+                k = int(bad[0])
+                st = b.status()[k]
+                _raise_status(st, self.df, b, prefix=f"trajectory {k}: aborted at iteration {st.err_iter}: ", b=k)
+            iters = sa["iter"].astype(np.int64)
             K = int(iters.max()) if len(iters) else 0
             rec = b.t["rec_energy"][:, :max(K, 1)].cpu().numpy()[:, :K]
             th = b.t["theta"][:, :D].cpu().numpy()
             thetas = (b.t["rec_theta"][:, :K].cpu().numpy()
                       if b.t["rec_theta"] is not None else None)
+        names = {code: N.REASONS.get(int(code), "max_iters") for code in np.unique(sa["reason"])}
         return EnsembleResult(theta=th, energies=rec, iterations=iters,
-                              reasons=[N.REASONS.get(int(st.reason), "max_iters") for st in sts],
-                              thetas=thetas, n_pairs=np.array([st.n_pairs for st in sts]))
+                              reasons=[names[r] for r in sa["reason"]],
+                              thetas=thetas, n_pairs=sa["n_pairs"].astype(np.int64))
 
 
 _runner_cache = _IdCache()
@@ -803,7 +854,7 @@ def fold_ensemble(chain, confs, fld, step, record_theta: bool = False) -> Ensemb
                                lambda: EnsembleRunner(chain, fld, len(confs), step, record_theta=record_theta))
     if runner.df.solvation and step.max_iters > 0:
         check_cav_cutoff(fld.params, fld.config.solvation_cfg, fld.config.cutoffs.cav)
-    runner.load(np.stack([c.theta for c in confs]), np.stack([c.frozen for c in confs]))
+    runner.load([c.theta for c in confs], [c.frozen for c in confs])
     runner.run()
     return runner.result()
 

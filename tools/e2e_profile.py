@@ -14,7 +14,7 @@ for rep in range(3):
     key = (len(confs), repr(step), False, id(fld))
     runner = DV._runner_cache.get(ch, hash(key), lambda: None)
     t1 = time.perf_counter()
-    runner.load(np.stack([c.theta for c in confs]), np.stack([c.frozen for c in confs]))
+    runner.load([c.theta for c in confs], [c.frozen for c in confs])
     torch.cuda.synchronize(); t2 = time.perf_counter()
     runner.run(); torch.cuda.synchronize(); t3 = time.perf_counter()
     res = runner.result(); t4 = time.perf_counter()
