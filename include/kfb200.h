@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define KF_ABI_VERSION 9
+#define KF_ABI_VERSION 10
 
 /* ---- static chain tables (uploaded once per chain) ------------------------
  * Links are in the reference's topological order (parent < index, ground = 0),
@@ -149,6 +149,8 @@ typedef struct {
     int32_t *occ_offset;            /* [B+1] prefix of occ_count (cells)           */
     int32_t *chunk_pre;             /* [B][H] per occupied cell (list order): prefix
                                        of its 32-atom i-chunks ceil(cnt/32)        */
+    int32_t *item_cell;             /* [B][H] per local work item: its cell's list
+                                       position (the pair kernels' item -> cell map) */
     int32_t *chunk_count;           /* [B] i-chunks of the trajectory              */
     int32_t *chunk_offset;          /* [B+1] prefix of chunk_count (pair work items) */
     int32_t *atom_slot;             /* [B][n] slot of the atom's cell              */

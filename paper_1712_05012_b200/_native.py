@@ -13,7 +13,7 @@ import os
 from .errors import NativeLibraryError
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libkfb200.so")
-ABI_VERSION = 9
+ABI_VERSION = 10
 
 P = C.c_void_p
 I32 = C.c_int32
@@ -57,7 +57,7 @@ class KfBatch(C.Structure):
                 ("max_records", I32), ("pair_chunk", I32)] + [
         (name, P) for name in (
             "theta", "frozen", "link_T", "fk_scratch", "pos", "forces", "cell_key", "cell_cnt", "cell_start",
-            "occ", "occ_count", "occ_offset", "chunk_pre", "chunk_count", "chunk_offset",
+            "occ", "occ_count", "occ_offset", "chunk_pre", "item_cell", "chunk_count", "chunk_offset",
             "atom_slot", "atom_rank", "sorted_atom", "s_hi", "s_lo",
             "s_pos", "s_par", "s_aux", "s_tree", "cell_box", "work", "e_atom", "pair_count",
             "solv_acc", "solv_ovf", "pair_fj", "cav_atom", "f_exp", "a_exp", "wrench", "side_tot", "bb_suffix", "tau", "energy", "status",

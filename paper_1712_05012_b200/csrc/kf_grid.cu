@@ -111,8 +111,8 @@ __device__ __forceinline__ int block_excl_scan(int v, int *wsum) {
 __global__ void __launch_bounds__(1024)
 cell_scan_kernel(int H, int chunk, const int32_t *__restrict__ occ, const int32_t *__restrict__ occ_count,
                  const int32_t *__restrict__ cnt, int32_t *__restrict__ start, int32_t *__restrict__ chunk_pre,
-                 int32_t *__restrict__ chunk_count, const kf_status_t *status, int32_t *__restrict__ occ_offset,
-                 int32_t *__restrict__ chunk_offset) {
+                 int32_t *__restrict__ item_cell, int32_t *__restrict__ chunk_count, const kf_status_t *status,
+                 int32_t *__restrict__ occ_offset, int32_t *__restrict__ chunk_offset) {
     // occ_offset / chunk_offset non-null (one trajectory): the work prefixes are
     // written here and occ_prefix_kernel is skipped
     const int b = blockIdx.x;
@@ -136,10 +136,13 @@ cell_scan_kernel(int H, int chunk, const int32_t *__restrict__ occ, const int32_
     __shared__ int wsum[32];
     int run = block_excl_scan(local, wsum);
     int crun = block_excl_scan(lchunk, wsum);
+    int32_t *ib = item_cell + (size_t)b * H;
     for (int k = lo; k < hi; ++k) {
-        const int c = cb[ob[k]];
+        const int c = cb[ob[k]], nc = (c + chunk - 1) / chunk;
         sb[ob[k]] = run; run += c;
-        pb[k] = crun; crun += (c + chunk - 1) / chunk;
+        pb[k] = crun;
+        for (int q = 0; q < nc; ++q) ib[crun + q] = k;
+        crun += nc;
     }
     if (threadIdx.x == blockDim.x - 1) {
         chunk_count[b] = crun;
@@ -336,7 +339,7 @@ __global__ void __launch_bounds__(BF_THREADS)
 bin_fused_kernel(const __grid_constant__ kf_field_t f, int B, int n, int chunk, const double *__restrict__ pos,
                  unsigned long long *__restrict__ keys, int32_t *__restrict__ cnt, int32_t *__restrict__ start,
                  int32_t *__restrict__ occ, int32_t *__restrict__ occ_count, int32_t *__restrict__ chunk_pre,
-                 int32_t *__restrict__ chunk_count, int32_t *__restrict__ occ_offset,
+                 int32_t *__restrict__ item_cell, int32_t *__restrict__ chunk_count, int32_t *__restrict__ occ_offset,
                  int32_t *__restrict__ chunk_offset, int32_t *__restrict__ atom_slot,
                  int32_t *__restrict__ atom_rank, int32_t *__restrict__ sorted_atom, float4 *__restrict__ s_hi,
                  float4 *__restrict__ s_lo, double4 *__restrict__ s_pos, float4 *__restrict__ s_par,
@@ -403,10 +406,13 @@ bin_fused_kernel(const __grid_constant__ kf_field_t f, int B, int n, int chunk, 
         }
         int run = block_excl_scan(local, wsum);
         int crun = block_excl_scan(lchunk, wsum);
+        int32_t *ti = item_cell + b * H;
         for (int k = lo; k < hi; ++k) {
-            const int c = tc[to[k]];
+            const int c = tc[to[k]], nc = (c + chunk - 1) / chunk;
             ts[to[k]] = run; run += c;
-            tp[k] = crun; crun += (c + chunk - 1) / chunk;
+            tp[k] = crun;
+            for (int q = 0; q < nc; ++q) ti[crun + q] = k;
+            crun += nc;
         }
         if (threadIdx.x == blockDim.x - 1) { occ_count[b] = m; chunk_count[b] = crun; }
         __syncthreads();
@@ -442,7 +448,7 @@ __global__ void __launch_bounds__(FL_THREADS)
 bin_flat_kernel(const __grid_constant__ kf_field_t f, int B, int n, int chunk, const double *__restrict__ pos,
                 unsigned long long *__restrict__ keys, int32_t *__restrict__ cnt, int32_t *__restrict__ start,
                 int32_t *__restrict__ occ, int32_t *__restrict__ occ_count, int32_t *__restrict__ chunk_pre,
-                int32_t *__restrict__ chunk_count, int32_t *__restrict__ occ_offset,
+                int32_t *__restrict__ item_cell, int32_t *__restrict__ chunk_count, int32_t *__restrict__ occ_offset,
                 int32_t *__restrict__ chunk_offset, int32_t *__restrict__ atom_slot,
                 int32_t *__restrict__ atom_rank, int32_t *__restrict__ sorted_atom, float4 *__restrict__ s_hi,
                 float4 *__restrict__ s_lo, double4 *__restrict__ s_pos, float4 *__restrict__ s_par,
@@ -499,6 +505,7 @@ bin_flat_kernel(const __grid_constant__ kf_field_t f, int B, int n, int chunk, c
         const int slot = slot_s;
         const double ctr[3] = {((double)cell_s[0] + 0.5) * f.cell, ((double)cell_s[1] + 0.5) * f.cell,
                                ((double)cell_s[2] + 0.5) * f.cell};
+        for (int q = threadIdx.x; q < (n + chunk - 1) / chunk; q += blockDim.x) item_cell[b * H + q] = 0;
         const bool tree = !f.uniform_weights;
         float bl[3] = {INFINITY, INFINITY, INFINITY}, bh[3] = {-INFINITY, -INFINITY, -INFINITY};
         int far = 0;
@@ -553,7 +560,7 @@ int kf_bin_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s) {
     if (f->flat) {   // FieldConfig(use_hash=False)
         bin_flat_kernel<<<B, FL_THREADS, 0, s>>>(
             *f, B, n, kf_pair_chunk(B, n, w->pair_chunk, f->precision), w->pos, w->cell_key, w->cell_cnt,
-            w->cell_start, w->occ, w->occ_count, w->chunk_pre, w->chunk_count, w->occ_offset, w->chunk_offset,
+            w->cell_start, w->occ, w->occ_count, w->chunk_pre, w->item_cell, w->chunk_count, w->occ_offset, w->chunk_offset,
             w->atom_slot, w->atom_rank, w->sorted_atom, reinterpret_cast<float4 *>(w->s_hi),
             reinterpret_cast<float4 *>(w->s_lo), reinterpret_cast<double4 *>(w->s_pos),
             reinterpret_cast<float4 *>(w->s_par), reinterpret_cast<int4 *>(w->s_aux),
@@ -564,7 +571,7 @@ int kf_bin_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s) {
     if (n <= BF_MAX_ATOMS && B >= 32) {   // ensembles: one CTA per trajectory does the whole binning
         bin_fused_kernel<<<B, BF_THREADS, 0, s>>>(
             *f, B, n, kf_pair_chunk(B, n, w->pair_chunk, f->precision), w->pos, w->cell_key, w->cell_cnt,
-            w->cell_start, w->occ, w->occ_count, w->chunk_pre, w->chunk_count, w->occ_offset, w->chunk_offset,
+            w->cell_start, w->occ, w->occ_count, w->chunk_pre, w->item_cell, w->chunk_count, w->occ_offset, w->chunk_offset,
             w->atom_slot, w->atom_rank, w->sorted_atom, reinterpret_cast<float4 *>(w->s_hi),
             reinterpret_cast<float4 *>(w->s_lo), reinterpret_cast<double4 *>(w->s_pos),
             reinterpret_cast<float4 *>(w->s_par), reinterpret_cast<int4 *>(w->s_aux),
@@ -581,7 +588,7 @@ int kf_bin_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s) {
                                                             w->occ_count, w->atom_slot, w->atom_rank, w->status);
     KF_LAUNCH_CHECK("bin_insert_kernel");
     cell_scan_kernel<<<B, 1024, 0, s>>>(H, kf_pair_chunk(B, n, w->pair_chunk, f->precision), w->occ, w->occ_count,
-                                         w->cell_cnt, w->cell_start, w->chunk_pre, w->chunk_count, w->status,
+                                         w->cell_cnt, w->cell_start, w->chunk_pre, w->item_cell, w->chunk_count, w->status,
                                          B == 1 ? w->occ_offset : nullptr, B == 1 ? w->chunk_offset : nullptr);
     KF_LAUNCH_CHECK("cell_scan_kernel");
     if (B > 1) {

@@ -218,6 +218,7 @@ __global__ void __launch_bounds__((SPLIT ? SPLIT_WARPS : PAIR_WARPS) * 32, SPLIT
 pair_kernel(const __grid_constant__ kf_field_t f, const __grid_constant__ PairConst pc, int B, int n, int chunk, const unsigned long long *__restrict__ keys,
             const int32_t *__restrict__ cnt, const int32_t *__restrict__ start, const int32_t *__restrict__ occ,
             const int32_t *__restrict__ occ_count, const int32_t *__restrict__ chunk_pre,
+            const int32_t *__restrict__ item_cell,
             const int32_t *__restrict__ chunk_offset, const float4 *__restrict__ s_hi,
             const float4 *__restrict__ s_lo, const double4 *__restrict__ s_pos, const float4 *__restrict__ s_par,
             const int4 *__restrict__ s_aux, const int4 *__restrict__ s_tree, const float4 *__restrict__ cell_box,
@@ -260,11 +261,7 @@ pair_kernel(const __grid_constant__ kf_field_t f, const __grid_constant__ PairCo
         const int b = item_owner(chunk_offset, B, item);
         const size_t hb = (size_t)b * H, nb = (size_t)b * n;
         const int local = item - chunk_offset[b];
-        int klo = 0, khi = occ_count[b] - 1;          // last k with chunk_pre[k] <= local
-        while (klo < khi) {
-            const int mid = (klo + khi + 1) >> 1;
-            if (chunk_pre[hb + mid] <= local) klo = mid; else khi = mid - 1;
-        }
+        const int klo = item_cell[hb + local];        // the item's cell (list position)
         const int slot = occ[hb + klo];
         const int ic = (local - chunk_pre[hb + klo]) * chunk;
         int cx, cy, cz;
@@ -483,6 +480,7 @@ pair_dense_kernel(const __grid_constant__ kf_field_t f, const __grid_constant__ 
                   const unsigned long long *__restrict__ keys, const int32_t *__restrict__ cnt,
                   const int32_t *__restrict__ start, const int32_t *__restrict__ occ,
                   const int32_t *__restrict__ occ_count, const int32_t *__restrict__ chunk_pre,
+            const int32_t *__restrict__ item_cell,
                   const int32_t *__restrict__ chunk_offset, const float4 *__restrict__ s_hi,
                   const float4 *__restrict__ s_lo, const double4 *__restrict__ s_pos,
                   const float4 *__restrict__ s_par, const int4 *__restrict__ s_aux, const int4 *__restrict__ s_tree,
@@ -525,11 +523,7 @@ pair_dense_kernel(const __grid_constant__ kf_field_t f, const __grid_constant__ 
         const int b = item_owner(chunk_offset, B, item);
         const size_t hb = (size_t)b * H, nb = (size_t)b * n;
         const int local = item - chunk_offset[b];
-        int klo = 0, khi = occ_count[b] - 1;          // last k with chunk_pre[k] <= local
-        while (klo < khi) {
-            const int mid = (klo + khi + 1) >> 1;
-            if (chunk_pre[hb + mid] <= local) klo = mid; else khi = mid - 1;
-        }
+        const int klo = item_cell[hb + local];        // the item's cell (list position)
         const int slot = occ[hb + klo];
         const int ic = (local - chunk_pre[hb + klo]) * chunk;
         int cx, cy, cz;
@@ -888,7 +882,7 @@ int kf_pairs_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s) {
     pc.dconst = f->dielectric_const; pc.uniform = f->uniform_weights;
     pc.te_is_cut = fabs(f->thr_elec2 - f->cut_pair2) < 1e-6 ? 1 : 0;
 #define KF_PAIR_ARGS                                                                                          \
-    *f, pc, w->B, n, chunk, w->cell_key, w->cell_cnt, w->cell_start, w->occ, w->occ_count, w->chunk_pre,       \
+    *f, pc, w->B, n, chunk, w->cell_key, w->cell_cnt, w->cell_start, w->occ, w->occ_count, w->chunk_pre, w->item_cell, \
         w->chunk_offset, reinterpret_cast<const float4 *>(w->s_hi), reinterpret_cast<const float4 *>(w->s_lo), \
         reinterpret_cast<const double4 *>(w->s_pos), reinterpret_cast<const float4 *>(w->s_par),              \
         reinterpret_cast<const int4 *>(w->s_aux), reinterpret_cast<const int4 *>(w->s_tree),                  \

@@ -464,7 +464,7 @@ class Batch:
                 pos=z(B, n, 3), forces=z(B, n, 3),
                 cell_key=z(B, H, dtype=torch.int64), cell_cnt=z(B, H, dtype=i32),
                 cell_start=z(B, H, dtype=i32), occ=z(B, H, dtype=i32), occ_count=z(B, dtype=i32),
-                occ_offset=z(B + 1, dtype=i32), chunk_pre=z(B, H, dtype=i32),
+                occ_offset=z(B + 1, dtype=i32), chunk_pre=z(B, H, dtype=i32), item_cell=z(B, H, dtype=i32),
                 chunk_count=z(B, dtype=i32), chunk_offset=z(B + 1, dtype=i32), atom_slot=z(B, n, dtype=i32), atom_rank=z(B, n, dtype=i32),
                 sorted_atom=z(B, n, dtype=i32), s_hi=z(B, n, 4, dtype=torch.float32),
                 s_lo=z(B, n, 4, dtype=torch.float32), s_pos=z(B, n, 4),
