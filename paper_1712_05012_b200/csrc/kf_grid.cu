@@ -328,14 +328,17 @@ KF_DEV void publish_prefixes(int B, const int32_t *occ_count, const int32_t *chu
 // block barriers in place of kernel boundaries and the table cleared by its own
 // CTA (no memsets).  The last CTA to finish (ticket in work[2]) builds the
 // work-item prefixes over trajectories from the published counts.
-constexpr int BF_THREADS = 512;
+constexpr int BF_THREADS = 512;    // many trajectories: 4 CTAs per SM
+constexpr int BF_THREADS_FEW = 1024;   // < 256 trajectories (about one CTA per SM): wider CTAs
+constexpr int BF_FEW_B = 256;
 #ifndef BF_MAX_ATOMS
 #define BF_MAX_ATOMS 8192   // per-trajectory atoms below which binning runs fused
 #endif
-constexpr int BF_WARPS = BF_THREADS / 32;
-constexpr int BF_CAP = 512;   // per-warp rank-sort buffer (larger cells: serial insertion sort)
+// per-warp rank-sort buffer (larger cells: serial insertion sort): 32 KB per CTA either way
+template <int NT> constexpr int bf_cap() { return NT >= 1024 ? 256 : 512; }
 
-__global__ void __launch_bounds__(BF_THREADS)
+template <int NT>
+__global__ void __launch_bounds__(NT)
 bin_fused_kernel(const __grid_constant__ kf_field_t f, int B, int n, int chunk, const double *__restrict__ pos,
                  unsigned long long *__restrict__ keys, int32_t *__restrict__ cnt, int32_t *__restrict__ start,
                  int32_t *__restrict__ occ, int32_t *__restrict__ occ_count, int32_t *__restrict__ chunk_pre,
@@ -347,7 +350,8 @@ bin_fused_kernel(const __grid_constant__ kf_field_t f, int B, int n, int chunk, 
                  int32_t *__restrict__ ticket, kf_status_t *status) {
     __shared__ int m_s;
     __shared__ int wsum[32];
-    __shared__ int buf[BF_WARPS][BF_CAP];
+    constexpr int NWB = NT / 32, CAP = bf_cap<NT>();
+    __shared__ int buf[NWB][CAP];
     const int b = blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const size_t H = (size_t)1 << f.hash_bits;
@@ -422,8 +426,8 @@ bin_fused_kernel(const __grid_constant__ kf_field_t f, int B, int n, int chunk, 
             sorted_atom[(size_t)b * n + ts[atom_slot[ga]] + atom_rank[ga]] = a;
         }
         __syncthreads();
-        for (int k = warp; k < m; k += BF_WARPS) {
-            finalize_cell(f, b, n, H, to[k], lane, buf[warp], BF_CAP, pos, keys, cnt, start, sorted_atom, s_hi, s_lo, s_pos,
+        for (int k = warp; k < m; k += NWB) {
+            finalize_cell(f, b, n, H, to[k], lane, buf[warp], CAP, pos, keys, cnt, start, sorted_atom, s_hi, s_lo, s_pos,
                           s_par, s_aux, s_tree, cell_box);
             __syncwarp();
         }
@@ -569,7 +573,8 @@ int kf_bin_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s) {
         return 0;
     }
     if (n <= BF_MAX_ATOMS && B >= 32) {   // ensembles: one CTA per trajectory does the whole binning
-        bin_fused_kernel<<<B, BF_THREADS, 0, s>>>(
+        auto kern = B < BF_FEW_B ? bin_fused_kernel<BF_THREADS_FEW> : bin_fused_kernel<BF_THREADS>;
+        kern<<<B, B < BF_FEW_B ? BF_THREADS_FEW : BF_THREADS, 0, s>>>(
             *f, B, n, kf_pair_chunk(B, n, w->pair_chunk, f->precision), w->pos, w->cell_key, w->cell_cnt,
             w->cell_start, w->occ, w->occ_count, w->chunk_pre, w->item_cell, w->chunk_count, w->occ_offset, w->chunk_offset,
             w->atom_slot, w->atom_rank, w->sorted_atom, reinterpret_cast<float4 *>(w->s_hi),
