@@ -470,9 +470,13 @@ int kf_torque_launch(const kf_chain_t *c, const kf_field_t *f, kf_batch_t *w, co
     if (fuse_wrench && !fuse) {
         if (kf_wrench_launch(c, w->B, w->pos, w->forces, const_cast<double *>(wrench), w->status, s)) return 1;
     }
-    // one CTA per trajectory: 512 threads for a lone chain (its latency is the
-    // iteration's), 256 for ensembles (more trajectories per SM)
-    const bool wide = w->B < 64;
+    // one CTA per trajectory: 512 threads while the batch leaves SMs to spare (its
+    // latency is the iteration's; measured B=128: 20.5 vs 24.6 us), 256 for large
+    // ensembles (more trajectories per SM; B=1024: 101 vs 117 us)
+#ifndef TQ_WIDE_B
+#define TQ_WIDE_B 384
+#endif
+    const bool wide = w->B < TQ_WIDE_B;
     auto kern = wide ? torque_step_kernel<TQ_THREADS> : torque_step_kernel<TQ_THREADS / 2>;
     if (fuse) {
         static size_t opted[2] = {0, 0};
