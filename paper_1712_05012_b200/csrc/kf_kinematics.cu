@@ -117,6 +117,9 @@ fk_scan_kernel(kf_chain_t c, const double *__restrict__ theta_all, double *__res
 // the joint axes) and of the atom positions, which this kernel also computes:
 // one global write per link and per atom instead of several read-modify-writes.
 constexpr int FKS_THREADS = 128;
+#ifndef FK_SHFL_SCAN
+#define FK_SHFL_SCAN 1   // chunk-total scan by warp shuffles (12 KB less shared memory per CTA)
+#endif
 constexpr int FKS_STRIDE = 12;
 
 __global__ void __launch_bounds__(FKS_THREADS)
@@ -125,7 +128,7 @@ fk_smem_kernel(const __grid_constant__ kf_chain_t c, const double *__restrict__ 
     const int b = blockIdx.x;
     if (status && status[b].done) return;
     extern __shared__ __align__(16) double S[];     // [L][12], then the int tables below
-    __shared__ double chunk[FKS_THREADS][12];
+    __shared__ double chunk[FK_SHFL_SCAN ? FKS_THREADS / 32 : FKS_THREADS][12];
     const int L = c.n_links, D = c.n_dof, n = c.n_atoms, nb = c.n_bb, ns = c.n_side;
     const double *theta = theta_all + (size_t)b * D;
     // the chain tables the serial phases walk, staged once (one global round trip
@@ -173,6 +176,32 @@ fk_smem_kernel(const __grid_constant__ kf_chain_t c, const double *__restrict__ 
         acc = xf_compose(acc, xf_load(slot));
         xf_store(slot, acc);
     }
+#if FK_SHFL_SCAN
+    // scan of the chunk totals: warp-level Hillis-Steele on registers (shuffles),
+    // then the warp totals composed in warp order (no per-step block barriers)
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    Xf incl = acc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        Xf up;
+#pragma unroll
+        for (int q = 0; q < 9; ++q) up.m[q] = __shfl_up_sync(0xffffffffu, incl.m[q], o);
+#pragma unroll
+        for (int q = 0; q < 3; ++q) up.p[q] = __shfl_up_sync(0xffffffffu, incl.p[q], o);
+        if (lane >= o) incl = xf_compose(up, incl);
+    }
+    if (lane == 31) xf_store(chunk[wid], incl);
+    __syncthreads();
+    Xf wpre = xf_identity();
+    for (int w2 = 0; w2 < wid; ++w2) wpre = xf_compose(wpre, xf_load(chunk[w2]));
+    Xf pre;   // exclusive prefix of this thread's chunk
+#pragma unroll
+    for (int q = 0; q < 9; ++q) pre.m[q] = __shfl_up_sync(0xffffffffu, incl.m[q], 1);
+#pragma unroll
+    for (int q = 0; q < 3; ++q) pre.p[q] = __shfl_up_sync(0xffffffffu, incl.p[q], 1);
+    if (lane == 0) pre = wpre;
+    else if (wid > 0) pre = xf_compose(wpre, pre);
+#else
     xf_store(chunk[threadIdx.x], acc);
     __syncthreads();
     for (int off = 1; off < (int)blockDim.x; off <<= 1) {
@@ -183,8 +212,10 @@ fk_smem_kernel(const __grid_constant__ kf_chain_t c, const double *__restrict__ 
         xf_store(chunk[threadIdx.x], r);
         __syncthreads();
     }
+    Xf pre = xf_identity();
+    if (threadIdx.x > 0) pre = xf_load(chunk[threadIdx.x - 1]);
+#endif
     if (threadIdx.x > 0 && lo < hi) {
-        const Xf pre = xf_load(chunk[threadIdx.x - 1]);
         for (int k = lo; k < hi; ++k) {
             double *slot = S + FKS_STRIDE * sh_bb[k];
             xf_store(slot, xf_compose(pre, xf_load(slot)));
