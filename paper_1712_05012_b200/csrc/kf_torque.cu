@@ -15,6 +15,9 @@
 
 namespace {
 
+#ifndef TQ_SHFL_SCAN
+#define TQ_SHFL_SCAN 1   // backbone suffix scan of chunk totals by warp shuffles
+#endif
 constexpr int TQ_THREADS = 512;
 
 struct W6 { double f[3], t[3]; };
@@ -145,7 +148,7 @@ torque_step_kernel(kf_chain_t c, kf_field_t f, TorqueArgs ta, kf_batch_t w, kf_s
     kf_status_t *st = w.status ? w.status + b : nullptr;
     if (st && st->done) return;
     __shared__ double red[32];
-    __shared__ double chunk[NT][6];
+    __shared__ double chunk[TQ_SHFL_SCAN ? NT / 32 : NT][6];
     __shared__ int stop_reason;
     if (st && st->error) {   // domain error this iteration: freeze, no record, no step
         if (threadIdx.x == 0) st->done = 1;
@@ -189,6 +192,37 @@ torque_step_kernel(kf_chain_t c, kf_field_t f, TorqueArgs ta, kf_batch_t w, kf_s
         if (r >= 0) w6_add(acc, w6_load(side + 6 * r));
         w6_store(suf + 6 * k, acc);
     }
+#if TQ_SHFL_SCAN
+    // suffix scan of the chunk totals: warp-level (shuffles, right to left), then
+    // the later warps' totals added in a fixed order (no per-step block barriers)
+    W6 later;
+    {
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+        double v[6] = {acc.f[0], acc.f[1], acc.f[2], acc.t[0], acc.t[1], acc.t[2]};
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            double u[6];
+#pragma unroll
+            for (int q = 0; q < 6; ++q) u[q] = __shfl_down_sync(0xffffffffu, v[q], o);
+            if (lane + o < 32)
+#pragma unroll
+                for (int q = 0; q < 6; ++q) v[q] += u[q];
+        }
+        if (lane == 0)
+            for (int q = 0; q < 6; ++q) chunk[wid][q] = v[q];
+        __syncthreads();
+        double tail[6] = {0, 0, 0, 0, 0, 0};   // totals of the later warps, last first
+        for (int w2 = nw - 1; w2 > wid; --w2)
+            for (int q = 0; q < 6; ++q) tail[q] += chunk[w2][q];
+        double ex[6];
+#pragma unroll
+        for (int q = 0; q < 6; ++q) {
+            const double nx = __shfl_down_sync(0xffffffffu, v[q], 1);
+            ex[q] = lane < 31 ? nx + tail[q] : tail[q];
+        }
+        for (int q = 0; q < 3; ++q) { later.f[q] = ex[q]; later.t[q] = ex[3 + q]; }
+    }
+#else
     for (int q = 0; q < 3; ++q) { chunk[threadIdx.x][q] = acc.f[q]; chunk[threadIdx.x][3 + q] = acc.t[q]; }
     __syncthreads();
     // inclusive suffix scan of chunk totals (Hillis-Steele, right to left)
@@ -203,6 +237,7 @@ torque_step_kernel(kf_chain_t c, kf_field_t f, TorqueArgs ta, kf_batch_t w, kf_s
     }
     W6 later = w6_zero();
     if (threadIdx.x + 1 < blockDim.x) later = w6_load(chunk[threadIdx.x + 1]);
+#endif
     for (int k = lo; k < hi; ++k) {
         const int l = c.bb_by_dof[k];
         W6 s = w6_load(suf + 6 * k);
