@@ -251,11 +251,9 @@ torque_step_kernel(kf_chain_t c, kf_field_t f, TorqueArgs ta, kf_batch_t w, kf_s
     // 3. tau_max over free joints (kcm.py:325-326)
     const uint8_t *frozen = w.frozen + (size_t)b * D;
     double tmax = 0.0;
-    if (mode == 1) {
+    if (mode == 1)
         for (int d = threadIdx.x; d < D; d += blockDim.x)
             if (!frozen[d]) tmax = fmax(tmax, fabs(tau[d]));
-        tmax = block_max(tmax, red);
-    }
 
     // 4. energies: full-list halves summed in a fixed order
     const int n = c.n_atoms;
@@ -268,11 +266,22 @@ torque_step_kernel(kf_chain_t c, kf_field_t f, TorqueArgs ta, kf_batch_t w, kf_s
         sp += (double)(pc & 0xffffffffLL);
         sp5 += (double)(pc >> 32);
     }
-    se = block_sum(se, red);
-    sv = block_sum(sv, red);
-    sc = f.solvation ? block_sum(sc, red) : 0.0;
-    sp = block_sum(sp, red);
-    sp5 = block_sum(sp5, red);
+    // one block reduction for all six (warp trees, then the warps in order: 2 barriers)
+    {
+        __shared__ double red6[32][6];
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+        double v[6] = {warp_max(tmax), warp_sum(se), warp_sum(sv), warp_sum(sc), warp_sum(sp), warp_sum(sp5)};
+        __syncthreads();
+        if (lane == 0)
+            for (int q = 0; q < 6; ++q) red6[wid][q] = v[q];
+        __syncthreads();
+        for (int q = 0; q < 6; ++q) v[q] = red6[0][q];
+        for (int w2 = 1; w2 < nw; ++w2) {
+            v[0] = fmax(v[0], red6[w2][0]);
+            for (int q = 1; q < 6; ++q) v[q] += red6[w2][q];
+        }
+        tmax = v[0]; se = v[1]; sv = v[2]; sc = v[3]; sp = v[4]; sp5 = v[5];
+    }
     const double ge = 0.5 * se, gv = 0.5 * sv, gc = sc;
     if (mode == 2) {   // Field.evaluate: energies only
         if (threadIdx.x == 0) {
