@@ -12,6 +12,9 @@
 
 namespace {
 
+#ifndef FK_SHFL_SCAN
+#define FK_SHFL_SCAN 1   // chunk-total scan by warp shuffles (12 KB less shared memory per CTA)
+#endif
 constexpr int FK_THREADS = 256;
 
 // Rodrigues R = I + sin(t) K + (1 - cos(t)) K^2 (geometry.py:26-41), t in radians
@@ -31,6 +34,39 @@ KF_DEV Xf local_transform(const double *axis, double theta_deg, const double *bo
     t.m[6] = -s * y + omc * k02; t.m[7] = s * x + omc * k12; t.m[8] = 1.0 + omc * k22;
     t.p[0] = body_parent[0]; t.p[1] = body_parent[1]; t.p[2] = body_parent[2];
     return t;
+}
+
+// Block-wide scan of the threads' transforms in thread order (composition is
+// associative, not commutative): warp-level Hillis-Steele on registers by
+// shuffles, then the warp totals (wtot, one row per warp) composed in warp
+// order.  Returns the thread's exclusive prefix (identity for thread 0) and,
+// in incl, its inclusive one.  Two block barriers instead of two per step.
+KF_DEV Xf xf_block_scan(const Xf &acc, double (*wtot)[12], Xf &incl) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    incl = acc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        Xf up;
+#pragma unroll
+        for (int q = 0; q < 9; ++q) up.m[q] = __shfl_up_sync(0xffffffffu, incl.m[q], o);
+#pragma unroll
+        for (int q = 0; q < 3; ++q) up.p[q] = __shfl_up_sync(0xffffffffu, incl.p[q], o);
+        if (lane >= o) incl = xf_compose(up, incl);
+    }
+    __syncthreads();
+    if (lane == 31) xf_store(wtot[wid], incl);
+    __syncthreads();
+    Xf wpre = xf_identity();
+    for (int w2 = 0; w2 < wid; ++w2) wpre = xf_compose(wpre, xf_load(wtot[w2]));
+    Xf pre;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) pre.m[q] = __shfl_up_sync(0xffffffffu, incl.m[q], 1);
+#pragma unroll
+    for (int q = 0; q < 3; ++q) pre.p[q] = __shfl_up_sync(0xffffffffu, incl.p[q], 1);
+    if (wid > 0) incl = xf_compose(wpre, incl);
+    if (lane == 0) pre = wpre;
+    else if (wid > 0) pre = xf_compose(wpre, pre);
+    return pre;
 }
 
 // One CTA per trajectory: local transforms, blocked backbone scan, side levels.
@@ -117,9 +153,6 @@ fk_scan_kernel(kf_chain_t c, const double *__restrict__ theta_all, double *__res
 // the joint axes) and of the atom positions, which this kernel also computes:
 // one global write per link and per atom instead of several read-modify-writes.
 constexpr int FKS_THREADS = 128;
-#ifndef FK_SHFL_SCAN
-#define FK_SHFL_SCAN 1   // chunk-total scan by warp shuffles (12 KB less shared memory per CTA)
-#endif
 constexpr int FKS_STRIDE = 12;
 
 __global__ void __launch_bounds__(FKS_THREADS)
@@ -177,30 +210,8 @@ fk_smem_kernel(const __grid_constant__ kf_chain_t c, const double *__restrict__ 
         xf_store(slot, acc);
     }
 #if FK_SHFL_SCAN
-    // scan of the chunk totals: warp-level Hillis-Steele on registers (shuffles),
-    // then the warp totals composed in warp order (no per-step block barriers)
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    Xf incl = acc;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        Xf up;
-#pragma unroll
-        for (int q = 0; q < 9; ++q) up.m[q] = __shfl_up_sync(0xffffffffu, incl.m[q], o);
-#pragma unroll
-        for (int q = 0; q < 3; ++q) up.p[q] = __shfl_up_sync(0xffffffffu, incl.p[q], o);
-        if (lane >= o) incl = xf_compose(up, incl);
-    }
-    if (lane == 31) xf_store(chunk[wid], incl);
-    __syncthreads();
-    Xf wpre = xf_identity();
-    for (int w2 = 0; w2 < wid; ++w2) wpre = xf_compose(wpre, xf_load(chunk[w2]));
-    Xf pre;   // exclusive prefix of this thread's chunk
-#pragma unroll
-    for (int q = 0; q < 9; ++q) pre.m[q] = __shfl_up_sync(0xffffffffu, incl.m[q], 1);
-#pragma unroll
-    for (int q = 0; q < 3; ++q) pre.p[q] = __shfl_up_sync(0xffffffffu, incl.p[q], 1);
-    if (lane == 0) pre = wpre;
-    else if (wid > 0) pre = xf_compose(wpre, pre);
+    Xf incl;
+    const Xf pre = xf_block_scan(acc, chunk, incl);
 #else
     xf_store(chunk[threadIdx.x], acc);
     __syncthreads();
@@ -296,7 +307,7 @@ fk_seg_scan_kernel(kf_chain_t c, const double *__restrict__ theta_all, double *_
     const int L = c.n_links, D = c.n_dof, nb = c.n_bb;
     const double *theta = theta_all + (size_t)b * D;
     double *T = T_all + (size_t)b * L * KF_XF_STRIDE;
-    __shared__ double chunk[FK_THREADS][12];
+    __shared__ double chunk[FK_SHFL_SCAN ? FK_THREADS / 32 : FK_THREADS][12];
     const int lo = min(nb, g * SEG + (int)threadIdx.x * SEG_PER), hi = min(nb, lo + SEG_PER);
     Xf acc = xf_identity();
     for (int k = lo; k < hi; ++k) {
@@ -306,6 +317,17 @@ fk_seg_scan_kernel(kf_chain_t c, const double *__restrict__ theta_all, double *_
         acc = xf_compose(acc, loc);
         xf_store(T + KF_XF_STRIDE * l, acc);
     }
+#if FK_SHFL_SCAN
+    Xf incl;
+    const Xf pre = xf_block_scan(acc, chunk, incl);
+    if (threadIdx.x > 0 && lo < hi) {
+        for (int k = lo; k < hi; ++k) {
+            double *slot = T + KF_XF_STRIDE * c.bb_order[k];
+            xf_store(slot, xf_compose(pre, xf_load(slot)));
+        }
+    }
+    if (threadIdx.x == blockDim.x - 1) xf_store(seg_tot + ((size_t)b * n_seg + g) * 12, incl);
+#else
     xf_store(chunk[threadIdx.x], acc);
     __syncthreads();
     for (int off = 1; off < (int)blockDim.x; off <<= 1) {
@@ -324,6 +346,7 @@ fk_seg_scan_kernel(kf_chain_t c, const double *__restrict__ theta_all, double *_
         }
     }
     if (threadIdx.x == blockDim.x - 1) xf_store(seg_tot + ((size_t)b * n_seg + g) * 12, xf_load(chunk[threadIdx.x]));
+#endif
 }
 
 // exclusive prefix of the segment totals, in place (one thread per trajectory: few segments)
