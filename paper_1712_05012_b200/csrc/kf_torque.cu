@@ -130,6 +130,46 @@ KF_DEV void finish_iteration(const kf_chain_t &c, const kf_batch_t &w, const kf_
     if (threadIdx.x == 0) close_iteration(st, step, it, reason);
 }
 
+// Block-wide suffix scan of the threads' 6-vectors (later threads first):
+// warp-level by shuffles, then the later warps' totals (wtot, one row per
+// warp) added in a fixed order.  Returns the thread's exclusive suffix (the sum
+// over later threads) and, in total, the block's sum.  Two block barriers.
+KF_DEV W6 w6_block_suffix(const W6 &acc, double (*wtot)[6], W6 &total) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    double v[6] = {acc.f[0], acc.f[1], acc.f[2], acc.t[0], acc.t[1], acc.t[2]};
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        double u[6];
+#pragma unroll
+        for (int q = 0; q < 6; ++q) u[q] = __shfl_down_sync(0xffffffffu, v[q], o);
+        if (lane + o < 32)
+#pragma unroll
+            for (int q = 0; q < 6; ++q) v[q] += u[q];
+    }
+    __syncthreads();
+    if (lane == 0)
+        for (int q = 0; q < 6; ++q) wtot[wid][q] = v[q];
+    __syncthreads();
+    double tail[6] = {0, 0, 0, 0, 0, 0};   // totals of the later warps, last first
+    for (int w2 = nw - 1; w2 > wid; --w2)
+        for (int q = 0; q < 6; ++q) tail[q] += wtot[w2][q];
+    double ex[6];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+        const double nx = __shfl_down_sync(0xffffffffu, v[q], 1);
+        ex[q] = lane < 31 ? nx + tail[q] : tail[q];
+    }
+    double all[6] = {0, 0, 0, 0, 0, 0};
+    for (int w2 = nw - 1; w2 >= 0; --w2)
+        for (int q = 0; q < 6; ++q) all[q] += wtot[w2][q];
+    W6 later;
+    for (int q = 0; q < 3; ++q) {
+        later.f[q] = ex[q]; later.t[q] = ex[3 + q];
+        total.f[q] = all[q]; total.t[q] = all[3 + q];
+    }
+    return later;
+}
+
 struct TorqueArgs {
     const double *link_T;      // [B][L][KF_XF_STRIDE]
     const double *wrench;      // [B][L][6]
@@ -193,35 +233,8 @@ torque_step_kernel(kf_chain_t c, kf_field_t f, TorqueArgs ta, kf_batch_t w, kf_s
         w6_store(suf + 6 * k, acc);
     }
 #if TQ_SHFL_SCAN
-    // suffix scan of the chunk totals: warp-level (shuffles, right to left), then
-    // the later warps' totals added in a fixed order (no per-step block barriers)
-    W6 later;
-    {
-        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-        double v[6] = {acc.f[0], acc.f[1], acc.f[2], acc.t[0], acc.t[1], acc.t[2]};
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            double u[6];
-#pragma unroll
-            for (int q = 0; q < 6; ++q) u[q] = __shfl_down_sync(0xffffffffu, v[q], o);
-            if (lane + o < 32)
-#pragma unroll
-                for (int q = 0; q < 6; ++q) v[q] += u[q];
-        }
-        if (lane == 0)
-            for (int q = 0; q < 6; ++q) chunk[wid][q] = v[q];
-        __syncthreads();
-        double tail[6] = {0, 0, 0, 0, 0, 0};   // totals of the later warps, last first
-        for (int w2 = nw - 1; w2 > wid; --w2)
-            for (int q = 0; q < 6; ++q) tail[q] += chunk[w2][q];
-        double ex[6];
-#pragma unroll
-        for (int q = 0; q < 6; ++q) {
-            const double nx = __shfl_down_sync(0xffffffffu, v[q], 1);
-            ex[q] = lane < 31 ? nx + tail[q] : tail[q];
-        }
-        for (int q = 0; q < 3; ++q) { later.f[q] = ex[q]; later.t[q] = ex[3 + q]; }
-    }
+    W6 total_unused;
+    const W6 later = w6_block_suffix(acc, chunk, total_unused);
 #else
     for (int q = 0; q < 3; ++q) { chunk[threadIdx.x][q] = acc.f[q]; chunk[threadIdx.x][3 + q] = acc.t[q]; }
     __syncthreads();
@@ -314,7 +327,7 @@ torque_seg_kernel(kf_chain_t c, TorqueArgs ta, kf_batch_t w, int n_seg) {
     const int g = blockIdx.x, b = blockIdx.y;
     const kf_status_t *st = w.status + b;
     if (st->done || st->error) return;
-    __shared__ double chunk[TQ_THREADS][6];
+    __shared__ double chunk[TQ_SHFL_SCAN ? TQ_THREADS / 32 : TQ_THREADS][6];
     __shared__ double red[32];
     const int L = c.n_links, D = c.n_dof, nb = c.n_bb;
     const double *T = ta.link_T + (size_t)b * L * KF_XF_STRIDE;
@@ -344,6 +357,23 @@ torque_seg_kernel(kf_chain_t c, TorqueArgs ta, kf_batch_t w, int n_seg) {
         }
         w6_store(suf + 6 * k, acc);
     }
+#if TQ_SHFL_SCAN
+    W6 seg_total;
+    const W6 later = w6_block_suffix(acc, chunk, seg_total);
+    if (threadIdx.x + 1 < blockDim.x) {
+        for (int k = lo; k < hi; ++k) {
+            W6 s6 = w6_load(suf + 6 * k);
+            w6_add(s6, later);
+            w6_store(suf + 6 * k, s6);
+        }
+    }
+    tmax = block_max(tmax, red);
+    double *sc = w.fk_scratch + ((size_t)b * n_seg + g) * 12;
+    if (threadIdx.x == 0) {
+        w6_store(sc, seg_total);
+        sc[6] = tmax;
+    }
+#else
     for (int q = 0; q < 3; ++q) { chunk[threadIdx.x][q] = acc.f[q]; chunk[threadIdx.x][3 + q] = acc.t[q]; }
     __syncthreads();
     for (int off = 1; off < (int)blockDim.x; off <<= 1) {
@@ -369,6 +399,7 @@ torque_seg_kernel(kf_chain_t c, TorqueArgs ta, kf_batch_t w, int n_seg) {
         w6_store(sc, w6_load(chunk[0]));
         sc[6] = tmax;
     }
+#endif
 }
 
 __global__ void __launch_bounds__(TQ_THREADS)
