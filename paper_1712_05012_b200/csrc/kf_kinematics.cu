@@ -12,9 +12,6 @@
 
 namespace {
 
-#ifndef FK_SHFL_SCAN
-#define FK_SHFL_SCAN 1   // chunk-total scan by warp shuffles (12 KB less shared memory per CTA)
-#endif
 constexpr int FK_THREADS = 256;
 
 // Rodrigues R = I + sin(t) K + (1 - cos(t)) K^2 (geometry.py:26-41), t in radians
@@ -78,7 +75,7 @@ fk_scan_kernel(kf_chain_t c, const double *__restrict__ theta_all, double *__res
     const int L = c.n_links, D = c.n_dof;
     const double *theta = theta_all + (size_t)b * D;
     double *T = T_all + (size_t)b * L * KF_XF_STRIDE;
-    __shared__ double chunk[FK_THREADS][12];
+    __shared__ double chunk[FK_THREADS / 32][12];   // warp totals of the block scan
 
     // 1. local transforms (ground = identity)
     for (int l = threadIdx.x; l < L; l += blockDim.x) {
@@ -103,22 +100,9 @@ fk_scan_kernel(kf_chain_t c, const double *__restrict__ theta_all, double *__res
         acc = xf_compose(acc, xf_load(slot));
         xf_store(slot, acc);
     }
-    {
-        double *s = chunk[threadIdx.x];
-        for (int k = 0; k < 9; ++k) s[k] = acc.m[k];
-        for (int k = 0; k < 3; ++k) s[9 + k] = acc.p[k];
-    }
-    __syncthreads();
-    for (int off = 1; off < (int)blockDim.x; off <<= 1) {
-        Xf mine = xf_load(chunk[threadIdx.x]);
-        Xf r = mine;
-        if ((int)threadIdx.x >= off) r = xf_compose(xf_load(chunk[threadIdx.x - off]), mine);
-        __syncthreads();
-        xf_store(chunk[threadIdx.x], r);
-        __syncthreads();
-    }
+    Xf incl;
+    const Xf pre = xf_block_scan(acc, chunk, incl);
     if (threadIdx.x > 0 && lo < hi) {
-        const Xf pre = xf_load(chunk[threadIdx.x - 1]);
         for (int k = lo; k < hi; ++k) {
             double *slot = T + KF_XF_STRIDE * c.bb_order[k];
             xf_store(slot, xf_compose(pre, xf_load(slot)));
@@ -161,7 +145,7 @@ fk_smem_kernel(const __grid_constant__ kf_chain_t c, const double *__restrict__ 
     const int b = blockIdx.x;
     if (status && status[b].done) return;
     extern __shared__ __align__(16) double S[];     // [L][12], then the int tables below
-    __shared__ double chunk[FK_SHFL_SCAN ? FKS_THREADS / 32 : FKS_THREADS][12];
+    __shared__ double chunk[FKS_THREADS / 32][12];   // warp totals of the block scan
     const int L = c.n_links, D = c.n_dof, n = c.n_atoms, nb = c.n_bb, ns = c.n_side;
     const double *theta = theta_all + (size_t)b * D;
     // the chain tables the serial phases walk, staged once (one global round trip
@@ -209,23 +193,8 @@ fk_smem_kernel(const __grid_constant__ kf_chain_t c, const double *__restrict__ 
         acc = xf_compose(acc, xf_load(slot));
         xf_store(slot, acc);
     }
-#if FK_SHFL_SCAN
     Xf incl;
     const Xf pre = xf_block_scan(acc, chunk, incl);
-#else
-    xf_store(chunk[threadIdx.x], acc);
-    __syncthreads();
-    for (int off = 1; off < (int)blockDim.x; off <<= 1) {
-        Xf mine = xf_load(chunk[threadIdx.x]);
-        Xf r = mine;
-        if ((int)threadIdx.x >= off) r = xf_compose(xf_load(chunk[threadIdx.x - off]), mine);
-        __syncthreads();
-        xf_store(chunk[threadIdx.x], r);
-        __syncthreads();
-    }
-    Xf pre = xf_identity();
-    if (threadIdx.x > 0) pre = xf_load(chunk[threadIdx.x - 1]);
-#endif
     if (threadIdx.x > 0 && lo < hi) {
         for (int k = lo; k < hi; ++k) {
             double *slot = S + FKS_STRIDE * sh_bb[k];
@@ -307,7 +276,7 @@ fk_seg_scan_kernel(kf_chain_t c, const double *__restrict__ theta_all, double *_
     const int L = c.n_links, D = c.n_dof, nb = c.n_bb;
     const double *theta = theta_all + (size_t)b * D;
     double *T = T_all + (size_t)b * L * KF_XF_STRIDE;
-    __shared__ double chunk[FK_SHFL_SCAN ? FK_THREADS / 32 : FK_THREADS][12];
+    __shared__ double chunk[FK_THREADS / 32][12];   // warp totals of the block scan
     const int lo = min(nb, g * SEG + (int)threadIdx.x * SEG_PER), hi = min(nb, lo + SEG_PER);
     Xf acc = xf_identity();
     for (int k = lo; k < hi; ++k) {
@@ -317,7 +286,6 @@ fk_seg_scan_kernel(kf_chain_t c, const double *__restrict__ theta_all, double *_
         acc = xf_compose(acc, loc);
         xf_store(T + KF_XF_STRIDE * l, acc);
     }
-#if FK_SHFL_SCAN
     Xf incl;
     const Xf pre = xf_block_scan(acc, chunk, incl);
     if (threadIdx.x > 0 && lo < hi) {
@@ -327,26 +295,6 @@ fk_seg_scan_kernel(kf_chain_t c, const double *__restrict__ theta_all, double *_
         }
     }
     if (threadIdx.x == blockDim.x - 1) xf_store(seg_tot + ((size_t)b * n_seg + g) * 12, incl);
-#else
-    xf_store(chunk[threadIdx.x], acc);
-    __syncthreads();
-    for (int off = 1; off < (int)blockDim.x; off <<= 1) {
-        Xf mine = xf_load(chunk[threadIdx.x]);
-        Xf r = mine;
-        if ((int)threadIdx.x >= off) r = xf_compose(xf_load(chunk[threadIdx.x - off]), mine);
-        __syncthreads();
-        xf_store(chunk[threadIdx.x], r);
-        __syncthreads();
-    }
-    if (threadIdx.x > 0 && lo < hi) {
-        const Xf pre = xf_load(chunk[threadIdx.x - 1]);
-        for (int k = lo; k < hi; ++k) {
-            double *slot = T + KF_XF_STRIDE * c.bb_order[k];
-            xf_store(slot, xf_compose(pre, xf_load(slot)));
-        }
-    }
-    if (threadIdx.x == blockDim.x - 1) xf_store(seg_tot + ((size_t)b * n_seg + g) * 12, xf_load(chunk[threadIdx.x]));
-#endif
 }
 
 // exclusive prefix of the segment totals, in place (one thread per trajectory: few segments)

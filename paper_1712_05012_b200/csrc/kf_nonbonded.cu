@@ -64,9 +64,6 @@ struct WarpSmem {
     unsigned short list[1024]; // candidate (owner << 5 | t) pairs of the tile, owner-major
 };
 
-#ifndef EXACT_BITWISE
-#define EXACT_BITWISE 1   // exact-band membership test without short-circuit branches
-#endif
 
 // fp32 constants of the fast path, passed by value (kernel parameter space:
 // constant-bank operands, no registers).
@@ -160,14 +157,9 @@ KF_DEV void pair_eval(const kf_field_t &f, const PairConst &pc, float4 hi, float
     const float we = pc.we[cls - 1], wv = pc.wv[cls - 1];   // constant-bank loads, indexed
     // exact recomputation near a threshold: |d2 - t| <= band for t in {cut, te, tv}
     // (te == cut to ~1e-14 for the default cut-offs: pc.te_is_cut folds the test)
-#if EXACT_BITWISE
     // non-short-circuit: predicated compares instead of a branch per threshold
     const bool exact = F64 || ((fabsf(d2f - cut2f) <= band) | (fabsf(d2f - tvf) <= band) |
                                (!pc.te_is_cut & (fabsf(d2f - tef) <= band)) | (d2f < pc.f64_d2));
-#else
-    const bool exact = F64 || fabsf(d2f - cut2f) <= band || fabsf(d2f - tvf) <= band ||
-                       (!pc.te_is_cut && fabsf(d2f - tef) <= band) || d2f < pc.f64_d2;
-#endif
     if (exact) {
         // the outlined path writes through pointers: give it its own stack
         // temporaries so out / pce / pcv stay in registers on the fast path

@@ -15,9 +15,6 @@
 
 namespace {
 
-#ifndef TQ_SHFL_SCAN
-#define TQ_SHFL_SCAN 1   // backbone suffix scan of chunk totals by warp shuffles
-#endif
 constexpr int TQ_THREADS = 512;
 
 struct W6 { double f[3], t[3]; };
@@ -188,7 +185,7 @@ torque_step_kernel(kf_chain_t c, kf_field_t f, TorqueArgs ta, kf_batch_t w, kf_s
     kf_status_t *st = w.status ? w.status + b : nullptr;
     if (st && st->done) return;
     __shared__ double red[32];
-    __shared__ double chunk[TQ_SHFL_SCAN ? NT / 32 : NT][6];
+    __shared__ double chunk[NT / 32][6];   // warp totals of the suffix scan
     __shared__ int stop_reason;
     if (st && st->error) {   // domain error this iteration: freeze, no record, no step
         if (threadIdx.x == 0) st->done = 1;
@@ -232,25 +229,8 @@ torque_step_kernel(kf_chain_t c, kf_field_t f, TorqueArgs ta, kf_batch_t w, kf_s
         if (r >= 0) w6_add(acc, w6_load(side + 6 * r));
         w6_store(suf + 6 * k, acc);
     }
-#if TQ_SHFL_SCAN
     W6 total_unused;
     const W6 later = w6_block_suffix(acc, chunk, total_unused);
-#else
-    for (int q = 0; q < 3; ++q) { chunk[threadIdx.x][q] = acc.f[q]; chunk[threadIdx.x][3 + q] = acc.t[q]; }
-    __syncthreads();
-    // inclusive suffix scan of chunk totals (Hillis-Steele, right to left)
-    for (int off = 1; off < (int)blockDim.x; off <<= 1) {
-        double v[6];
-        for (int q = 0; q < 6; ++q) v[q] = chunk[threadIdx.x][q];
-        if (threadIdx.x + off < blockDim.x)
-            for (int q = 0; q < 6; ++q) v[q] += chunk[threadIdx.x + off][q];
-        __syncthreads();
-        for (int q = 0; q < 6; ++q) chunk[threadIdx.x][q] = v[q];
-        __syncthreads();
-    }
-    W6 later = w6_zero();
-    if (threadIdx.x + 1 < blockDim.x) later = w6_load(chunk[threadIdx.x + 1]);
-#endif
     for (int k = lo; k < hi; ++k) {
         const int l = c.bb_by_dof[k];
         W6 s = w6_load(suf + 6 * k);
@@ -327,7 +307,7 @@ torque_seg_kernel(kf_chain_t c, TorqueArgs ta, kf_batch_t w, int n_seg) {
     const int g = blockIdx.x, b = blockIdx.y;
     const kf_status_t *st = w.status + b;
     if (st->done || st->error) return;
-    __shared__ double chunk[TQ_SHFL_SCAN ? TQ_THREADS / 32 : TQ_THREADS][6];
+    __shared__ double chunk[TQ_THREADS / 32][6];   // warp totals of the suffix scan
     __shared__ double red[32];
     const int L = c.n_links, D = c.n_dof, nb = c.n_bb;
     const double *T = ta.link_T + (size_t)b * L * KF_XF_STRIDE;
@@ -357,7 +337,6 @@ torque_seg_kernel(kf_chain_t c, TorqueArgs ta, kf_batch_t w, int n_seg) {
         }
         w6_store(suf + 6 * k, acc);
     }
-#if TQ_SHFL_SCAN
     W6 seg_total;
     const W6 later = w6_block_suffix(acc, chunk, seg_total);
     if (threadIdx.x + 1 < blockDim.x) {
@@ -373,33 +352,6 @@ torque_seg_kernel(kf_chain_t c, TorqueArgs ta, kf_batch_t w, int n_seg) {
         w6_store(sc, seg_total);
         sc[6] = tmax;
     }
-#else
-    for (int q = 0; q < 3; ++q) { chunk[threadIdx.x][q] = acc.f[q]; chunk[threadIdx.x][3 + q] = acc.t[q]; }
-    __syncthreads();
-    for (int off = 1; off < (int)blockDim.x; off <<= 1) {
-        double v[6];
-        for (int q = 0; q < 6; ++q) v[q] = chunk[threadIdx.x][q];
-        if (threadIdx.x + off < blockDim.x)
-            for (int q = 0; q < 6; ++q) v[q] += chunk[threadIdx.x + off][q];
-        __syncthreads();
-        for (int q = 0; q < 6; ++q) chunk[threadIdx.x][q] = v[q];
-        __syncthreads();
-    }
-    if (threadIdx.x + 1 < blockDim.x) {
-        const W6 later = w6_load(chunk[threadIdx.x + 1]);
-        for (int k = lo; k < hi; ++k) {
-            W6 s6 = w6_load(suf + 6 * k);
-            w6_add(s6, later);
-            w6_store(suf + 6 * k, s6);
-        }
-    }
-    tmax = block_max(tmax, red);
-    double *sc = w.fk_scratch + ((size_t)b * n_seg + g) * 12;
-    if (threadIdx.x == 0) {
-        w6_store(sc, w6_load(chunk[0]));
-        sc[6] = tmax;
-    }
-#endif
 }
 
 __global__ void __launch_bounds__(TQ_THREADS)
