@@ -376,7 +376,7 @@ def main():
     # HBM rooflines of the byte-bound phases (north star: binning, scans, kinematics):
     # algorithmic bytes per trajectory (SURVEY.md §8(d) formulas) x B / phase time
     n_at, L = ch.n_atoms, len(ch.links)
-    H = 1 << int(np.ceil(np.log2(max(2 * n_at, 2))))
+    H = 1 << max(6, int(np.ceil(np.log2(n_at + 1))))
     phase_bytes = {
         # theta in; link transforms (16 f64) and positions out
         "fk": 8 * D + 128 * L + 24 * n_at,

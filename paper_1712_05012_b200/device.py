@@ -402,7 +402,9 @@ class DeviceField(ParamTables):
         s.stencil = t["stencil"].data_ptr()
         s.n_stencil = len(sten)
         assert s.n_stencil <= 32, "one-cell reach stencil expected (27 cells)"
-        s.hash_bits = max(6, int(math.ceil(math.log2(max(2 * n, 2)))))
+        # H > n buckets: room for the worst case (one cell per atom) with one empty slot
+        # to end every probe, and for the item -> cell map (items <= n)
+        s.hash_bits = max(6, int(math.ceil(math.log2(n + 1))))
         s.precision = 1 if _precision["pair"] == "fp64" else 0
         self.n = n
         self._batches = {}
