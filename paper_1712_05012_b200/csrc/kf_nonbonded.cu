@@ -761,7 +761,8 @@ __global__ void fj_combine_kernel(int B, int n, long long *__restrict__ fj, doub
     const long long lo = p[q], hi = p[plane + q];
     if (lo || hi) {
         forces[gid] += (double)hi * FJ_HI + (double)lo * FJ_LO;
-        p[q] = 0; p[plane + q] = 0;
+        if (lo) p[q] = 0;             // clear only what was written (the hi plane is rarely
+        if (hi) p[plane + q] = 0;     // touched: no 8-byte store per component for it)
     }
 }
 
