@@ -331,6 +331,9 @@ KF_DEV void publish_prefixes(int B, const int32_t *occ_count, const int32_t *chu
 constexpr int BF_THREADS = 512;    // many trajectories: 4 CTAs per SM
 constexpr int BF_THREADS_FEW = 1024;   // < 256 trajectories (about one CTA per SM): wider CTAs
 constexpr int BF_FEW_B = 256;
+#ifndef BF_MIN_B
+#define BF_MIN_B 32   // trajectories from which binning runs fused (one CTA each)
+#endif
 #ifndef BF_MAX_ATOMS
 #define BF_MAX_ATOMS 8192   // per-trajectory atoms below which binning runs fused
 #endif
@@ -572,7 +575,7 @@ int kf_bin_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s) {
         KF_LAUNCH_CHECK("bin_flat_kernel");
         return 0;
     }
-    if (n <= BF_MAX_ATOMS && B >= 32) {   // ensembles: one CTA per trajectory does the whole binning
+    if (n <= BF_MAX_ATOMS && B >= BF_MIN_B) {   // ensembles: one CTA per trajectory does the whole binning
         auto kern = B < BF_FEW_B ? bin_fused_kernel<BF_THREADS_FEW> : bin_fused_kernel<BF_THREADS>;
         kern<<<B, B < BF_FEW_B ? BF_THREADS_FEW : BF_THREADS, 0, s>>>(
             *f, B, n, kf_pair_chunk(B, n, w->pair_chunk, f->precision), w->pos, w->cell_key, w->cell_cnt,
