@@ -1,6 +1,7 @@
 // Shared device helpers for the kfb200 kernels (sm_100a).
 #pragma once
 #include <cstdlib>
+#include <utility>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <math.h>
@@ -63,6 +64,27 @@ inline int kf_pair_chunk(int B, int n, int requested, int precision) {
     // measured on B200 (C2 chains, graph-replayed): ensembles of 128+ trajectories
     // run fastest with 16-atom items (B=128: 396k vs 375k traj-it/s at 8), 64 with 8
     return atoms < 4000 ? 4 : atoms < 150000 ? 8 : 16;
+}
+
+
+// Programmatic dependent launch (single trajectories): a kernel launched with
+// kf_launch(pdl = true, ...) may be scheduled while its predecessor runs; it
+// waits here for the predecessor's completion (and memory) before touching
+// anything.  Both are no-ops for kernels launched without the attribute.
+KF_DEV void kf_pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+KF_DEV void kf_pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t kf_launch(bool pdl, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                             Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid; cfg.blockDim = block; cfg.dynamicSmemBytes = smem; cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
 }
 
 struct Xf { double m[9]; double p[3]; };

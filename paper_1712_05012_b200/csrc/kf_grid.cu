@@ -38,6 +38,8 @@ __global__ void bin_insert_kernel(kf_field_t f, int B, int n, const double *__re
                                   int32_t *__restrict__ occ, int32_t *__restrict__ occ_count,
                                   int32_t *__restrict__ atom_slot, int32_t *__restrict__ atom_rank,
                                   kf_status_t *status) {
+    kf_pdl_wait();      // after the predecessor (programmatic launch: single trajectories)
+    kf_pdl_trigger();
     const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (gid >= (long long)B * n) return;
     const int b = (int)(gid / n);
@@ -113,6 +115,8 @@ cell_scan_kernel(int H, int chunk, const int32_t *__restrict__ occ, const int32_
                  const int32_t *__restrict__ cnt, int32_t *__restrict__ start, int32_t *__restrict__ chunk_pre,
                  int32_t *__restrict__ item_cell, int32_t *__restrict__ chunk_count, const kf_status_t *status,
                  int32_t *__restrict__ occ_offset, int32_t *__restrict__ chunk_offset) {
+    kf_pdl_wait();      // after the predecessor (programmatic launch: single trajectories)
+    kf_pdl_trigger();
     // occ_offset / chunk_offset non-null (one trajectory): the work prefixes are
     // written here and occ_prefix_kernel is skipped
     const int b = blockIdx.x;
@@ -154,6 +158,8 @@ cell_scan_kernel(int H, int chunk, const int32_t *__restrict__ occ, const int32_
 // one kernel node instead of three memsets.
 __global__ void bin_clear_kernel(long long n_tab, int B, unsigned long long *__restrict__ keys,
                                  int32_t *__restrict__ cnt, int32_t *__restrict__ occ_count) {
+    kf_pdl_wait();      // after the predecessor (programmatic launch: single trajectories)
+    kf_pdl_trigger();
     for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < n_tab;
          q += (long long)gridDim.x * blockDim.x) {
         keys[q] = EMPTY;
@@ -189,6 +195,8 @@ occ_prefix_kernel(int B, const int32_t *__restrict__ occ_count, int32_t *__restr
 __global__ void bin_scatter_kernel(kf_field_t f, int B, int n, const int32_t *__restrict__ atom_slot,
                                    const int32_t *__restrict__ atom_rank, const int32_t *__restrict__ start,
                                    int32_t *__restrict__ sorted_atom, const kf_status_t *status) {
+    kf_pdl_wait();      // after the predecessor (programmatic launch: single trajectories)
+    kf_pdl_trigger();
     const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (gid >= (long long)B * n) return;
     const int b = (int)(gid / n), a = (int)(gid % n);
@@ -280,6 +288,8 @@ bin_finalize_kernel(const __grid_constant__ kf_field_t f, int B, int n, const do
                     double4 *__restrict__ s_pos, float4 *__restrict__ s_par,
                     int4 *__restrict__ s_aux, int4 *__restrict__ s_tree,
                     float4 *__restrict__ cell_box, const kf_status_t *status) {
+    kf_pdl_wait();      // after the predecessor (programmatic launch: single trajectories)
+    kf_pdl_trigger();
     __shared__ int buf[FIN_WARPS][FIN_CAP];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int total = occ_offset[B];
@@ -588,24 +598,28 @@ int kf_bin_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s) {
         return 0;
     }
     const long long n_tab = (long long)B * H;
-    bin_clear_kernel<<<(unsigned)std::min<long long>(kf_blocks(n_tab, 256), 4 * 148), 256, 0, s>>>(
-        n_tab, B, w->cell_key, w->cell_cnt, w->occ_count);
+    const bool pdl = B < 64;
+    (void)kf_launch(pdl, bin_clear_kernel, dim3((unsigned)std::min<long long>(kf_blocks(n_tab, 256), 4 * 148)),
+                    dim3(256), 0, s, n_tab, B, w->cell_key, w->cell_cnt, w->occ_count);
     KF_LAUNCH_CHECK("bin_clear_kernel");
     const long long total = (long long)B * n;
-    bin_insert_kernel<<<kf_blocks(total, 256), 256, 0, s>>>(*f, B, n, w->pos, w->cell_key, w->cell_cnt, w->occ,
-                                                            w->occ_count, w->atom_slot, w->atom_rank, w->status);
+    (void)kf_launch(pdl, bin_insert_kernel, dim3(kf_blocks(total, 256)), dim3(256), 0, s, *f, B, n,
+                    (const double *)w->pos, w->cell_key, w->cell_cnt, w->occ, w->occ_count, w->atom_slot,
+                    w->atom_rank, w->status);
     KF_LAUNCH_CHECK("bin_insert_kernel");
-    cell_scan_kernel<<<B, 1024, 0, s>>>(H, kf_pair_chunk(B, n, w->pair_chunk, f->precision), w->occ, w->occ_count,
-                                         w->cell_cnt, w->cell_start, w->chunk_pre, w->item_cell, w->chunk_count, w->status,
-                                         B == 1 ? w->occ_offset : nullptr, B == 1 ? w->chunk_offset : nullptr);
+    (void)kf_launch(pdl, cell_scan_kernel, dim3(B), dim3(1024), 0, s, H, kf_pair_chunk(B, n, w->pair_chunk, f->precision),
+                    (const int32_t *)w->occ, (const int32_t *)w->occ_count, (const int32_t *)w->cell_cnt,
+                    w->cell_start, w->chunk_pre, w->item_cell, w->chunk_count, (const kf_status_t *)w->status,
+                    B == 1 ? w->occ_offset : (int32_t *)nullptr, B == 1 ? w->chunk_offset : (int32_t *)nullptr);
     KF_LAUNCH_CHECK("cell_scan_kernel");
     if (B > 1) {
         occ_prefix_kernel<<<1, 1024, 0, s>>>(B, w->occ_count, w->occ_offset, w->chunk_count, w->chunk_offset,
                                              w->status);
         KF_LAUNCH_CHECK("occ_prefix_kernel");
     }
-    bin_scatter_kernel<<<kf_blocks(total, 256), 256, 0, s>>>(*f, B, n, w->atom_slot, w->atom_rank, w->cell_start,
-                                                             w->sorted_atom, w->status);
+    (void)kf_launch(pdl, bin_scatter_kernel, dim3(kf_blocks(total, 256)), dim3(256), 0, s, *f, B, n,
+                    (const int32_t *)w->atom_slot, (const int32_t *)w->atom_rank, (const int32_t *)w->cell_start,
+                    w->sorted_atom, (const kf_status_t *)w->status);
     KF_LAUNCH_CHECK("bin_scatter_kernel");
     static int fin_grid = 0;
     if (fin_grid == 0) {
@@ -615,7 +629,8 @@ int kf_bin_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bin_finalize_kernel, FIN_WARPS * 32, 0);
         fin_grid = sms * (per_sm > 0 ? per_sm : 1);
     }
-    bin_finalize_kernel<<<(unsigned)std::min<long long>(fin_grid, kf_blocks(total, FIN_WARPS)), FIN_WARPS * 32, 0, s>>>(
+    (void)kf_launch(pdl, bin_finalize_kernel, dim3((unsigned)std::min<long long>(fin_grid, kf_blocks(total, FIN_WARPS))),
+        dim3(FIN_WARPS * 32), 0, s,
         *f, B, n, w->pos, w->cell_key, w->occ, w->occ_offset, w->cell_cnt, w->cell_start, w->sorted_atom,
         reinterpret_cast<float4 *>(w->s_hi), reinterpret_cast<float4 *>(w->s_lo),
         reinterpret_cast<double4 *>(w->s_pos), reinterpret_cast<float4 *>(w->s_par),

@@ -142,6 +142,8 @@ constexpr int FKS_STRIDE = 12;
 __global__ void __launch_bounds__(FKS_THREADS)
 fk_smem_kernel(const __grid_constant__ kf_chain_t c, const double *__restrict__ theta_all,
                double *__restrict__ T_all, double *__restrict__ pos_all, const kf_status_t *__restrict__ status) {
+    kf_pdl_wait();      // after the predecessor (programmatic launch: single trajectories)
+    kf_pdl_trigger();
     const int b = blockIdx.x;
     if (status && status[b].done) return;
     extern __shared__ __align__(16) double S[];     // [L][12], then the int tables below
@@ -407,7 +409,8 @@ int kf_fk_launch(const kf_chain_t *c, kf_batch_t *w, const kf_status_t *status, 
                     "fk smem");
             opted = smem;
         }
-        fk_smem_kernel<<<w->B, FKS_THREADS, smem, s>>>(*c, w->theta, w->link_T, w->pos, status);
+        (void)kf_launch(w->B < 64, fk_smem_kernel, dim3(w->B), dim3(FKS_THREADS), smem, s, *c,
+                        (const double *)w->theta, w->link_T, w->pos, status);
         KF_LAUNCH_CHECK("fk_smem_kernel");
         return 0;
     }

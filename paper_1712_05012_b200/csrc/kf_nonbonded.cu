@@ -479,6 +479,8 @@ pair_dense_kernel(const __grid_constant__ kf_field_t f, const __grid_constant__ 
                   const float4 *__restrict__ cell_box, int32_t *__restrict__ work, double *__restrict__ forces,
                   double *__restrict__ e_atom, long long *__restrict__ pair_count, kf_status_t *status,
                   long long *__restrict__ fj_fixed) {
+    kf_pdl_wait();      // after the predecessor (programmatic launch: single trajectories)
+    kf_pdl_trigger();
     const long long fj_plane = 3LL * B * n;
     using T = typename std::conditional<F64, double, float>::type;
     constexpr int NW = SPLIT ? SPLIT_WARPS : PAIR_WARPS;
@@ -890,7 +892,8 @@ int kf_pairs_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s) {
         auto kern = half ? (split ? pair_dense_kernel<false, true, true> : pair_dense_kernel<false, false, true>)
                          : f->precision ? (split ? pair_dense_kernel<true, true, false> : pair_dense_kernel<true, false, false>)
                                         : (split ? pair_dense_kernel<false, true, false> : pair_dense_kernel<false, false, false>);
-        kern<<<resident_grid(kern, nw * 32, 0), nw * 32, 0, s>>>(KF_PAIR_ARGS, w->pair_fj);
+        (void)kf_launch(w->B < 64, kern, dim3(resident_grid(kern, nw * 32, 0)), dim3(nw * 32), 0, s, KF_PAIR_ARGS,
+                        w->pair_fj);
         if (half) {
             KF_LAUNCH_CHECK("pair_kernel");
             const long long total = 3LL * w->B * n;

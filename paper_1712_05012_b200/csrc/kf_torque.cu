@@ -181,6 +181,8 @@ template <int NT>
 __global__ void __launch_bounds__(NT)
 torque_step_kernel(kf_chain_t c, kf_field_t f, TorqueArgs ta, kf_batch_t w, kf_step_t step, int mode,
                    int fuse_wrench) {
+    kf_pdl_wait();      // after the predecessor (programmatic launch: single trajectories)
+    kf_pdl_trigger();
     const int b = blockIdx.x;
     kf_status_t *st = w.status ? w.status + b : nullptr;
     if (st && st->done) return;
@@ -512,7 +514,8 @@ int kf_torque_launch(const kf_chain_t *c, const kf_field_t *f, kf_batch_t *w, co
             opted[wide] = wsm;
         }
     }
-    kern<<<w->B, wide ? TQ_THREADS : TQ_THREADS / 2, fuse ? wsm : 0, s>>>(*c, fz, ta, *w, st, mode, fuse ? 1 : 0);
+    (void)kf_launch(w->B < 64, kern, dim3(w->B), dim3(wide ? TQ_THREADS : TQ_THREADS / 2), fuse ? wsm : 0, s, *c, fz, ta,
+                    *w, st, mode, fuse ? 1 : 0);
     KF_LAUNCH_CHECK("torque_step_kernel");
     return 0;
 }
