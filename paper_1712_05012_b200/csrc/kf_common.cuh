@@ -74,6 +74,9 @@ inline int kf_pair_chunk(int B, int n, int requested, int precision) {
 KF_DEV void kf_pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 KF_DEV void kf_pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
 
+#ifndef KF_PDL_B
+#define KF_PDL_B 64   // batches below this launch the iteration chain with PDL
+#endif
 template <typename... KArgs, typename... Args>
 inline cudaError_t kf_launch(bool pdl, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                              Args &&...args) {

@@ -598,7 +598,7 @@ int kf_bin_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s) {
         return 0;
     }
     const long long n_tab = (long long)B * H;
-    const bool pdl = B < 64;
+    const bool pdl = B < KF_PDL_B;
     (void)kf_launch(pdl, bin_clear_kernel, dim3((unsigned)std::min<long long>(kf_blocks(n_tab, 256), 4 * 148)),
                     dim3(256), 0, s, n_tab, B, w->cell_key, w->cell_cnt, w->occ_count);
     KF_LAUNCH_CHECK("bin_clear_kernel");

@@ -409,7 +409,7 @@ int kf_fk_launch(const kf_chain_t *c, kf_batch_t *w, const kf_status_t *status, 
                     "fk smem");
             opted = smem;
         }
-        (void)kf_launch(w->B < 64, fk_smem_kernel, dim3(w->B), dim3(FKS_THREADS), smem, s, *c,
+        (void)kf_launch(w->B < KF_PDL_B, fk_smem_kernel, dim3(w->B), dim3(FKS_THREADS), smem, s, *c,
                         (const double *)w->theta, w->link_T, w->pos, status);
         KF_LAUNCH_CHECK("fk_smem_kernel");
         return 0;

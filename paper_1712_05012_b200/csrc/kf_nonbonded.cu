@@ -892,7 +892,7 @@ int kf_pairs_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s) {
         auto kern = half ? (split ? pair_dense_kernel<false, true, true> : pair_dense_kernel<false, false, true>)
                          : f->precision ? (split ? pair_dense_kernel<true, true, false> : pair_dense_kernel<true, false, false>)
                                         : (split ? pair_dense_kernel<false, true, false> : pair_dense_kernel<false, false, false>);
-        (void)kf_launch(w->B < 64, kern, dim3(resident_grid(kern, nw * 32, 0)), dim3(nw * 32), 0, s, KF_PAIR_ARGS,
+        (void)kf_launch(w->B < KF_PDL_B, kern, dim3(resident_grid(kern, nw * 32, 0)), dim3(nw * 32), 0, s, KF_PAIR_ARGS,
                         w->pair_fj);
         if (half) {
             KF_LAUNCH_CHECK("pair_kernel");

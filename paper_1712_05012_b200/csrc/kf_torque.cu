@@ -514,7 +514,7 @@ int kf_torque_launch(const kf_chain_t *c, const kf_field_t *f, kf_batch_t *w, co
             opted[wide] = wsm;
         }
     }
-    (void)kf_launch(w->B < 64, kern, dim3(w->B), dim3(wide ? TQ_THREADS : TQ_THREADS / 2), fuse ? wsm : 0, s, *c, fz, ta,
+    (void)kf_launch(w->B < KF_PDL_B, kern, dim3(w->B), dim3(wide ? TQ_THREADS : TQ_THREADS / 2), fuse ? wsm : 0, s, *c, fz, ta,
                     *w, st, mode, fuse ? 1 : 0);
     KF_LAUNCH_CHECK("torque_step_kernel");
     return 0;
