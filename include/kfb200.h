@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define KF_ABI_VERSION 10
+#define KF_ABI_VERSION 11
 
 /* ---- static chain tables (uploaded once per chain) ------------------------
  * Links are in the reference's topological order (parent < index, ground = 0),
@@ -174,9 +174,10 @@ typedef struct {
     long long *solv_acc;            /* [B][n][3] int64 fixed point                 */
     int32_t *solv_ovf;              /* [1 + 2 B n]: count, (b, atom) pairs deferred to
                                        the large-capacity solvation pass            */
-    long long *pair_fj;             /* [2][B][n][3] half-list j-side forces, fixed point
-                                       (lo plane in 2^-28, hi plane in 2^12); kept zero
-                                       between launches; NULL: full-list kernel     */
+    long long *pair_fj;             /* [3][B][n][3] half-list j-side forces and exact-path
+                                       forces: fixed point (lo plane in 2^-28, hi plane
+                                       in 2^12) + an fp64 plane for |f| >= 2^72; kept
+                                       zero between launches; NULL: full-list kernel */
     double  *cav_atom;              /* [B][n] gamma_i * a_exp_i                    */
     double  *f_exp;                 /* [B][n] exposure ratio (NULL: not stored)    */
     double  *a_exp;                 /* [B][n] exposed area (NULL: not stored)      */
@@ -309,13 +310,15 @@ int kf_classify_pairs(const kf_field_t *f, const int64_t *i, const int64_t *j, i
                       int64_t *cls, void *stream);
 
 /* elec/vdW over an explicit pair list (forcefield.py:98-172): per-pair energy
- * and magnitude in fp64, forces scattered with fp64 atomics. kind: 0 elec, 1 vdW. */
+ * and magnitude in fp64; forces (if non-NULL, n atoms) scattered in np.bincount
+ * order, bit-identical to the reference and deterministic. kind: 0 elec, 1 vdW. */
 int kf_pair_terms(const kf_field_t *f, const double *pos, int n, const int64_t *i,
                   const int64_t *j, const double *d, const double *w /* NULL: classify */,
                   int64_t n_pairs, int kind, double *e_pair, double *mag,
                   double *forces /* [n][3] or NULL */, void *stream);
-/* accumulate_pair_forces (forcefield.py:116-117, :162-172). */
-int kf_scatter_pair_forces(const double *pos, const int64_t *i, const int64_t *j,
+/* accumulate_pair_forces (forcefield.py:116-117, :162-172): forces [n][3] +=
+ * bincount(i, f) then -= bincount(j, f), in the reference's order (deterministic). */
+int kf_scatter_pair_forces(const double *pos, int n, const int64_t *i, const int64_t *j,
                            const double *d, const double *mag, int64_t m, double *forces,
                            void *stream);
 /* build_grid's occupied cells and their starts from dense per-key counts. */

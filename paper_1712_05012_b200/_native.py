@@ -13,7 +13,7 @@ import os
 from .errors import NativeLibraryError
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libkfb200.so")
-ABI_VERSION = 10
+ABI_VERSION = 11
 
 P = C.c_void_p
 I32 = C.c_int32
@@ -101,7 +101,7 @@ _PROTOS = {
     "kf_scan_exclusive_i64": (I32, [P, C.c_int64, P, P, P]),
     "kf_classify_pairs": (I32, [P, P, P, C.c_int64, P, P]),
     "kf_pair_terms": (I32, [P, P, C.c_int, P, P, P, P, C.c_int64, C.c_int, P, P, P, P]),
-    "kf_scatter_pair_forces": (I32, [P, P, P, P, P, C.c_int64, P, P]),
+    "kf_scatter_pair_forces": (I32, [P, C.c_int, P, P, P, P, C.c_int64, P, P]),
     "kf_grid_occupied": (I32, [P, P, C.c_int64, P, P, P, P, P]),
     "kf_row_kept_offsets": (I32, [P, C.c_int, P, P, P]),
     "kf_argmin_f64": (I32, [P, C.c_int64, P, P]),

@@ -37,7 +37,12 @@ int kf_kcm_step_launch(const double *tau, const double *theta, const uint8_t *fr
 namespace {
 thread_local std::string g_last_error;
 std::mutex g_graph_mu;
-std::unordered_map<std::string, cudaGraphExec_t> g_graphs;
+// instantiated fold graphs keyed on the launch's struct bytes (buffer pointers
+// included), least recently used evicted past KF_GRAPH_CAP entries
+struct GraphEntry { cudaGraphExec_t exec; unsigned long long used; };
+std::unordered_map<std::string, GraphEntry> g_graphs;
+unsigned long long g_graph_clock = 0;
+constexpr size_t KF_GRAPH_CAP = 48;
 
 std::string graph_key(const kf_chain_t *c, const kf_field_t *f, const kf_batch_t *w, const kf_step_t *st,
                       int n_iters, cudaStream_t s) {
@@ -149,7 +154,10 @@ static int fold_graph(const kf_chain_t *c, const kf_field_t *f, kf_batch_t *w, c
     {
         std::lock_guard<std::mutex> lk(g_graph_mu);
         auto it = g_graphs.find(key);
-        if (it != g_graphs.end()) exec = it->second;
+        if (it != g_graphs.end()) {
+            exec = it->second.exec;
+            it->second.used = ++g_graph_clock;
+        }
     }
     if (!exec) {
         cudaGraph_t graph = nullptr;
@@ -163,7 +171,15 @@ static int fold_graph(const kf_chain_t *c, const kf_field_t *f, kf_batch_t *w, c
         cudaGraphDestroy(graph);
         KF_CUDA(e, "graph instantiate");
         std::lock_guard<std::mutex> lk(g_graph_mu);
-        g_graphs[key] = exec;
+        if (g_graphs.size() >= KF_GRAPH_CAP) {
+            auto old = g_graphs.begin();
+            for (auto it = g_graphs.begin(); it != g_graphs.end(); ++it)
+                if (it->second.used < old->second.used) old = it;
+            cudaStreamSynchronize(s);   // the evicted graph may still be in flight on this stream
+            cudaGraphExecDestroy(old->second.exec);
+            g_graphs.erase(old);
+        }
+        g_graphs[key] = GraphEntry{exec, ++g_graph_clock};
     }
     if (launch) KF_CUDA(cudaGraphLaunch(exec, s), "graph launch");
     return 0;
@@ -171,7 +187,7 @@ static int fold_graph(const kf_chain_t *c, const kf_field_t *f, kf_batch_t *w, c
 
 void kf_graph_cache_clear(void) {
     std::lock_guard<std::mutex> lk(g_graph_mu);
-    for (auto &kv : g_graphs) cudaGraphExecDestroy(kv.second);
+    for (auto &kv : g_graphs) cudaGraphExecDestroy(kv.second.exec);
     g_graphs.clear();
 }
 

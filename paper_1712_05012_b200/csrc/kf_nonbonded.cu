@@ -40,10 +40,31 @@ constexpr double MIN_DISTANCE = 1e-6;
 // 2^12, lo (the exact remainder, |r| <= 2^11) in units of 2^-28
 constexpr double FJ_HI = 4096.0, FJ_HI_INV = 1.0 / 4096.0;
 constexpr double FJ_LO = 1.0 / 268435456.0, FJ_LO_INV = 268435456.0;
+// beyond this magnitude a contribution would overflow the hi plane's int64 once a
+// few are summed (|hi| <= 2^60 each): it goes to the fp64 plane instead (pairs
+// closer than ~0.05 A only)
+constexpr double FJ_SAT = 4722366482869645213696.0;   // 2^72
 constexpr int PAIR_WARPS = 4;        // warps per CTA, warp-per-cell variant
 constexpr int SPLIT_WARPS = 4;       // warps per CTA (one cell), split variant
 constexpr unsigned FULL = 0xffffffffu;
 
+
+// Adds v to one component of the half-list kernel's j-side accumulator:
+// planes = [lo int64 | hi int64 | big fp64], each [B][n][3], plane = 3 B n.
+// Integer atomics are order-free, so the sum is schedule-independent; only
+// |v| >= 2^72 (never a fast-path pair) takes the fp64 atomic.
+KF_DEV void fj_add(long long *planes, long long plane, size_t idx, double v) {
+    if (v == 0.0) return;
+    if (!(fabs(v) < FJ_SAT)) {
+        atomicAdd(reinterpret_cast<double *>(planes + 2 * plane + idx), v);
+        return;
+    }
+    const long long hi_u = __double2ll_rn(v * FJ_HI_INV);     // units of 2^12
+    const double rem = v - (double)hi_u * FJ_HI;               // exact, |rem| <= 2^11
+    const long long lo_u = __double2ll_rn(rem * FJ_LO_INV);    // units of 2^-28
+    if (lo_u) atomicAdd(reinterpret_cast<unsigned long long *>(planes + idx), (unsigned long long)lo_u);
+    if (hi_u) atomicAdd(reinterpret_cast<unsigned long long *>(planes + plane + idx), (unsigned long long)hi_u);
+}
 
 struct Tile {
     float4 hi[32];
@@ -131,10 +152,12 @@ __device__ __noinline__ void slow_pair(bool f64, const kf_field_t *A, const doub
 // class window, and fp32 energy/force -- with the exact fp64 recomputation in
 // the 1e-3 A^2 threshold bands and below f64_d2 (always, in fp64 mode).
 // out = force on i (x, y, z), elec and vdW energy.  Shared by both kernels.
+// Returns true when the exact fp64 path ran: its results are then in sd[5]
+// (fp64, never rounded to T: clash-range forces overflow fp32) and out[] is 0.
 template <bool F64, typename T>
-KF_DEV void pair_eval(const kf_field_t &f, const PairConst &pc, float4 hi, float4 li, float4 qi, int4 ai, int4 cm,
+KF_DEV bool pair_eval(const kf_field_t &f, const PairConst &pc, float4 hi, float4 li, float4 qi, int4 ai, int4 cm,
                       float4 hj, float4 lj, float4 qj, int4 aj, const double4 *pos_i, const double4 *pos_j,
-                      kf_status_t *st, T out[5], int &pce, int &pcv) {
+                      kf_status_t *st, T out[5], int &pce, int &pcv, double sd[5]) {
     const float cut2f = pc.cut2, tvf = pc.tv2, tef = pc.te2;
     const float band = 1e-3f;
     const int i = ai.x, j = aj.x;
@@ -142,7 +165,7 @@ KF_DEV void pair_eval(const kf_field_t &f, const PairConst &pc, float4 hi, float
     const float dyf = (hi.y - hj.y) + (li.y - lj.y);
     const float dzf = (hi.z - hj.z) + (li.z - lj.z);
     const float d2f = dxf * dxf + dyf * dyf + dzf * dzf;
-    if (i == j || d2f > cut2f + band) return;
+    if (i == j || d2f > cut2f + band) return false;
     // static class window: 2-bit codes for j - i in [-32, 32)
     int cls = 4;
     if (!pc.uniform) {
@@ -163,12 +186,12 @@ KF_DEV void pair_eval(const kf_field_t &f, const PairConst &pc, float4 hi, float
     if (exact) {
         // the outlined path writes through pointers: give it its own stack
         // temporaries so out / pce / pcv stay in registers on the fast path
-        T so[5] = {0, 0, 0, 0, 0};
+        double so[5] = {0, 0, 0, 0, 0};
         int sce = 0, scv = 0;
-        slow_pair<T>(F64, &f, pos_i, pos_j, i, j, cls, so, &sce, &scv, st);
-        out[0] = so[0]; out[1] = so[1]; out[2] = so[2]; out[3] = so[3]; out[4] = so[4];
+        slow_pair<double>(F64, &f, pos_i, pos_j, i, j, cls, so, &sce, &scv, st);
+        sd[0] = so[0]; sd[1] = so[1]; sd[2] = so[2]; sd[3] = so[3]; sd[4] = so[4];
         pce = sce; pcv = scv;
-        return;
+        return true;
     }
     // (here d2f < cut2f - band: nearer the cut-off went exact, beyond it returned above)
     const bool ke = d2f <= tef, kv = d2f <= tvf;
@@ -195,6 +218,7 @@ KF_DEV void pair_eval(const kf_field_t &f, const PairConst &pc, float4 hi, float
     float g = ke ? e * inv_r2 : 0.f;
     g = kv ? __fmaf_rn(12.f * weps * (s6 - s3), inv_r2, g) : g;
     out[0] = g * dxf; out[1] = g * dyf; out[2] = g * dzf;
+    return false;
 }
 
 #ifndef PAIR_MINB_W
@@ -385,8 +409,11 @@ pair_kernel(const __grid_constant__ kf_field_t f, const __grid_constant__ PairCo
                             const int t = e & 31;
                             const int4 ai = I.aux[o], aj = S.J.aux[t];
                             const float4 hi = I.hi[o], li = I.lo[o], hj = S.J.hi[t], lj = S.J.lo[t];
-                            pair_eval<F64, T>(f, pc, hi, li, I.par[o], ai, itree[o], hj, lj, S.J.par[t], aj,
-                                              s_pos + nb + s0 + ic + o, s_pos + nb + aj.w, status + b, out, pce, pcv);
+                            double sd[5];
+                            if (pair_eval<F64, T>(f, pc, hi, li, I.par[o], ai, itree[o], hj, lj, S.J.par[t], aj,
+                                                  s_pos + nb + s0 + ic + o, s_pos + nb + aj.w, status + b, out, pce,
+                                                  pcv, sd))
+                                for (int q = 0; q < 5; ++q) out[q] = (T)sd[q];   // fp64 mode: T = double
                         }
                         // energies and counts only enter per-chunk totals: the computing lane keeps them
                         fe += out[3]; fv += out[4];
@@ -621,8 +648,17 @@ pair_dense_kernel(const __grid_constant__ kf_field_t f, const __grid_constant__ 
                     int pce = 0, pcv = 0;
                     if (pass) {
                         const int4 aj = J.aux[t];
-                        pair_eval<F64, T>(f, pc, hi, li, qi, ai, cm, hj, J.lo[t], J.par[t], aj, s_pos + ki,
-                                          s_pos + nb + aj.w, status + b, out, pce, pcv);
+                        double sd[5];
+                        if (pair_eval<F64, T>(f, pc, hi, li, qi, ai, cm, hj, J.lo[t], J.par[t], aj, s_pos + ki,
+                                              s_pos + nb + aj.w, status + b, out, pce, pcv, sd)) {
+                            // exact path: fp64 forces straight into both atoms' fixed point
+                            // (i gets +f, j gets -f; fj_combine adds the planes to every atom)
+                            for (int q = 0; q < 3; ++q) {
+                                fj_add(fj_fixed, fj_plane, 3 * (nb + ai.x) + q, sd[q]);
+                                fj_add(fj_fixed, fj_plane, 3 * (nb + aj.x) + q, -sd[q]);
+                            }
+                            ee += sd[3]; ev += sd[4];
+                        }
                     }
                     fx += out[0]; fy += out[1]; fz += out[2]; fe += out[3]; fv += out[4];
                     ce += pce; cv += pcv;
@@ -648,17 +684,8 @@ pair_dense_kernel(const __grid_constant__ kf_field_t f, const __grid_constant__ 
                         }
                         v[q] = (double)acc;
                     }
-                    // planes: lo [B n 3] then hi [B n 3] (the hi plane is rarely touched)
-                    long long *dst = fj_fixed + 3 * (nb + J.aux[lane].x);
-                    for (int q = 0; q < 3; ++q) {
-                        if (v[q] == 0.0) continue;
-                        const long long hi_u = __double2ll_rn(v[q] * FJ_HI_INV);     // units of 2^12
-                        const double rem = v[q] - (double)hi_u * FJ_HI;            // exact, |rem| <= 2^11
-                        const long long lo_u = __double2ll_rn(rem * FJ_LO_INV);     // units of 2^-28
-                        if (lo_u) atomicAdd(reinterpret_cast<unsigned long long *>(dst + q), (unsigned long long)lo_u);
-                        if (hi_u) atomicAdd(reinterpret_cast<unsigned long long *>(dst + fj_plane + q),
-                                            (unsigned long long)hi_u);
-                    }
+                    // planes: lo [B n 3], hi [B n 3], fp64 [B n 3] (the last two rarely touched)
+                    for (int q = 0; q < 3; ++q) fj_add(fj_fixed, fj_plane, 3 * (nb + J.aux[lane].x) + q, v[q]);
                 }
             } else {
                 // this lane's prefilter hits over the tile (bit kt: j = ph + kt * nph), then
@@ -677,8 +704,11 @@ pair_dense_kernel(const __grid_constant__ kf_field_t f, const __grid_constant__ 
                     T out[5] = {0, 0, 0, 0, 0};
                     int pce = 0, pcv = 0;
                     const int4 aj = J.aux[t];
-                    pair_eval<F64, T>(f, pc, hi, li, qi, ai, cm, J.hi[t], J.lo[t], J.par[t], aj, s_pos + ki,
-                                      s_pos + nb + aj.w, status + b, out, pce, pcv);
+                    double sd[5];
+                    if (pair_eval<F64, T>(f, pc, hi, li, qi, ai, cm, J.hi[t], J.lo[t], J.par[t], aj, s_pos + ki,
+                                          s_pos + nb + aj.w, status + b, out, pce, pcv, sd)) {
+                        ax += sd[0]; ay += sd[1]; az += sd[2]; ee += sd[3]; ev += sd[4];   // fp64 sums directly
+                    }
                     fx += out[0]; fy += out[1]; fz += out[2]; fe += out[3]; fv += out[4];
                     ce += pce; cv += pcv;
                 }
@@ -761,10 +791,13 @@ __global__ void fj_combine_kernel(int B, int n, long long *__restrict__ fj, doub
     long long *p = fj + 3 * a;
     const long long plane = 3LL * B * n;
     const long long lo = p[q], hi = p[plane + q];
-    if (lo || hi) {
-        forces[gid] += (double)hi * FJ_HI + (double)lo * FJ_LO;
-        if (lo) p[q] = 0;             // clear only what was written (the hi plane is rarely
-        if (hi) p[plane + q] = 0;     // touched: no 8-byte store per component for it)
+    double *big = reinterpret_cast<double *>(fj + 2 * plane) + 3 * a + q;
+    const double bg = *big;
+    if (lo || hi || bg != 0.0) {
+        forces[gid] += ((double)hi * FJ_HI + (double)lo * FJ_LO) + bg;
+        if (lo) p[q] = 0;             // clear only what was written (the hi and fp64 planes
+        if (hi) p[plane + q] = 0;     // are rarely touched: no 8-byte store per component)
+        if (bg != 0.0) *big = 0.0;
     }
 }
 

@@ -275,7 +275,7 @@ __global__ void classify_kernel(kf_field_t f, const int64_t *pi_, const int64_t 
 // Reference formulas verbatim in fp64 (forcefield.py:98-113, :162-172).
 __global__ void pair_terms_kernel(kf_field_t f, const double *pos, const int64_t *pi_, const int64_t *pj_,
                                   const double *dd_, const double *w_in, int64_t m, int kind, double *e_out,
-                                  double *mag_out, double *forces) {
+                                  double *mag_out, double *fvec) {
     const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= m) return;
     const int i = (int)pi_[p], j = (int)pj_[p];
@@ -304,24 +304,34 @@ __global__ void pair_terms_kernel(kf_field_t f, const double *pos, const int64_t
     }
     if (e_out) e_out[p] = e;
     if (mag_out) mag_out[p] = mag;
-    if (forces) {   // e = (r_i - r_j) / d; f = mag e; out[i] += f, out[j] -= f (forcefield.py:167-171)
-        for (int k = 0; k < 3; ++k) {
-            const double fk = mag * ((pos[3 * (size_t)i + k] - pos[3 * (size_t)j + k]) / d);
-            atomicAdd(&forces[3 * (size_t)i + k], fk);
-            atomicAdd(&forces[3 * (size_t)j + k], -fk);
-        }
-    }
+    if (fvec)   // e = (r_i - r_j) / d; f = mag e (forcefield.py:167-168); scattered by bincount_apply
+        for (int k = 0; k < 3; ++k)
+            fvec[3 * p + k] = mag * ((pos[3 * (size_t)i + k] - pos[3 * (size_t)j + k]) / d);
 }
 
-__global__ void scatter_pair_forces_kernel(const double *pos, const int64_t *pi_, const int64_t *pj_,
-                                           const double *dd_, const double *mag, int64_t m, double *forces) {
+// Per-pair force vectors f = mag * ((r_i - r_j) / d) (forcefield.py:167-168).
+__global__ void pair_fvec_kernel(const double *pos, const int64_t *pi_, const int64_t *pj_, const double *dd_,
+                                 const double *mag, int64_t m, double *fvec) {
     const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= m) return;
     const int64_t i = pi_[p], j = pj_[p];
+    for (int k = 0; k < 3; ++k) fvec[3 * p + k] = mag[p] * ((pos[3 * i + k] - pos[3 * j + k]) / dd_[p]);
+}
+
+// The reference's scatter, bit for bit (forcefield.py:169-171): per component,
+// out += np.bincount(i, f), then out -= np.bincount(j, f).  np.bincount adds
+// the weights of each bin sequentially in pair order starting from 0.0; the
+// stable counting sorts by i and by j list each atom's pairs in that order, so
+// one thread per atom reproduces both sums and the result is deterministic.
+__global__ void bincount_apply_kernel(int n, const int64_t *st_i, const int64_t *ord_i, const int64_t *st_j,
+                                      const int64_t *ord_j, const double *fvec, double *forces) {
+    const int a = blockIdx.x * blockDim.x + threadIdx.x;
+    if (a >= n) return;
     for (int k = 0; k < 3; ++k) {
-        const double fk = mag[p] * ((pos[3 * i + k] - pos[3 * j + k]) / dd_[p]);
-        atomicAdd(&forces[3 * i + k], fk);
-        atomicAdd(&forces[3 * j + k], -fk);
+        double si = 0.0, sj = 0.0;
+        for (int64_t e = st_i[a]; e < st_i[a + 1]; ++e) si = xadd(si, fvec[3 * ord_i[e] + k]);
+        for (int64_t e = st_j[a]; e < st_j[a + 1]; ++e) sj = xadd(sj, fvec[3 * ord_j[e] + k]);
+        forces[3 * (size_t)a + k] = xsub(xadd(forces[3 * (size_t)a + k], si), sj);
     }
 }
 
@@ -401,6 +411,34 @@ int kf_u8_to_i64_launch(const uint8_t *in, int64_t n, int64_t *out, cudaStream_t
     return 0;
 }
 
+int kf_counting_sort_launch(const int64_t *key, int n, int64_t n_keys, int32_t *counts, int64_t *starts,
+                            int64_t *order, int64_t *scratch, cudaStream_t s);
+
+// forces[a] = (forces[a] + bincount(i, f)[a]) - bincount(j, f)[a] for the m
+// per-pair vectors fvec (stream-ordered scratch for the two stable sorts).
+static int scatter_bincount(int n, const int64_t *i, const int64_t *j, int64_t m, const double *fvec,
+                            double *forces, cudaStream_t s) {
+    if (m > 0x7fffffffLL) { kf_set_error("scatter_bincount", cudaErrorInvalidValue); return 1; }
+    const size_t bytes = sizeof(int32_t) * (size_t)n + sizeof(int64_t) * (2 * ((size_t)n + 1) + 2 * (size_t)m +
+                                                                          (size_t)n + 1024);
+    char *buf = nullptr;
+    KF_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&buf), bytes, s), "scatter scratch");
+    int64_t *st_i = reinterpret_cast<int64_t *>(buf), *st_j = st_i + n + 1, *ord_i = st_j + n + 1,
+            *ord_j = ord_i + m, *scratch = ord_j + m;
+    int32_t *counts = reinterpret_cast<int32_t *>(scratch + n + 1024);
+    int rc = kf_counting_sort_launch(i, (int)m, n, counts, st_i, ord_i, scratch, s);
+    if (!rc) rc = kf_counting_sort_launch(j, (int)m, n, counts, st_j, ord_j, scratch, s);
+    if (!rc && n > 0) {
+        bincount_apply_kernel<<<kf_blocks(n, 128), 128, 0, s>>>(n, st_i, ord_i, st_j, ord_j, fvec, forces);
+        kf_count_launch();
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) { kf_set_error("bincount_apply_kernel", e); rc = 1; }
+    }
+    cudaError_t e = cudaFreeAsync(buf, s);
+    if (!rc && e != cudaSuccess) { kf_set_error("scatter scratch free", e); rc = 1; }
+    return rc;
+}
+
 extern "C" {
 
 int kf_bbox(const double *pos, int n, double *out, void *stream) {
@@ -419,7 +457,13 @@ int kf_grid_cells(const double *pos, int n, const double *r_min, double cell, co
 
 int kf_counting_sort(const int64_t *key, int n, int64_t n_keys, int32_t *counts, int64_t *starts,
                      int64_t *order, int64_t *scratch, void *stream) {
-    cudaStream_t s = (cudaStream_t)stream;
+    return kf_counting_sort_launch(key, n, n_keys, counts, starts, order, scratch, (cudaStream_t)stream);
+}
+
+}  // extern "C"
+
+int kf_counting_sort_launch(const int64_t *key, int n, int64_t n_keys, int32_t *counts, int64_t *starts,
+                            int64_t *order, int64_t *scratch, cudaStream_t s) {
     KF_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * n_keys, s), "memset counts");
     if (n > 0) {
         count_keys_kernel<<<kf_blocks(n, 256), 256, 0, s>>>(key, n, counts);
@@ -439,6 +483,8 @@ int kf_counting_sort(const int64_t *key, int n, int64_t n_keys, int32_t *counts,
     }
     return 0;
 }
+
+extern "C" {
 
 int kf_neighbor_rows_count(const int64_t *cell_index, const int64_t *dims, int n, const int64_t *cell_start,
                            const int32_t *stencil, int n_stencil, int64_t *row_len, void *stream) {
@@ -507,20 +553,29 @@ int kf_classify_pairs(const kf_field_t *f, const int64_t *i, const int64_t *j, i
 int kf_pair_terms(const kf_field_t *f, const double *pos, int n, const int64_t *i, const int64_t *j,
                   const double *d, const double *w, int64_t n_pairs, int kind, double *e_pair, double *mag,
                   double *forces, void *stream) {
-    (void)n;
     if (n_pairs == 0) return 0;
-    pair_terms_kernel<<<kf_blocks(n_pairs, 256), 256, 0, (cudaStream_t)stream>>>(*f, pos, i, j, d, w, n_pairs,
-                                                                                 kind, e_pair, mag, forces);
+    cudaStream_t s = (cudaStream_t)stream;
+    double *fvec = nullptr;
+    if (forces) KF_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&fvec), sizeof(double) * 3 * n_pairs, s), "fvec");
+    pair_terms_kernel<<<kf_blocks(n_pairs, 256), 256, 0, s>>>(*f, pos, i, j, d, w, n_pairs, kind, e_pair, mag, fvec);
     KF_LAUNCH_CHECK("pair_terms_kernel");
-    return 0;
+    if (!forces) return 0;
+    const int rc = scatter_bincount(n, i, j, n_pairs, fvec, forces, s);
+    KF_CUDA(cudaFreeAsync(fvec, s), "fvec free");
+    return rc;
 }
 
-int kf_scatter_pair_forces(const double *pos, const int64_t *i, const int64_t *j, const double *d,
+int kf_scatter_pair_forces(const double *pos, int n, const int64_t *i, const int64_t *j, const double *d,
                            const double *mag, int64_t m, double *forces, void *stream) {
     if (m == 0) return 0;
-    scatter_pair_forces_kernel<<<kf_blocks(m, 256), 256, 0, (cudaStream_t)stream>>>(pos, i, j, d, mag, m, forces);
-    KF_LAUNCH_CHECK("scatter_pair_forces_kernel");
-    return 0;
+    cudaStream_t s = (cudaStream_t)stream;
+    double *fvec = nullptr;
+    KF_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&fvec), sizeof(double) * 3 * m, s), "fvec");
+    pair_fvec_kernel<<<kf_blocks(m, 256), 256, 0, s>>>(pos, i, j, d, mag, m, fvec);
+    KF_LAUNCH_CHECK("pair_fvec_kernel");
+    const int rc = scatter_bincount(n, i, j, m, fvec, forces, s);
+    KF_CUDA(cudaFreeAsync(fvec, s), "fvec free");
+    return rc;
 }
 
 int kf_grid_occupied(const int32_t *counts, const int64_t *starts, int64_t n_keys, int64_t *scratch,

@@ -475,7 +475,7 @@ class Batch:
                 work=z(4, dtype=i32),
                 e_atom=z(B, n, 2), pair_count=z(B, n, dtype=torch.int64),
                 solv_acc=z(B, n, 3, dtype=torch.int64), solv_ovf=z(1 + 2 * B * n, dtype=i32),
-                pair_fj=z(B, n, 6, dtype=torch.int64), cav_atom=z(B, n),
+                pair_fj=z(B, n, 9, dtype=torch.int64), cav_atom=z(B, n),
                 f_exp=z(B, n) if store_sasa else None, a_exp=z(B, n) if store_sasa else None,
                 wrench=z(B, L, 6), side_tot=z(B, max(R, 1), 6), bb_suffix=z(B, max(nbb, 1), 6),
                 tau=z(B, max(D, 1)), energy=z(B, 3),
@@ -675,7 +675,9 @@ def fold(chain, conf, fld, step):
         except ConfigurationError as exc:
             raise ConfigurationError(f"aborted at iteration 0: {exc}") from exc
     K = int(step.max_iters)
-    b = Batch(dc, df, 1, max_records=K, record_theta=True)
+    # one cached workspace per (chain, K): repeated folds reuse its buffers and
+    # hence the CUDA graphs captured on them
+    b = df.batch(dc, 1, max_records=K, record_theta=True)
     s = stream()
     phase = {}
 
@@ -851,9 +853,15 @@ _runner_cache = _IdCache()
 
 def fold_ensemble(chain, confs, fld, step, record_theta: bool = False) -> EnsembleResult:
     confs = list(confs)
-    key = (len(confs), repr(step), bool(record_theta), id(fld))
+    dc = device_chain(chain)
+    df = device_field(fld, dc.n_atoms)
+    # the device tables in the key: a re-uploaded chain or field (mutated arrays,
+    # another pair precision) builds a new runner instead of reusing stale tables
+    key = (len(confs), repr(step), bool(record_theta), id(fld), id(dc), id(df), pair_precision())
     runner = _runner_cache.get(chain, hash(key),
                                lambda: EnsembleRunner(chain, fld, len(confs), step, record_theta=record_theta))
+    if runner.dc is not dc or runner.df is not df:
+        runner = EnsembleRunner(chain, fld, len(confs), step, record_theta=record_theta)
     if runner.df.solvation and step.max_iters > 0:
         check_cav_cutoff(fld.params, fld.config.solvation_cfg, fld.config.cutoffs.cav)
     runner.load([c.theta for c in confs], [c.frozen for c in confs])
@@ -1143,7 +1151,7 @@ def accumulate_pair_forces(n, positions, i, j, d, mag) -> np.ndarray:
         out = torch.zeros(n, 3, dtype=torch.float64, device=p.device)
         if m:
             it, jt, dt, mt = _up(i, np.int64), _up(j, np.int64), _up(d, np.float64), _up(mag, np.float64)
-            _call("kf_scatter_pair_forces", _p(p), _p(it), _p(jt), _p(dt), _p(mt), m, _p(out), _sp())
+            _call("kf_scatter_pair_forces", _p(p), int(n), _p(it), _p(jt), _p(dt), _p(mt), m, _p(out), _sp())
         return out.cpu().numpy()
 
 

@@ -1,0 +1,195 @@
+"""GPU parity of exactly what the bench times, against the reference's own numbers.
+
+The goldens (tests/golden/make_golden_bench.py) are outputs of the real
+``kinefold`` on the bench's inputs:
+
+* the first 32 trajectories of the C5 ensemble (``--init random --seed 1``),
+  one KCM iteration each;
+* the C3 (14,954 atoms) and C4 (99,990 atoms) single-trajectory starts;
+* the C2 start in water.
+
+Each ensemble test runs ``fold_ensemble``'s runner at the batch size that
+selects a given kernel decomposition.  The kernel choice (kf_pairs_launch,
+kf_bin_launch, kf_torque_launch) depends on the batch B:
+
+* B = 1024 is the bench's C5 configuration;
+* B = 384 is the first B with 256-thread torque CTAs;
+* B = 32 is the first fused-binning B.
+
+The comparison covers the first 32 trajectories, against the goldens.  The
+iteration's forces are read from the batch's force buffer (the test hook).
+
+Bars:
+
+* per-atom |dF| <= 1e-5 sum_j |f_aj|, with the reference's own scale;
+* energies <= 1e-6 of (|g_elec| + |g_vdw| + |g_cav|);
+* tau_max <= 1e-5 relative;
+* theta' within 1e-5 kappa;
+* the pair counts P9 and P5 bit-exact, since membership is decided exactly.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import golden
+from oracle import kcm_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+KAPPA = 0.5
+_cache = {}
+
+
+def _P():
+    import paper_1712_05012_b200 as P
+    return P
+
+
+def _system(config, solvation=False):
+    key = (config, solvation)
+    if key not in _cache:
+        from paper_1712_05012_b200 import workloads
+        _cache[key] = workloads.system(config, solvation=solvation)
+    return _cache[key]
+
+
+def _wrapped(a, b):
+    return np.abs((np.asarray(a) - np.asarray(b) + 180.0) % 360.0 - 180.0)
+
+
+def _check_forces(forces, g_forces, g_scale, what):
+    err = np.linalg.norm(forces - g_forces.astype(np.float64), axis=-1)
+    scale = np.maximum(g_scale.astype(np.float64), 1e-300)
+    ratio = err / scale
+    assert np.all(ratio <= 1e-5), (what, float(ratio.max()), np.unravel_index(ratio.argmax(), ratio.shape))
+    return float(ratio.max())
+
+
+def _one_iteration_ensemble(B, solvation=False, iters=1):
+    from paper_1712_05012_b200 import device as DV
+    from paper_1712_05012_b200 import workloads
+    P = _P()
+    ch, params, w, fld = _system("C2", solvation)
+    thetas = workloads.random_thetas(ch, B, seed=1)
+    step = P.StepConfig(kappa=KAPPA, max_iters=iters, torque_tol_rel=0.0, energy_window=0)
+    runner = DV.EnsembleRunner(ch, fld, B, step)
+    runner.load(thetas, np.zeros((B, ch.n_dof), bool))
+    runner.run()
+    forces = runner.batch.t["forces"][:32].cpu().numpy()   # hook: this iteration's forces
+    sa = runner.batch.status_array()
+    return thetas, forces, runner.result(), sa
+
+
+@pytest.mark.parametrize("B", [32, 384, 1024])
+def test_ensemble_iteration_matches_reference(B):
+    """One iteration of the bench ensemble: forces, energies, tau_max, theta'
+    and pair counts of the first 32 trajectories vs kinefold."""
+    g = golden("bench_c2_batch32")
+    thetas, forces, res, sa = _one_iteration_ensemble(B)
+    assert np.array_equal(thetas[:32], g["theta0"])
+    _check_forces(forces, g["forces"], g["scale"], f"B={B}")
+    E = res.energies[:32, 0, :3]
+    scale = np.abs(g["energies"]).sum(axis=1)
+    assert np.all(np.abs(E - g["energies"]).sum(axis=1) <= 1e-6 * scale)
+    tm = res.energies[:32, 0, 3]
+    assert np.all(np.abs(tm - g["tau_max"]) <= 1e-5 * g["tau_max"])
+    assert _wrapped(res.theta[:32], g["theta_next"]).max() <= 1e-5 * KAPPA
+    assert np.array_equal(sa["n_pairs"][:32], g["p9"])
+    assert np.array_equal(sa["n_pairs_vdw"][:32], g["p5"])
+    assert res.iterations.tolist() == [1] * B
+
+
+def test_ensemble_rows_independent_of_batch_position():
+    """The 32 pinned starts placed at the end of a 1024 batch give the same
+    results as at its start: no cross-trajectory leakage in the batched kernels."""
+    from paper_1712_05012_b200 import device as DV
+    from paper_1712_05012_b200 import workloads
+    P = _P()
+    g = golden("bench_c2_batch32")
+    ch, params, w, fld = _system("C2")
+    thetas = workloads.random_thetas(ch, 1024, seed=1)
+    thetas = np.concatenate([thetas[32:], thetas[:32]])
+    step = P.StepConfig(kappa=KAPPA, max_iters=1, torque_tol_rel=0.0, energy_window=0)
+    runner = DV.EnsembleRunner(ch, fld, 1024, step)
+    runner.load(thetas, np.zeros((1024, ch.n_dof), bool))
+    runner.run()
+    forces = runner.batch.t["forces"][-32:].cpu().numpy()
+    _check_forces(forces, g["forces"], g["scale"], "tail rows")
+    sa = runner.batch.status_array()
+    assert np.array_equal(sa["n_pairs"][-32:], g["p9"])
+
+
+@pytest.mark.parametrize("config", ["C3", "C4"])
+def test_single_evaluate_matches_reference(config):
+    """Field.evaluate at the C3 / C4 start (the single-trajectory fp32 paths:
+    C3 full list, C4 half list with fixed-point j forces) vs kinefold."""
+    g = golden(f"bench_{config.lower()}_eval")
+    ch, params, w, fld = _system(config)
+    pos = O.fk(ch, g["theta0"])[3]
+    res = fld.evaluate(pos)
+    _check_forces(res.forces, g["forces"], g["scale"], config)
+    e = np.array([res.energy.g_elec, res.energy.g_vdw, res.energy.g_cav])
+    assert np.abs(e - g["energies"]).sum() <= 1e-6 * np.abs(g["energies"]).sum()
+
+
+@pytest.mark.parametrize("config", ["C3", "C4"])
+def test_single_fold_iteration_matches_reference(config):
+    """One fold() iteration through the graph-replayed single-trajectory loop
+    (multi-CTA FK and torque passes at C3 / C4): record energy, tau_max, theta'."""
+    P = _P()
+    g = golden(f"bench_{config.lower()}_eval")
+    ch, params, w, fld = _system(config)
+    conf = P.Conformation(g["theta0"], np.zeros(ch.n_dof, bool), ch.n_residues)
+    tr = P.fold(ch, conf, fld, P.StepConfig(kappa=KAPPA, max_iters=1, torque_tol_rel=0.0, energy_window=0))
+    r = tr.records[0]
+    E = np.array([r.energy.g_elec, r.energy.g_vdw, r.energy.g_cav])
+    assert np.abs(E - g["energies"]).sum() <= 1e-6 * np.abs(g["energies"]).sum()
+    assert abs(r.tau_max - g["tau_max"]) <= 1e-5 * g["tau_max"]
+    assert _wrapped(tr.final.theta, g["theta_next"]).max() <= 1e-5 * KAPPA
+
+
+def test_water_evaluate_matches_reference():
+    """C2 start in water: pair forces within the bar, solvation exact
+    (f_exp bit-identical, g_cav to 1e-13)."""
+    g = golden("bench_c2_water")
+    ch, params, w, fld = _system("C2", solvation=True)
+    pos = O.fk(ch, g["theta0"])[3]
+    res = fld.evaluate(pos)
+    _, _, extra = O.OracleField(params, w).evaluate(pos)
+    from test_gpu_parity import pair_scale
+    scale = pair_scale(params, w, pos, extra["i"], extra["j"], extra["d"])
+    err = np.linalg.norm(res.forces - g["forces"], axis=1)
+    assert np.all(err <= 1e-5 * np.maximum(scale, 1e-300)), float((err / scale).max())
+    assert np.array_equal(res.sasa.f_exp, g["f_exp"])
+    assert np.array_equal(res.sasa.a_exp, g["a_exp"])
+    assert res.energy.g_cav == pytest.approx(float(g["energies"][2]), rel=1e-13)
+    assert abs(res.energy.g_elec - g["energies"][0]) + abs(res.energy.g_vdw - g["energies"][1]) \
+        <= 1e-6 * np.abs(g["energies"]).sum()
+
+
+@pytest.mark.parametrize("B", [1, 1024])
+def test_water_fold_matches_reference(B):
+    """Two water iterations of the C2 start (B = 1: fold(); B = 1024: the bench's
+    water ensemble, trajectory 0) vs the reference's 2-iteration fold."""
+    g = golden("bench_c2_water")
+    ref_E = g["fold_energies"]
+    scale = np.abs(ref_E).sum(axis=1)
+    if B == 1:
+        P = _P()
+        ch, params, w, fld = _system("C2", solvation=True)
+        conf = P.Conformation(g["theta0"], np.zeros(ch.n_dof, bool), ch.n_residues)
+        tr = P.fold(ch, conf, fld, P.StepConfig(kappa=KAPPA, max_iters=2, torque_tol_rel=0.0, energy_window=0))
+        E = np.array([[r.energy.g_elec, r.energy.g_vdw, r.energy.g_cav] for r in tr.records])
+        tm = np.array([r.tau_max for r in tr.records])
+        final = tr.final.theta
+    else:
+        thetas, _, res, _ = _one_iteration_ensemble(B, solvation=True, iters=2)
+        assert np.array_equal(thetas[0], g["theta0"])
+        E, tm, final = res.energies[0, :, :3], res.energies[0, :, 3], res.theta[0]
+    assert np.all(np.abs(E - ref_E).sum(axis=1) <= 1e-5 * scale)
+    # the start conformation is the reference's bit for bit: its exposure is exact
+    assert abs(E[0, 2] - ref_E[0, 2]) <= 1e-12 * abs(ref_E[0, 2])
+    assert np.all(np.abs(tm - g["fold_tau_max"]) <= 1e-5 * g["fold_tau_max"])
+    assert _wrapped(final, g["fold_final"]).max() <= 1e-5 * KAPPA

@@ -608,3 +608,64 @@ def test_use_hash_false_extent_guard():
     pos[0] += 5000.0
     with pytest.raises(ConfigurationError, match="use_hash=False"):
         _flat(fld).evaluate(pos)
+
+
+_CLOSE_PAIR_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, 'tests'); sys.path.insert(0, '.')
+from conftest import golden, make_system
+from oracle import kcm_oracle as O
+from test_gpu_parity import pair_scale
+g = golden("c2_random")
+ch, params, w, fld = make_system(g["seq"])
+pos = np.array(g["positions"], float)
+a, b = 100, 700                      # far apart along the chain: class 4, weight 1
+pos[a] = pos[b] + np.array([0.02, 0.0, 0.0])
+res = fld.evaluate(pos)
+f_ref, e_ref, extra = O.OracleField(params, w).evaluate(pos)
+scale = pair_scale(params, w, pos, extra["i"], extra["j"], extra["d"])
+assert np.all(np.isfinite(res.forces))
+err = np.linalg.norm(res.forces - f_ref, axis=1)
+assert np.all(err <= 1e-5 * np.maximum(scale, 1e-300)), float((err / scale).max())
+assert abs(res.energy.g_vdw - e_ref[1]) <= 1e-6 * abs(e_ref[1])
+print("ok", float(np.abs(f_ref[a]).max()))
+"""
+
+
+@pytest.mark.parametrize("variant", ["3"])
+def test_half_list_clash_range_pair(variant):
+    """A pair at 0.02 A (vdW force ~1e28, past the half list's two-level fixed
+    point) through the half-list kernel (KFB200_PAIR_KERNEL=3, read once per
+    process, hence the subprocess): forces finite and within the bar of the
+    oracle, Newton's third law kept (the exact path adds +f and -f in fp64)."""
+    import os
+    import subprocess
+    import sys
+    from conftest import ROOT
+    env = dict(os.environ, KFB200_PAIR_KERNEL=variant)
+    out = subprocess.run([sys.executable, "-c", _CLOSE_PAIR_SCRIPT], cwd=ROOT, env=env, capture_output=True,
+                         text=True, timeout=600)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]
+
+
+def test_forcefield_api_deterministic_bincount_order():
+    """elec_forces / vdw_forces scatter in np.bincount order (forcefield.py:169-171):
+    run-to-run deterministic, and accumulate_pair_forces (given magnitudes) is
+    bit-identical to the reference's scatter."""
+    P = _P()
+    g = golden("c2_random")
+    ch, params, w, _ = make_system(g["seq"])
+    grid = P.build_grid(g["positions"])
+    tb = P.build_neighbor_table(grid, 9.0)
+    i, j, d = g["pairs_i"], g["pairs_j"], g["pairs_d"]
+    kv = d <= 5.0
+    _, mv = O.vdw_terms(params, i[kv], j[kv], d[kv], O.pair_weights(w, i[kv], j[kv], "vdw"))
+    ref = O.scatter(len(g["positions"]), g["positions"], i[kv], j[kv], d[kv], mv)
+    a = P.vdw_forces(g["positions"], params, tb, w)
+    b = P.vdw_forces(g["positions"], params, tb, w)
+    assert np.array_equal(a, b)
+    # pair magnitudes use CUDA pow (<= 2 ulp from glibc's): equal to rounding
+    assert np.abs(a - ref).max() <= 1e-12 * np.abs(ref).max()
+    from paper_1712_05012_b200.forcefield import accumulate_pair_forces
+    acc = accumulate_pair_forces(len(g["positions"]), g["positions"], i[kv], j[kv], d[kv], mv)
+    assert np.array_equal(acc, ref)
