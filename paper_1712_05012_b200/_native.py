@@ -12,7 +12,8 @@ import os
 
 from .errors import NativeLibraryError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libkfb200.so")
+LIB_PATH = os.environ.get("KFB200_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib",
+                                                         "libkfb200.so")   # KFB200_LIB: A/B builds
 ABI_VERSION = 11
 
 P = C.c_void_p

@@ -1,0 +1,585 @@
+// Cluster-pair elec + vdW kernel for ensembles (K3c): one CTA per trajectory,
+// the whole trajectory's pair work on chip.
+//
+// Reference: Field.evaluate's force phase (/root/reference/pkg/src/kinefold/
+// kcm.py:110-127) = extract_pairs (forcefield.py:81-89 -> spatial.py:233-241),
+// TreeWeights.weights_for (topology.py:153-195), elec/vdw_pair_quantities
+// (forcefield.py:98-113) and the bincount scatter (forcefield.py:162-172).
+// The pair SET is the reference's exactly (membership decided as in
+// kf_nonbonded.cu: fp32 d^2 outside a 1e-3 A^2 band around each threshold, the
+// reference's fp64 einsum-order d^2 inside it), so the grid the reference
+// builds (spatial.py:83-230) never needs to exist here: any superset of the
+// cut-off pairs gives the same result.
+//
+// Layout.  Atoms keep the chain's index order, which is spatially compact
+// along a polymer: consecutive atoms are bonded or one residue apart.  So no
+// binning pass is needed:
+//   * j-clusters are octets (atoms 8O..8O+7): each has a centre on a 2^-8 A
+//     grid, a half-extent box, and per-atom fp32 offsets from the centre;
+//   * i-clusters are quads (atoms 4Q..4Q+3), with the same kind of frame.
+// Grid centres make the shift between two frames exact in fp32, so a pair's
+// difference vector is (o_i - o_j) + (C_Q - c_O).  Its error is that of the
+// fp32 offsets, <= ~1e-6 A.  Pairs closer than 1 A (or inside a cut-off band)
+// take the exact fp64 path.
+//
+// Work.  Each trajectory is one CTA of 16 warps.  Warps take i-quads from a
+// shared counter.  Per i-quad, lanes test the box distance to the candidate
+// octets O >= Q/2 (half list: every unordered pair once, with j > i inside the
+// diagonal octet), 32 octets per ballot.  Each surviving (quad, octet) is one
+// warp round of 4 x 8 = 32 pairs, lane = (i of the quad, j of the octet):
+//   * the pair math is fp32, branch-free, with predicated selects;
+//   * the force on i accumulates in the lane's registers;
+//   * the force on j (-f) is summed over the 4 i-lanes by xor shuffles and
+//     added to a shared-memory int64 fixed point (2^-28 A units).
+// Integer sums are order-free, so the result does not depend on the schedule.
+// Vacuum rounds skip the vdW term when the boxes are more than 5 A apart.
+// Exact-path pairs add their fp64 forces to the global fixed-point planes
+// (fj_add, shared with kf_nonbonded.cu).  The CTA folds those in only if it
+// wrote any.
+#include "kf_common.cuh"
+
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr double COULOMB_K = 332.06;
+constexpr double MIN_DISTANCE = 1e-6;
+constexpr float FIXF = 268435456.f;             // 2^28: force fixed point (2^-28 A units)
+constexpr double FIX_INV = 1.0 / 268435456.0;
+constexpr double FJ_HI = 4096.0, FJ_HI_INV = 1.0 / 4096.0;
+constexpr double FJ_LO = 1.0 / 268435456.0, FJ_LO_INV = 268435456.0;
+constexpr double FJ_SAT = 4722366482869645213696.0;   // 2^72
+constexpr float FAR = 1.0e6f;                   // offset of padding atoms
+constexpr double GRID = 256.0;                  // frame centres on a 2^-8 A grid
+constexpr double CENTRE_MAX = 32768.0;          // |centre| < 2^15: grid values exact in fp32
+
+struct ClConst {
+    float we[4], wv[4];           // weights by class 1..4
+    float cut2, cutlo, tv2, te2;  // cut-offs (A^2); cutlo = cut2 - band
+    float band, f64_d2;
+    float pre2, pre2v;            // box pretests: cut2 + 1e-2, tv2 + 1e-2
+    float kap_inv;
+    int uniform, w4_nonzero;      // UniformWeights; class-4 weights not both zero
+};
+
+// j-side / exact-path accumulation into the global planes [lo | hi | fp64]
+// (same planes and units as kf_nonbonded.cu's half list, cleared by the reader).
+KF_DEV void cl_fj_add(long long *planes, long long plane, size_t idx, double v) {
+    if (v == 0.0) return;
+    if (!(fabs(v) < FJ_SAT)) {
+        atomicAdd(reinterpret_cast<double *>(planes + 2 * plane + idx), v);
+        return;
+    }
+    const long long hi_u = __double2ll_rn(v * FJ_HI_INV);
+    const double rem = v - (double)hi_u * FJ_HI;
+    const long long lo_u = __double2ll_rn(rem * FJ_LO_INV);
+    if (lo_u) atomicAdd(reinterpret_cast<unsigned long long *>(planes + idx), (unsigned long long)lo_u);
+    if (hi_u) atomicAdd(reinterpret_cast<unsigned long long *>(planes + plane + idx), (unsigned long long)hi_u);
+}
+
+__device__ __noinline__ int cl_slow_class(const kf_field_t &f, int i, int j) {
+    if (!f.tchain[i] || !f.tchain[j] || abs(f.tres[i] - f.tres[j]) > 1) return 4;
+    const int pi = f.tparent[i], gpi = f.tgp[i], ggi = f.tggp[i];
+    const int pj = f.tparent[j], gpj = f.tgp[j], ggj = f.tggp[j];
+    if (pi == j || pj == i) return 1;
+    if (gpi == j || gpj == i || (pi >= 0 && pi == pj)) return 2;
+    if (ggi == j || ggj == i || (gpi >= 0 && gpi == pj) || (gpj >= 0 && gpj == pi)) return 3;
+    return 4;
+}
+
+// The reference's pair in fp64 (forcefield.py:98-113 with kcm.py:115-126's
+// per-term cut-offs): membership from the einsum-order d^2, clash guard,
+// fp64 force into the global planes (+f on i, -f on j).  Returns the counts;
+// energies through e[2].
+__device__ __forceinline__ int2 cl_exact_pair(const kf_field_t &f, const double *pos, int i, int j, int cls,
+                                           long long *planes, long long plane, size_t nb, kf_status_t *st,
+                                           double *e) {
+    const double dx = xsub(pos[3 * i], pos[3 * j]), dy = xsub(pos[3 * i + 1], pos[3 * j + 1]),
+                 dz = xsub(pos[3 * i + 2], pos[3 * j + 2]);
+    const double d2 = d2_einsum(dx, dy, dz);
+    if (d2 > f.cut_pair2) return make_int2(0, 0);
+    const bool ke = d2 <= f.thr_elec2, kv = d2 <= f.thr_vdw2;
+    const double d = sqrt(d2);
+    if (d < MIN_DISTANCE) {
+        atomicMin(&st->dmin_bits, (unsigned long long)__double_as_longlong(d));
+        if (atomicCAS(&st->error, KF_ERR_NONE, KF_ERR_CLASH) == KF_ERR_NONE) st->err_iter = st->iter;
+        return make_int2(ke, kv);
+    }
+    const double we = f.uniform_weights ? f.uniform_value : f.w_elec[cls - 1];
+    const double wv = f.uniform_weights ? f.uniform_value : f.w_vdw[cls - 1];
+    const double inv_d = 1.0 / d;
+    double mag = 0.0;
+    if (ke) {
+        const double num = COULOMB_K * we * f.q[i] * f.q[j];
+        const double ee = f.dielectric_const ? num * inv_d / f.kappa : num * inv_d * inv_d;
+        e[0] += ee;
+        mag += ee * inv_d;
+    }
+    if (kv) {
+        const double eps = sqrt(f.eps[i] * f.eps[j]);
+        const double r = (f.R[i] + f.R[j]) * inv_d;
+        const double r2 = r * r, r6 = r2 * r2 * r2;
+        e[1] += wv * eps * (r6 * r6 - 2.0 * r6);
+        mag += 12.0 * wv * eps * (r6 * r6 - r6) * inv_d;
+    }
+    const double g = mag * inv_d;
+    const double fv[3] = {g * dx, g * dy, g * dz};
+    for (int q = 0; q < 3; ++q) {
+        cl_fj_add(planes, plane, 3 * (nb + i) + q, fv[q]);
+        cl_fj_add(planes, plane, 3 * (nb + j) + q, -fv[q]);
+    }
+    return make_int2(ke, kv);
+}
+
+// Shared-memory layout for trajectories of up to NCAP atoms (a compile-time
+// capacity, so every section offset is an immediate).
+template <int NCAP>
+struct ClLayout {
+    static constexpr int NO = NCAP / 8, NQ = NCAP / 4;
+    static constexpr int OQ = 0;                        // float4 [NCAP]: octet-frame offset xyz, q
+    static constexpr int RS = OQ + 16 * NCAP;           // float2 [NCAP]: R, sqrt(eps)
+    static constexpr int ACC_LO = RS + 8 * NCAP;        // u32 [3 NCAP]: force fixed point, bits 0-19 (+ carries)
+    static constexpr int ACC_MID = ACC_LO + 12 * NCAP;  // u32 [3 NCAP]: bits 20-39 (+ carries)
+    static constexpr int ACC_HI = ACC_MID + 12 * NCAP;  // i32 [3 NCAP]: bits 40- (2^-28 A units overall)
+    static constexpr int OCT_C = ACC_HI + 12 * NCAP;    // float4 [NO]: octet centre
+    static constexpr int OCT_H = OCT_C + 16 * NO;       // float4 [NO]: octet half-extent
+    static constexpr int OCT_RES = OCT_H + 16 * NO;     // int2 [NO]: residue range of the octet
+    static constexpr int Q_C = OCT_RES + 8 * NO;        // float4 [NQ]: quad centre
+    static constexpr int Q_H = Q_C + 16 * NQ;           // float4 [NQ]: quad half-extent
+    static constexpr int TOTAL = Q_H + 16 * NQ;
+};
+constexpr int CL_CAPS[] = {512, 1024, 1536, 2048, 2944};
+constexpr int CL_NCAPS = 5;
+#ifndef CL_WARPS_N
+#define CL_WARPS_N 16
+#endif
+#ifndef CL_MINB
+#define CL_MINB 2   // CTAs per SM asked of ptxas for trajectories of <= 1536 atoms
+#endif
+constexpr int CL_WARPS = CL_WARPS_N;
+
+KF_DEV double grid_round(double v) { return rint(v * GRID) * (1.0 / GRID); }
+
+KF_DEV unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+// Exact fixed-point add without returning atomics: v = a 2^40 + b 2^20 + c with
+// b, c in [0, 2^20) goes to three 32-bit words by fire-and-forget shared REDs.
+// The unsigned low and middle words stay exact for < 4096 adds per element
+// (an atom gets one per i-quad reaching its octet plus its own: <= n/4 + 1, and
+// shared memory limits the cluster path to n < 3k), the signed top word carries
+// |v| < 2^55 (|F| < 2^27 per add).  Integer adds commute: the total is order-free.
+template <int NCAP>
+KF_DEV void acc_add(unsigned base, int k, long long v) {
+    using L = ClLayout<NCAP>;
+    const unsigned c = (unsigned)v & 0xfffffu, b = (unsigned)(v >> 20) & 0xfffffu;
+    const int a = (int)(v >> 40);
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(base + L::ACC_LO + 4 * k), "r"(c) : "memory");
+    if (b) asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(base + L::ACC_MID + 4 * k), "r"(b) : "memory");
+    if (a) asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(base + L::ACC_HI + 4 * k), "r"(a) : "memory");
+}
+
+template <typename T>
+KF_DEV T lds(unsigned addr);
+template <> KF_DEV float4 lds<float4>(unsigned a) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    return v;
+}
+template <> KF_DEV float2 lds<float2>(unsigned a) {
+    float2 v;
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
+    return v;
+}
+
+template <bool DCONST, int NCAP>
+__global__ void __launch_bounds__(CL_WARPS * 32, NCAP <= 1536 ? CL_MINB : 1)
+cluster_pair_kernel(const __grid_constant__ kf_field_t f, const __grid_constant__ ClConst c, int n,
+                    const double *__restrict__ pos_all, double *__restrict__ forces, double *__restrict__ e_atom,
+                    long long *__restrict__ pair_count, kf_status_t *status, long long *__restrict__ planes) {
+    using L = ClLayout<NCAP>;
+    constexpr int CL_THREADS = CL_WARPS * 32;
+    const int b = blockIdx.x;
+    if (status[b].done) return;
+    extern __shared__ __align__(16) unsigned char sm[];
+    __shared__ int next_q, slow_used, extent_bad;
+    __shared__ unsigned cnt_e, cnt_v;
+    __shared__ double2 slow_e[CL_WARPS];
+    __shared__ int quad_res[CL_WARPS][2];    // residue range of the warp's current quad (slow-class test)
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int no = (n + 7) / 8, nq = (n + 3) / 4;
+    const unsigned base = smem_u32(sm);
+    const double *pos = pos_all + 3 * (size_t)b * n;
+    const float4 *apar = reinterpret_cast<const float4 *>(f.atom_par);
+    const int4 *aaux = reinterpret_cast<const int4 *>(f.atom_aux);
+    float4 *s_qc = reinterpret_cast<float4 *>(sm + L::Q_C);
+    float4 *s_qh = reinterpret_cast<float4 *>(sm + L::Q_H);
+    // each quad's (elec, vdW) energy goes to e_atom[quad] (global scratch, read back
+    // in quad order at the end; the totals then sit at atom 0)
+    double *e_q = e_atom + 2 * (size_t)b * n;
+    if (threadIdx.x == 0) { next_q = CL_WARPS; slow_used = 0; extent_bad = 0; cnt_e = 0; cnt_v = 0; }
+
+    // ---- 1. frames: octet and quad grid centres, half-extent boxes, offsets ----
+    for (int a0 = 32 * warp; a0 < 8 * no; a0 += 32 * CL_WARPS) {
+        const int a = a0 + lane;
+        const bool ok = a < n;
+        double x = 0.0, y = 0.0, z = 0.0;
+        if (ok) { x = pos[3 * a]; y = pos[3 * a + 1]; z = pos[3 * a + 2]; }
+        double lo[3] = {ok ? x : INFINITY, ok ? y : INFINITY, ok ? z : INFINITY};
+        double hi[3] = {ok ? x : -INFINITY, ok ? y : -INFINITY, ok ? z : -INFINITY};
+        int rlo = ok ? aaux[a].y : 0x7fffffff, rhi = ok ? aaux[a].y : -0x7fffffff;
+        // every octet / quad below no / nq holds at least one atom; lanes past
+        // the last one only take part in the shuffles
+        const bool in_oct = a < 8 * no, in_quad = (a >> 2) < nq;
+        bool bad = false;
+#pragma unroll
+        for (int m = 1; m < 8; m <<= 1) {
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                lo[q] = fmin(lo[q], __shfl_xor_sync(FULL, lo[q], m));
+                hi[q] = fmax(hi[q], __shfl_xor_sync(FULL, hi[q], m));
+            }
+            rlo = min(rlo, __shfl_xor_sync(FULL, rlo, m));
+            rhi = max(rhi, __shfl_xor_sync(FULL, rhi, m));
+            if (m == 2 && (lane & 3) == 0 && in_quad) {   // quad frame (lanes 4k..4k+3 reduced)
+                float cq[3], hq[3];
+#pragma unroll
+                for (int q = 0; q < 3; ++q) {
+                    const double ctr = grid_round(0.5 * (lo[q] + hi[q]));
+                    bad |= !(fabs(ctr) < CENTRE_MAX);
+                    cq[q] = (float)ctr;
+                    hq[q] = __double2float_ru(fmax(hi[q] - ctr, ctr - lo[q]));
+                }
+                s_qc[a >> 2] = make_float4(cq[0], cq[1], cq[2], 0.f);
+                s_qh[a >> 2] = make_float4(hq[0], hq[1], hq[2], 0.f);
+            }
+        }
+        double ctr[3];
+        float hx[3];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            ctr[q] = grid_round(0.5 * (lo[q] + hi[q]));
+            hx[q] = __double2float_ru(fmax(hi[q] - ctr[q], ctr[q] - lo[q]));
+        }
+        bad |= in_oct && !(fabs(ctr[0]) < CENTRE_MAX && fabs(ctr[1]) < CENTRE_MAX && fabs(ctr[2]) < CENTRE_MAX);
+        if (bad) extent_bad = 1;
+        const float4 par = ok ? apar[a] : make_float4(0.f, 0.f, 0.f, 0.f);
+        if (in_oct) {
+            reinterpret_cast<float4 *>(sm + L::OQ)[a] =
+                ok ? make_float4(__double2float_rn(x - ctr[0]), __double2float_rn(y - ctr[1]),
+                                 __double2float_rn(z - ctr[2]), par.x)
+                   : make_float4(FAR, FAR, FAR, 0.f);
+            reinterpret_cast<float2 *>(sm + L::RS)[a] = make_float2(par.y, par.z);
+        }
+        if ((lane & 7) == 0 && in_oct) {
+            const int O = a >> 3;
+            reinterpret_cast<float4 *>(sm + L::OCT_C)[O] = make_float4((float)ctr[0], (float)ctr[1], (float)ctr[2], 0.f);
+            reinterpret_cast<float4 *>(sm + L::OCT_H)[O] = make_float4(hx[0], hx[1], hx[2], 0.f);
+            reinterpret_cast<int2 *>(sm + L::OCT_RES)[O] = make_int2(rlo, rhi);
+        }
+    }
+    for (int k = threadIdx.x; k < 9 * NCAP; k += CL_THREADS)   // the three adjacent word planes
+        reinterpret_cast<unsigned *>(sm + L::ACC_LO)[k] = 0u;
+    __syncthreads();
+    if (extent_bad) {   // centres past 2^15 A: the exact-shift frames do not hold
+        if (threadIdx.x == 0 && atomicCAS(&status[b].error, KF_ERR_NONE, KF_ERR_EXTENT) == KF_ERR_NONE)
+            status[b].err_iter = status[b].iter;
+        return;
+    }
+
+    // ---- 2. i-quads against candidate octets --------------------------------
+    const int ii = lane & 3, js = lane >> 2;
+    int Q = warp;
+    while (Q < nq) {
+        const int i = 4 * Q + ii;
+        const bool vi = i < n;
+        float oi0 = -FAR, oi1 = -FAR, oi2 = -FAR, qK4 = 0.f, ws4 = 0.f, Ri = 0.f;
+        bool slow_i = false;
+        {
+            const float4 cq4 = s_qc[Q];
+            if (vi) {
+                oi0 = __double2float_rn(pos[3 * i] - (double)cq4.x);
+                oi1 = __double2float_rn(pos[3 * i + 1] - (double)cq4.y);
+                oi2 = __double2float_rn(pos[3 * i + 2] - (double)cq4.z);
+                const float4 pi4 = apar[i];
+                qK4 = (float)COULOMB_K * pi4.x * c.we[3];   // K q_i w_elec(4)
+                ws4 = pi4.z * c.wv[3];                      // sqrt(eps_i) w_vdw(4)
+                Ri = pi4.y;
+                slow_i = aaux[i].w != 0;
+            }
+        }
+        // class lookups only for octets within the 64-atom window of the quad
+        // (O <= o_near), or near a slow atom's residue (a tree partner beyond the
+        // window, class_window in device.py): then the quad's residue range
+        const int o_near = c.uniform ? -1 : (4 * Q + 34) >> 3;
+        const bool q_slow = !c.uniform && __any_sync(FULL, slow_i);
+        if (q_slow) {
+            int r = vi ? aaux[i].y : 0x7fffffff, h = vi ? aaux[i].y : -0x7fffffff;
+            r = min(r, __shfl_xor_sync(FULL, r, 1)); r = min(r, __shfl_xor_sync(FULL, r, 2));
+            h = max(h, __shfl_xor_sync(FULL, h, 1)); h = max(h, __shfl_xor_sync(FULL, h, 2));
+            if (lane == 0) { quad_res[warp][0] = r; quad_res[warp][1] = h; }
+        }
+        float fx = 0.f, fy = 0.f, fz = 0.f, ee = 0.f, ev = 0.f;
+        int ce = 0, cv = 0;
+        if (lane == 0) slow_e[warp] = make_double2(0.0, 0.0);   // exact-path energies of this quad
+        __syncwarp();
+        const int O0 = Q >> 1;
+        for (int ob = O0; ob < no; ob += 32) {
+            // box pretest of 32 candidate octets at once
+            const int Oc = ob + lane;
+            float bd2 = 3.0e38f;
+            if (Oc < no) {
+                const float4 oc = lds<float4>(base + L::OCT_C + 16 * Oc), oh = lds<float4>(base + L::OCT_H + 16 * Oc);
+                const float4 cq = s_qc[Q], hq = s_qh[Q];
+                const float gx = fmaxf(fabsf(cq.x - oc.x) - (hq.x + oh.x), 0.f);
+                const float gy = fmaxf(fabsf(cq.y - oc.y) - (hq.y + oh.y), 0.f);
+                const float gz = fmaxf(fabsf(cq.z - oc.z) - (hq.z + oh.z), 0.f);
+                bd2 = gx * gx + gy * gy + gz * gz;
+            }
+            unsigned cand = __ballot_sync(FULL, bd2 <= c.pre2);
+            const unsigned vmask = __ballot_sync(FULL, bd2 <= c.pre2v);
+            while (cand) {
+                const int t = __ffs(cand) - 1;
+                cand &= cand - 1u;
+                const int O = ob + t;
+                const float4 cq = s_qc[Q];
+                const float4 oc = lds<float4>(base + L::OCT_C + 16 * O);
+                const int j = 8 * O + js;
+                const float4 oj = lds<float4>(base + L::OQ + 16 * j);
+                const float2 rj = lds<float2>(base + L::RS + 8 * j);
+                const float dx = (oi0 - oj.x) + (cq.x - oc.x);   // frame shift exact
+                const float dy = (oi1 - oj.y) + (cq.y - oc.y);
+                const float dz = (oi2 - oj.z) + (cq.z - oc.z);
+                const float d2 = dx * dx + dy * dy + dz * dz;
+                bool live = vi;
+                if (O == O0) live &= j > i;              // diagonal octet: each pair once
+                float qq = qK4 * oj.w, weps = ws4 * rj.y;
+                bool wnz = c.w4_nonzero;
+                int cls = 4;
+                if (O <= o_near ||
+                    (q_slow && reinterpret_cast<const int2 *>(sm + L::OCT_RES)[O].x <= quad_res[warp][1] + 1 &&
+                     reinterpret_cast<const int2 *>(sm + L::OCT_RES)[O].y >= quad_res[warp][0] - 1)) {
+                    const int off = j - i + 32;
+                    if ((unsigned)off < 64u) {
+                        const int4 cm = reinterpret_cast<const int4 *>(f.class_map)[vi ? i : 0];
+                        const unsigned wd = off < 32 ? (off < 16 ? cm.x : cm.y) : (off < 48 ? cm.z : cm.w);
+                        cls = 4 - (int)((wd >> (2 * (off & 15))) & 3u);
+                    } else if (live && slow_i && j < n) {
+                        cls = cl_slow_class(f, i, j);
+                    }
+                    const float we = c.we[cls - 1], wv = c.wv[cls - 1];
+                    const float4 pi4 = apar[vi ? i : 0];
+                    qq = (float)COULOMB_K * pi4.x * we * oj.w;
+                    weps = wv * pi4.z * rj.y;
+                    wnz = (we != 0.f) | (wv != 0.f);
+                }
+                // exact path: inside a threshold band, or closer than f64_d2 with a
+                // nonzero weight (or at clash range whatever the weight)
+                const float dev = fminf(fminf(fabsf(d2 - c.cut2), fabsf(d2 - c.tv2)), fabsf(d2 - c.te2));
+                const bool exact = live && ((dev <= c.band) | ((d2 < c.f64_d2) & (wnz | (d2 < 1e-4f))));
+                if (__any_sync(FULL, exact)) {
+                    double se[2] = {0.0, 0.0};
+                    if (exact) {
+                        const int2 k2 = cl_exact_pair(f, pos, i, j, cls, planes, 3LL * gridDim.x * n,
+                                                      (size_t)b * n, status + b, se);
+                        ce += k2.x; cv += k2.y;
+                    }
+                    // fixed lane tree, then in round order: deterministic
+                    const double te = warp_sum(se[0]), tv = warp_sum(se[1]);
+                    if (lane == 0) {
+                        slow_e[warp].x += te; slow_e[warp].y += tv;
+                        slow_used = 1;
+                    }
+                }
+                const bool fast = live && !exact && d2 < c.cutlo;
+                if (!__any_sync(FULL, fast)) continue;
+                float inv_r;
+                asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(inv_r) : "f"(d2));
+                const float inv_r2 = inv_r * inv_r;
+                const bool ke = fast && d2 <= c.te2;
+                const float e = DCONST ? qq * c.kap_inv * inv_r : qq * inv_r2;
+                float g = ke ? e * inv_r2 : 0.f;
+                ee += ke ? e : 0.f;
+                ce += ke;
+                if ((vmask >> t) & 1u) {   // boxes within the vdW reach
+                    const bool kv = fast && d2 <= c.tv2;
+                    const float D = Ri + rj.x;
+                    const float sr = D * D * inv_r2;
+                    const float s3 = sr * sr * sr;
+                    const float s6 = s3 * s3;
+                    ev += kv ? weps * (s6 - 2.f * s3) : 0.f;
+                    g = kv ? __fmaf_rn(12.f * weps * (s6 - s3), inv_r2, g) : g;
+                    cv += kv;
+                }
+                const float gx = g * dx, gy = g * dy, gz = g * dz;
+                fx += gx; fy += gy; fz += gz;
+                // force on j = -(sum over the quad's 4 lanes)
+                float tx = gx, ty = gy, tz = gz;
+                tx += __shfl_xor_sync(FULL, tx, 1); ty += __shfl_xor_sync(FULL, ty, 1); tz += __shfl_xor_sync(FULL, tz, 1);
+                tx += __shfl_xor_sync(FULL, tx, 2); ty += __shfl_xor_sync(FULL, ty, 2); tz += __shfl_xor_sync(FULL, tz, 2);
+                const float v = ii == 0 ? tx : (ii == 1 ? ty : tz);
+                if (ii < 3 && j < n && v != 0.f) acc_add<NCAP>(base, 3 * j + ii, __float2ll_rn(-v * FIXF));
+            }
+        }
+        // i forces: sum over the 8 j-lanes of each i, then into the fixed point
+#pragma unroll
+        for (int m = 4; m < 32; m <<= 1) {
+            fx += __shfl_xor_sync(FULL, fx, m);
+            fy += __shfl_xor_sync(FULL, fy, m);
+            fz += __shfl_xor_sync(FULL, fz, m);
+        }
+        {
+            const float v = js == 0 ? fx : (js == 1 ? fy : fz);
+            if (vi && js < 3 && v != 0.f) acc_add<NCAP>(base, 3 * i + js, __float2ll_rn(v * FIXF));
+        }
+        // the quad's energies (fixed xor tree: deterministic) and counts (order-free)
+#pragma unroll
+        for (int m = 16; m > 0; m >>= 1) {
+            ee += __shfl_xor_sync(FULL, ee, m);
+            ev += __shfl_xor_sync(FULL, ev, m);
+        }
+        const int tce = __reduce_add_sync(FULL, ce), tcv = __reduce_add_sync(FULL, cv);
+        __syncwarp();
+        if (lane == 0) {
+            e_q[2 * Q] = (double)ee + slow_e[warp].x;
+            e_q[2 * Q + 1] = (double)ev + slow_e[warp].y;
+            atomicAdd(&cnt_e, (unsigned)tce);
+            atomicAdd(&cnt_v, (unsigned)tcv);
+            Q = atomicAdd(&next_q, 1);
+        }
+        Q = __shfl_sync(FULL, Q, 0);
+    }
+    __syncthreads();
+
+    // ---- 3. forces out (+ the exact-path planes if any), energies, counts ----
+    const bool with_planes = slow_used != 0;
+    const size_t nb = (size_t)b * n;
+    const long long plane = 3LL * gridDim.x * n;
+    const unsigned *acc_lo = reinterpret_cast<const unsigned *>(sm + L::ACC_LO);
+    const unsigned *acc_mid = reinterpret_cast<const unsigned *>(sm + L::ACC_MID);
+    const int *acc_hi = reinterpret_cast<const int *>(sm + L::ACC_HI);
+    for (int k = threadIdx.x; k < 3 * n; k += CL_THREADS) {
+        const long long a64 = ((long long)acc_hi[k] << 40) + ((long long)acc_mid[k] << 20) + (long long)acc_lo[k];
+        double v = (double)a64 * FIX_INV;
+        if (with_planes) {
+            long long *p = planes + 3 * nb + k;
+            double *big = reinterpret_cast<double *>(planes + 2 * plane) + 3 * nb + k;
+            const long long lo = p[0], hi = p[plane];
+            const double bg = *big;
+            if (lo || hi || bg != 0.0) {
+                v += ((double)hi * FJ_HI + (double)lo * FJ_LO) + bg;
+                p[0] = 0; p[plane] = 0; *big = 0.0;
+            }
+        }
+        forces[3 * nb + k] = v;
+    }
+    if (warp == 0) {
+        double de = 0.0, dv = 0.0;
+        for (int q = lane; q < nq; q += 32) { de += e_q[2 * q]; dv += e_q[2 * q + 1]; }
+        de = warp_sum(de);
+        dv = warp_sum(dv);
+        if (lane == 0) {   // doubled: the energy reduction halves (full-list convention)
+            e_atom[2 * nb] = 2.0 * de;
+            e_atom[2 * nb + 1] = 2.0 * dv;
+            pair_count[nb] = 2LL * cnt_e + ((2LL * cnt_v) << 32);
+        }
+    }
+}
+
+template <int NCAP>
+inline int launch_cap(bool dconst, const kf_field_t *f, const ClConst &c, kf_batch_t *w, int n, cudaStream_t s) {
+    constexpr size_t smem = ClLayout<NCAP>::TOTAL;
+    auto kern = dconst ? cluster_pair_kernel<true, NCAP> : cluster_pair_kernel<false, NCAP>;
+    static bool opted[2] = {false, false};
+    if (!opted[dconst]) {
+        KF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "cluster smem");
+        opted[dconst] = true;
+    }
+    kern<<<w->B, CL_WARPS * 32, smem, s>>>(*f, c, n, w->pos, w->forces, w->e_atom, w->pair_count, w->status,
+                                          w->pair_fj);
+    KF_LAUNCH_CHECK("cluster_pair_kernel");
+    return 0;
+}
+
+// On error only, cluster path (no cell table was built): smallest (i, j), i < j,
+// among pairs at the minimum distance, by a direct sweep (forcefield.py:84-88).
+__global__ void cl_clash_report_kernel(kf_field_t f, int B, int n, const double *__restrict__ pos_all,
+                                       kf_status_t *status) {
+    const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid >= (long long)B * n) return;
+    const int b = (int)(gid / n), i = (int)(gid % n);
+    if (status[b].error != KF_ERR_CLASH) return;
+    const double *pos = pos_all + 3 * (size_t)b * n;
+    const unsigned long long target = status[b].dmin_bits;
+    for (int j = i + 1; j < n; ++j) {
+        const double d2 = d2_einsum(xsub(pos[3 * i], pos[3 * j]), xsub(pos[3 * i + 1], pos[3 * j + 1]),
+                                    xsub(pos[3 * i + 2], pos[3 * j + 2]));
+        if (d2 > f.cut_pair2) continue;
+        if ((unsigned long long)__double_as_longlong(sqrt(d2)) == target)
+            atomicMin(reinterpret_cast<unsigned long long *>(&status[b].clash_key),
+                      ((unsigned long long)i << 32) | (unsigned)j);
+    }
+}
+
+}  // namespace
+
+int kf_cluster_clash_report_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s) {
+    const long long total = (long long)w->B * n;
+    cl_clash_report_kernel<<<kf_blocks(total, 128), 128, 0, s>>>(*f, w->B, n, w->pos, w->status);
+    KF_LAUNCH_CHECK("cl_clash_report_kernel");
+    return 0;
+}
+
+// The cluster path applies to fp32 pair math on ensembles whose trajectories fit
+// one CTA's shared memory; KFB200_CLUSTER=0 disables it, KFB200_CLUSTER_MIN_B
+// moves the batch threshold (measurements).  kf_bin_launch, kf_pairs_launch and
+// kf_torque_launch all consult this, so one launch configuration is consistent.
+#ifndef CL_MIN_B
+#define CL_MIN_B 96
+#endif
+
+int kf_cluster_path(const kf_field_t *f, const kf_batch_t *w, int n) {
+    static int env_on = -1, env_min_b = -1;
+    static size_t smem_max = 0;
+    if (env_on < 0) {
+        const char *e = getenv("KFB200_CLUSTER");
+        env_on = e ? atoi(e) : 1;
+        const char *m = getenv("KFB200_CLUSTER_MIN_B");
+        env_min_b = m ? atoi(m) : CL_MIN_B;
+        int dev = 0, v = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        smem_max = (size_t)v;
+    }
+    if (!f || !w || !env_on || f->precision || f->flat || !w->pair_fj || n < 1) return 0;
+    if (w->B < env_min_b) return 0;
+    return n <= CL_CAPS[CL_NCAPS - 1] && (size_t)ClLayout<2944>::TOTAL <= smem_max ? 1 : 0;
+}
+
+int kf_cluster_pairs_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s) {
+    ClConst c;
+    for (int q = 0; q < 4; ++q) {
+        c.we[q] = (float)(f->uniform_weights ? f->uniform_value : f->w_elec[q]);
+        c.wv[q] = (float)(f->uniform_weights ? f->uniform_value : f->w_vdw[q]);
+    }
+    c.band = 1e-3f;
+    c.cut2 = (float)f->cut_pair2;
+    c.cutlo = c.cut2 - c.band;
+    c.tv2 = (float)f->thr_vdw2;
+    c.te2 = (float)f->thr_elec2;
+    c.pre2 = (float)(f->cut_pair2 + 1e-2);
+    c.pre2v = (float)(f->thr_vdw2 + 1e-2);
+    static float f64_below = -1.f;   // KFB200_PAIR_F64_BELOW (A), as kf_nonbonded.cu
+    if (f64_below < 0.f) {
+        const char *env = getenv("KFB200_PAIR_F64_BELOW");
+        f64_below = env ? (float)atof(env) : 1.0f;
+    }
+    c.f64_d2 = f64_below * f64_below;
+    c.kap_inv = f->dielectric_const ? (float)(1.0 / f->kappa) : 1.0f;
+    c.uniform = f->uniform_weights;
+    c.w4_nonzero = (c.we[3] != 0.f) || (c.wv[3] != 0.f);
+    const bool dc = f->dielectric_const != 0;
+    if (n <= 512) return launch_cap<512>(dc, f, c, w, n, s);
+    if (n <= 1024) return launch_cap<1024>(dc, f, c, w, n, s);
+    if (n <= 1536) return launch_cap<1536>(dc, f, c, w, n, s);
+    if (n <= 2048) return launch_cap<2048>(dc, f, c, w, n, s);
+    return launch_cap<2944>(dc, f, c, w, n, s);
+}

@@ -572,7 +572,11 @@ bin_flat_kernel(const __grid_constant__ kf_field_t f, int B, int n, int chunk, c
 
 }  // namespace
 
+int kf_cluster_path(const kf_field_t *f, const kf_batch_t *w, int n);
+
 int kf_bin_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s) {
+    // the cluster-pair kernel needs no cell table; only the solvation pass does
+    if (!f->solvation && kf_cluster_path(f, w, n)) return 0;
     const int B = w->B, H = 1 << f->hash_bits;
     if (f->flat) {   // FieldConfig(use_hash=False)
         bin_flat_kernel<<<B, FL_THREADS, 0, s>>>(

@@ -853,7 +853,13 @@ int resident_grid(K kern, int threads, size_t dyn) {
 
 }  // namespace
 
+int kf_cluster_path(const kf_field_t *f, const kf_batch_t *w, int n);
+int kf_cluster_pairs_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s);
+int kf_cluster_clash_report_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s);
+
 int kf_pairs_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s) {
+    // ensembles with fp32 pair math: the cluster-pair kernel (kf_cluster.cu)
+    if (kf_cluster_path(f, w, n)) return kf_cluster_pairs_launch(f, w, n, s);
     if (g_sms == 0) {
         int dev = 0;
         cudaGetDevice(&dev);
@@ -939,6 +945,7 @@ int kf_pairs_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s) {
 }
 
 int kf_clash_report_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s) {
+    if (kf_cluster_path(f, w, n)) return kf_cluster_clash_report_launch(f, w, n, s);
     const long long total = (long long)w->B * n;
     clash_report_kernel<<<kf_blocks(total, 128), 128, 0, s>>>(
         *f, w->B, n, w->cell_key, w->cell_cnt, w->cell_start, w->atom_slot,

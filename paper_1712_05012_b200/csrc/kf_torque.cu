@@ -180,7 +180,7 @@ struct TorqueArgs {
 template <int NT>
 __global__ void __launch_bounds__(NT)
 torque_step_kernel(kf_chain_t c, kf_field_t f, TorqueArgs ta, kf_batch_t w, kf_step_t step, int mode,
-                   int fuse_wrench) {
+                   int fuse_wrench, int e_first) {
     kf_pdl_wait();      // after the predecessor (programmatic launch: single trajectories)
     kf_pdl_trigger();
     const int b = blockIdx.x;
@@ -254,9 +254,11 @@ torque_step_kernel(kf_chain_t c, kf_field_t f, TorqueArgs ta, kf_batch_t w, kf_s
     const int n = c.n_atoms;
     const double *ea = w.e_atom + (size_t)b * n * 2;
     double se = 0.0, sv = 0.0, sc = 0.0, sp = 0.0, sp5 = 0.0;
+    // (e_first: the cluster-pair kernel left its totals at atom 0 only)
     for (int a = threadIdx.x; a < n; a += blockDim.x) {
-        se += ea[2 * a]; sv += ea[2 * a + 1];
         if (f.solvation) sc += w.cav_atom[(size_t)b * n + a];
+        if (e_first && a) continue;
+        se += ea[2 * a]; sv += ea[2 * a + 1];
         const long long pc = w.pair_count[(size_t)b * n + a];
         sp += (double)(pc & 0xffffffffLL);
         sp5 += (double)(pc >> 32);
@@ -357,7 +359,7 @@ torque_seg_kernel(kf_chain_t c, TorqueArgs ta, kf_batch_t w, int n_seg) {
 }
 
 __global__ void __launch_bounds__(TQ_THREADS)
-torque_seg_project_kernel(kf_chain_t c, kf_field_t f, TorqueArgs ta, kf_batch_t w, int n_seg) {
+torque_seg_project_kernel(kf_chain_t c, kf_field_t f, TorqueArgs ta, kf_batch_t w, int n_seg, int e_first) {
     const int g = blockIdx.x, b = blockIdx.y;
     const kf_status_t *st = w.status + b;
     if (st->done || st->error) return;
@@ -387,8 +389,9 @@ torque_seg_project_kernel(kf_chain_t c, kf_field_t f, TorqueArgs ta, kf_batch_t 
     const double *ea = w.e_atom + (size_t)b * n * 2;
     double se = 0.0, sv = 0.0, scv = 0.0, sp = 0.0, sp5 = 0.0;
     for (int a = a0 + threadIdx.x; a < a1; a += blockDim.x) {
-        se += ea[2 * a]; sv += ea[2 * a + 1];
         if (f.solvation) scv += w.cav_atom[(size_t)b * n + a];
+        if (e_first && a) continue;
+        se += ea[2 * a]; sv += ea[2 * a + 1];
         const long long pc = w.pair_count[(size_t)b * n + a];
         sp += (double)(pc & 0xffffffffLL);
         sp5 += (double)(pc >> 32);
@@ -462,6 +465,8 @@ __global__ void kcm_step_api_kernel(const double *tau, const double *theta, cons
 
 }  // namespace
 
+int kf_cluster_path(const kf_field_t *f, const kf_batch_t *w, int n);
+
 int kf_wrench_launch(const kf_chain_t *c, int B, const double *pos, const double *forces, double *wrench,
                      const kf_status_t *status, cudaStream_t s) {
     const long long total = (long long)B * c->n_links;
@@ -479,12 +484,13 @@ int kf_torque_launch(const kf_chain_t *c, const kf_field_t *f, kf_batch_t *w, co
     kf_field_t fz{};
     if (f) fz = *f;
     const int n_seg = (c->n_bb + TQ_SEG - 1) / TQ_SEG;
+    const int e_first = (f && mode != 0) ? kf_cluster_path(f, w, c->n_atoms) : 0;
     if (mode == 1 && n_seg > 1 && w->B * n_seg <= 4 * 148 && w->fk_scratch && bb_suffix) {
         if (fuse_wrench &&
             kf_wrench_launch(c, w->B, w->pos, w->forces, const_cast<double *>(wrench), w->status, s)) return 1;
         torque_seg_kernel<<<dim3(n_seg, w->B), TQ_THREADS, 0, s>>>(*c, ta, *w, n_seg);
         KF_LAUNCH_CHECK("torque_seg_kernel");
-        torque_seg_project_kernel<<<dim3(n_seg, w->B), TQ_THREADS, 0, s>>>(*c, fz, ta, *w, n_seg);
+        torque_seg_project_kernel<<<dim3(n_seg, w->B), TQ_THREADS, 0, s>>>(*c, fz, ta, *w, n_seg, e_first);
         KF_LAUNCH_CHECK("torque_seg_project_kernel");
         torque_seg_finish_kernel<<<w->B, 32, 0, s>>>(*c, ta, *w, st, n_seg);
         KF_LAUNCH_CHECK("torque_seg_finish_kernel");
@@ -515,7 +521,7 @@ int kf_torque_launch(const kf_chain_t *c, const kf_field_t *f, kf_batch_t *w, co
         }
     }
     (void)kf_launch(w->B < KF_PDL_B, kern, dim3(w->B), dim3(wide ? TQ_THREADS : TQ_THREADS / 2), fuse ? wsm : 0, s, *c, fz, ta,
-                    *w, st, mode, fuse ? 1 : 0);
+                    *w, st, mode, fuse ? 1 : 0, e_first);
     KF_LAUNCH_CHECK("torque_step_kernel");
     return 0;
 }
