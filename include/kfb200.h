@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define KF_ABI_VERSION 11
+#define KF_ABI_VERSION 12
 
 /* ---- static chain tables (uploaded once per chain) ------------------------
  * Links are in the reference's topological order (parent < index, ground = 0),
@@ -101,6 +101,11 @@ typedef struct {
     const float *atom_par;          /* [n][4]: q, R, sqrt(eps), 0 (fp32)           */
     const int32_t *atom_aux;        /* [n][4]: atom, residue, chain flag, class_slow (0 if uniform) */
     double r_off_max;               /* max R_off over atoms (solvation cell pruning) */
+    /* cluster-pair kernel (kf_cluster.cu): for quad Q (atoms 4Q..4Q+3) and the
+       octets O = Q/2 + k, k = 0..4 (atoms 8O..8O+7), the 2-bit (4 - class) codes
+       of the 32 pairs (i = 4Q + l%4, j = 8O + l/4) at bits 2l; host-built from the
+       bond tree (topology.py:153-178).  NULL for UniformWeights.               */
+    const unsigned long long *class_codes;   /* [ceil(n/4)][5] */
 } kf_field_t;
 
 /* ---- per-trajectory status block ----------------------------------------- */

@@ -58,7 +58,8 @@ struct ClConst {
     float band, f64_d2;
     float pre2, pre2v;            // box pretests: cut2 + 1e-2, tv2 + 1e-2
     float kap_inv;
-    int uniform, w4_nonzero;      // UniformWeights; class-4 weights not both zero
+    float kwe[4];                 // K w_elec by class
+    int uniform, wnz_mask;        // UniformWeights; bit c-1: class c has a nonzero weight
 };
 
 // j-side / exact-path accumulation into the global planes [lo | hi | fp64]
@@ -130,6 +131,14 @@ __device__ __forceinline__ int2 cl_exact_pair(const kf_field_t &f, const double 
     return make_int2(ke, kv);
 }
 
+#ifndef CL_WARPS_N
+#define CL_WARPS_N 16
+#endif
+#ifndef CL_MINB
+#define CL_MINB 2   // CTAs per SM asked of ptxas for trajectories of <= 1536 atoms
+#endif
+constexpr int CL_WARPS = CL_WARPS_N;
+
 // Shared-memory layout for trajectories of up to NCAP atoms (a compile-time
 // capacity, so every section offset is an immediate).
 template <int NCAP>
@@ -142,20 +151,10 @@ struct ClLayout {
     static constexpr int ACC_HI = ACC_MID + 12 * NCAP;  // i32 [3 NCAP]: bits 40- (2^-28 A units overall)
     static constexpr int OCT_C = ACC_HI + 12 * NCAP;    // float4 [NO]: octet centre
     static constexpr int OCT_H = OCT_C + 16 * NO;       // float4 [NO]: octet half-extent
-    static constexpr int OCT_RES = OCT_H + 16 * NO;     // int2 [NO]: residue range of the octet
-    static constexpr int Q_C = OCT_RES + 8 * NO;        // float4 [NQ]: quad centre
-    static constexpr int Q_H = Q_C + 16 * NQ;           // float4 [NQ]: quad half-extent
-    static constexpr int TOTAL = Q_H + 16 * NQ;
+    static constexpr int TOTAL = OCT_H + 16 * NO;
 };
 constexpr int CL_CAPS[] = {512, 1024, 1536, 2048, 2944};
 constexpr int CL_NCAPS = 5;
-#ifndef CL_WARPS_N
-#define CL_WARPS_N 16
-#endif
-#ifndef CL_MINB
-#define CL_MINB 2   // CTAs per SM asked of ptxas for trajectories of <= 1536 atoms
-#endif
-constexpr int CL_WARPS = CL_WARPS_N;
 
 KF_DEV double grid_round(double v) { return rint(v * GRID) * (1.0 / GRID); }
 
@@ -177,17 +176,26 @@ KF_DEV void acc_add(unsigned base, int k, long long v) {
     if (a) asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(base + L::ACC_HI + 4 * k), "r"(a) : "memory");
 }
 
-template <typename T>
-KF_DEV T lds(unsigned addr);
-template <> KF_DEV float4 lds<float4>(unsigned a) {
+
+KF_DEV float4 lds4(unsigned a) {
     float4 v;
-    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
     return v;
 }
-template <> KF_DEV float2 lds<float2>(unsigned a) {
+KF_DEV float2 lds2(unsigned a) {
     float2 v;
-    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
+    asm("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
     return v;
+}
+
+// Class of pair (i, j) in a round of quad Q x octet O that may hold a class < 4
+// pair: the host-built codes for the 5 octets of the 64-atom window, else the
+// bond-tree test for atoms with a partner beyond the window (class_window).
+__device__ __noinline__ int near_class(const kf_field_t &f, int Q, int O, int lane, bool live, int i, int j) {
+    const int k = O - (Q >> 1);
+    if (k <= 4) return 4 - (int)((f.class_codes[5 * Q + k] >> (2 * lane)) & 3ull);
+    if (live && f.class_slow[i]) return cl_slow_class(f, i, j);
+    return 4;
 }
 
 template <bool DCONST, int NCAP>
@@ -203,15 +211,12 @@ cluster_pair_kernel(const __grid_constant__ kf_field_t f, const __grid_constant_
     __shared__ int next_q, slow_used, extent_bad;
     __shared__ unsigned cnt_e, cnt_v;
     __shared__ double2 slow_e[CL_WARPS];
-    __shared__ int quad_res[CL_WARPS][2];    // residue range of the warp's current quad (slow-class test)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int no = (n + 7) / 8, nq = (n + 3) / 4;
     const unsigned base = smem_u32(sm);
     const double *pos = pos_all + 3 * (size_t)b * n;
     const float4 *apar = reinterpret_cast<const float4 *>(f.atom_par);
     const int4 *aaux = reinterpret_cast<const int4 *>(f.atom_aux);
-    float4 *s_qc = reinterpret_cast<float4 *>(sm + L::Q_C);
-    float4 *s_qh = reinterpret_cast<float4 *>(sm + L::Q_H);
     // each quad's (elec, vdW) energy goes to e_atom[quad] (global scratch, read back
     // in quad order at the end; the totals then sit at atom 0)
     double *e_q = e_atom + 2 * (size_t)b * n;
@@ -225,10 +230,9 @@ cluster_pair_kernel(const __grid_constant__ kf_field_t f, const __grid_constant_
         if (ok) { x = pos[3 * a]; y = pos[3 * a + 1]; z = pos[3 * a + 2]; }
         double lo[3] = {ok ? x : INFINITY, ok ? y : INFINITY, ok ? z : INFINITY};
         double hi[3] = {ok ? x : -INFINITY, ok ? y : -INFINITY, ok ? z : -INFINITY};
-        int rlo = ok ? aaux[a].y : 0x7fffffff, rhi = ok ? aaux[a].y : -0x7fffffff;
         // every octet / quad below no / nq holds at least one atom; lanes past
         // the last one only take part in the shuffles
-        const bool in_oct = a < 8 * no, in_quad = (a >> 2) < nq;
+        const bool in_oct = a < 8 * no;
         bool bad = false;
 #pragma unroll
         for (int m = 1; m < 8; m <<= 1) {
@@ -236,20 +240,6 @@ cluster_pair_kernel(const __grid_constant__ kf_field_t f, const __grid_constant_
             for (int q = 0; q < 3; ++q) {
                 lo[q] = fmin(lo[q], __shfl_xor_sync(FULL, lo[q], m));
                 hi[q] = fmax(hi[q], __shfl_xor_sync(FULL, hi[q], m));
-            }
-            rlo = min(rlo, __shfl_xor_sync(FULL, rlo, m));
-            rhi = max(rhi, __shfl_xor_sync(FULL, rhi, m));
-            if (m == 2 && (lane & 3) == 0 && in_quad) {   // quad frame (lanes 4k..4k+3 reduced)
-                float cq[3], hq[3];
-#pragma unroll
-                for (int q = 0; q < 3; ++q) {
-                    const double ctr = grid_round(0.5 * (lo[q] + hi[q]));
-                    bad |= !(fabs(ctr) < CENTRE_MAX);
-                    cq[q] = (float)ctr;
-                    hq[q] = __double2float_ru(fmax(hi[q] - ctr, ctr - lo[q]));
-                }
-                s_qc[a >> 2] = make_float4(cq[0], cq[1], cq[2], 0.f);
-                s_qh[a >> 2] = make_float4(hq[0], hq[1], hq[2], 0.f);
             }
         }
         double ctr[3];
@@ -273,7 +263,6 @@ cluster_pair_kernel(const __grid_constant__ kf_field_t f, const __grid_constant_
             const int O = a >> 3;
             reinterpret_cast<float4 *>(sm + L::OCT_C)[O] = make_float4((float)ctr[0], (float)ctr[1], (float)ctr[2], 0.f);
             reinterpret_cast<float4 *>(sm + L::OCT_H)[O] = make_float4(hx[0], hx[1], hx[2], 0.f);
-            reinterpret_cast<int2 *>(sm + L::OCT_RES)[O] = make_int2(rlo, rhi);
         }
     }
     for (int k = threadIdx.x; k < 9 * NCAP; k += CL_THREADS)   // the three adjacent word planes
@@ -286,52 +275,50 @@ cluster_pair_kernel(const __grid_constant__ kf_field_t f, const __grid_constant_
     }
 
     // ---- 2. i-quads against candidate octets --------------------------------
-    const int ii = lane & 3, js = lane >> 2;
+    // (lane and the shared base are pinned in registers: the compiler would
+    // otherwise rematerialise them from special registers in every round)
+    int lane_p = lane;
+    unsigned sb = base;
+    asm volatile("" : "+r"(lane_p), "+r"(sb));
+    const int ii = lane_p & 3, js = lane_p >> 2;
     int Q = warp;
     while (Q < nq) {
         const int i = 4 * Q + ii;
         const bool vi = i < n;
-        float oi0 = -FAR, oi1 = -FAR, oi2 = -FAR, qK4 = 0.f, ws4 = 0.f, Ri = 0.f;
-        bool slow_i = false;
-        {
-            const float4 cq4 = s_qc[Q];
-            if (vi) {
-                oi0 = __double2float_rn(pos[3 * i] - (double)cq4.x);
-                oi1 = __double2float_rn(pos[3 * i + 1] - (double)cq4.y);
-                oi2 = __double2float_rn(pos[3 * i + 2] - (double)cq4.z);
-                const float4 pi4 = apar[i];
-                qK4 = (float)COULOMB_K * pi4.x * c.we[3];   // K q_i w_elec(4)
-                ws4 = pi4.z * c.wv[3];                      // sqrt(eps_i) w_vdw(4)
-                Ri = pi4.y;
-                slow_i = aaux[i].w != 0;
+        const float4 oi = lds4(sb + L::OQ + 16 * (vi ? i : 0));
+        const float2 ri = lds2(sb + L::RS + 8 * (vi ? i : 0));
+        const float4 ci = lds4(sb + L::OCT_C + 16 * (Q >> 1));
+        const float oix = vi ? oi.x : -FAR, oiy = vi ? oi.y : -FAR, oiz = vi ? oi.z : -FAR;
+        // the quad's box in its octet's frame (lanes of equal ii hold the same atom)
+        float blo[3] = {vi ? oi.x : 3e30f, vi ? oi.y : 3e30f, vi ? oi.z : 3e30f};
+        float bhi[3] = {vi ? oi.x : -3e30f, vi ? oi.y : -3e30f, vi ? oi.z : -3e30f};
+#pragma unroll
+        for (int m = 1; m < 4; m <<= 1)
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                blo[q] = fminf(blo[q], __shfl_xor_sync(FULL, blo[q], m));
+                bhi[q] = fmaxf(bhi[q], __shfl_xor_sync(FULL, bhi[q], m));
             }
-        }
-        // class lookups only for octets within the 64-atom window of the quad
-        // (O <= o_near), or near a slow atom's residue (a tree partner beyond the
-        // window, class_window in device.py): then the quad's residue range
-        const int o_near = c.uniform ? -1 : (4 * Q + 34) >> 3;
-        const bool q_slow = !c.uniform && __any_sync(FULL, slow_i);
-        if (q_slow) {
-            int r = vi ? aaux[i].y : 0x7fffffff, h = vi ? aaux[i].y : -0x7fffffff;
-            r = min(r, __shfl_xor_sync(FULL, r, 1)); r = min(r, __shfl_xor_sync(FULL, r, 2));
-            h = max(h, __shfl_xor_sync(FULL, h, 1)); h = max(h, __shfl_xor_sync(FULL, h, 2));
-            if (lane == 0) { quad_res[warp][0] = r; quad_res[warp][1] = h; }
-        }
+        const float qK = (float)COULOMB_K * oi.w;        // K q_i
+        const float qK4 = qK * c.we[3], ws4 = ri.y * c.wv[3];
+        const bool slow_q = !c.uniform && __any_sync(FULL, vi && aaux[vi ? i : 0].w != 0);
         float fx = 0.f, fy = 0.f, fz = 0.f, ee = 0.f, ev = 0.f;
         int ce = 0, cv = 0;
-        if (lane == 0) slow_e[warp] = make_double2(0.0, 0.0);   // exact-path energies of this quad
+        if (lane_p == 0) slow_e[warp] = make_double2(0.0, 0.0);   // exact-path energies of this quad
         __syncwarp();
         const int O0 = Q >> 1;
         for (int ob = O0; ob < no; ob += 32) {
-            // box pretest of 32 candidate octets at once
-            const int Oc = ob + lane;
+            // box pretest of 32 candidate octets at once: gap between [ci + blo,
+            // ci + bhi] and [oc - oh, oc + oh] (frame shift exact; the rest rounds
+            // far below the pretest's 1e-2 A^2 margin)
+            const int Oc = ob + lane_p;
             float bd2 = 3.0e38f;
             if (Oc < no) {
-                const float4 oc = lds<float4>(base + L::OCT_C + 16 * Oc), oh = lds<float4>(base + L::OCT_H + 16 * Oc);
-                const float4 cq = s_qc[Q], hq = s_qh[Q];
-                const float gx = fmaxf(fabsf(cq.x - oc.x) - (hq.x + oh.x), 0.f);
-                const float gy = fmaxf(fabsf(cq.y - oc.y) - (hq.y + oh.y), 0.f);
-                const float gz = fmaxf(fabsf(cq.z - oc.z) - (hq.z + oh.z), 0.f);
+                const float4 oc = lds4(sb + L::OCT_C + 16 * Oc), oh = lds4(sb + L::OCT_H + 16 * Oc);
+                const float sx = ci.x - oc.x, sy = ci.y - oc.y, sz = ci.z - oc.z;
+                const float gx = fmaxf(fmaxf((sx + blo[0]) - oh.x, -(sx + bhi[0]) - oh.x), 0.f);
+                const float gy = fmaxf(fmaxf((sy + blo[1]) - oh.y, -(sy + bhi[1]) - oh.y), 0.f);
+                const float gz = fmaxf(fmaxf((sz + blo[2]) - oh.z, -(sz + bhi[2]) - oh.z), 0.f);
                 bd2 = gx * gx + gy * gy + gz * gz;
             }
             unsigned cand = __ballot_sync(FULL, bd2 <= c.pre2);
@@ -340,36 +327,29 @@ cluster_pair_kernel(const __grid_constant__ kf_field_t f, const __grid_constant_
                 const int t = __ffs(cand) - 1;
                 cand &= cand - 1u;
                 const int O = ob + t;
-                const float4 cq = s_qc[Q];
-                const float4 oc = lds<float4>(base + L::OCT_C + 16 * O);
+                const float4 oc = lds4(sb + L::OCT_C + 16 * O);
                 const int j = 8 * O + js;
-                const float4 oj = lds<float4>(base + L::OQ + 16 * j);
-                const float2 rj = lds<float2>(base + L::RS + 8 * j);
-                const float dx = (oi0 - oj.x) + (cq.x - oc.x);   // frame shift exact
-                const float dy = (oi1 - oj.y) + (cq.y - oc.y);
-                const float dz = (oi2 - oj.z) + (cq.z - oc.z);
+                const float4 oj = lds4(sb + L::OQ + 16 * j);
+                const float2 rj = lds2(sb + L::RS + 8 * j);
+                const float dx = (oix - oj.x) + (ci.x - oc.x);   // frame shift exact
+                const float dy = (oiy - oj.y) + (ci.y - oc.y);
+                const float dz = (oiz - oj.z) + (ci.z - oc.z);
                 const float d2 = dx * dx + dy * dy + dz * dz;
                 bool live = vi;
-                if (O == O0) live &= j > i;              // diagonal octet: each pair once
+                if (O == O0) live &= j > i;              // own octet: each pair once
                 float qq = qK4 * oj.w, weps = ws4 * rj.y;
-                bool wnz = c.w4_nonzero;
+                bool wnz = (c.wnz_mask >> 3) & 1;
                 int cls = 4;
-                if (O <= o_near ||
-                    (q_slow && reinterpret_cast<const int2 *>(sm + L::OCT_RES)[O].x <= quad_res[warp][1] + 1 &&
-                     reinterpret_cast<const int2 *>(sm + L::OCT_RES)[O].y >= quad_res[warp][0] - 1)) {
-                    const int off = j - i + 32;
-                    if ((unsigned)off < 64u) {
-                        const int4 cm = reinterpret_cast<const int4 *>(f.class_map)[vi ? i : 0];
-                        const unsigned wd = off < 32 ? (off < 16 ? cm.x : cm.y) : (off < 48 ? cm.z : cm.w);
-                        cls = 4 - (int)((wd >> (2 * (off & 15))) & 3u);
-                    } else if (live && slow_i && j < n) {
+                // class 4 unless the octet lies in the quad's 64-atom window (host-built
+                // codes) or a slow atom's tree partner may be here (class_window)
+                if (!c.uniform && (O - O0 <= 4 || slow_q)) {
+                    if (O - O0 <= 4)
+                        cls = 4 - (int)((f.class_codes[5 * Q + (O - O0)] >> (2 * lane_p)) & 3ull);
+                    else if (live && j < n && f.class_slow[i])
                         cls = cl_slow_class(f, i, j);
-                    }
-                    const float we = c.we[cls - 1], wv = c.wv[cls - 1];
-                    const float4 pi4 = apar[vi ? i : 0];
-                    qq = (float)COULOMB_K * pi4.x * we * oj.w;
-                    weps = wv * pi4.z * rj.y;
-                    wnz = (we != 0.f) | (wv != 0.f);
+                    qq = qK * c.we[cls - 1] * oj.w;
+                    weps = c.wv[cls - 1] * ri.y * rj.y;
+                    wnz = (c.wnz_mask >> (cls - 1)) & 1;
                 }
                 // exact path: inside a threshold band, or closer than f64_d2 with a
                 // nonzero weight (or at clash range whatever the weight)
@@ -384,7 +364,7 @@ cluster_pair_kernel(const __grid_constant__ kf_field_t f, const __grid_constant_
                     }
                     // fixed lane tree, then in round order: deterministic
                     const double te = warp_sum(se[0]), tv = warp_sum(se[1]);
-                    if (lane == 0) {
+                    if (lane_p == 0) {
                         slow_e[warp].x += te; slow_e[warp].y += tv;
                         slow_used = 1;
                     }
@@ -401,7 +381,7 @@ cluster_pair_kernel(const __grid_constant__ kf_field_t f, const __grid_constant_
                 ce += ke;
                 if ((vmask >> t) & 1u) {   // boxes within the vdW reach
                     const bool kv = fast && d2 <= c.tv2;
-                    const float D = Ri + rj.x;
+                    const float D = ri.x + rj.x;
                     const float sr = D * D * inv_r2;
                     const float s3 = sr * sr * sr;
                     const float s6 = s3 * s3;
@@ -416,7 +396,7 @@ cluster_pair_kernel(const __grid_constant__ kf_field_t f, const __grid_constant_
                 tx += __shfl_xor_sync(FULL, tx, 1); ty += __shfl_xor_sync(FULL, ty, 1); tz += __shfl_xor_sync(FULL, tz, 1);
                 tx += __shfl_xor_sync(FULL, tx, 2); ty += __shfl_xor_sync(FULL, ty, 2); tz += __shfl_xor_sync(FULL, tz, 2);
                 const float v = ii == 0 ? tx : (ii == 1 ? ty : tz);
-                if (ii < 3 && j < n && v != 0.f) acc_add<NCAP>(base, 3 * j + ii, __float2ll_rn(-v * FIXF));
+                if (ii < 3 && j < n && v != 0.f) acc_add<NCAP>(sb, 3 * j + ii, __float2ll_rn(-v * FIXF));
             }
         }
         // i forces: sum over the 8 j-lanes of each i, then into the fixed point
@@ -428,7 +408,7 @@ cluster_pair_kernel(const __grid_constant__ kf_field_t f, const __grid_constant_
         }
         {
             const float v = js == 0 ? fx : (js == 1 ? fy : fz);
-            if (vi && js < 3 && v != 0.f) acc_add<NCAP>(base, 3 * i + js, __float2ll_rn(v * FIXF));
+            if (vi && js < 3 && v != 0.f) acc_add<NCAP>(sb, 3 * i + js, __float2ll_rn(v * FIXF));
         }
         // the quad's energies (fixed xor tree: deterministic) and counts (order-free)
 #pragma unroll
@@ -438,7 +418,7 @@ cluster_pair_kernel(const __grid_constant__ kf_field_t f, const __grid_constant_
         }
         const int tce = __reduce_add_sync(FULL, ce), tcv = __reduce_add_sync(FULL, cv);
         __syncwarp();
-        if (lane == 0) {
+        if (lane_p == 0) {
             e_q[2 * Q] = (double)ee + slow_e[warp].x;
             e_q[2 * Q + 1] = (double)ev + slow_e[warp].y;
             atomicAdd(&cnt_e, (unsigned)tce);
@@ -575,7 +555,11 @@ int kf_cluster_pairs_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStrea
     c.f64_d2 = f64_below * f64_below;
     c.kap_inv = f->dielectric_const ? (float)(1.0 / f->kappa) : 1.0f;
     c.uniform = f->uniform_weights;
-    c.w4_nonzero = (c.we[3] != 0.f) || (c.wv[3] != 0.f);
+    c.wnz_mask = 0;
+    for (int q = 0; q < 4; ++q) {
+        c.kwe[q] = (float)COULOMB_K * c.we[q];
+        if (c.we[q] != 0.f || c.wv[q] != 0.f) c.wnz_mask |= 1 << q;
+    }
     const bool dc = f->dielectric_const != 0;
     if (n <= 512) return launch_cap<512>(dc, f, c, w, n, s);
     if (n <= 1024) return launch_cap<1024>(dc, f, c, w, n, s);

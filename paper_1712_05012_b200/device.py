@@ -302,6 +302,26 @@ def class_window(tree):
     return words.view(np.int32), slow
 
 
+def class_codes(tree) -> np.ndarray:
+    """Static pair classes for the cluster-pair kernel (kf_cluster.cu): for quad Q
+    (atoms 4Q..4Q+3) and the octets O = Q//2 + k, k = 0..4, a uint64 of 2-bit
+    (4 - class) codes, pair (i = 4Q + l % 4, j = 8O + l // 4) at bits 2l.  These
+    octets hold every partner within the 64-atom window of the quad; partners
+    beyond it are class 4 except for class_window's slow atoms."""
+    n = len(tree.parent)
+    nq = (n + 3) // 4
+    lane = np.arange(32)
+    Q = np.repeat(np.arange(nq), 5)
+    k = np.tile(np.arange(5), nq)
+    i = (4 * Q)[:, None] + (lane % 4)[None, :]
+    j = (8 * (Q // 2 + k))[:, None] + (lane // 4)[None, :]
+    ok = (i < n) & (j < n) & (j != i)
+    c = np.full(i.shape, 4, np.int64)
+    c[ok] = tree_classes(tree, i[ok], j[ok])
+    code = ((4 - c).astype(np.uint64) << (2 * lane).astype(np.uint64)[None, :]).sum(axis=1, dtype=np.uint64)
+    return code.reshape(nq, 5)
+
+
 class ParamTables:
     """Per-atom parameters + pair-weight provider + dielectric on the device."""
 
@@ -329,7 +349,8 @@ class ParamTables:
             t.update(tparent=_up(tree.parent, np.int32), tgp=_up(tree.grandparent, np.int32),
                      tggp=_up(tree.greatgrand, np.int32), tres=_up(tree.residue_of, np.int32),
                      tchain=_up(tree.chain_mask, np.uint8), class_map=_up(cmap, np.int32),
-                     class_slow=_up(slow, np.uint8))
+                     class_slow=_up(slow, np.uint8),
+                     class_codes=_up(class_codes(tree).view(np.int64), np.int64))
             aux[:, 3] = slow.astype(np.int32)
             s.uniform_weights = 0
             for k, v in enumerate(np.asarray(weights.table.elec_by_class())[1:5]):
