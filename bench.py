@@ -5,9 +5,9 @@ trajectories of the 140-residue / 1,499-atom synthetic A/C/S chain (C2),
 random +-90 starts (`--init random --seed 1 --batch 1024` semantics), vacuum
 FieldConfig() defaults, fixed iteration count (torque_tol_rel = 0,
 energy_window = 0).  A step is one KCM iteration of every trajectory (FK ->
-hash binning -> elec/vdW pair forces -> wrenches -> suffix-scan torques ->
-max-normalised step), replayed from CUDA graphs.  With N GPUs (torchrun) the
-1024 trajectories are split into contiguous blocks, one per rank; there is no
+elec/vdW pair forces -> wrenches -> suffix-scan torques -> max-normalised
+step), replayed from CUDA graphs.  With N GPUs (torchrun) the 1024
+trajectories are split into contiguous blocks, one per rank; there is no
 per-iteration communication and one NCCL all-gather of the final per-trajectory
 records at the end of the timed region (scaling "strong": total work fixed).
 
@@ -15,7 +15,11 @@ Output: one JSON line on rank 0 (see the README of the driver contract):
 value = trajectory-iterations/s of the whole job; e2e = the same through the
 public `fold_ensemble` API with host inputs/outputs; roofline of the dominant
 kernel; cpu_baseline = the oracle (numpy restatement of the reference,
-`oracle/kcm_oracle.py`) timed on this host; single-trajectory C2/C3 numbers.
+`oracle/kcm_oracle.py`) timed on this host.  Extra legs on rank 0 at N = 1:
+C5 in water (FieldConfig(solvation=True)) with its solvation-coverage rate,
+C5 with fp64 pair math (the strict-parity mode), the single-trajectory
+configs C1-C4 on the GPU (C3 also through the `fold()` API), and C1 / C3 / C4
+on the CPU reference path.
 
 `--impl reference` times the reference CPU algorithm (the oracle port; the
 reference is a pure-Python package) on all host cores with a process pool.
@@ -41,6 +45,7 @@ if ROOT not in sys.path:
 ENSEMBLE = 1024
 METRIC = "KCM iterations/sec"
 UNIT = "trajectory-iterations/s"
+REF_ITERS = 20      # iterations per reference-arm task (one trajectory per core per step)
 
 
 def parse():
@@ -50,16 +55,42 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--ensemble", type=int, default=ENSEMBLE)
-    ap.add_argument("--water", action="store_true", help="FieldConfig(solvation=True)")
-    ap.add_argument("--no-extras", action="store_true", help="skip single-trajectory and CPU legs")
+    ap.add_argument("--water", action="store_true", help="headline in FieldConfig(solvation=True)")
+    ap.add_argument("--no-extras", action="store_true", help="skip the water / fp64 / single-trajectory / CPU legs")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     return ap.parse_args()
 
 
-def workload_name(args) -> str:
-    mode = "water" if args.water else "vacuum"
+def workload_name(args, water=None) -> str:
+    mode = "water" if (args.water if water is None else water) else "vacuum"
     return (f"C5: ensemble of {args.ensemble} x C2 chain (140 random A/C/S residues, 1499 atoms), "
             f"random +-90 starts, {mode}, fixed iterations")
+
+
+def config_of(args, n_atoms=1499, dofs=518, world=1) -> dict:
+    return {"workload": workload_name(args), "ensemble": args.ensemble, "atoms_per_trajectory": n_atoms,
+            "dofs": dofs, "parallelism": f"trajectory-parallel x{world}",
+            "l2": "working set per step > 126 MB L2 (positions, forces, link transforms of 1.5M atoms / "
+                  "530k links), no explicit flush"}
+
+
+def host_cores() -> dict:
+    logical = os.cpu_count() or 1
+    physical = logical
+    try:
+        import psutil
+        physical = psutil.cpu_count(logical=False) or logical
+    except ImportError:
+        pass
+    model = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"logical": logical, "physical": physical, "model": model}
 
 
 # --------------------------------------------------------------------------
@@ -126,15 +157,24 @@ class Clocks:
 # reference arm: the reference CPU algorithm on all host cores
 # --------------------------------------------------------------------------
 
-def _cpu_worker(payload):
-    thetas, iters = payload
+_W = {}
+
+
+def _ref_init(water: bool):
+    """Pool initializer: the C2 system and the oracle field once per worker
+    (setup is outside every timed task)."""
     from oracle import kcm_oracle as O
     from paper_1712_05012_b200 import workloads
     ch, params, w, _ = workloads.system("C2")
-    of = O.OracleField(params, w)
-    for th in thetas:
-        O.fold(ch, th, np.zeros(ch.n_dof, bool), of, max_iters=iters, torque_tol_rel=0.0, energy_window=0)
-    return len(thetas) * iters
+    _W["ch"], _W["of"] = ch, O.OracleField(params, w, solvation=water)
+
+
+def _ref_task(theta):
+    from oracle import kcm_oracle as O
+    ch = _W["ch"]
+    O.fold(ch, theta, np.zeros(ch.n_dof, bool), _W["of"], max_iters=REF_ITERS, torque_tol_rel=0.0,
+           energy_window=0)
+    return REF_ITERS
 
 
 def reference_arm(args, rank: int):
@@ -143,56 +183,116 @@ def reference_arm(args, rank: int):
     from paper_1712_05012_b200 import workloads
     if rank != 0:
         return
-    cores = os.cpu_count() or 1
+    hc = host_cores()
+    cores = hc["logical"]
     ch = workloads.system("C2")[0]
-    thetas = workloads.random_thetas(ch, cores, seed=1)
-    iters = 2
+    # the bench's own starts: trajectory r of the seed-1 stream, cores of them per step
+    thetas = workloads.random_thetas(ch, args.ensemble, seed=1)
     ctx = mp.get_context("fork")
-    with ctx.Pool(cores) as pool:
-        def one_step():
-            t0 = time.perf_counter()
-            done = sum(pool.map(_cpu_worker, [([thetas[k]], iters) for k in range(cores)]))
-            return done, time.perf_counter() - t0
-        for _ in range(max(args.warmup, 1)):
-            one_step()
-        tot, secs = 0, 0.0
+    with ctx.Pool(cores, initializer=_ref_init, initargs=(args.water,)) as pool:
+        pool.map(_ref_task, [thetas[k] for k in range(cores)], chunksize=1)    # warm-up: imports, caches
+        for _ in range(max(args.warmup, 1) - 1):
+            pool.map(_ref_task, [thetas[k] for k in range(cores)], chunksize=1)
+        tot, secs, nxt = 0, 0.0, 0
         for _ in range(args.steps):
-            d, s = one_step()
-            tot, secs = tot + d, secs + s
+            batch = [thetas[(nxt + k) % args.ensemble] for k in range(cores)]
+            nxt += cores
+            t0 = time.perf_counter()
+            tot += sum(pool.map(_ref_task, batch, chunksize=1))
+            secs += time.perf_counter() - t0
     value = tot / secs
-    sample = (f"{cores} C2 trajectories x {iters} oracle KCM iterations per step on a {cores}-process pool, "
-              f"{args.steps} steps")
+    sample = (f"per step: {cores} of the C5 ensemble's trajectories (consecutive starts of the seed-1 stream) x "
+              f"{REF_ITERS} oracle KCM iterations, one per process of a {cores}-process pool (system and field "
+              f"built once per worker); {args.steps} steps")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": workload_name(args), "ensemble": args.ensemble},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+            "data": "synthetic", "config": config_of(args),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
+                             "host": hc, "per_core": value / cores},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 # --------------------------------------------------------------------------
-# CPU baseline leg (rank 0, N = 1): oracle fold, one trajectory, bounded time
+# CPU legs (rank 0, N = 1): the oracle fold, one process, bounded time
 # --------------------------------------------------------------------------
 
-def cpu_fold_rate(config: str, budget_s: float, min_iters: int = 2):
+def cpu_fold_rate(config: str, budget_s: float, min_iters: int = 1, fixed_iters: int | None = None):
+    """(it/s, iterations timed) of the oracle fold of one `config` trajectory.
+    The first iteration is a warm-up unless `fixed_iters` is given (then all of
+    them are timed, as for C1's 1000-iteration run)."""
     from oracle import kcm_oracle as O
     from paper_1712_05012_b200 import workloads
     ch, params, w, fld = workloads.system(config)
     of = O.OracleField(params, w, solvation=fld.config.solvation)
     theta = workloads.start_theta(config, ch)
+    frozen = np.zeros(ch.n_dof, bool)
+    if fixed_iters is None:
+        t0 = time.perf_counter()
+        O.fold(ch, theta, frozen, of, max_iters=1, torque_tol_rel=0.0, energy_window=0)
+        one = time.perf_counter() - t0
+        iters = max(min_iters, int(budget_s / max(one, 1e-6)))
+    else:
+        iters = fixed_iters
     t0 = time.perf_counter()
-    O.fold(ch, theta, np.zeros(ch.n_dof, bool), of, max_iters=1, torque_tol_rel=0.0, energy_window=0)
-    one = time.perf_counter() - t0
-    iters = max(min_iters, int(budget_s / max(one, 1e-6)))
-    t0 = time.perf_counter()
-    O.fold(ch, theta, np.zeros(ch.n_dof, bool), of, max_iters=iters, torque_tol_rel=0.0, energy_window=0)
+    O.fold(ch, theta, frozen, of, max_iters=iters, torque_tol_rel=0.0, energy_window=0)
     return iters / (time.perf_counter() - t0), iters
 
 
 # --------------------------------------------------------------------------
 # GPU arm
 # --------------------------------------------------------------------------
+
+def time_graph(runner, K, s):
+    """Device time (ms) of K graph-replayed iterations of a prepared runner."""
+    import torch
+    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(s):
+        a0.record(s)
+        runner.run_graph(K)
+        a1.record(s)
+    s.synchronize()
+    return a0.elapsed_time(a1)
+
+
+def ensemble_leg(P, DV, workloads, ch, fld, thetas, K, W, s):
+    """(traj-it/s over K graph-replayed iterations, ms/step) of a full ensemble."""
+    B = len(thetas)
+    step = P.StepConfig(kappa=0.5, max_iters=W + K, torque_tol_rel=0.0, energy_window=0)
+    r = DV.EnsembleRunner(ch, fld, B, step, chunk=8)
+    r.load(thetas, np.zeros((B, ch.n_dof), bool))
+    r.prepare(W)
+    r.prepare(K)
+    with __import__("torch").cuda.stream(s):
+        r.run_graph(W)
+    s.synchronize()
+    ms = time_graph(r, K, s)
+    if any(st.error for st in r.batch.status()):
+        raise SystemExit("device error in an ensemble leg")
+    return B * K / (ms * 1e-3), ms / K, r
+
+
+def coverage_tests(P, ch, params, fld, thetas) -> float:
+    """Reference-equivalent solvation coverage tests of one evaluation (SURVEY.md
+    §8(d)): T = sum_i N |A_i| + sum_{gamma_i != 0} 3 (|K0_i| |A_i| + |K1_i|), with A_i
+    the 8 A cavity lists and K0 / K1 the exposed / singly covered samples, from
+    this package's own sasa_pass on the given start conformations (mean)."""
+    sphere = fld.sphere()
+    cfg = fld.config.solvation_cfg
+    gamma = np.asarray(params.gamma, float) != 0.0
+    out = []
+    for th in thetas:
+        pos = P.forward_kinematics(ch, P.Conformation(th, np.zeros(ch.n_dof, bool), ch.n_residues))
+        lists = P.filtered_lists(P.build_neighbor_table(P.build_grid(pos), fld.config.cutoffs.cav), pos,
+                                 fld.config.cutoffs.cav)
+        _, states = P.sasa_pass(pos, params, lists, sphere, cfg)
+        a = np.array([len(x) for x in lists], float)
+        k0 = (states.counts == 0).sum(axis=1)
+        k1 = (states.counts == 1).sum(axis=1)
+        out.append(float((sphere.n * a).sum() + (3.0 * (k0 * a + k1))[gamma].sum()))
+    return float(np.mean(out))
+
 
 def main():
     args = parse()
@@ -213,12 +313,11 @@ def main():
 
     torch.cuda.set_device(local)
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
 
     ch, params, w, fld = workloads.system("C2", solvation=args.water)
-    if args.water:
-        fld = P.Field(params, w, P.FieldConfig(solvation=True))
     thetas_all = workloads.random_thetas(ch, args.ensemble, seed=1)
     lo, hi = ENS.shard(args.ensemble, rank, world)
     B = hi - lo
@@ -316,56 +415,125 @@ def main():
     # ---- e2e: the public API with host conformations in, host results out
     confs = [P.Conformation(thetas_all[r], np.zeros(D, bool), ch.n_residues) for r in range(lo, hi)]
     e2e_step = P.StepConfig(kappa=0.5, max_iters=K, torque_tol_rel=0.0, energy_window=0)
-    P.fold_ensemble(ch, confs, fld, e2e_step)      # warm: buffers and graphs cached
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    res = P.fold_ensemble(ch, confs, fld, e2e_step)
-    if world > 1:
-        ENS.gather_records(ENS.pack_result(res), args.ensemble, device=dev)
-    torch.cuda.synchronize()
-    e2e_s = time.perf_counter() - t0
-    e2e_t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
-    if world > 1:
-        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
-    e2e_value = args.ensemble * K / float(e2e_t.item())
+
+    def e2e_rate(f_):
+        P.fold_ensemble(ch, confs, f_, e2e_step)      # warm: buffers and graphs cached
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = P.fold_ensemble(ch, confs, f_, e2e_step)
+        if world > 1:
+            ENS.gather_records(ENS.pack_result(res), args.ensemble, device=dev)
+        torch.cuda.synchronize()
+        t = torch.tensor([time.perf_counter() - t0], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return args.ensemble * K / float(t.item())
+
+    e2e_value = e2e_rate(fld)
     h2d = args.ensemble * D * (8 + 1) / K
     d2h = args.ensemble * (D * 8 + K * 4 * 8 + 64) / K
 
-    extras = {}
-    cpu = None
+    extras, water, fp64, cpu, cpu_configs = {}, None, None, None, {}
     if rank == 0 and world == 1 and not args.no_extras:
-        # single-trajectory C2 / C3 on one GPU (graph-replayed), and CPU legs
-        for cfg in ("C2", "C3", "C4"):   # C4: ~100k atoms (GPU only; the CPU port needs ~20 s/iteration)
+        Ke = max(3, min(K, 10))
+        # C5 in water (the reference's dominant CPU cost: solvation.py:135-255)
+        if not args.water:
+            wch, wparams, ww, wfld = workloads.system("C2", solvation=True)
+            w_rate, w_ms, wr = ensemble_leg(P, DV, workloads, wch, wfld, thetas_all, Ke, 3, s)
+            wcs, wfs, wbs = N.ref(wr.dc.struct), N.ref(wr.df.struct_for(False)), N.ref(wr.batch.struct)
+            wr.load(thetas_all, np.zeros((args.ensemble, D), bool))   # fresh status: every trajectory live
+            with torch.cuda.stream(s):
+                a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                N.check(lib.kf_fk(wcs, wbs, DV._sp()), "fk")
+                N.check(lib.kf_bin(wfs, wbs, DV._sp()), "bin")
+                N.check(lib.kf_pairs(wfs, wbs, DV._sp()), "pairs")
+                a0.record(s)
+                N.check(lib.kf_solvation(wfs, wbs, DV._sp()), "solv")
+                a1.record(s)
+            s.synchronize()
+            solv_ms = a0.elapsed_time(a1)
+            T = coverage_tests(P, wch, wparams, wfld, thetas_all[:4])
+            tests_per_launch = T * args.ensemble
+            dflop = 8.0 * tests_per_launch
+            confs_w = [P.Conformation(thetas_all[r], np.zeros(D, bool), ch.n_residues) for r in range(lo, hi)]
+            ws = P.StepConfig(kappa=0.5, max_iters=Ke, torque_tol_rel=0.0, energy_window=0)
+            P.fold_ensemble(wch, confs_w, wfld, ws)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            P.fold_ensemble(wch, confs_w, wfld, ws)
+            torch.cuda.synchronize()
+            w_e2e = args.ensemble * Ke / (time.perf_counter() - t0)
+            water = {"workload": workload_name(args, water=True), "value": w_rate, "unit": UNIT,
+                     "ms_per_step": w_ms, "steps": Ke,
+                     "e2e": {"value": w_e2e, "unit": UNIT, "h2d_bytes_per_step": args.ensemble * D * 9 / Ke,
+                             "d2h_bytes_per_step": args.ensemble * (D * 8 + Ke * 32 + 64) / Ke},
+                     "solvation_ms_per_step": solv_ms,
+                     "coverage_tests_per_s": tests_per_launch / (solv_ms * 1e-3),
+                     "solvation_roofline": {
+                         "bound": "fp64", "unit": "TFLOP/s", "peak": peak64 / 1e12,
+                         "achieved": dflop / (solv_ms * 1e-3) / 1e12,
+                         "frac": dflop / (solv_ms * 1e-3) / peak64,
+                         "work": "8 DFLOP per reference-equivalent coverage test (SURVEY.md §8(d)); T per "
+                                 f"trajectory = {T:.4g} (mean over 4 start conformations, this package's "
+                                 "sasa_pass); the kernel's group masks and early exits skip most of them, so "
+                                 "this is reference-equivalent work over executed time"}}
+            del wr
+        # C5 with fp64 pair math (the strict trajectory-parity mode)
+        P.set_pair_precision("fp64")
+        try:
+            f64fld = P.Field(params, w, P.FieldConfig(solvation=args.water))
+            f_rate, f_ms, fr = ensemble_leg(P, DV, workloads, ch, f64fld, thetas_all, Ke, 3, s)
+            fp64 = {"value": f_rate, "unit": UNIT, "ms_per_step": f_ms, "steps": Ke,
+                    "kernel": "pair_kernel<1,0> (compacted list, fp64 pair math)"}
+            del fr
+        finally:
+            P.set_pair_precision("fp32")
+        # single trajectories on one GPU (graph-replayed), C1 over the 1000-iteration config
+        for cfg in ("C1", "C2", "C3", "C4"):
             c_ch, c_p, c_w, c_f = workloads.system(cfg, solvation=args.water)
-            r1 = DV.EnsembleRunner(c_ch, c_f, 1, P.StepConfig(max_iters=W + K, torque_tol_rel=0.0,
+            Kc = 1000 if cfg == "C1" else K
+            r1 = DV.EnsembleRunner(c_ch, c_f, 1, P.StepConfig(max_iters=W + Kc, torque_tol_rel=0.0,
                                                             energy_window=0), chunk=16)
             r1.load(workloads.start_theta(cfg, c_ch)[None, :], np.zeros((1, c_ch.n_dof), bool))
             r1.prepare(W)
-            r1.prepare(K)
+            r1.prepare(Kc)
             with torch.cuda.stream(s):
                 r1.run_graph(W)
-                s.synchronize()
-                a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a0.record(s)
-                r1.run_graph(K)
-                a1.record(s)
             s.synchronize()
+            msc = time_graph(r1, Kc, s)
             st1 = r1.batch.status()[0]
-            extras[cfg] = {"atoms": c_ch.n_atoms, "it_per_s": K / (a0.elapsed_time(a1) * 1e-3),
+            extras[cfg] = {"atoms": c_ch.n_atoms, "it_per_s": Kc / (msc * 1e-3), "iterations": Kc,
                            "pairs_9A": int(st1.n_pairs)}
-        cpu_rate, cpu_iters = cpu_fold_rate("C2", args.cpu_seconds)
-        extras["C2"]["cpu_it_per_s"] = cpu_rate
-        extras["C2"]["speedup_vs_cpu"] = extras["C2"]["it_per_s"] / cpu_rate
+        # C3 through the public fold() API (host Trajectory records out, wall clock)
+        c_ch, c_p, c_w, c_f = workloads.system("C3", solvation=args.water)
+        conf3 = P.Conformation(workloads.start_theta("C3", c_ch), np.zeros(c_ch.n_dof, bool), c_ch.n_residues)
+        st3 = P.StepConfig(kappa=0.5, max_iters=K, torque_tol_rel=0.0, energy_window=0)
+        P.fold(c_ch, conf3, c_f, st3)
+        t0 = time.perf_counter()
+        tr3 = P.fold(c_ch, conf3, c_f, st3)
+        extras["C3"]["fold_api_it_per_s"] = tr3.iterations / (time.perf_counter() - t0)
+        # CPU reference path (oracle port), one process
+        cpu_rate, cpu_iters = cpu_fold_rate("C2", args.cpu_seconds, min_iters=2)
+        c1_rate, c1_iters = cpu_fold_rate("C1", 0.0, fixed_iters=1000)
         c3_rate, c3_iters = cpu_fold_rate("C3", args.cpu_seconds / 3, min_iters=2)
-        extras["C3"]["cpu_it_per_s"] = c3_rate
-        extras["C3"]["cpu_iters_timed"] = c3_iters
-        extras["C3"]["speedup_vs_cpu"] = extras["C3"]["it_per_s"] / c3_rate
-        cpu = {"value": cpu_rate, "unit": UNIT, "cores": 1, "kind": "port",
-               "sample": f"oracle fold of one C2 trajectory, {cpu_iters} iterations, 1 thread "
-                         f"(value in trajectory-iterations/s; the C5 ensemble is {args.ensemble} such "
-                         f"trajectories, so the 1-core ensemble rate equals this)"}
+        c4_rate, c4_iters = cpu_fold_rate("C4", 0.0, fixed_iters=1)
+        cpu_configs = {"C1": {"it_per_s": c1_rate, "iterations_timed": c1_iters,
+                              "note": "BASELINE config 1: 30 x ALA, 1000 KCM iterations, reference CPU path"},
+                       "C2": {"it_per_s": cpu_rate, "iterations_timed": cpu_iters},
+                       "C3": {"it_per_s": c3_rate, "iterations_timed": c3_iters},
+                       "C4": {"it_per_s": c4_rate, "iterations_timed": c4_iters,
+                              "note": "one timed iteration (the reference's ~20 s per iteration)"}}
+        for cfg, v in cpu_configs.items():
+            extras[cfg]["cpu_it_per_s"] = v["it_per_s"]
+            extras[cfg]["speedup_vs_cpu"] = extras[cfg]["it_per_s"] / v["it_per_s"]
+        hc = host_cores()
+        cpu = {"value": cpu_rate, "unit": UNIT, "cores": 1, "kind": "port", "host": hc,
+               "sample": f"oracle fold of one C2 trajectory, {cpu_iters} iterations, 1 thread (value in "
+                         f"trajectory-iterations/s; the C5 ensemble is {args.ensemble} such trajectories, so "
+                         f"the 1-core ensemble rate equals this)",
+               "configs": cpu_configs}
 
     if rank != 0:
         if world > 1:
@@ -376,16 +544,15 @@ def main():
     # HBM rooflines of the byte-bound phases (north star: binning, scans, kinematics):
     # algorithmic bytes per trajectory (SURVEY.md §8(d) formulas) x B / phase time
     n_at, L = ch.n_atoms, len(ch.links)
-    H = 1 << max(6, int(np.ceil(np.log2(n_at + 1))))
     phase_bytes = {
         # theta in; link transforms (16 f64) and positions out
         "fk": 8 * D + 128 * L + 24 * n_at,
-        # positions in; hash table (key 8 + count/start/occ/chunk 4x4 + box 32) and the
-        # cell-ordered SoA (hi/lo/par/aux/tree 5x16 + fp64 position 32) + slot/rank/sorted out
-        "bin": 24 * n_at + H * (8 + 16 + 32) + n_at * (5 * 16 + 32 + 12),
         # transforms, positions, forces, per-atom energies/counts in; tau, theta out
         "torque": 128 * L + 48 * n_at + 24 * n_at + 16 * D,
     }
+    if acc.get("bin", 0.0) > 0.01:   # binning runs only where a cell table is needed (water)
+        H = 1 << max(6, int(np.ceil(np.log2(n_at + 1))))
+        phase_bytes["bin"] = 24 * n_at + H * (8 + 16 + 32) + n_at * (5 * 16 + 32 + 12)
     phase_roofline = {}
     for ph, by in phase_bytes.items():
         t = acc.get(ph, 0.0)
@@ -393,11 +560,11 @@ def main():
             gbs = by * B / (t * 1e-3) / 1e9
             phase_roofline[ph] = {"bound": "hbm", "bytes_per_launch": by * B, "achieved": gbs, "peak": hbm_peak,
                                   "unit": "GB/s", "frac": gbs / hbm_peak}
-    # the dominant kernel of this run (kf_nonbonded.cu: half-list dense lanes for
-    # fp32 ensembles, the compacted list for fp64) and its DRAM traffic per launch from
+    # the dominant kernel of this run and its DRAM traffic / issue counts per launch from
     # the committed `ncu --set full` capture of the same workload, if there is one
-    kernel = "pair_kernel<1,0>" if P.pair_precision() == "fp64" else \
-        ("pair_dense_kernel<0,0,1>" if B * ch.n_atoms >= 40000 else "pair_dense_kernel<0,1,0>")
+    kind = int(lib.kf_pair_kernel_kind(fs, bs, n_at))
+    kernel = ["pair_kernel<1,0>", "pair_dense_kernel<0,1,0>", "pair_dense_kernel<0,0,1>",
+              "cluster_pair_kernel"][kind]
     traffic, traffic_src, prof = None, None, {}
     prof_path = os.path.join(ROOT, "profiles", "pair_kernel_traffic.json")
     if os.path.exists(prof_path):
@@ -408,41 +575,24 @@ def main():
                     traffic, traffic_src, prof = rec.get("bytes_per_launch"), rec.get("source"), rec
         except (OSError, ValueError, AttributeError):
             traffic = None
-    # shared-memory bandwidth of the pair kernel (north star): the capture's shared
-    # wavefronts per launch (128 B each) over the live-measured launch time, against
-    # the nominal 32 banks x 4 B per clock per SM at the clock seen under load
-    smem = None
-    wf = prof.get("smem_wavefronts_per_launch")
-    if wf and pair_ms > 0:
-        mhz = (clk or {}).get("sm_mhz") or 1965.0
-        sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
-        smem_peak = 128.0 * sm_count * mhz * 1e6 / 1e9
-        smem_gbs = wf * 128.0 / (pair_ms * 1e-3) / 1e9
-        smem = {"achieved": smem_gbs, "peak": smem_peak, "unit": "GB/s", "frac": smem_gbs / smem_peak,
-                "wavefronts_per_launch": wf, "fma_pipe_pct_of_active": prof.get("fma_pipe_pct"),
-                "issue_active_pct": prof.get("issue_active_pct"),
-                "peak_source": f"nominal 128 B/clk/SM x {sm_count} SMs at {mhz:.0f} MHz"}
+    mhz = (clk or {}).get("sm_mhz") or 1965.0
+    sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
     # instruction issue (the kernel's actual bound): the capture's warp-instructions per
     # launch over the live launch time, against 4 schedulers x 1 warp-instruction/clk per SM
     issue = None
     wi = prof.get("warp_instructions_per_launch")
     if wi and pair_ms > 0:
-        mhz = (clk or {}).get("sm_mhz") or 1965.0
-        sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
         ipk = 4.0 * sm_count * mhz * 1e6 / 1e9
         got = wi / (pair_ms * 1e-3) / 1e9
         issue = {"achieved": got, "peak": ipk, "unit": "G warp-instructions/s", "frac": got / ipk,
-                 "warp_instructions_per_launch": wi,
-                 "per_pair": wi / max(1.0, float(p9)),
+                 "warp_instructions_per_launch": wi, "per_pair": wi / max(1.0, float(p9)),
+                 "fma_pipe_pct_of_active": prof.get("fma_pipe_pct"),
+                 "issue_active_pct": prof.get("issue_active_pct"),
                  "peak_source": f"4 issue slots/clk/SM x {sm_count} SMs at {mhz:.0f} MHz"}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "f64+f32", "data": "synthetic",
-        "config": {"workload": workload_name(args), "ensemble": args.ensemble, "atoms_per_trajectory": ch.n_atoms,
-                   "dofs": D, "parallelism": f"trajectory-parallel x{world}",
-                   "l2": "working set per step > 126 MB L2 (sorted positions, forces, link transforms "
-                         "of 1.5M atoms / 530k links), no explicit flush"},
+        "dtype": "f64+f32", "data": "synthetic", "config": config_of(args, n_at, D, world),
         "pair_interactions_per_s": pairs_per_step * K / (ms_max * 1e-3),
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "api": "paper_1712_05012_b200.fold_ensemble (host numpy in, host Trajectory data out)"},
@@ -453,13 +603,14 @@ def main():
                              f"on this rank's {B} trajectories",
                      "peak_source": "kf_peak_flops FFMA microbenchmark, this GPU, this run",
                      "fp64_peak_tflops": peak64 / 1e12,
-                     "kernel_share_of_step": pair_ms / step_ms_eager,
-                     "smem": smem, "issue": issue},
+                     "kernel_share_of_step": pair_ms / step_ms_eager, "issue": issue},
         "phase_ms_per_step": acc,
         "phase_rooflines": phase_roofline,
         "gpu_launches": launches,
         "clocks": clk,
         "cpu_baseline": cpu,
+        "water": water,
+        "fp64_pairs": fp64,
         "single_trajectory": extras or None,
         "hbm_peak_gbs": hbm_peak,
     }

@@ -260,6 +260,12 @@ void kf_graph_cache_clear(void);
  * StericClashError message (forcefield.py:84-88).  Run only on error. */
 int kf_clash_report(const kf_field_t *f, kf_batch_t *w, void *stream);
 
+/* The elec/vdW pair kernel kf_pairs (and the fold loop) selects for this field,
+ * batch and atom count: 0 compacted list (fp64 pair math), 1 dense lanes with
+ * full list, 2 dense lanes with half list, 3 cluster pairs (one CTA per
+ * trajectory, no binning pass in vacuum). */
+int kf_pair_kernel_kind(const kf_field_t *f, const kf_batch_t *w, int n);
+
 /* Kernel launches this library has enqueued so far (host counter; a captured
  * CUDA graph replays the launches counted while it was captured). */
 unsigned long long kf_launch_counter(void);

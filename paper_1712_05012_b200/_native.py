@@ -102,6 +102,7 @@ _PROTOS = {
     "kf_scan_exclusive_i64": (I32, [P, C.c_int64, P, P, P]),
     "kf_classify_pairs": (I32, [P, P, P, C.c_int64, P, P]),
     "kf_pair_terms": (I32, [P, P, C.c_int, P, P, P, P, C.c_int64, C.c_int, P, P, P, P]),
+    "kf_pair_kernel_kind": (I32, [P, P, C.c_int]),
     "kf_scatter_pair_forces": (I32, [P, C.c_int, P, P, P, P, C.c_int64, P, P]),
     "kf_grid_occupied": (I32, [P, P, C.c_int64, P, P, P, P, P]),
     "kf_row_kept_offsets": (I32, [P, C.c_int, P, P, P]),

@@ -857,6 +857,31 @@ int kf_cluster_path(const kf_field_t *f, const kf_batch_t *w, int n);
 int kf_cluster_pairs_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s);
 int kf_cluster_clash_report_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s);
 
+// The pair kernel a launch of (f, w, n) selects: 0 compacted list (fp64 pair math),
+// 1 dense lanes full list, 2 dense lanes half list, 3 cluster pairs (kf_cluster.cu).
+static int pair_variant(const kf_field_t *f, const kf_batch_t *w, int n) {
+    if (kf_cluster_path(f, w, n)) return 3;
+    static long long split_below = -1;
+    if (split_below < 0) {
+        const char *env = getenv("KFB200_PAIR_SPLIT_BELOW");
+        split_below = env ? atoll(env) : 40000;
+    }
+    static int env_variant = -1;
+    if (env_variant < 0) {
+        const char *env = getenv("KFB200_PAIR_KERNEL");
+        env_variant = env ? atoi(env) : 0;
+    }
+    const bool split = (long long)w->B * n < split_below;
+    int variant = env_variant ? env_variant : (f->precision ? 1 : split ? 2 : 3);
+    const int chunk = kf_pair_chunk(w->B, n, w->pair_chunk, f->precision);
+    if (variant == 3 && (f->precision || !w->pair_fj || chunk > 16)) variant = f->precision ? 1 : 2;
+    return variant - 1;
+}
+
+extern "C" int kf_pair_kernel_kind(const kf_field_t *f, const kf_batch_t *w, int n) {
+    return pair_variant(f, w, n);
+}
+
 int kf_pairs_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s) {
     // ensembles with fp32 pair math: the cluster-pair kernel (kf_cluster.cu)
     if (kf_cluster_path(f, w, n)) return kf_cluster_pairs_launch(f, w, n, s);

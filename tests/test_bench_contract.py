@@ -35,7 +35,7 @@ def test_bench_line_contract():
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     r = d["roofline"]
     assert set(r) >= {"bound", "achieved", "peak", "unit", "frac", "traffic"} and 0 < r["frac"] < 1
-    assert d["gpu_launches"] >= 3 * 4
+    assert d["gpu_launches"] >= 3 * 3   # FK, pairs, torque step per iteration (+ binning in water)
     assert set(d["clocks"]) >= {"sm_mhz", "sm_max_mhz", "reasons"}
     c = d["cpu_baseline"]
     assert set(c) >= {"value", "unit", "cores", "kind", "sample"} and c["kind"] in ("port", "reference")

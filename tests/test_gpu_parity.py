@@ -669,3 +669,41 @@ def test_forcefield_api_deterministic_bincount_order():
     from paper_1712_05012_b200.forcefield import accumulate_pair_forces
     acc = accumulate_pair_forces(len(g["positions"]), g["positions"], i[kv], j[kv], d[kv], mv)
     assert np.array_equal(acc, ref)
+
+
+def _abs_pair_energy(params, w, ex):
+    """sum_ij |e_ij| over the elec and vdW pairs: the scale of fp32 energy rounding
+    (the totals cancel: a compact 4-residue chain has |g| ~ 1e-2 sum |e_ij|)."""
+    i, j, d = ex["i"], ex["j"], ex["d"]
+    ke, kv = d <= 9.0, d <= 5.0
+    ee, _ = O.elec_terms(params, i[ke], j[ke], d[ke], O.pair_weights(w, i[ke], j[ke], "elec"))
+    ev, _ = O.vdw_terms(params, i[kv], j[kv], d[kv], O.pair_weights(w, i[kv], j[kv], "vdw"))
+    return float(np.abs(ee).sum() + np.abs(ev).sum())
+
+
+def test_scans_match_oracle():
+    """ramachandran_scan / hinge_scan (kcm.py:358-419) against the oracle's
+    evaluation of the same grid conformations: totals within 1e-6 of the pair
+    energies' magnitude sum (the fp32 pair math's rounding scale)."""
+    P = _P()
+    ch, params, w, fld = make_system(["ALA", "SER", "CYS", "ALA"])
+    of = O.OracleField(params, w)
+    grid = P.ramachandran_scan(ch, 2, 5, fld)
+    conf = ch.conf_zp()
+    for a in range(grid.g_total.shape[0]):
+        for b in range(grid.g_total.shape[1]):
+            th = conf.theta.copy()
+            th[ch.dof_phi(2)] = grid.axes[0][a] + 180.0
+            th[ch.dof_psi(2)] = grid.axes[1][b] + 180.0
+            _, e, ex = of.evaluate(O.fk(ch, th)[3])
+            assert abs(grid.g_total[a, b] - sum(e)) <= 1e-6 * _abs_pair_energy(params, w, ex), (a, b)
+    dofs = [ch.dof_phi(1), ch.dof_psi(1)]
+    hg = P.hinge_scan(ch, dofs, 30.0, 3, fld, conf)
+    assert hg.g_total.shape == (3, 3)
+    for a in range(3):
+        for b in range(3):
+            th = conf.theta.copy()
+            th[dofs[0]] = np.mod(conf.theta[dofs[0]] + hg.axes[0][a], 360.0)
+            th[dofs[1]] = np.mod(conf.theta[dofs[1]] + hg.axes[1][b], 360.0)
+            _, e, ex = of.evaluate(O.fk(ch, th)[3])
+            assert abs(hg.g_total[a, b] - sum(e)) <= 1e-6 * _abs_pair_energy(params, w, ex), (a, b)
