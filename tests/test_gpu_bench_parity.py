@@ -12,9 +12,10 @@ Each ensemble test runs ``fold_ensemble``'s runner at the batch size that
 selects a given kernel decomposition.  The kernel choice (kf_pairs_launch,
 kf_bin_launch, kf_torque_launch) depends on the batch B:
 
-* B = 1024 is the bench's C5 configuration;
+* B = 1024 is the bench's C5 configuration (cluster-pair kernel);
 * B = 384 is the first B with 256-thread torque CTAs;
-* B = 32 is the first fused-binning B.
+* B = 128 takes the dense half-list kernel with fixed-point j forces;
+* B = 32 is the first fused-binning B (dense full list).
 
 The comparison covers the first 32 trajectories, against the goldens.  The
 iteration's forces are read from the batch's force buffer (the test hook).
@@ -82,7 +83,7 @@ def _one_iteration_ensemble(B, solvation=False, iters=1):
     return thetas, forces, runner.result(), sa
 
 
-@pytest.mark.parametrize("B", [32, 384, 1024])
+@pytest.mark.parametrize("B", [32, 128, 384, 1024])
 def test_ensemble_iteration_matches_reference(B):
     """One iteration of the bench ensemble: forces, energies, tau_max, theta'
     and pair counts of the first 32 trajectories vs kinefold."""
