@@ -198,6 +198,24 @@ def forward_kinematics(chain, conf: Conformation) -> np.ndarray:
     return device.kinematic_state(chain, conf.theta, positions_only=True)
 
 
+def measure_backbone_dihedrals(chain: Chain, positions: np.ndarray):
+    """(phi, psi) of every residue measured from coordinates, NaN where the
+    neighbouring residue is missing (chain.py:279-294 of the reference: phi from
+    C(i-1), N, CA, C; psi from N, CA, C, N(i+1)).  Host geometry, not on the
+    iteration's path."""
+    m = chain.n_residues
+    pos = np.asarray(positions, float)
+    phi = np.full(m, np.nan)
+    psi = np.full(m, np.nan)
+    for r in range(m):
+        n_r, ca_r, c_r = (pos[chain.atom_index(r, a)] for a in ("N", "CA", "C"))
+        if r > 0:
+            phi[r] = dihedral_angle(pos[chain.atom_index(r - 1, "C")], n_r, ca_r, c_r)
+        if r + 1 < m:
+            psi[r] = dihedral_angle(n_r, ca_r, c_r, pos[chain.atom_index(r + 1, "N")])
+    return phi, psi
+
+
 def link_transforms(chain, conf: Conformation) -> list:
     state = kinematic_state(chain, conf)
     out = [None] * (len(chain.links) - 1)

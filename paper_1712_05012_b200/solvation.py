@@ -116,6 +116,10 @@ def force_quantum(params, r_off: np.ndarray, nq: int, delta_r: float):
     return np.round(delta / quantum).astype(np.int64), quantum
 
 
+# the reference's private name (solvation.py:184), kept for code written against it
+_force_quantum = force_quantum
+
+
 def sample_groups(points: np.ndarray, size: int = 32):
     """Order the sample directions into compact groups of <= `size` for the hot
     solvation kernel (one warp per group, lane = sample).
