@@ -194,3 +194,27 @@ def test_water_fold_matches_reference(B):
     assert abs(E[0, 2] - ref_E[0, 2]) <= 1e-12 * abs(ref_E[0, 2])
     assert np.all(np.abs(tm - g["fold_tau_max"]) <= 1e-5 * g["fold_tau_max"])
     assert _wrapped(final, g["fold_final"]).max() <= 1e-5 * KAPPA
+
+
+@pytest.mark.parametrize("B", [128, 256])
+def test_ensemble_bitwise_repeatable(B):
+    """Run-to-run bitwise determinism of the batched kernels (dense half list at
+    B = 128, cluster pairs at B = 256): every force sum is an order-free integer
+    fixed point or a fixed-order tree, so a data race (shared-memory or global)
+    would show up here as a difference.  (compute-sanitizer is closed on this
+    GPU pool: profiles/r2_compute_sanitizer_refused.txt.)"""
+    from paper_1712_05012_b200 import device as DV
+    from paper_1712_05012_b200 import workloads
+    P = _P()
+    ch, params, w, fld = _system("C2")
+    thetas = workloads.random_thetas(ch, B, seed=2)
+    step = P.StepConfig(kappa=0.5, max_iters=5, torque_tol_rel=0.0, energy_window=0)
+    out = []
+    for _ in range(2):
+        runner = DV.EnsembleRunner(ch, fld, B, step)
+        runner.load(thetas, np.zeros((B, ch.n_dof), bool))
+        runner.run()
+        res = runner.result()
+        out.append((res.theta.copy(), res.energies.copy(), runner.batch.t["forces"].cpu().numpy()))
+    for a, b in zip(out[0], out[1]):
+        assert np.array_equal(a, b)
