@@ -198,19 +198,97 @@ __device__ __noinline__ int near_class(const kf_field_t &f, int Q, int O, int la
     return 4;
 }
 
+// One warp round: quad Q (i = 4 Q + ii) against octet O (j = 8 O + js), 32 pairs.
+// GEN: the octet may hold class < 4 pairs or the quad's own atoms (class codes,
+// own-octet test); otherwise every pair is class 4.  Pairs inside a threshold
+// band or closer than f64_d2 (nonzero weight) are queued for the exact path.
+template <bool DCONST, int NCAP, bool GEN>
+KF_DEV void round(const kf_field_t &f, const ClConst &c, unsigned sb, int n, int O, int O0, int Q, int i, bool vi,
+                  int ii, int js, int lane, float oix, float oiy, float oiz, const float4 &ci, float qK, float qK4,
+                  float ws4, const float2 &ri, bool vdw_round, float &fx, float &fy, float &fz, float &ee,
+                  float &ev, int &ce, int &cv, unsigned *exq, int exq_cap, int *exq_n) {
+    using L = ClLayout<NCAP>;
+    const float4 oc = lds4(sb + L::OCT_C + 16 * O);
+    const int j = 8 * O + js;
+    const float4 oj = lds4(sb + L::OQ + 16 * j);
+    const float2 rj = lds2(sb + L::RS + 8 * j);
+    const float dx = (oix - oj.x) + (ci.x - oc.x);   // frame shift exact
+    const float dy = (oiy - oj.y) + (ci.y - oc.y);
+    const float dz = (oiz - oj.z) + (ci.z - oc.z);
+    const float d2 = dx * dx + dy * dy + dz * dz;
+    bool live = vi;
+    float qq = qK4 * oj.w, weps = ws4 * rj.y;
+    bool wnz = (c.wnz_mask >> 3) & 1;
+    int code = 0;                                    // 4 - class
+    if (GEN) {
+        if (O == O0) live &= j > i;                  // own octet: each pair once
+        if (!c.uniform) {
+            const int k = O - O0;
+            if (k <= 4)
+                code = (int)((f.class_codes[5 * Q + k] >> (2 * lane)) & 3ull);
+            else if (live && j < n && f.class_slow[i])
+                code = 4 - cl_slow_class(f, i, j);   // tree partner beyond the window
+            qq = qK * c.we[3 - code] * oj.w;
+            weps = c.wv[3 - code] * ri.y * rj.y;
+            wnz = (c.wnz_mask >> (3 - code)) & 1;
+        }
+    }
+    // exact path (queued): inside a threshold band, or closer than f64_d2 with a
+    // nonzero weight (or at clash range whatever the weight)
+    const float dev = fminf(fminf(fabsf(d2 - c.cut2), fabsf(d2 - c.tv2)), fabsf(d2 - c.te2));
+    const bool exact = live && ((dev <= c.band) | ((d2 < c.f64_d2) & (wnz | (d2 < 1e-4f))));
+    const unsigned em = __ballot_sync(FULL, exact);
+    if (em) {
+        int base = 0;
+        if (lane == __ffs(em) - 1) base = atomicAdd(exq_n, __popc(em));
+        base = __shfl_sync(FULL, base, __ffs(em) - 1);
+        const int slot = base + __popc(em & ((1u << lane) - 1u));
+        if (exact && slot < exq_cap) exq[slot] = (unsigned)i | ((unsigned)j << 12) | ((unsigned)code << 24);
+    }
+    const bool fast = live && !exact && d2 < c.cutlo;
+    if (!__any_sync(FULL, fast)) return;
+    float inv_r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(inv_r) : "f"(d2));
+    const float inv_r2 = inv_r * inv_r;
+    const bool ke = fast && d2 <= c.te2;
+    const float e = DCONST ? qq * c.kap_inv * inv_r : qq * inv_r2;
+    float g = ke ? e * inv_r2 : 0.f;
+    ee += ke ? e : 0.f;
+    ce += ke;
+    if (vdw_round) {   // boxes within the vdW reach
+        const bool kv = fast && d2 <= c.tv2;
+        const float D = ri.x + rj.x;
+        const float sr = D * D * inv_r2;
+        const float s3 = sr * sr * sr;
+        const float s6 = s3 * s3;
+        ev += kv ? weps * (s6 - 2.f * s3) : 0.f;
+        g = kv ? __fmaf_rn(12.f * weps * (s6 - s3), inv_r2, g) : g;
+        cv += kv;
+    }
+    const float gx = g * dx, gy = g * dy, gz = g * dz;
+    fx += gx; fy += gy; fz += gz;
+    // force on j = -(sum over the quad's 4 lanes)
+    float tx = gx, ty = gy, tz = gz;
+    tx += __shfl_xor_sync(FULL, tx, 1); ty += __shfl_xor_sync(FULL, ty, 1); tz += __shfl_xor_sync(FULL, tz, 1);
+    tx += __shfl_xor_sync(FULL, tx, 2); ty += __shfl_xor_sync(FULL, ty, 2); tz += __shfl_xor_sync(FULL, tz, 2);
+    const float v = ii == 0 ? tx : (ii == 1 ? ty : tz);
+    if (ii < 3 && j < n && v != 0.f) acc_add<NCAP>(sb, 3 * j + ii, __float2ll_rn(-v * FIXF));
+}
+
 template <bool DCONST, int NCAP>
 __global__ void __launch_bounds__(CL_WARPS * 32, NCAP <= 1536 ? CL_MINB : 1)
 cluster_pair_kernel(const __grid_constant__ kf_field_t f, const __grid_constant__ ClConst c, int n,
                     const double *__restrict__ pos_all, double *__restrict__ forces, double *__restrict__ e_atom,
-                    long long *__restrict__ pair_count, kf_status_t *status, long long *__restrict__ planes) {
+                    long long *__restrict__ pair_count, kf_status_t *status, long long *__restrict__ planes,
+                    unsigned *__restrict__ exq_all, int exq_cap) {
     using L = ClLayout<NCAP>;
     constexpr int CL_THREADS = CL_WARPS * 32;
     const int b = blockIdx.x;
     if (status[b].done) return;
     extern __shared__ __align__(16) unsigned char sm[];
-    __shared__ int next_q, slow_used, extent_bad;
+    __shared__ int next_q, extent_bad, exq_n;
     __shared__ unsigned cnt_e, cnt_v;
-    __shared__ double2 slow_e[CL_WARPS];
+    __shared__ double red_e[CL_WARPS][2];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int no = (n + 7) / 8, nq = (n + 3) / 4;
     const unsigned base = smem_u32(sm);
@@ -220,7 +298,11 @@ cluster_pair_kernel(const __grid_constant__ kf_field_t f, const __grid_constant_
     // each quad's (elec, vdW) energy goes to e_atom[quad] (global scratch, read back
     // in quad order at the end; the totals then sit at atom 0)
     double *e_q = e_atom + 2 * (size_t)b * n;
-    if (threadIdx.x == 0) { next_q = CL_WARPS; slow_used = 0; extent_bad = 0; cnt_e = 0; cnt_v = 0; }
+    if (threadIdx.x == 0) { next_q = CL_WARPS; extent_bad = 0; cnt_e = 0; cnt_v = 0; exq_n = 0; }
+    // exact-path pairs are queued (packed i | j << 12 | class << 24) into this
+    // trajectory's share of a scratch buffer and evaluated after the sweep, in
+    // sorted order (deterministic), off the hot loop
+    unsigned *exq = exq_all + (size_t)b * exq_cap * 2;
 
     // ---- 1. frames: octet and quad grid centres, half-extent boxes, offsets ----
     for (int a0 = 32 * warp; a0 < 8 * no; a0 += 32 * CL_WARPS) {
@@ -304,8 +386,6 @@ cluster_pair_kernel(const __grid_constant__ kf_field_t f, const __grid_constant_
         const bool slow_q = !c.uniform && __any_sync(FULL, vi && aaux[vi ? i : 0].w != 0);
         float fx = 0.f, fy = 0.f, fz = 0.f, ee = 0.f, ev = 0.f;
         int ce = 0, cv = 0;
-        if (lane_p == 0) slow_e[warp] = make_double2(0.0, 0.0);   // exact-path energies of this quad
-        __syncwarp();
         const int O0 = Q >> 1;
         for (int ob = O0; ob < no; ob += 32) {
             // box pretest of 32 candidate octets at once: gap between [ci + blo,
@@ -323,80 +403,26 @@ cluster_pair_kernel(const __grid_constant__ kf_field_t f, const __grid_constant_
             }
             unsigned cand = __ballot_sync(FULL, bd2 <= c.pre2);
             const unsigned vmask = __ballot_sync(FULL, bd2 <= c.pre2v);
+            // rounds whose octet lies in the quad's 64-atom class window (O <= O0 + 4, only
+            // in the first block) or may hold a slow atom's tree partner take the
+            // general path; all others are class 4 with no own-octet test
+            const unsigned gen = c.uniform ? (ob == O0 ? 1u : 0u)
+                                           : (slow_q ? ~0u : (ob == O0 ? 0x1fu : 0u));
+            unsigned cand_gen = cand & gen;
+            cand &= ~gen;
+            while (cand_gen) {
+                const int t = __ffs(cand_gen) - 1;
+                cand_gen &= cand_gen - 1u;
+                round<DCONST, NCAP, true>(f, c, sb, n, ob + t, O0, Q, i, vi, ii, js, lane_p, oix, oiy, oiz, ci,
+                                          qK, qK4, ws4, ri, (vmask >> t) & 1u, fx, fy, fz, ee, ev, ce, cv,
+                                          exq, exq_cap, &exq_n);
+            }
             while (cand) {
                 const int t = __ffs(cand) - 1;
                 cand &= cand - 1u;
-                const int O = ob + t;
-                const float4 oc = lds4(sb + L::OCT_C + 16 * O);
-                const int j = 8 * O + js;
-                const float4 oj = lds4(sb + L::OQ + 16 * j);
-                const float2 rj = lds2(sb + L::RS + 8 * j);
-                const float dx = (oix - oj.x) + (ci.x - oc.x);   // frame shift exact
-                const float dy = (oiy - oj.y) + (ci.y - oc.y);
-                const float dz = (oiz - oj.z) + (ci.z - oc.z);
-                const float d2 = dx * dx + dy * dy + dz * dz;
-                bool live = vi;
-                if (O == O0) live &= j > i;              // own octet: each pair once
-                float qq = qK4 * oj.w, weps = ws4 * rj.y;
-                bool wnz = (c.wnz_mask >> 3) & 1;
-                int cls = 4;
-                // class 4 unless the octet lies in the quad's 64-atom window (host-built
-                // codes) or a slow atom's tree partner may be here (class_window)
-                if (!c.uniform && (O - O0 <= 4 || slow_q)) {
-                    if (O - O0 <= 4)
-                        cls = 4 - (int)((f.class_codes[5 * Q + (O - O0)] >> (2 * lane_p)) & 3ull);
-                    else if (live && j < n && f.class_slow[i])
-                        cls = cl_slow_class(f, i, j);
-                    qq = qK * c.we[cls - 1] * oj.w;
-                    weps = c.wv[cls - 1] * ri.y * rj.y;
-                    wnz = (c.wnz_mask >> (cls - 1)) & 1;
-                }
-                // exact path: inside a threshold band, or closer than f64_d2 with a
-                // nonzero weight (or at clash range whatever the weight)
-                const float dev = fminf(fminf(fabsf(d2 - c.cut2), fabsf(d2 - c.tv2)), fabsf(d2 - c.te2));
-                const bool exact = live && ((dev <= c.band) | ((d2 < c.f64_d2) & (wnz | (d2 < 1e-4f))));
-                if (__any_sync(FULL, exact)) {
-                    double se[2] = {0.0, 0.0};
-                    if (exact) {
-                        const int2 k2 = cl_exact_pair(f, pos, i, j, cls, planes, 3LL * gridDim.x * n,
-                                                      (size_t)b * n, status + b, se);
-                        ce += k2.x; cv += k2.y;
-                    }
-                    // fixed lane tree, then in round order: deterministic
-                    const double te = warp_sum(se[0]), tv = warp_sum(se[1]);
-                    if (lane_p == 0) {
-                        slow_e[warp].x += te; slow_e[warp].y += tv;
-                        slow_used = 1;
-                    }
-                }
-                const bool fast = live && !exact && d2 < c.cutlo;
-                if (!__any_sync(FULL, fast)) continue;
-                float inv_r;
-                asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(inv_r) : "f"(d2));
-                const float inv_r2 = inv_r * inv_r;
-                const bool ke = fast && d2 <= c.te2;
-                const float e = DCONST ? qq * c.kap_inv * inv_r : qq * inv_r2;
-                float g = ke ? e * inv_r2 : 0.f;
-                ee += ke ? e : 0.f;
-                ce += ke;
-                if ((vmask >> t) & 1u) {   // boxes within the vdW reach
-                    const bool kv = fast && d2 <= c.tv2;
-                    const float D = ri.x + rj.x;
-                    const float sr = D * D * inv_r2;
-                    const float s3 = sr * sr * sr;
-                    const float s6 = s3 * s3;
-                    ev += kv ? weps * (s6 - 2.f * s3) : 0.f;
-                    g = kv ? __fmaf_rn(12.f * weps * (s6 - s3), inv_r2, g) : g;
-                    cv += kv;
-                }
-                const float gx = g * dx, gy = g * dy, gz = g * dz;
-                fx += gx; fy += gy; fz += gz;
-                // force on j = -(sum over the quad's 4 lanes)
-                float tx = gx, ty = gy, tz = gz;
-                tx += __shfl_xor_sync(FULL, tx, 1); ty += __shfl_xor_sync(FULL, ty, 1); tz += __shfl_xor_sync(FULL, tz, 1);
-                tx += __shfl_xor_sync(FULL, tx, 2); ty += __shfl_xor_sync(FULL, ty, 2); tz += __shfl_xor_sync(FULL, tz, 2);
-                const float v = ii == 0 ? tx : (ii == 1 ? ty : tz);
-                if (ii < 3 && j < n && v != 0.f) acc_add<NCAP>(sb, 3 * j + ii, __float2ll_rn(-v * FIXF));
+                round<DCONST, NCAP, false>(f, c, sb, n, ob + t, O0, Q, i, vi, ii, js, lane_p, oix, oiy, oiz, ci,
+                                           qK, qK4, ws4, ri, (vmask >> t) & 1u, fx, fy, fz, ee, ev, ce, cv,
+                                           exq, exq_cap, &exq_n);
             }
         }
         // i forces: sum over the 8 j-lanes of each i, then into the fixed point
@@ -419,8 +445,8 @@ cluster_pair_kernel(const __grid_constant__ kf_field_t f, const __grid_constant_
         const int tce = __reduce_add_sync(FULL, ce), tcv = __reduce_add_sync(FULL, cv);
         __syncwarp();
         if (lane_p == 0) {
-            e_q[2 * Q] = (double)ee + slow_e[warp].x;
-            e_q[2 * Q + 1] = (double)ev + slow_e[warp].y;
+            e_q[2 * Q] = (double)ee;
+            e_q[2 * Q + 1] = (double)ev;
             atomicAdd(&cnt_e, (unsigned)tce);
             atomicAdd(&cnt_v, (unsigned)tcv);
             Q = atomicAdd(&next_q, 1);
@@ -429,8 +455,48 @@ cluster_pair_kernel(const __grid_constant__ kf_field_t f, const __grid_constant_
     }
     __syncthreads();
 
+    // ---- 2b. the queued exact-path pairs: sorted (unique keys: a rank sort), then
+    // evaluated in fp64 (forces into the global fixed-point planes), energies summed
+    // per thread in sorted order and over the block in a fixed tree: deterministic
+    const int m = exq_n;
+    double xe = 0.0, xv = 0.0;
+    if (m > 0) {
+        if (m > exq_cap) {
+            if (threadIdx.x == 0 && atomicCAS(&status[b].error, KF_ERR_NONE, KF_ERR_CAPACITY) == KF_ERR_NONE) {
+                status[b].err_iter = status[b].iter;
+                status[b].overflow = -m;   // negative: the exact-pair queue (not solvation)
+            }
+        } else {
+            unsigned *sorted = exq + exq_cap;
+            for (int e = threadIdx.x; e < m; e += CL_THREADS) {
+                const unsigned key = exq[e];
+                const unsigned k = (key & 0xffffffu) | ((key >> 24) << 30);   // order by (j, i), class last
+                int r = 0;
+                for (int q = 0; q < m; ++q) {
+                    const unsigned o = exq[q];
+                    r += ((o & 0xffffffu) | ((o >> 24) << 30)) < k;
+                }
+                sorted[r] = key;
+            }
+            __syncthreads();
+            const long long plane = 3LL * gridDim.x * n;
+            for (int e = threadIdx.x; e < m; e += CL_THREADS) {
+                const unsigned key = sorted[e];
+                double se[2] = {0.0, 0.0};
+                const int2 k2 = cl_exact_pair(f, pos, (int)(key & 0xfffu), (int)((key >> 12) & 0xfffu),
+                                              4 - (int)(key >> 24), planes, plane, (size_t)b * n, status + b, se);
+                xe += se[0]; xv += se[1];
+                if (k2.x) atomicAdd(&cnt_e, (unsigned)k2.x);
+                if (k2.y) atomicAdd(&cnt_v, (unsigned)k2.y);
+            }
+        }
+    }
+    xe = warp_sum(xe); xv = warp_sum(xv);
+    if (lane == 0) { red_e[warp][0] = xe; red_e[warp][1] = xv; }
+    __syncthreads();
+
     // ---- 3. forces out (+ the exact-path planes if any), energies, counts ----
-    const bool with_planes = slow_used != 0;
+    const bool with_planes = m > 0;
     const size_t nb = (size_t)b * n;
     const long long plane = 3LL * gridDim.x * n;
     const unsigned *acc_lo = reinterpret_cast<const unsigned *>(sm + L::ACC_LO);
@@ -456,6 +522,7 @@ cluster_pair_kernel(const __grid_constant__ kf_field_t f, const __grid_constant_
         for (int q = lane; q < nq; q += 32) { de += e_q[2 * q]; dv += e_q[2 * q + 1]; }
         de = warp_sum(de);
         dv = warp_sum(dv);
+        for (int w2 = 0; w2 < CL_WARPS; ++w2) { de += red_e[w2][0]; dv += red_e[w2][1]; }   // exact pairs
         if (lane == 0) {   // doubled: the energy reduction halves (full-list convention)
             e_atom[2 * nb] = 2.0 * de;
             e_atom[2 * nb + 1] = 2.0 * dv;
@@ -473,8 +540,10 @@ inline int launch_cap(bool dconst, const kf_field_t *f, const ClConst &c, kf_bat
         KF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "cluster smem");
         opted[dconst] = true;
     }
+    // exact-pair queue + its sorted copy: the SoA low-word buffer ([B][n][4] u32), which
+    // the cluster path does not otherwise use (binning writes it, nothing later reads it)
     kern<<<w->B, CL_WARPS * 32, smem, s>>>(*f, c, n, w->pos, w->forces, w->e_atom, w->pair_count, w->status,
-                                          w->pair_fj);
+                                          w->pair_fj, reinterpret_cast<unsigned *>(w->s_lo), 2 * n);
     KF_LAUNCH_CHECK("cluster_pair_kernel");
     return 0;
 }

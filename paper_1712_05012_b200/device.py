@@ -552,6 +552,9 @@ def _raise_status(st, df: DeviceField | None, batch: Batch, prefix: str = "", b:
         raise ConfigurationError(f"{prefix}use_hash=False: an atom lies more than 2048 A from the structure's "
                                  "centroid cell (fp32 offset range of the all-pairs layout)")
     if st.error == N.ERR_CAPACITY:
+        if st.overflow < 0:   # the cluster-pair kernel's exact-path queue (2 n pairs)
+            raise NativeLibraryError(f"{prefix}{-st.overflow} pairs need the exact fp64 path, more than the "
+                                     f"cluster-pair kernel's queue of {2 * batch.n}")
         raise NativeLibraryError(f"{prefix}solvation neighbour capacity exceeded "
                                  f"({st.overflow} > {batch.struct.nb_cap})")
 
