@@ -203,10 +203,11 @@ __device__ __noinline__ int near_class(const kf_field_t &f, int Q, int O, int la
 // own-octet test); otherwise every pair is class 4.  Pairs inside a threshold
 // band or closer than f64_d2 (nonzero weight) are queued for the exact path.
 template <bool DCONST, int NCAP, bool GEN>
-KF_DEV void round(const kf_field_t &f, const ClConst &c, unsigned sb, int n, int O, int O0, int Q, int i, bool vi,
+KF_DEV void round(const kf_field_t &f, const ClConst &c, const unsigned long long *qcodes, unsigned sb, int n, int O,
+                  int O0, int Q, int i, bool vi,
                   int ii, int js, int lane, float oix, float oiy, float oiz, const float4 &ci, float qK, float qK4,
-                  float ws4, const float2 &ri, bool vdw_round, float &fx, float &fy, float &fz, float &ee,
-                  float &ev, int &ce, int &cv, unsigned *exq, int exq_cap, int *exq_n) {
+                  float ws4, const float2 &ri, bool vdw_round, bool wnz4, float &fx, float &fy, float &fz,
+                  float &ee, float &ev, int &ce, int &cv, unsigned *exq, int exq_cap, int *exq_n) {
     using L = ClLayout<NCAP>;
     const float4 oc = lds4(sb + L::OCT_C + 16 * O);
     const int j = 8 * O + js;
@@ -218,14 +219,14 @@ KF_DEV void round(const kf_field_t &f, const ClConst &c, unsigned sb, int n, int
     const float d2 = dx * dx + dy * dy + dz * dz;
     bool live = vi;
     float qq = qK4 * oj.w, weps = ws4 * rj.y;
-    bool wnz = (c.wnz_mask >> 3) & 1;
+    bool wnz = wnz4;
     int code = 0;                                    // 4 - class
     if (GEN) {
         if (O == O0) live &= j > i;                  // own octet: each pair once
         if (!c.uniform) {
             const int k = O - O0;
-            if (k <= 4)
-                code = (int)((f.class_codes[5 * Q + k] >> (2 * lane)) & 3ull);
+            if (k <= 4)   // the quad's 5 window codes, staged per warp at the quad's start
+                code = (int)((qcodes[k] >> (2 * lane)) & 3ull);
             else if (live && j < n && f.class_slow[i])
                 code = 4 - cl_slow_class(f, i, j);   // tree partner beyond the window
             qq = qK * c.we[3 - code] * oj.w;
@@ -236,7 +237,7 @@ KF_DEV void round(const kf_field_t &f, const ClConst &c, unsigned sb, int n, int
     // exact path (queued): inside a threshold band, or closer than f64_d2 with a
     // nonzero weight (or at clash range whatever the weight)
     const float dev = fminf(fminf(fabsf(d2 - c.cut2), fabsf(d2 - c.tv2)), fabsf(d2 - c.te2));
-    const bool exact = live && ((dev <= c.band) | ((d2 < c.f64_d2) & (wnz | (d2 < 1e-4f))));
+    const bool exact = live & ((dev <= c.band) | ((d2 < c.f64_d2) & (wnz | (d2 < 1e-4f))));
     const unsigned em = __ballot_sync(FULL, exact);
     if (em) {
         int base = 0;
@@ -245,7 +246,7 @@ KF_DEV void round(const kf_field_t &f, const ClConst &c, unsigned sb, int n, int
         const int slot = base + __popc(em & ((1u << lane) - 1u));
         if (exact && slot < exq_cap) exq[slot] = (unsigned)i | ((unsigned)j << 12) | ((unsigned)code << 24);
     }
-    const bool fast = live && !exact && d2 < c.cutlo;
+    const bool fast = live & !exact & (d2 < c.cutlo);
     if (!__any_sync(FULL, fast)) return;
     float inv_r;
     asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(inv_r) : "f"(d2));
@@ -271,8 +272,9 @@ KF_DEV void round(const kf_field_t &f, const ClConst &c, unsigned sb, int n, int
     float tx = gx, ty = gy, tz = gz;
     tx += __shfl_xor_sync(FULL, tx, 1); ty += __shfl_xor_sync(FULL, ty, 1); tz += __shfl_xor_sync(FULL, tz, 1);
     tx += __shfl_xor_sync(FULL, tx, 2); ty += __shfl_xor_sync(FULL, ty, 2); tz += __shfl_xor_sync(FULL, tz, 2);
+    // (padding atoms past n have accumulator words too: the layout holds NCAP >= 8 no atoms)
     const float v = ii == 0 ? tx : (ii == 1 ? ty : tz);
-    if (ii < 3 && j < n && v != 0.f) acc_add<NCAP>(sb, 3 * j + ii, __float2ll_rn(-v * FIXF));
+    if (ii < 3 && v != 0.f) acc_add<NCAP>(sb, 3 * j + ii, __float2ll_rn(-v * FIXF));
 }
 
 template <bool DCONST, int NCAP>
@@ -289,6 +291,7 @@ cluster_pair_kernel(const __grid_constant__ kf_field_t f, const __grid_constant_
     __shared__ int next_q, extent_bad, exq_n;
     __shared__ unsigned cnt_e, cnt_v;
     __shared__ double red_e[CL_WARPS][2];
+    __shared__ unsigned long long qcodes[CL_WARPS][5];   // the current quad's window class codes
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int no = (n + 7) / 8, nq = (n + 3) / 4;
     const unsigned base = smem_u32(sm);
@@ -363,6 +366,8 @@ cluster_pair_kernel(const __grid_constant__ kf_field_t f, const __grid_constant_
     unsigned sb = base;
     asm volatile("" : "+r"(lane_p), "+r"(sb));
     const int ii = lane_p & 3, js = lane_p >> 2;
+    const bool wnz4 = (c.wnz_mask >> 3) & 1;          // class 4 has a nonzero weight
+    int ce = 0, cv = 0;                               // pair counts: integers, order-free across quads
     int Q = warp;
     while (Q < nq) {
         const int i = 4 * Q + ii;
@@ -384,8 +389,9 @@ cluster_pair_kernel(const __grid_constant__ kf_field_t f, const __grid_constant_
         const float qK = (float)COULOMB_K * oi.w;        // K q_i
         const float qK4 = qK * c.we[3], ws4 = ri.y * c.wv[3];
         const bool slow_q = !c.uniform && __any_sync(FULL, vi && aaux[vi ? i : 0].w != 0);
+        if (!c.uniform && lane_p < 5) qcodes[warp][lane_p] = f.class_codes[5 * Q + lane_p];
+        __syncwarp();
         float fx = 0.f, fy = 0.f, fz = 0.f, ee = 0.f, ev = 0.f;
-        int ce = 0, cv = 0;
         const int O0 = Q >> 1;
         for (int ob = O0; ob < no; ob += 32) {
             // box pretest of 32 candidate octets at once: gap between [ci + blo,
@@ -413,16 +419,16 @@ cluster_pair_kernel(const __grid_constant__ kf_field_t f, const __grid_constant_
             while (cand_gen) {
                 const int t = __ffs(cand_gen) - 1;
                 cand_gen &= cand_gen - 1u;
-                round<DCONST, NCAP, true>(f, c, sb, n, ob + t, O0, Q, i, vi, ii, js, lane_p, oix, oiy, oiz, ci,
-                                          qK, qK4, ws4, ri, (vmask >> t) & 1u, fx, fy, fz, ee, ev, ce, cv,
-                                          exq, exq_cap, &exq_n);
+                round<DCONST, NCAP, true>(f, c, qcodes[warp], sb, n, ob + t, O0, Q, i, vi, ii, js, lane_p, oix, oiy,
+                                          oiz, ci, qK, qK4, ws4, ri, (vmask >> t) & 1u, wnz4, fx, fy, fz, ee, ev,
+                                          ce, cv, exq, exq_cap, &exq_n);
             }
             while (cand) {
                 const int t = __ffs(cand) - 1;
                 cand &= cand - 1u;
-                round<DCONST, NCAP, false>(f, c, sb, n, ob + t, O0, Q, i, vi, ii, js, lane_p, oix, oiy, oiz, ci,
-                                           qK, qK4, ws4, ri, (vmask >> t) & 1u, fx, fy, fz, ee, ev, ce, cv,
-                                           exq, exq_cap, &exq_n);
+                round<DCONST, NCAP, false>(f, c, qcodes[warp], sb, n, ob + t, O0, Q, i, vi, ii, js, lane_p, oix, oiy,
+                                           oiz, ci, qK, qK4, ws4, ri, (vmask >> t) & 1u, wnz4, fx, fy, fz, ee, ev,
+                                           ce, cv, exq, exq_cap, &exq_n);
             }
         }
         // i forces: sum over the 8 j-lanes of each i, then into the fixed point
@@ -442,16 +448,17 @@ cluster_pair_kernel(const __grid_constant__ kf_field_t f, const __grid_constant_
             ee += __shfl_xor_sync(FULL, ee, m);
             ev += __shfl_xor_sync(FULL, ev, m);
         }
-        const int tce = __reduce_add_sync(FULL, ce), tcv = __reduce_add_sync(FULL, cv);
         __syncwarp();
         if (lane_p == 0) {
             e_q[2 * Q] = (double)ee;
             e_q[2 * Q + 1] = (double)ev;
-            atomicAdd(&cnt_e, (unsigned)tce);
-            atomicAdd(&cnt_v, (unsigned)tcv);
             Q = atomicAdd(&next_q, 1);
         }
         Q = __shfl_sync(FULL, Q, 0);
+    }
+    {
+        const int tce = __reduce_add_sync(FULL, ce), tcv = __reduce_add_sync(FULL, cv);
+        if (lane_p == 0) { atomicAdd(&cnt_e, (unsigned)tce); atomicAdd(&cnt_v, (unsigned)tcv); }
     }
     __syncthreads();
 

@@ -10,8 +10,10 @@ cd "$root/paper_1712_05012_b200/csrc"
 objs=""
 for f in kf_api kf_kinematics kf_grid kf_nonbonded kf_solvation kf_torque kf_refgrid kf_peak kf_cluster; do
   if [ "$f" = kf_cluster ] || [ ! -f build/$f.o ]; then
-    nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -I../../include \
-      --expt-relaxed-constexpr "$@" -c $f.cu -o "$out/$f.o" &
+    src=$f.cu
+    [ "$f" = kf_cluster ] && [ -n "$CLSRC" ] && src=$CLSRC   # CLSRC: an alternative kf_cluster.cu (A/B)
+    nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -I../../include -I. \
+      --expt-relaxed-constexpr "$@" -c $src -o "$out/$f.o" &
     objs="$objs $out/$f.o"
   else
     objs="$objs build/$f.o"
