@@ -389,7 +389,13 @@ cluster_pair_kernel(const __grid_constant__ kf_field_t f, const __grid_constant_
         const float qK = (float)COULOMB_K * oi.w;        // K q_i
         const float qK4 = qK * c.we[3], ws4 = ri.y * c.wv[3];
         const bool slow_q = !c.uniform && __any_sync(FULL, vi && aaux[vi ? i : 0].w != 0);
-        if (!c.uniform && lane_p < 5) qcodes[warp][lane_p] = f.class_codes[5 * Q + lane_p];
+        // window octets whose 32 pairs are all class 4 (most of k = 3, 4) take the lean path too
+        unsigned win = 1u;                                // the own octet always (j > i test)
+        if (!c.uniform) {
+            unsigned long long code = 0ull;
+            if (lane_p < 5) qcodes[warp][lane_p] = code = f.class_codes[5 * Q + lane_p];
+            win = __ballot_sync(FULL, lane_p < 5 && code != 0ull) | 1u;
+        }
         __syncwarp();
         float fx = 0.f, fy = 0.f, fz = 0.f, ee = 0.f, ev = 0.f;
         const int O0 = Q >> 1;
@@ -412,8 +418,7 @@ cluster_pair_kernel(const __grid_constant__ kf_field_t f, const __grid_constant_
             // rounds whose octet lies in the quad's 64-atom class window (O <= O0 + 4, only
             // in the first block) or may hold a slow atom's tree partner take the
             // general path; all others are class 4 with no own-octet test
-            const unsigned gen = c.uniform ? (ob == O0 ? 1u : 0u)
-                                           : (slow_q ? ~0u : (ob == O0 ? 0x1fu : 0u));
+            const unsigned gen = slow_q ? ~0u : (ob == O0 ? win : 0u);
             unsigned cand_gen = cand & gen;
             cand &= ~gen;
             while (cand_gen) {
