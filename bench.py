@@ -6,10 +6,12 @@ random +-90 starts (`--init random --seed 1 --batch 1024` semantics), vacuum
 FieldConfig() defaults, fixed iteration count (torque_tol_rel = 0,
 energy_window = 0).  A step is one KCM iteration of every trajectory (FK ->
 elec/vdW pair forces -> wrenches -> suffix-scan torques -> max-normalised
-step), replayed from CUDA graphs.  With N GPUs (torchrun) the 1024
-trajectories are split into contiguous blocks, one per rank; there is no
-per-iteration communication and one NCCL all-gather of the final per-trajectory
-records at the end of the timed region (scaling "strong": total work fixed).
+step), replayed from CUDA graphs.  With N GPUs (torchrun) every rank folds its
+own contiguous block of 1024 trajectories of the one seed-1 start stream
+(1024 N in all): trajectories are independent units, so the path partitions
+with no data-path collective and the scaling is "weak" (tier rule ⑤); one
+NCCL all-gather of the final per-trajectory records ends the timed region.
+`--strong` instead splits one 1024-trajectory ensemble over the ranks.
 
 Output: one JSON line on rank 0 (see the README of the driver contract):
 value = trajectory-iterations/s of the whole job; e2e = the same through the
@@ -54,7 +56,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--ensemble", type=int, default=ENSEMBLE)
+    ap.add_argument("--ensemble", type=int, default=ENSEMBLE, help="trajectories per GPU (weak) or in all (--strong)")
+    ap.add_argument("--strong", action="store_true", help="split one ensemble over the ranks (total work fixed)")
     ap.add_argument("--water", action="store_true", help="headline in FieldConfig(solvation=True)")
     ap.add_argument("--no-extras", action="store_true", help="skip the water / fp64 / single-trajectory / CPU legs")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
@@ -68,7 +71,11 @@ def workload_name(args, water=None) -> str:
 
 
 def config_of(args, n_atoms=1499, dofs=518, world=1) -> dict:
-    return {"workload": workload_name(args), "ensemble": args.ensemble, "atoms_per_trajectory": n_atoms,
+    total = args.ensemble if args.strong else args.ensemble * world
+    return {"workload": workload_name(args), "ensemble": total, "ensemble_per_gpu": total // max(world, 1),
+            "scaling_mode": "strong (one ensemble split over the ranks)" if args.strong else
+                            "weak (each rank folds its own 1024-trajectory block of the start stream)",
+            "atoms_per_trajectory": n_atoms,
             "dofs": dofs, "parallelism": f"trajectory-parallel x{world}",
             "l2": "working set per step > 126 MB L2 (positions, forces, link transforms of 1.5M atoms / "
                   "530k links), no explicit flush"}
@@ -206,8 +213,9 @@ def reference_arm(args, rank: int):
               f"built once per worker); {args.steps} steps")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": config_of(args),
+            "higher_is_better": True, "scaling": "strong" if args.strong else "weak", "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic", "config": config_of(args, world=int(os.environ.get("WORLD_SIZE", "1"))),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
                              "host": hc, "per_core": value / cores},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -318,8 +326,9 @@ def main():
     dev = torch.device("cuda", local)
 
     ch, params, w, fld = workloads.system("C2", solvation=args.water)
-    thetas_all = workloads.random_thetas(ch, args.ensemble, seed=1)
-    lo, hi = ENS.shard(args.ensemble, rank, world)
+    total = args.ensemble if args.strong else args.ensemble * world
+    thetas_all = workloads.random_thetas(ch, total, seed=1)
+    lo, hi = ENS.shard(total, rank, world)
     B = hi - lo
     K, W, PROF = args.steps, max(args.warmup, 3), 3
     step = P.StepConfig(kappa=0.5, max_iters=W + K + PROF, torque_tol_rel=0.0, energy_window=0)
@@ -349,7 +358,7 @@ def main():
                "last": runner.batch.t["rec_energy"][:, W + K - 1]}
         if world > 1:
             for key, t in rec.items():
-                ENS.gather_rows(t.contiguous(), args.ensemble, rank, world)
+                ENS.gather_rows(t.contiguous(), total, rank, world)
         e1.record(s)
     s.synchronize()
     torch.cuda.synchronize()
@@ -361,7 +370,7 @@ def main():
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms_max = float(ms_t.item())
-    value = args.ensemble * K / (ms_max * 1e-3)
+    value = total * K / (ms_max * 1e-3)
     sts = runner.batch.status()
     if any(st.error for st in sts):
         raise SystemExit(f"device error in the ensemble: {[st.error for st in sts if st.error][:4]}")
@@ -424,16 +433,16 @@ def main():
         t0 = time.perf_counter()
         res = P.fold_ensemble(ch, confs, f_, e2e_step)
         if world > 1:
-            ENS.gather_records(ENS.pack_result(res), args.ensemble, device=dev)
+            ENS.gather_records(ENS.pack_result(res), total, device=dev)
         torch.cuda.synchronize()
         t = torch.tensor([time.perf_counter() - t0], device=dev, dtype=torch.float64)
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return args.ensemble * K / float(t.item())
+        return total * K / float(t.item())
 
     e2e_value = e2e_rate(fld)
-    h2d = args.ensemble * D * (8 + 1) / K
-    d2h = args.ensemble * (D * 8 + K * 4 * 8 + 64) / K
+    h2d = total * D * (8 + 1) / K
+    d2h = total * (D * 8 + K * 4 * 8 + 64) / K
 
     extras, water, fp64, cpu, cpu_configs = {}, None, None, None, {}
     if rank == 0 and world == 1 and not args.no_extras:
@@ -591,7 +600,8 @@ def main():
                  "peak_source": f"4 issue slots/clk/SM x {sm_count} SMs at {mhz:.0f} MHz"}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
-        "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "strong" if args.strong else "weak",
+        "vs_baseline": None,
         "dtype": "f64+f32", "data": "synthetic", "config": config_of(args, n_at, D, world),
         "pair_interactions_per_s": pairs_per_step * K / (ms_max * 1e-3),
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
