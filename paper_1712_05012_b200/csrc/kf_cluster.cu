@@ -132,7 +132,7 @@ __device__ __forceinline__ int2 cl_exact_pair(const kf_field_t &f, const double 
 }
 
 #ifndef CL_WARPS_N
-#define CL_WARPS_N 16
+#define CL_WARPS_N 12   // measured: 12 (80 registers) 0.99 ms vs 16 (64, spilling) 1.15 ms per C5 launch
 #endif
 #ifndef CL_MINB
 #define CL_MINB 2   // CTAs per SM asked of ptxas for trajectories of <= 1536 atoms
@@ -198,34 +198,33 @@ __device__ __noinline__ int near_class(const kf_field_t &f, int Q, int O, int la
     return 4;
 }
 
-// One warp round: quad Q (i = 4 Q + ii) against octet O (j = 8 O + js), 32 pairs.
-// GEN: the octet may hold class < 4 pairs or the quad's own atoms (class codes,
-// own-octet test); otherwise every pair is class 4.  Pairs inside a threshold
-// band or closer than f64_d2 (nonzero weight) are queued for the exact path.
+// Half of a unit round: quad Q (i = 4 Q + ii) against octet O (j = 8 O + js), 32
+// pairs, with the octet's data (oj, rj) and the frame shift (c_unit - c_O) loaded by
+// the caller.  GEN: the octet may hold class < 4 pairs or the quad's own atoms
+// (class codes, own-octet test); otherwise every pair is class 4.  Pairs inside a
+// threshold band or closer than f64_d2 (nonzero weight) are queued for the exact
+// path.  The force on j accumulates in gj (reduced by the caller once per octet).
 template <bool DCONST, int NCAP, bool GEN>
-KF_DEV void round(const kf_field_t &f, const ClConst &c, const unsigned long long *qcodes, unsigned sb, int n, int O,
-                  int O0, int Q, int i, bool vi,
-                  int ii, int js, int lane, float oix, float oiy, float oiz, const float4 &ci, float qK, float qK4,
-                  float ws4, const float2 &ri, bool vdw_round, bool wnz4, float &fx, float &fy, float &fz,
-                  float &ee, float &ev, int &ce, int &cv, unsigned *exq, int exq_cap, int *exq_n) {
-    using L = ClLayout<NCAP>;
-    const float4 oc = lds4(sb + L::OCT_C + 16 * O);
-    const int j = 8 * O + js;
-    const float4 oj = lds4(sb + L::OQ + 16 * j);
-    const float2 rj = lds2(sb + L::RS + 8 * j);
-    const float dx = (oix - oj.x) + (ci.x - oc.x);   // frame shift exact
-    const float dy = (oiy - oj.y) + (ci.y - oc.y);
-    const float dz = (oiz - oj.z) + (ci.z - oc.z);
+KF_DEV void half(const kf_field_t &f, const ClConst &c, const unsigned long long *qcodes, int n, int O, int Q,
+                 int i, bool vi, int lane, const float4 &oi, const float2 &ri, const float4 &oj, const float2 &rj,
+                 float sx, float sy, float sz, bool vdw_round, bool wnz4, float &fx, float &fy, float &fz,
+                 float &gjx, float &gjy, float &gjz, float &ee, float &ev, int &ce, int &cv, unsigned *exq,
+                 int exq_cap, int *exq_n) {
+    const int j = 8 * O + (lane >> 2);
+    const float dx = (oi.x - oj.x) + sx;   // frame shift exact
+    const float dy = (oi.y - oj.y) + sy;
+    const float dz = (oi.z - oj.z) + sz;
     const float d2 = dx * dx + dy * dy + dz * dz;
     bool live = vi;
-    float qq = qK4 * oj.w, weps = ws4 * rj.y;
+    const float qK = (float)COULOMB_K * oi.w;
+    float qq = qK * c.we[3] * oj.w, weps = c.wv[3] * ri.y * rj.y;
     bool wnz = wnz4;
     int code = 0;                                    // 4 - class
     if (GEN) {
-        if (O == O0) live &= j > i;                  // own octet: each pair once
+        if (O == (Q >> 1)) live &= j > i;            // own octet: each pair once
         if (!c.uniform) {
-            const int k = O - O0;
-            if (k <= 4)   // the quad's 5 window codes, staged per warp at the quad's start
+            const int k = O - (Q >> 1);
+            if (k <= 4)   // the quad's 5 window codes, staged per warp at the unit's start
                 code = (int)((qcodes[k] >> (2 * lane)) & 3ull);
             else if (live && j < n && f.class_slow[i])
                 code = 4 - cl_slow_class(f, i, j);   // tree partner beyond the window
@@ -268,13 +267,7 @@ KF_DEV void round(const kf_field_t &f, const ClConst &c, const unsigned long lon
     }
     const float gx = g * dx, gy = g * dy, gz = g * dz;
     fx += gx; fy += gy; fz += gz;
-    // force on j = -(sum over the quad's 4 lanes)
-    float tx = gx, ty = gy, tz = gz;
-    tx += __shfl_xor_sync(FULL, tx, 1); ty += __shfl_xor_sync(FULL, ty, 1); tz += __shfl_xor_sync(FULL, tz, 1);
-    tx += __shfl_xor_sync(FULL, tx, 2); ty += __shfl_xor_sync(FULL, ty, 2); tz += __shfl_xor_sync(FULL, tz, 2);
-    // (padding atoms past n have accumulator words too: the layout holds NCAP >= 8 no atoms)
-    const float v = ii == 0 ? tx : (ii == 1 ? ty : tz);
-    if (ii < 3 && v != 0.f) acc_add<NCAP>(sb, 3 * j + ii, __float2ll_rn(-v * FIXF));
+    gjx += gx; gjy += gy; gjz += gz;
 }
 
 template <bool DCONST, int NCAP>
@@ -291,7 +284,7 @@ cluster_pair_kernel(const __grid_constant__ kf_field_t f, const __grid_constant_
     __shared__ int next_q, extent_bad, exq_n;
     __shared__ unsigned cnt_e, cnt_v;
     __shared__ double red_e[CL_WARPS][2];
-    __shared__ unsigned long long qcodes[CL_WARPS][5];   // the current quad's window class codes
+    __shared__ unsigned long long qcodes[CL_WARPS][10];  // the current unit's window class codes (2 quads)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int no = (n + 7) / 8, nq = (n + 3) / 4;
     const unsigned base = smem_u32(sm);
@@ -359,7 +352,11 @@ cluster_pair_kernel(const __grid_constant__ kf_field_t f, const __grid_constant_
         return;
     }
 
-    // ---- 2. i-quads against candidate octets --------------------------------
+    // ---- 2. units of two quads (one i-octet) against candidate octets ---------
+    // Unit U = quads 2U and 2U+1 = the atoms of octet U, so both quads share U's
+    // frame: per candidate octet O the j data and the frame shift are loaded once,
+    // the two quads' rounds run back to back (4 x 8 pairs each), and the force on j
+    // is reduced over the quad lanes once per octet.
     // (lane and the shared base are pinned in registers: the compiler would
     // otherwise rematerialise them from special registers in every round)
     int lane_p = lane;
@@ -367,87 +364,102 @@ cluster_pair_kernel(const __grid_constant__ kf_field_t f, const __grid_constant_
     asm volatile("" : "+r"(lane_p), "+r"(sb));
     const int ii = lane_p & 3, js = lane_p >> 2;
     const bool wnz4 = (c.wnz_mask >> 3) & 1;          // class 4 has a nonzero weight
-    int ce = 0, cv = 0;                               // pair counts: integers, order-free across quads
-    int Q = warp;
-    while (Q < nq) {
-        const int i = 4 * Q + ii;
-        const bool vi = i < n;
-        const float4 oi = lds4(sb + L::OQ + 16 * (vi ? i : 0));
-        const float2 ri = lds2(sb + L::RS + 8 * (vi ? i : 0));
-        const float4 ci = lds4(sb + L::OCT_C + 16 * (Q >> 1));
-        const float oix = vi ? oi.x : -FAR, oiy = vi ? oi.y : -FAR, oiz = vi ? oi.z : -FAR;
-        // the quad's box in its octet's frame (lanes of equal ii hold the same atom)
-        float blo[3] = {vi ? oi.x : 3e30f, vi ? oi.y : 3e30f, vi ? oi.z : 3e30f};
-        float bhi[3] = {vi ? oi.x : -3e30f, vi ? oi.y : -3e30f, vi ? oi.z : -3e30f};
-#pragma unroll
-        for (int m = 1; m < 4; m <<= 1)
-#pragma unroll
-            for (int q = 0; q < 3; ++q) {
-                blo[q] = fminf(blo[q], __shfl_xor_sync(FULL, blo[q], m));
-                bhi[q] = fmaxf(bhi[q], __shfl_xor_sync(FULL, bhi[q], m));
-            }
-        const float qK = (float)COULOMB_K * oi.w;        // K q_i
-        const float qK4 = qK * c.we[3], ws4 = ri.y * c.wv[3];
-        const bool slow_q = !c.uniform && __any_sync(FULL, vi && aaux[vi ? i : 0].w != 0);
-        // window octets whose 32 pairs are all class 4 (most of k = 3, 4) take the lean path too
-        unsigned win = 1u;                                // the own octet always (j > i test)
+    int ce = 0, cv = 0;                               // pair counts: integers, order-free across units
+    int U = warp;
+    while (U < no) {
+        const int QA = 2 * U, QB = 2 * U + 1;
+        const int iA = 4 * QA + ii, iB = 4 * QB + ii;
+        const bool vA = iA < n, vB = iB < n && QB < nq;
+        const float4 oiA = vA ? lds4(sb + L::OQ + 16 * iA) : make_float4(-FAR, -FAR, -FAR, 0.f);
+        const float4 oiB = vB ? lds4(sb + L::OQ + 16 * iB) : make_float4(-FAR, -FAR, -FAR, 0.f);
+        const float2 riA = lds2(sb + L::RS + 8 * (vA ? iA : 0)), riB = lds2(sb + L::RS + 8 * (vB ? iB : 0));
+        const float4 cu = lds4(sb + L::OCT_C + 16 * U), hu = lds4(sb + L::OCT_H + 16 * U);
+        const bool slow_u = !c.uniform && __any_sync(FULL, (vA && aaux[vA ? iA : 0].w != 0) ||
+                                                           (vB && aaux[vB ? iB : 0].w != 0));
+        // window octets whose 32 pairs are all class 4 (most of k = 3, 4) take the lean path
+        unsigned winA = 1u, winB = 1u;                    // the own octet always (j > i test)
         if (!c.uniform) {
             unsigned long long code = 0ull;
-            if (lane_p < 5) qcodes[warp][lane_p] = code = f.class_codes[5 * Q + lane_p];
-            win = __ballot_sync(FULL, lane_p < 5 && code != 0ull) | 1u;
+            if (lane_p < 5) code = f.class_codes[5 * QA + lane_p];
+            else if (lane_p >= 8 && lane_p < 13 && QB < nq) code = f.class_codes[5 * QB + lane_p - 8];
+            if (lane_p < 5 || (lane_p >= 8 && lane_p < 13)) qcodes[warp][lane_p < 5 ? lane_p : lane_p - 3] = code;
+            const unsigned m = __ballot_sync(FULL, code != 0ull);
+            winA = (m & 0x1fu) | 1u;
+            winB = ((m >> 8) & 0x1fu) | 1u;
         }
         __syncwarp();
-        float fx = 0.f, fy = 0.f, fz = 0.f, ee = 0.f, ev = 0.f;
-        const int O0 = Q >> 1;
-        for (int ob = O0; ob < no; ob += 32) {
-            // box pretest of 32 candidate octets at once: gap between [ci + blo,
-            // ci + bhi] and [oc - oh, oc + oh] (frame shift exact; the rest rounds
-            // far below the pretest's 1e-2 A^2 margin)
+        float fxA = 0.f, fyA = 0.f, fzA = 0.f, fxB = 0.f, fyB = 0.f, fzB = 0.f, ee = 0.f, ev = 0.f;
+        for (int ob = U; ob < no; ob += 32) {
+            // box pretest of 32 candidate octets at once against the unit's octet box
             const int Oc = ob + lane_p;
             float bd2 = 3.0e38f;
             if (Oc < no) {
                 const float4 oc = lds4(sb + L::OCT_C + 16 * Oc), oh = lds4(sb + L::OCT_H + 16 * Oc);
-                const float sx = ci.x - oc.x, sy = ci.y - oc.y, sz = ci.z - oc.z;
-                const float gx = fmaxf(fmaxf((sx + blo[0]) - oh.x, -(sx + bhi[0]) - oh.x), 0.f);
-                const float gy = fmaxf(fmaxf((sy + blo[1]) - oh.y, -(sy + bhi[1]) - oh.y), 0.f);
-                const float gz = fmaxf(fmaxf((sz + blo[2]) - oh.z, -(sz + bhi[2]) - oh.z), 0.f);
+                const float gx = fmaxf(fabsf(cu.x - oc.x) - (hu.x + oh.x), 0.f);
+                const float gy = fmaxf(fabsf(cu.y - oc.y) - (hu.y + oh.y), 0.f);
+                const float gz = fmaxf(fabsf(cu.z - oc.z) - (hu.z + oh.z), 0.f);
                 bd2 = gx * gx + gy * gy + gz * gz;
             }
             unsigned cand = __ballot_sync(FULL, bd2 <= c.pre2);
             const unsigned vmask = __ballot_sync(FULL, bd2 <= c.pre2v);
-            // rounds whose octet lies in the quad's 64-atom class window (O <= O0 + 4, only
-            // in the first block) or may hold a slow atom's tree partner take the
-            // general path; all others are class 4 with no own-octet test
-            const unsigned gen = slow_q ? ~0u : (ob == O0 ? win : 0u);
-            unsigned cand_gen = cand & gen;
-            cand &= ~gen;
-            while (cand_gen) {
-                const int t = __ffs(cand_gen) - 1;
-                cand_gen &= cand_gen - 1u;
-                round<DCONST, NCAP, true>(f, c, qcodes[warp], sb, n, ob + t, O0, Q, i, vi, ii, js, lane_p, oix, oiy,
-                                          oiz, ci, qK, qK4, ws4, ri, (vmask >> t) & 1u, wnz4, fx, fy, fz, ee, ev,
-                                          ce, cv, exq, exq_cap, &exq_n);
-            }
+            // octets in a quad's 64-atom class window (only in the first block) or near
+            // a slow atom's tree partner take the general path
+            const unsigned genA = slow_u ? ~0u : (ob == U ? winA : 0u);
+            const unsigned genB = slow_u ? ~0u : (ob == U ? winB : 0u);
             while (cand) {
                 const int t = __ffs(cand) - 1;
                 cand &= cand - 1u;
-                round<DCONST, NCAP, false>(f, c, qcodes[warp], sb, n, ob + t, O0, Q, i, vi, ii, js, lane_p, oix, oiy,
-                                           oiz, ci, qK, qK4, ws4, ri, (vmask >> t) & 1u, wnz4, fx, fy, fz, ee, ev,
-                                           ce, cv, exq, exq_cap, &exq_n);
+                const int O = ob + t;
+                const float4 oc = lds4(sb + L::OCT_C + 16 * O);
+                const int j = 8 * O + js;
+                const float4 oj = lds4(sb + L::OQ + 16 * j);
+                const float2 rj = lds2(sb + L::RS + 8 * j);
+                const float sx = cu.x - oc.x, sy = cu.y - oc.y, sz = cu.z - oc.z;   // exact
+                const bool vr = (vmask >> t) & 1u;
+                float gjx = 0.f, gjy = 0.f, gjz = 0.f;
+                if ((genA >> t) & 1u)
+                    half<DCONST, NCAP, true>(f, c, qcodes[warp], n, O, QA, iA, vA, lane_p, oiA, riA, oj, rj, sx, sy,
+                                             sz, vr, wnz4, fxA, fyA, fzA, gjx, gjy, gjz, ee, ev, ce, cv, exq, exq_cap,
+                                             &exq_n);
+                else
+                    half<DCONST, NCAP, false>(f, c, qcodes[warp], n, O, QA, iA, vA, lane_p, oiA, riA, oj, rj, sx, sy,
+                                              sz, vr, wnz4, fxA, fyA, fzA, gjx, gjy, gjz, ee, ev, ce, cv, exq,
+                                              exq_cap, &exq_n);
+                if ((genB >> t) & 1u)
+                    half<DCONST, NCAP, true>(f, c, qcodes[warp] + 5, n, O, QB, iB, vB, lane_p, oiB, riB, oj, rj, sx,
+                                             sy, sz, vr, wnz4, fxB, fyB, fzB, gjx, gjy, gjz, ee, ev, ce, cv, exq,
+                                             exq_cap, &exq_n);
+                else
+                    half<DCONST, NCAP, false>(f, c, qcodes[warp] + 5, n, O, QB, iB, vB, lane_p, oiB, riB, oj, rj, sx,
+                                              sy, sz, vr, wnz4, fxB, fyB, fzB, gjx, gjy, gjz, ee, ev, ce, cv, exq,
+                                              exq_cap, &exq_n);
+                // force on j = -(sum over the quad lanes of both halves), once per octet
+                gjx += __shfl_xor_sync(FULL, gjx, 1); gjy += __shfl_xor_sync(FULL, gjy, 1);
+                gjz += __shfl_xor_sync(FULL, gjz, 1);
+                gjx += __shfl_xor_sync(FULL, gjx, 2); gjy += __shfl_xor_sync(FULL, gjy, 2);
+                gjz += __shfl_xor_sync(FULL, gjz, 2);
+                const float v = ii == 0 ? gjx : (ii == 1 ? gjy : gjz);
+                // (padding atoms past n have accumulator words too: NCAP >= 8 no atoms)
+                if (ii < 3 && v != 0.f) acc_add<NCAP>(sb, 3 * j + ii, __float2ll_rn(-v * FIXF));
             }
         }
         // i forces: sum over the 8 j-lanes of each i, then into the fixed point
 #pragma unroll
         for (int m = 4; m < 32; m <<= 1) {
-            fx += __shfl_xor_sync(FULL, fx, m);
-            fy += __shfl_xor_sync(FULL, fy, m);
-            fz += __shfl_xor_sync(FULL, fz, m);
+            fxA += __shfl_xor_sync(FULL, fxA, m); fyA += __shfl_xor_sync(FULL, fyA, m);
+            fzA += __shfl_xor_sync(FULL, fzA, m);
+            fxB += __shfl_xor_sync(FULL, fxB, m); fyB += __shfl_xor_sync(FULL, fyB, m);
+            fzB += __shfl_xor_sync(FULL, fzB, m);
         }
         {
-            const float v = js == 0 ? fx : (js == 1 ? fy : fz);
-            if (vi && js < 3 && v != 0.f) acc_add<NCAP>(sb, 3 * i + js, __float2ll_rn(v * FIXF));
+            // lanes js = 0..2 take quad A's x / y / z, js = 4..6 quad B's
+            const int q = js & 3;
+            const float va = q == 0 ? fxA : (q == 1 ? fyA : fzA), vb = q == 0 ? fxB : (q == 1 ? fyB : fzB);
+            const float v = js < 4 ? va : vb;
+            const int i = js < 4 ? iA : iB;
+            if ((js < 4 ? vA : vB) && q < 3 && v != 0.f) acc_add<NCAP>(sb, 3 * i + q, __float2ll_rn(v * FIXF));
         }
-        // the quad's energies (fixed xor tree: deterministic) and counts (order-free)
+        // the unit's energies (fixed xor tree: deterministic)
 #pragma unroll
         for (int m = 16; m > 0; m >>= 1) {
             ee += __shfl_xor_sync(FULL, ee, m);
@@ -455,11 +467,11 @@ cluster_pair_kernel(const __grid_constant__ kf_field_t f, const __grid_constant_
         }
         __syncwarp();
         if (lane_p == 0) {
-            e_q[2 * Q] = (double)ee;
-            e_q[2 * Q + 1] = (double)ev;
-            Q = atomicAdd(&next_q, 1);
+            e_q[2 * U] = (double)ee;
+            e_q[2 * U + 1] = (double)ev;
+            U = atomicAdd(&next_q, 1);
         }
-        Q = __shfl_sync(FULL, Q, 0);
+        U = __shfl_sync(FULL, U, 0);
     }
     {
         const int tce = __reduce_add_sync(FULL, ce), tcv = __reduce_add_sync(FULL, cv);
@@ -531,7 +543,7 @@ cluster_pair_kernel(const __grid_constant__ kf_field_t f, const __grid_constant_
     }
     if (warp == 0) {
         double de = 0.0, dv = 0.0;
-        for (int q = lane; q < nq; q += 32) { de += e_q[2 * q]; dv += e_q[2 * q + 1]; }
+        for (int q = lane; q < no; q += 32) { de += e_q[2 * q]; dv += e_q[2 * q + 1]; }
         de = warp_sum(de);
         dv = warp_sum(dv);
         for (int w2 = 0; w2 < CL_WARPS; ++w2) { de += red_e[w2][0]; dv += red_e[w2][1]; }   // exact pairs
