@@ -33,6 +33,7 @@ int kf_torque_launch(const kf_chain_t *c, const kf_field_t *f, kf_batch_t *w, co
                      const kf_step_t *step, int mode, cudaStream_t s, int fuse_wrench = 0);
 int kf_kcm_step_launch(const double *tau, const double *theta, const uint8_t *frozen, int D, double kappa,
                        double *theta_out, double *deltas, cudaStream_t s);
+int kf_fused_iteration(const kf_chain_t *c, const kf_field_t *f, kf_batch_t *w, const kf_step_t *st, cudaStream_t s);
 
 namespace {
 thread_local std::string g_last_error;
@@ -61,6 +62,9 @@ std::string graph_key(const kf_chain_t *c, const kf_field_t *f, const kf_batch_t
 int enqueue_iteration(const kf_chain_t *c, const kf_field_t *f, kf_batch_t *w, const kf_step_t *st,
                       cudaStream_t s) {
     const int n = c->n_atoms;
+    // vacuum ensembles on the cluster path: the whole iteration in one kernel
+    const int fused = kf_fused_iteration(c, f, w, st, s);
+    if (fused >= 0) return fused;
     if (kf_fk_launch(c, w, w->status, s)) return 1;
     if (kf_bin_launch(f, w, n, s)) return 1;
     if (kf_pairs_launch(f, w, n, s)) return 1;

@@ -270,17 +270,15 @@ KF_DEV void half(const kf_field_t &f, const ClConst &c, const unsigned long long
     gjx += gx; gjy += gy; gjz += gz;
 }
 
+// The pair phase of trajectory b by one CTA (sm: the ClLayout<NCAP> dynamic
+// shared memory).  Also the middle phase of the fused fold iteration below.
 template <bool DCONST, int NCAP>
-__global__ void __launch_bounds__(CL_WARPS * 32, NCAP <= 1536 ? CL_MINB : 1)
-cluster_pair_kernel(const __grid_constant__ kf_field_t f, const __grid_constant__ ClConst c, int n,
-                    const double *__restrict__ pos_all, double *__restrict__ forces, double *__restrict__ e_atom,
-                    long long *__restrict__ pair_count, kf_status_t *status, long long *__restrict__ planes,
-                    unsigned *__restrict__ exq_all, int exq_cap) {
+KF_DEV void cluster_pairs_cta(const kf_field_t &f, const ClConst &c, int n, int b, const double *__restrict__ pos_all,
+                              double *__restrict__ forces, double *__restrict__ e_atom,
+                              long long *__restrict__ pair_count, kf_status_t *status, long long *__restrict__ planes,
+                              unsigned *__restrict__ exq_all, int exq_cap, unsigned char *sm) {
     using L = ClLayout<NCAP>;
     constexpr int CL_THREADS = CL_WARPS * 32;
-    const int b = blockIdx.x;
-    if (status[b].done) return;
-    extern __shared__ __align__(16) unsigned char sm[];
     __shared__ int next_q, extent_bad, exq_n;
     __shared__ unsigned cnt_e, cnt_v;
     __shared__ double red_e[CL_WARPS][2];
@@ -555,6 +553,44 @@ cluster_pair_kernel(const __grid_constant__ kf_field_t f, const __grid_constant_
     }
 }
 
+template <bool DCONST, int NCAP>
+__global__ void __launch_bounds__(CL_WARPS * 32, NCAP <= 1536 ? CL_MINB : 1)
+cluster_pair_kernel(const __grid_constant__ kf_field_t f, const __grid_constant__ ClConst c, int n,
+                    const double *__restrict__ pos_all, double *__restrict__ forces, double *__restrict__ e_atom,
+                    long long *__restrict__ pair_count, kf_status_t *status, long long *__restrict__ planes,
+                    unsigned *__restrict__ exq_all, int exq_cap) {
+    const int b = blockIdx.x;
+    if (status[b].done) return;
+    extern __shared__ __align__(16) unsigned char sm[];
+    cluster_pairs_cta<DCONST, NCAP>(f, c, n, b, pos_all, forces, e_atom, pair_count, status, planes, exq_all, exq_cap,
+                                    sm);
+}
+
+// One whole KCM iteration of trajectory b in one CTA (vacuum ensembles on the
+// cluster path): forward kinematics (kf_kinematics.cu), the pair phase, then
+// wrenches, torques, record, stop tests and the step (kf_torque.cu), with the
+// phases separated by block barriers instead of kernel boundaries.  Each CTA
+// runs its own chain, so one trajectory's latency-bound FK / torque phases
+// overlap the other resident CTA's pair phase, and there is one grid tail per
+// iteration instead of three.  The phases reuse one dynamic shared buffer.
+template <bool DCONST, int NCAP>
+__global__ void __launch_bounds__(CL_WARPS * 32, NCAP <= 1536 ? CL_MINB : 1)
+fold_iteration_kernel(const __grid_constant__ kf_chain_t ch, const __grid_constant__ kf_field_t f,
+                      const __grid_constant__ ClConst c, const __grid_constant__ kf_batch_t w,
+                      const __grid_constant__ kf_step_t step) {
+    const int b = blockIdx.x;
+    if (w.status[b].done) return;
+    extern __shared__ __align__(16) unsigned char sm[];
+    const int n = ch.n_atoms;
+    fk_smem_cta<CL_WARPS * 32>(ch, b, w.theta, w.link_T, w.pos, reinterpret_cast<double *>(sm));
+    __syncthreads();
+    cluster_pairs_cta<DCONST, NCAP>(f, c, n, b, w.pos, w.forces, w.e_atom, w.pair_count, w.status, w.pair_fj,
+                                    reinterpret_cast<unsigned *>(w.s_lo), 2 * n, sm);
+    __syncthreads();
+    const TorqueArgs ta{w.link_T, w.wrench, w.side_tot, w.bb_suffix, w.tau};
+    torque_step_cta<CL_WARPS * 32>(ch, f, ta, w, step, 1, 1, 1, b, reinterpret_cast<double *>(sm));
+}
+
 template <int NCAP>
 inline int launch_cap(bool dconst, const kf_field_t *f, const ClConst &c, kf_batch_t *w, int n, cudaStream_t s) {
     constexpr size_t smem = ClLayout<NCAP>::TOTAL;
@@ -627,7 +663,7 @@ int kf_cluster_path(const kf_field_t *f, const kf_batch_t *w, int n) {
     return n <= CL_CAPS[CL_NCAPS - 1] && (size_t)ClLayout<2944>::TOTAL <= smem_max ? 1 : 0;
 }
 
-int kf_cluster_pairs_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s) {
+static ClConst cl_const(const kf_field_t *f) {
     ClConst c;
     for (int q = 0; q < 4; ++q) {
         c.we[q] = (float)(f->uniform_weights ? f->uniform_value : f->w_elec[q]);
@@ -653,10 +689,56 @@ int kf_cluster_pairs_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStrea
         c.kwe[q] = (float)COULOMB_K * c.we[q];
         if (c.we[q] != 0.f || c.wv[q] != 0.f) c.wnz_mask |= 1 << q;
     }
+    return c;
+}
+
+int kf_cluster_pairs_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s) {
+    const ClConst c = cl_const(f);
     const bool dc = f->dielectric_const != 0;
     if (n <= 512) return launch_cap<512>(dc, f, c, w, n, s);
     if (n <= 1024) return launch_cap<1024>(dc, f, c, w, n, s);
     if (n <= 1536) return launch_cap<1536>(dc, f, c, w, n, s);
     if (n <= 2048) return launch_cap<2048>(dc, f, c, w, n, s);
     return launch_cap<2944>(dc, f, c, w, n, s);
+}
+
+template <int NCAP>
+static int launch_fused(const kf_chain_t *ch, const kf_field_t *f, kf_batch_t *w, const kf_step_t *st,
+                        cudaStream_t s) {
+    const ClConst c = cl_const(f);
+    const bool dc = f->dielectric_const != 0;
+    size_t smem = ClLayout<NCAP>::TOTAL;
+    smem = std::max(smem, fk_smem_bytes(*ch));
+    smem = std::max(smem, (size_t)ch->n_links * 6 * sizeof(double));
+    auto kern = dc ? fold_iteration_kernel<true, NCAP> : fold_iteration_kernel<false, NCAP>;
+    static size_t opted[2] = {0, 0};
+    if (smem > opted[dc]) {
+        KF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "fused smem");
+        opted[dc] = smem;
+    }
+    kern<<<w->B, CL_WARPS * 32, smem, s>>>(*ch, *f, c, *w, *st);
+    KF_LAUNCH_CHECK("fold_iteration_kernel");
+    return 0;
+}
+
+// The fused iteration (KFB200_FUSED=1) applies to vacuum ensembles on the cluster
+// path whose chain fits (single-CTA FK and torque phases, wrenches in shared
+// memory).  Off by default: measured on C5, 1.21 ms per iteration fused vs 1.15
+// ms as three kernels.  Both resident CTAs of an SM tend to sit in their
+// latency-bound FK / torque phases together, and those phases run at 2 CTAs per
+// SM instead of the standalone kernels' 4.
+int kf_fused_iteration(const kf_chain_t *ch, const kf_field_t *f, kf_batch_t *w, const kf_step_t *st, cudaStream_t s) {
+    static int env_on = -1;
+    if (env_on < 0) {
+        const char *e = getenv("KFB200_FUSED");
+        env_on = e ? atoi(e) : 0;
+    }
+    const int n = ch->n_atoms;
+    if (!env_on || f->solvation || !st || !kf_cluster_path(f, w, n)) return -1;
+    if (fk_smem_bytes(*ch) > 200 * 1024 || (size_t)ch->n_links * 48 > 200 * 1024) return -1;
+    if (n <= 512) return launch_fused<512>(ch, f, w, st, s);
+    if (n <= 1024) return launch_fused<1024>(ch, f, w, st, s);
+    if (n <= 1536) return launch_fused<1536>(ch, f, w, st, s);
+    if (n <= 2048) return launch_fused<2048>(ch, f, w, st, s);
+    return launch_fused<2944>(ch, f, w, st, s);
 }

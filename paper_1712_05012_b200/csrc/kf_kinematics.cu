@@ -136,18 +136,18 @@ fk_scan_kernel(kf_chain_t c, const double *__restrict__ theta_all, double *__res
 // live in shared memory (12 doubles each) until the final write of T (with
 // the joint axes) and of the atom positions, which this kernel also computes:
 // one global write per link and per atom instead of several read-modify-writes.
-constexpr int FKS_THREADS = 128;
+#ifndef FKS_THREADS_N
+#define FKS_THREADS_N 128
+#endif
+constexpr int FKS_THREADS = FKS_THREADS_N;
 constexpr int FKS_STRIDE = 12;
 
-__global__ void __launch_bounds__(FKS_THREADS)
-fk_smem_kernel(const __grid_constant__ kf_chain_t c, const double *__restrict__ theta_all,
-               double *__restrict__ T_all, double *__restrict__ pos_all, const kf_status_t *__restrict__ status) {
-    kf_pdl_wait();      // after the predecessor (programmatic launch: single trajectories)
-    kf_pdl_trigger();
-    const int b = blockIdx.x;
-    if (status && status[b].done) return;
-    extern __shared__ __align__(16) double S[];     // [L][12], then the int tables below
-    __shared__ double chunk[FKS_THREADS / 32][12];   // warp totals of the block scan
+// The whole FK of trajectory b by one CTA of NT threads in S ([L][12] doubles, then
+// the walk tables): also the first phase of the fused fold iteration (kf_cluster.cu).
+template <int NT>
+KF_DEV void fk_smem_cta(const kf_chain_t &c, int b, const double *__restrict__ theta_all,
+                        double *__restrict__ T_all, double *__restrict__ pos_all, double *__restrict__ S) {
+    __shared__ double chunk[NT / 32][12];   // warp totals of the block scan
     const int L = c.n_links, D = c.n_dof, n = c.n_atoms, nb = c.n_bb, ns = c.n_side;
     const double *theta = theta_all + (size_t)b * D;
     // the chain tables the serial phases walk, staged once (one global round trip
@@ -256,6 +256,22 @@ fk_smem_kernel(const __grid_constant__ kf_chain_t c, const double *__restrict__ 
             pos[3 * a + 2] = t[11] + (t[6] * z[u][0] + t[7] * z[u][1] + t[8] * z[u][2]);
         }
     }
+}
+
+__global__ void __launch_bounds__(FKS_THREADS)
+fk_smem_kernel(const __grid_constant__ kf_chain_t c, const double *__restrict__ theta_all,
+               double *__restrict__ T_all, double *__restrict__ pos_all, const kf_status_t *__restrict__ status) {
+    kf_pdl_wait();      // after the predecessor (programmatic launch: single trajectories)
+    kf_pdl_trigger();
+    const int b = blockIdx.x;
+    if (status && status[b].done) return;
+    extern __shared__ __align__(16) double S[];     // [L][12], then the int tables
+    fk_smem_cta<FKS_THREADS>(c, b, theta_all, T_all, pos_all, S);
+}
+
+inline size_t fk_smem_bytes(const kf_chain_t &c) {
+    return (size_t)c.n_links * FKS_STRIDE * sizeof(double) +
+           sizeof(int32_t) * (2 * (size_t)c.n_links + c.n_bb + c.n_side);
 }
 
 // ---- long chains: the backbone scan spread over many CTAs --------------------

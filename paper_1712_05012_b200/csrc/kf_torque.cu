@@ -177,13 +177,12 @@ struct TorqueArgs {
 
 // One CTA per trajectory.  mode: 0 = torques only (API), 1 = fold iteration,
 // 2 = energy reduction only (Field.evaluate)
+// Torques (+ record, stop tests and step when mode == 1) of trajectory b by one CTA
+// of NT threads; wsm: L x 6 doubles of shared memory for the fused wrenches.  Also
+// the last phase of the fused fold iteration (kf_cluster.cu).
 template <int NT>
-__global__ void __launch_bounds__(NT)
-torque_step_kernel(kf_chain_t c, kf_field_t f, TorqueArgs ta, kf_batch_t w, kf_step_t step, int mode,
-                   int fuse_wrench, int e_first) {
-    kf_pdl_wait();      // after the predecessor (programmatic launch: single trajectories)
-    kf_pdl_trigger();
-    const int b = blockIdx.x;
+KF_DEV void torque_step_cta(const kf_chain_t &c, const kf_field_t &f, const TorqueArgs &ta, const kf_batch_t &w,
+                            const kf_step_t &step, int mode, int fuse_wrench, int e_first, int b, double *wsm) {
     kf_status_t *st = w.status ? w.status + b : nullptr;
     if (st && st->done) return;
     __shared__ double red[32];
@@ -197,7 +196,6 @@ torque_step_kernel(kf_chain_t c, kf_field_t f, TorqueArgs ta, kf_batch_t w, kf_s
     const double *T = ta.link_T + (size_t)b * L * KF_XF_STRIDE;
     const double *Wr = ta.wrench + (size_t)b * L * 6;
     if (fuse_wrench) {   // wrenches of this iteration straight into shared memory
-        extern __shared__ __align__(16) double wsm[];   // [L][6]
         const int n = c.n_atoms;
         for (int l = threadIdx.x; l < L; l += blockDim.x)
             link_wrench(c, l, w.pos + (size_t)b * n * 3, w.forces + (size_t)b * n * 3, wsm + 6 * l);
@@ -289,6 +287,16 @@ torque_step_kernel(kf_chain_t c, kf_field_t f, TorqueArgs ta, kf_batch_t w, kf_s
         return;
     }
     finish_iteration(c, w, step, b, tau, tmax, ge, gv, gc, sp, sp5, &stop_reason);
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT)
+torque_step_kernel(kf_chain_t c, kf_field_t f, TorqueArgs ta, kf_batch_t w, kf_step_t step, int mode,
+                   int fuse_wrench, int e_first) {
+    kf_pdl_wait();      // after the predecessor (programmatic launch: single trajectories)
+    kf_pdl_trigger();
+    extern __shared__ __align__(16) double wsm_dyn[];   // [L][6] when fuse_wrench
+    torque_step_cta<NT>(c, f, ta, w, step, mode, fuse_wrench, e_first, blockIdx.x, wsm_dyn);
 }
 
 // ---- long chains: the same iteration over several CTAs per trajectory ------
