@@ -272,6 +272,81 @@ KF_DEV void half(const kf_field_t &f, const ClConst &c, const unsigned long long
 
 // The pair phase of trajectory b by one CTA (sm: the ClLayout<NCAP> dynamic
 // shared memory).  Also the middle phase of the fused fold iteration below.
+// Membership half of a unit round (see half()): difference vector, class, the
+// exact-path queue.  Returns the lanes whose pair takes the fp32 path.
+struct Prep { float dx, dy, dz, d2, qq, weps; bool fast; };
+
+KF_DEV Prep prep(const kf_field_t &f, const ClConst &c, bool gen, const unsigned long long *qcodes, int n, int O,
+                 int Q, int i, bool vi, int lane, const float4 &oi, const float2 &ri, const float4 &oj,
+                 const float2 &rj, float sx, float sy, float sz, bool wnz4, unsigned *exq, int exq_cap, int *exq_n) {
+    Prep p;
+    const int j = 8 * O + (lane >> 2);
+    p.dx = (oi.x - oj.x) + sx;   // frame shift exact
+    p.dy = (oi.y - oj.y) + sy;
+    p.dz = (oi.z - oj.z) + sz;
+    p.d2 = p.dx * p.dx + p.dy * p.dy + p.dz * p.dz;
+    bool live = vi;
+    const float qK = (float)COULOMB_K * oi.w;
+    p.qq = qK * c.we[3] * oj.w;
+    p.weps = c.wv[3] * ri.y * rj.y;
+    bool wnz = wnz4;
+    int code = 0;                                    // 4 - class
+    if (gen) {
+        if (O == (Q >> 1)) live &= j > i;            // own octet: each pair once
+        if (!c.uniform) {
+            const int k = O - (Q >> 1);
+            if (k <= 4)   // the quad's 5 window codes, staged per warp at the unit's start
+                code = (int)((qcodes[k] >> (2 * lane)) & 3ull);
+            else if (live && j < n && f.class_slow[i])
+                code = 4 - cl_slow_class(f, i, j);   // tree partner beyond the window
+            p.qq = qK * c.we[3 - code] * oj.w;
+            p.weps = c.wv[3 - code] * ri.y * rj.y;
+            wnz = (c.wnz_mask >> (3 - code)) & 1;
+        }
+    }
+    const float d2 = p.d2;
+    const float dev = fminf(fminf(fabsf(d2 - c.cut2), fabsf(d2 - c.tv2)), fabsf(d2 - c.te2));
+    const bool exact = live & ((dev <= c.band) | ((d2 < c.f64_d2) & (wnz | (d2 < 1e-4f))));
+    const unsigned em = __ballot_sync(FULL, exact);
+    if (em) {
+        int base = 0;
+        if (lane == __ffs(em) - 1) base = atomicAdd(exq_n, __popc(em));
+        base = __shfl_sync(FULL, base, __ffs(em) - 1);
+        const int slot = base + __popc(em & ((1u << lane) - 1u));
+        if (exact && slot < exq_cap) exq[slot] = (unsigned)i | ((unsigned)j << 12) | ((unsigned)code << 24);
+    }
+    p.fast = live & !exact & (d2 < c.cutlo);
+    return p;
+}
+
+// Math half of a unit round for the fp32-path lanes (others add zeros).
+template <bool DCONST>
+KF_DEV void pair_math(const ClConst &c, const Prep &p, const float2 &ri, const float2 &rj, bool vdw_round,
+                      float &fx, float &fy, float &fz, float &gjx, float &gjy, float &gjz, float &ee, float &ev,
+                      int &ce, int &cv) {
+    float inv_r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(inv_r) : "f"(p.fast ? p.d2 : 1.f));
+    const float inv_r2 = inv_r * inv_r;
+    const bool ke = p.fast && p.d2 <= c.te2;
+    const float e = DCONST ? p.qq * c.kap_inv * inv_r : p.qq * inv_r2;
+    float g = ke ? e * inv_r2 : 0.f;
+    ee += ke ? e : 0.f;
+    ce += ke;
+    if (vdw_round) {   // boxes within the vdW reach
+        const bool kv = p.fast && p.d2 <= c.tv2;
+        const float D = ri.x + rj.x;
+        const float sr = D * D * inv_r2;
+        const float s3 = sr * sr * sr;
+        const float s6 = s3 * s3;
+        ev += kv ? p.weps * (s6 - 2.f * s3) : 0.f;
+        g = kv ? __fmaf_rn(12.f * p.weps * (s6 - s3), inv_r2, g) : g;
+        cv += kv;
+    }
+    const float gx = g * p.dx, gy = g * p.dy, gz = g * p.dz;
+    fx += gx; fy += gy; fz += gz;
+    gjx += gx; gjy += gy; gjz += gz;
+}
+
 template <bool DCONST, int NCAP>
 KF_DEV void cluster_pairs_cta(const kf_field_t &f, const ClConst &c, int n, int b, const double *__restrict__ pos_all,
                               double *__restrict__ forces, double *__restrict__ e_atom,
@@ -414,23 +489,17 @@ KF_DEV void cluster_pairs_cta(const kf_field_t &f, const ClConst &c, int n, int 
                 const float2 rj = lds2(sb + L::RS + 8 * j);
                 const float sx = cu.x - oc.x, sy = cu.y - oc.y, sz = cu.z - oc.z;   // exact
                 const bool vr = (vmask >> t) & 1u;
+                // both halves' membership first (more independent work in flight), one
+                // vote for the pair, then both halves' math with predicated lanes
+                const Prep pa = prep(f, c, (genA >> t) & 1u, qcodes[warp], n, O, QA, iA, vA, lane_p, oiA, riA, oj, rj,
+                                     sx, sy, sz, wnz4, exq, exq_cap, &exq_n);
+                const Prep pb = prep(f, c, (genB >> t) & 1u, qcodes[warp] + 5, n, O, QB, iB, vB, lane_p, oiB, riB, oj,
+                                     rj, sx, sy, sz, wnz4, exq, exq_cap, &exq_n);
+                const bool anyA = __any_sync(FULL, pa.fast), anyB = __any_sync(FULL, pb.fast);
+                if (!(anyA | anyB)) continue;
                 float gjx = 0.f, gjy = 0.f, gjz = 0.f;
-                if ((genA >> t) & 1u)
-                    half<DCONST, NCAP, true>(f, c, qcodes[warp], n, O, QA, iA, vA, lane_p, oiA, riA, oj, rj, sx, sy,
-                                             sz, vr, wnz4, fxA, fyA, fzA, gjx, gjy, gjz, ee, ev, ce, cv, exq, exq_cap,
-                                             &exq_n);
-                else
-                    half<DCONST, NCAP, false>(f, c, qcodes[warp], n, O, QA, iA, vA, lane_p, oiA, riA, oj, rj, sx, sy,
-                                              sz, vr, wnz4, fxA, fyA, fzA, gjx, gjy, gjz, ee, ev, ce, cv, exq,
-                                              exq_cap, &exq_n);
-                if ((genB >> t) & 1u)
-                    half<DCONST, NCAP, true>(f, c, qcodes[warp] + 5, n, O, QB, iB, vB, lane_p, oiB, riB, oj, rj, sx,
-                                             sy, sz, vr, wnz4, fxB, fyB, fzB, gjx, gjy, gjz, ee, ev, ce, cv, exq,
-                                             exq_cap, &exq_n);
-                else
-                    half<DCONST, NCAP, false>(f, c, qcodes[warp] + 5, n, O, QB, iB, vB, lane_p, oiB, riB, oj, rj, sx,
-                                              sy, sz, vr, wnz4, fxB, fyB, fzB, gjx, gjy, gjz, ee, ev, ce, cv, exq,
-                                              exq_cap, &exq_n);
+                if (anyA) pair_math<DCONST>(c, pa, riA, rj, vr, fxA, fyA, fzA, gjx, gjy, gjz, ee, ev, ce, cv);
+                if (anyB) pair_math<DCONST>(c, pb, riB, rj, vr, fxB, fyB, fzB, gjx, gjy, gjz, ee, ev, ce, cv);
                 // force on j = -(sum over the quad lanes of both halves), once per octet
                 gjx += __shfl_xor_sync(FULL, gjx, 1); gjy += __shfl_xor_sync(FULL, gjy, 1);
                 gjz += __shfl_xor_sync(FULL, gjz, 1);
