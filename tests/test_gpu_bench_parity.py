@@ -218,3 +218,50 @@ def test_ensemble_bitwise_repeatable(B):
         out.append((res.theta.copy(), res.energies.copy(), runner.batch.t["forces"].cpu().numpy()))
     for a, b in zip(out[0], out[1]):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("variant", ["constant_dielectric", "uniform_weights", "with_glycine"])
+def test_cluster_kernel_variants_match_oracle(variant):
+    """The cluster-pair kernel's other code paths against the oracle, one iteration
+    at B = 192 (cluster path): constant dielectric (the DCONST build),
+    UniformWeights (no class lookups), and a chain with glycines (other class
+    windows).  Forces of 4 trajectories to the per-atom bar, energies to 1e-6."""
+    from paper_1712_05012_b200 import device as DV
+    from paper_1712_05012_b200 import workloads
+    P = _P()
+    seq = workloads.sequence("C2")
+    if variant == "with_glycine":
+        seq = [r if k % 3 else "GLY" for k, r in enumerate(seq)]
+    ch = P.build_chain(seq)
+    ps = P.load_params()
+    params = ps.resolve(ch)
+    w = P.TreeWeights(P.build_tree(ch), ps.weights)
+    kw, okw = {}, {}
+    if variant == "constant_dielectric":
+        kw["dielectric"] = P.DielectricModel(mode="constant", kappa=4.0)
+        okw = dict(dielectric_mode="constant", kappa=4.0)
+    if variant == "uniform_weights":
+        w = P.UniformWeights(0.7)
+    fld = P.Field(params, w, P.FieldConfig(**kw))
+    B = 192
+    thetas = workloads.random_thetas(ch, B, seed=3)
+    runner = DV.EnsembleRunner(ch, fld, B, P.StepConfig(kappa=KAPPA, max_iters=1, torque_tol_rel=0.0,
+                                                        energy_window=0))
+    from paper_1712_05012_b200 import _native as N
+    assert N.lib().kf_pair_kernel_kind(N.ref(runner.df.struct_for(False)), N.ref(runner.batch.struct),
+                                       ch.n_atoms) == 3
+    runner.load(thetas, np.zeros((B, ch.n_dof), bool))
+    runner.run()
+    forces = runner.batch.t["forces"].cpu().numpy()
+    res = runner.result()
+    of = O.OracleField(params, w, **okw)
+    from test_gpu_parity import pair_scale
+    for r in (0, 57, 130, 191):
+        pos = O.fk(ch, thetas[r])[3]
+        f_ref, e_ref, ex = of.evaluate(pos)
+        scale = pair_scale(params, w, pos, ex["i"], ex["j"], ex["d"], **({"mode": "constant", "kappa": 4.0}
+                                                                        if okw else {}))
+        err = np.linalg.norm(forces[r] - f_ref, axis=1)
+        assert np.all(err <= 1e-5 * np.maximum(scale, 1e-300)), (r, float((err / scale).max()))
+        e = res.energies[r, 0, :3]
+        assert np.abs(e - np.array(e_ref)).sum() <= 1e-6 * np.abs(np.array(e_ref)).sum(), r
