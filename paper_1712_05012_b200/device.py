@@ -801,12 +801,14 @@ class EnsembleRunner:
         s = stream()
         s.synchronize()   # the previous run's copies out of the pinned buffers are done
         if isinstance(thetas, (list, tuple)):
-            np.stack(thetas, out=pin_t.numpy(), casting="same_kind")
-            fz = pin_f.numpy()
+            # one flat concatenate per array into the pinned buffers (about half the
+            # time of np.stack over 1024 small rows)
+            np.concatenate(thetas, out=pin_t.numpy().reshape(-1), casting="same_kind")
+            fz = pin_f.numpy().reshape(-1)
             if all(getattr(f, "dtype", None) == np.bool_ for f in frozen):
-                np.stack(frozen, out=fz.view(np.bool_))
+                np.concatenate(frozen, out=fz.view(np.bool_))
             else:
-                np.stack([np.asarray(f, np.uint8) for f in frozen], out=fz)
+                np.concatenate([np.asarray(f, np.uint8) for f in frozen], out=fz)
         else:
             pin_t.numpy()[...] = np.asarray(thetas, float)
             pin_f.numpy()[...] = np.asarray(frozen, np.uint8)
