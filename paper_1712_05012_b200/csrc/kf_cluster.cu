@@ -347,6 +347,71 @@ KF_DEV void pair_math(const ClConst &c, const Prep &p, const float2 &ri, const f
     gjx += gx; gjy += gy; gjz += gz;
 }
 
+// Both halves of a class-4 unit round at once in packed fp32 (FADD2 / FMUL2 /
+// FFMA2: two lanes' worth of arithmetic per issued instruction, same roundings
+// as the scalar ops).  .x = quad A, .y = quad B.  Returns false if neither half
+// has an fp32-path pair (nothing accumulated).
+KF_DEV float2 f2(float a) { return make_float2(a, a); }
+KF_DEV float2 sub2(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+
+template <bool DCONST>
+KF_DEV bool packed_round(const ClConst &c, int n, int O, int iA, int iB, bool vA, bool vB, int lane, float2 oix,
+                         float2 oiy, float2 oiz, float2 qKw, float2 Ri, float2 wsi, const float4 &oj,
+                         const float2 &rj, float sx, float sy, float sz, bool vdw_round, bool wnz4, float2 &fx,
+                         float2 &fy, float2 &fz, float2 &gj_x, float2 &gj_y, float2 &gj_z, float2 &ee, float2 &ev,
+                         int &ce, int &cv, unsigned *exq, int exq_cap, int *exq_n) {
+    const int j = 8 * O + (lane >> 2);
+    const float2 dx = __fadd2_rn(sub2(oix, f2(oj.x)), f2(sx));   // frame shift exact
+    const float2 dy = __fadd2_rn(sub2(oiy, f2(oj.y)), f2(sy));
+    const float2 dz = __fadd2_rn(sub2(oiz, f2(oj.z)), f2(sz));
+    const float2 d2 = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __fmul2_rn(dx, dx)));
+    const float2 a1 = sub2(d2, f2(c.cut2)), a2 = sub2(d2, f2(c.tv2)), a3 = sub2(d2, f2(c.te2));
+    const float devA = fminf(fminf(fabsf(a1.x), fabsf(a2.x)), fabsf(a3.x));
+    const float devB = fminf(fminf(fabsf(a1.y), fabsf(a2.y)), fabsf(a3.y));
+    const bool exA = vA & ((devA <= c.band) | ((d2.x < c.f64_d2) & (wnz4 | (d2.x < 1e-4f))));
+    const bool exB = vB & ((devB <= c.band) | ((d2.y < c.f64_d2) & (wnz4 | (d2.y < 1e-4f))));
+    if (__any_sync(FULL, exA | exB)) {   // rare: queue the exact-path pairs (class 4)
+        const unsigned ma = __ballot_sync(FULL, exA), mb = __ballot_sync(FULL, exB);
+        int base = 0;
+        if (lane == 0) base = atomicAdd(exq_n, __popc(ma) + __popc(mb));
+        base = __shfl_sync(FULL, base, 0);
+        const int sa = base + __popc(ma & ((1u << lane) - 1u));
+        const int sb2 = base + __popc(ma) + __popc(mb & ((1u << lane) - 1u));
+        if (exA && sa < exq_cap) exq[sa] = (unsigned)iA | ((unsigned)j << 12);
+        if (exB && sb2 < exq_cap) exq[sb2] = (unsigned)iB | ((unsigned)j << 12);
+    }
+    const bool fA = vA & !exA & (d2.x < c.cutlo), fB = vB & !exB & (d2.y < c.cutlo);
+    if (!__any_sync(FULL, fA | fB)) return false;
+    float2 inv_r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(inv_r.x) : "f"(fA ? d2.x : 1.f));
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(inv_r.y) : "f"(fB ? d2.y : 1.f));
+    const float2 inv_r2 = __fmul2_rn(inv_r, inv_r);
+    const bool keA = fA && d2.x <= c.te2, keB = fB && d2.y <= c.te2;
+    const float2 qq = __fmul2_rn(qKw, f2(oj.w));
+    const float2 e = DCONST ? __fmul2_rn(__fmul2_rn(qq, f2(c.kap_inv)), inv_r) : __fmul2_rn(qq, inv_r2);
+    const float2 ge = __fmul2_rn(e, inv_r2);
+    float2 g = make_float2(keA ? ge.x : 0.f, keB ? ge.y : 0.f);
+    ee = __fadd2_rn(ee, make_float2(keA ? e.x : 0.f, keB ? e.y : 0.f));
+    ce += keA + keB;
+    if (vdw_round) {   // boxes within the vdW reach
+        const bool kvA = fA && d2.x <= c.tv2, kvB = fB && d2.y <= c.tv2;
+        const float2 weps = __fmul2_rn(wsi, f2(rj.y));
+        const float2 D = __fadd2_rn(Ri, f2(rj.x));
+        const float2 sr = __fmul2_rn(__fmul2_rn(D, D), inv_r2);
+        const float2 s3 = __fmul2_rn(__fmul2_rn(sr, sr), sr);
+        const float2 s6 = __fmul2_rn(s3, s3);
+        const float2 evt = __fmul2_rn(weps, __ffma2_rn(f2(-2.f), s3, s6));     // weps (s6 - 2 s3)
+        ev = __fadd2_rn(ev, make_float2(kvA ? evt.x : 0.f, kvB ? evt.y : 0.f));
+        const float2 gv = __ffma2_rn(__fmul2_rn(__fmul2_rn(f2(12.f), weps), sub2(s6, s3)), inv_r2, g);
+        g = make_float2(kvA ? gv.x : g.x, kvB ? gv.y : g.y);
+        cv += kvA + kvB;
+    }
+    const float2 gx = __fmul2_rn(g, dx), gy = __fmul2_rn(g, dy), gz = __fmul2_rn(g, dz);
+    fx = __fadd2_rn(fx, gx); fy = __fadd2_rn(fy, gy); fz = __fadd2_rn(fz, gz);
+    gj_x = __fadd2_rn(gj_x, gx); gj_y = __fadd2_rn(gj_y, gy); gj_z = __fadd2_rn(gj_z, gz);
+    return true;
+}
+
 template <bool DCONST, int NCAP>
 KF_DEV void cluster_pairs_cta(const kf_field_t &f, const ClConst &c, int n, int b, const double *__restrict__ pos_all,
                               double *__restrict__ forces, double *__restrict__ e_atom,
@@ -461,7 +526,11 @@ KF_DEV void cluster_pairs_cta(const kf_field_t &f, const ClConst &c, int n, int 
             winB = ((m >> 8) & 0x1fu) | 1u;
         }
         __syncwarp();
-        float fxA = 0.f, fyA = 0.f, fzA = 0.f, fxB = 0.f, fyB = 0.f, fzB = 0.f, ee = 0.f, ev = 0.f;
+        // packed (quad A, quad B) operands and accumulators of the class-4 rounds
+        const float2 oix = make_float2(oiA.x, oiB.x), oiy = make_float2(oiA.y, oiB.y), oiz = make_float2(oiA.z, oiB.z);
+        const float2 qKw = make_float2((float)COULOMB_K * oiA.w * c.we[3], (float)COULOMB_K * oiB.w * c.we[3]);
+        const float2 Ri = make_float2(riA.x, riB.x), wsi = make_float2(c.wv[3] * riA.y, c.wv[3] * riB.y);
+        float2 fx = f2(0.f), fy = f2(0.f), fz = f2(0.f), ee2 = f2(0.f), ev2 = f2(0.f);
         for (int ob = U; ob < no; ob += 32) {
             // box pretest of 32 candidate octets at once against the unit's octet box
             const int Oc = ob + lane_p;
@@ -489,17 +558,30 @@ KF_DEV void cluster_pairs_cta(const kf_field_t &f, const ClConst &c, int n, int 
                 const float2 rj = lds2(sb + L::RS + 8 * j);
                 const float sx = cu.x - oc.x, sy = cu.y - oc.y, sz = cu.z - oc.z;   // exact
                 const bool vr = (vmask >> t) & 1u;
-                // both halves' membership first (more independent work in flight), one
-                // vote for the pair, then both halves' math with predicated lanes
-                const Prep pa = prep(f, c, (genA >> t) & 1u, qcodes[warp], n, O, QA, iA, vA, lane_p, oiA, riA, oj, rj,
-                                     sx, sy, sz, wnz4, exq, exq_cap, &exq_n);
-                const Prep pb = prep(f, c, (genB >> t) & 1u, qcodes[warp] + 5, n, O, QB, iB, vB, lane_p, oiB, riB, oj,
-                                     rj, sx, sy, sz, wnz4, exq, exq_cap, &exq_n);
-                const bool anyA = __any_sync(FULL, pa.fast), anyB = __any_sync(FULL, pb.fast);
-                if (!(anyA | anyB)) continue;
-                float gjx = 0.f, gjy = 0.f, gjz = 0.f;
-                if (anyA) pair_math<DCONST>(c, pa, riA, rj, vr, fxA, fyA, fzA, gjx, gjy, gjz, ee, ev, ce, cv);
-                if (anyB) pair_math<DCONST>(c, pb, riB, rj, vr, fxB, fyB, fzB, gjx, gjy, gjz, ee, ev, ce, cv);
+                float2 gj_x = f2(0.f), gj_y = f2(0.f), gj_z = f2(0.f);
+                if (!(((genA | genB) >> t) & 1u)) {
+                    // class 4 for both quads: one packed pass over both halves
+                    if (!packed_round<DCONST>(c, n, O, iA, iB, vA, vB, lane_p, oix, oiy, oiz, qKw, Ri, wsi, oj, rj, sx,
+                                              sy, sz, vr, wnz4, fx, fy, fz, gj_x, gj_y, gj_z, ee2, ev2, ce, cv, exq,
+                                              exq_cap, &exq_n))
+                        continue;
+                } else {
+                    // the class window / own octet: both halves' membership first, one vote,
+                    // then the math with predicated lanes
+                    const Prep pa = prep(f, c, (genA >> t) & 1u, qcodes[warp], n, O, QA, iA, vA, lane_p, oiA, riA, oj,
+                                         rj, sx, sy, sz, wnz4, exq, exq_cap, &exq_n);
+                    const Prep pb = prep(f, c, (genB >> t) & 1u, qcodes[warp] + 5, n, O, QB, iB, vB, lane_p, oiB, riB,
+                                         oj, rj, sx, sy, sz, wnz4, exq, exq_cap, &exq_n);
+                    const bool anyA = __any_sync(FULL, pa.fast), anyB = __any_sync(FULL, pb.fast);
+                    if (!(anyA | anyB)) continue;
+                    if (anyA)
+                        pair_math<DCONST>(c, pa, riA, rj, vr, fx.x, fy.x, fz.x, gj_x.x, gj_y.x, gj_z.x, ee2.x, ev2.x, ce,
+                                          cv);
+                    if (anyB)
+                        pair_math<DCONST>(c, pb, riB, rj, vr, fx.y, fy.y, fz.y, gj_x.y, gj_y.y, gj_z.y, ee2.y, ev2.y, ce,
+                                          cv);
+                }
+                float gjx = gj_x.x + gj_x.y, gjy = gj_y.x + gj_y.y, gjz = gj_z.x + gj_z.y;
                 // force on j = -(sum over the quad lanes of both halves), once per octet
                 gjx += __shfl_xor_sync(FULL, gjx, 1); gjy += __shfl_xor_sync(FULL, gjy, 1);
                 gjz += __shfl_xor_sync(FULL, gjz, 1);
@@ -511,6 +593,8 @@ KF_DEV void cluster_pairs_cta(const kf_field_t &f, const ClConst &c, int n, int 
             }
         }
         // i forces: sum over the 8 j-lanes of each i, then into the fixed point
+        float fxA = fx.x, fyA = fy.x, fzA = fz.x, fxB = fx.y, fyB = fy.y, fzB = fz.y;
+        float ee = ee2.x + ee2.y, ev = ev2.x + ev2.y;
 #pragma unroll
         for (int m = 4; m < 32; m <<= 1) {
             fxA += __shfl_xor_sync(FULL, fxA, m); fyA += __shfl_xor_sync(FULL, fyA, m);
