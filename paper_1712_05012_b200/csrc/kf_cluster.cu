@@ -60,6 +60,7 @@ struct ClConst {
     float kap_inv;
     float kwe[4];                 // K w_elec by class
     int uniform, wnz_mask;        // UniformWeights; bit c-1: class c has a nonzero weight
+    float mid, half, band_l;      // lean band test: ||d2 - mid| - half| <= band_l (the two distinct thresholds)
 };
 
 // j-side / exact-path accumulation into the global planes [lo | hi | fp64]
@@ -131,6 +132,9 @@ __device__ __forceinline__ int2 cl_exact_pair(const kf_field_t &f, const double 
     return make_int2(ke, kv);
 }
 
+#ifndef CL_LEAN
+#define CL_LEAN 1   // lean straight-line visits (off: the general rounds for every unit, A/B)
+#endif
 #ifndef CL_WARPS_N
 #define CL_WARPS_N 12   // measured: 12 (80 registers) 0.99 ms vs 16 (64, spilling) 1.15 ms per C5 launch
 #endif
@@ -412,7 +416,137 @@ KF_DEV bool packed_round(const ClConst &c, int n, int O, int iA, int iB, bool vA
     return true;
 }
 
-template <bool DCONST, int NCAP>
+// ---- lean visits: one (unit, octet) visit as straight-line predicated code ----
+// A visit is quads A and B of the unit against octet O: 64 pair slots, two per
+// lane (lane = (ii, js): i = 4 QA + ii and 4 QB + ii, j = 8 O + js), in packed
+// fp32 (.x = quad A, .y = quad B).  Versus the general rounds above: the pair
+// masks are folded into the inverse square distances (masked lanes add exact
+// zeros, no per-term selects), the two distinct cut-off thresholds are tested
+// as one band test (||d2 - mid| - half| <= band), the class weights come from a
+// per-lane register of 2-bit codes and a 4-entry shared table, the force on j is
+// reduced over the quad lanes by a transpose-reduce (3 shuffles), and the
+// fixed-point adds are predicated, not branched.  Only the exact-path queue
+// (pairs in a threshold band or closer than f64_d2: rare) and the vdW term
+// (boxes within the vdW reach) are behind warp-uniform branches.
+struct LeanUnit {
+    float2 ix, iy, iz;    // i offsets in the unit's octet frame
+    float2 qk;            // K q_i (class weight applied per visit)
+    float2 ri;            // R_i
+    float2 se;            // sqrt(eps_i)
+    bool vA, vB;
+    unsigned codes;       // bits 2k..: 4 - class of (iA, j) in window octet U + k; bits 10 + 2k..: iB
+};
+
+template <int NCAP>
+KF_DEV void red_pred(unsigned addr, unsigned v, bool p) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q red.shared.add.u32 [%0], %1;\n\t}" ::"r"(addr),
+                 "r"(v), "r"((unsigned)p)
+                 : "memory");
+}
+
+template <bool DCONST, int NCAP, bool EALL, bool GEN>
+KF_DEV void lean_visit(const ClConst &c, const LeanUnit &u, float2 &fx, float2 &fy, float2 &fz, float2 &ee,
+                       float2 &ev, int &ce, int &cv, int U, int O, int lane, int ii, int js, unsigned sb, float4 cu,
+                       bool vr, float close4, const float4 *wtab, unsigned *exq, int exq_cap, int *exq_n) {
+    using L = ClLayout<NCAP>;
+    const int j = 8 * O + js;
+    const int iA = 8 * U + ii, iB = iA + 4;
+    const float4 oc = lds4(sb + L::OCT_C + 16 * O);
+    const float4 oj = lds4(sb + L::OQ + 16 * j);
+    const float2 rj = lds2(sb + L::RS + 8 * j);
+    // j in the unit's frame (the frame shift cu - oc is exact: grid centres)
+    const float jx = oj.x - (cu.x - oc.x), jy = oj.y - (cu.y - oc.y), jz = oj.z - (cu.z - oc.z);
+    const float2 dx = __fadd2_rn(u.ix, f2(-jx)), dy = __fadd2_rn(u.iy, f2(-jy)), dz = __fadd2_rn(u.iz, f2(-jz));
+    const float2 d2 = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __fmul2_rn(dx, dx)));
+    bool vA = u.vA, vB = u.vB;
+    float2 qq, weps;
+    float closeA = close4, closeB = close4;
+    int codeA = 0, codeB = 0;
+    if (GEN) {
+        vA &= j > iA;   // the own octet: each pair once (always true for O > U)
+        vB &= j > iB;
+        const int k = O - U;
+        if (k <= 4) {
+            codeA = (int)(u.codes >> (2 * k)) & 3;
+            codeB = (int)(u.codes >> (10 + 2 * k)) & 3;
+        }
+        const float4 wa = wtab[codeA], wb = wtab[codeB];   // (w_elec, w_vdw, close threshold) by 4 - class
+        qq = __fmul2_rn(__fmul2_rn(u.qk, make_float2(wa.x, wb.x)), f2(oj.w));
+        weps = __fmul2_rn(__fmul2_rn(u.se, make_float2(wa.y, wb.y)), f2(rj.y));
+        closeA = wa.z;
+        closeB = wb.z;
+    } else {
+        qq = __fmul2_rn(u.qk, f2(c.we[3] * oj.w));
+        weps = __fmul2_rn(u.se, f2(c.wv[3] * rj.y));
+    }
+    // exact path: inside the band around either threshold, or close (see prep())
+    const float2 t = __fadd2_rn(d2, f2(-c.mid));
+    const float bA = fabsf(fabsf(t.x) - c.half), bB = fabsf(fabsf(t.y) - c.half);
+    const bool exA = vA & ((bA <= c.band_l) | (d2.x < closeA));
+    const bool exB = vB & ((bB <= c.band_l) | (d2.y < closeB));
+    if (__any_sync(FULL, exA | exB)) {   // rare: queue the exact-path pairs
+        const unsigned ma = __ballot_sync(FULL, exA), mb = __ballot_sync(FULL, exB);
+        int base = 0;
+        if (lane == 0) base = atomicAdd(exq_n, __popc(ma) + __popc(mb));
+        base = __shfl_sync(FULL, base, 0);
+        const int sa = base + __popc(ma & ((1u << lane) - 1u));
+        const int sb2 = base + __popc(ma) + __popc(mb & ((1u << lane) - 1u));
+        if (exA && sa < exq_cap) exq[sa] = (unsigned)iA | ((unsigned)j << 12) | ((unsigned)codeA << 24);
+        if (exB && sb2 < exq_cap) exq[sb2] = (unsigned)iB | ((unsigned)j << 12) | ((unsigned)codeB << 24);
+    }
+    const bool fA = vA & !exA & (d2.x < c.cutlo), fB = vB & !exB & (d2.y < c.cutlo);
+    if (!__any_sync(FULL, fA | fB)) return;
+    float2 ir;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(ir.x) : "f"(d2.x));
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(ir.y) : "f"(d2.y));
+    const float2 ir2 = __fmul2_rn(ir, ir);
+    // masks folded into the inverse distances: masked lanes (inf / NaN there) get 0
+    const bool keA = EALL ? fA : (fA && d2.x <= c.te2), keB = EALL ? fB : (fB && d2.y <= c.te2);
+    float2 g, e;
+    if (DCONST) {
+        const float2 irm = make_float2(keA ? ir.x : 0.f, keB ? ir.y : 0.f);
+        e = __fmul2_rn(__fmul2_rn(qq, f2(c.kap_inv)), irm);
+        g = __fmul2_rn(e, __fmul2_rn(irm, irm));
+    } else {
+        const float2 ir2e = make_float2(keA ? ir2.x : 0.f, keB ? ir2.y : 0.f);
+        e = __fmul2_rn(qq, ir2e);
+        g = __fmul2_rn(e, ir2e);
+    }
+    ee = __fadd2_rn(ee, e);
+    ce += (int)keA + (int)keB;
+    if (vr) {   // boxes within the vdW reach
+        const bool kvA = fA && d2.x <= c.tv2, kvB = fB && d2.y <= c.tv2;
+        const float2 ir2v = make_float2(kvA ? ir2.x : 0.f, kvB ? ir2.y : 0.f);
+        const float2 D = __fadd2_rn(u.ri, f2(rj.x));
+        const float2 sr = __fmul2_rn(__fmul2_rn(D, D), ir2v);
+        const float2 s3 = __fmul2_rn(__fmul2_rn(sr, sr), sr);
+        const float2 s6 = __fmul2_rn(s3, s3);
+        ev = __ffma2_rn(weps, __ffma2_rn(f2(-2.f), s3, s6), ev);                        // weps (s6 - 2 s3)
+        g = __ffma2_rn(__fmul2_rn(__fmul2_rn(f2(12.f), weps), __fadd2_rn(s6, __fmul2_rn(f2(-1.f), s3))), ir2v, g);
+        cv += (int)kvA + (int)kvB;
+    }
+    const float2 gx = __fmul2_rn(g, dx), gy = __fmul2_rn(g, dy), gz = __fmul2_rn(g, dz);
+    fx = __fadd2_rn(fx, gx); fy = __fadd2_rn(fy, gy); fz = __fadd2_rn(fz, gz);
+    // force on j: -(sum over both halves and the 4 quad lanes), transpose-reduced so
+    // that lane ii ends with component ii (lane 3 with 0)
+    const float sx = gx.x + gx.y, sy = gy.x + gy.y, sz = gz.x + gz.y;
+    const bool hi = ii & 2, od = ii & 1;
+    float k0 = hi ? sz : sx, k1 = hi ? 0.f : sy;
+    const float s0 = hi ? sx : sz, s1 = hi ? sy : 0.f;
+    k0 += __shfl_xor_sync(FULL, s0, 2);
+    k1 += __shfl_xor_sync(FULL, s1, 2);
+    const float snd = od ? k0 : k1;
+    float v = od ? k1 : k0;
+    v += __shfl_xor_sync(FULL, snd, 1);
+    const long long q = __float2ll_rn(-v * FIXF);
+    const unsigned addr = sb + 4 * (3 * j + (ii & 3));
+    const bool p = ii < 3;
+    red_pred<NCAP>(addr + L::ACC_LO, (unsigned)q & 0xfffffu, p);
+    red_pred<NCAP>(addr + L::ACC_MID, (unsigned)(q >> 20) & 0xfffffu, p);
+    red_pred<NCAP>(addr + L::ACC_HI, (unsigned)(int)(q >> 40), p);
+}
+
+template <bool DCONST, int NCAP, bool EALL>
 KF_DEV void cluster_pairs_cta(const kf_field_t &f, const ClConst &c, int n, int b, const double *__restrict__ pos_all,
                               double *__restrict__ forces, double *__restrict__ e_atom,
                               long long *__restrict__ pair_count, kf_status_t *status, long long *__restrict__ planes,
@@ -423,6 +557,11 @@ KF_DEV void cluster_pairs_cta(const kf_field_t &f, const ClConst &c, int n, int 
     __shared__ unsigned cnt_e, cnt_v;
     __shared__ double red_e[CL_WARPS][2];
     __shared__ unsigned long long qcodes[CL_WARPS][10];  // the current unit's window class codes (2 quads)
+    __shared__ float4 wtab[4];   // lean visits: (w_elec, w_vdw, close threshold, 0) by 4 - class
+    if (threadIdx.x < 4) {
+        const int cls = 3 - (int)threadIdx.x;   // index into the by-class arrays
+        wtab[threadIdx.x] = make_float4(c.we[cls], c.wv[cls], ((c.wnz_mask >> cls) & 1) ? c.f64_d2 : 1e-4f, 0.f);
+    }
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int no = (n + 7) / 8, nq = (n + 3) / 4;
     const unsigned base = smem_u32(sm);
@@ -502,6 +641,7 @@ KF_DEV void cluster_pairs_cta(const kf_field_t &f, const ClConst &c, int n, int 
     asm volatile("" : "+r"(lane_p), "+r"(sb));
     const int ii = lane_p & 3, js = lane_p >> 2;
     const bool wnz4 = (c.wnz_mask >> 3) & 1;          // class 4 has a nonzero weight
+    const float close4 = wnz4 ? c.f64_d2 : 1e-4f;     // lean class-4 visits: the close-pair threshold
     int ce = 0, cv = 0;                               // pair counts: integers, order-free across units
     int U = warp;
     while (U < no) {
@@ -531,6 +671,24 @@ KF_DEV void cluster_pairs_cta(const kf_field_t &f, const ClConst &c, int n, int 
         const float2 qKw = make_float2((float)COULOMB_K * oiA.w * c.we[3], (float)COULOMB_K * oiB.w * c.we[3]);
         const float2 Ri = make_float2(riA.x, riB.x), wsi = make_float2(c.wv[3] * riA.y, c.wv[3] * riB.y);
         float2 fx = f2(0.f), fy = f2(0.f), fz = f2(0.f), ee2 = f2(0.f), ev2 = f2(0.f);
+        const bool lean = CL_LEAN && !slow_u;
+        LeanUnit lu;
+        if (lean) {
+            lu.ix = oix; lu.iy = oiy; lu.iz = oiz;
+            lu.qk = make_float2((float)COULOMB_K * oiA.w, (float)COULOMB_K * oiB.w);
+            lu.ri = Ri;
+            lu.se = make_float2(riA.y, riB.y);
+            lu.vA = vA; lu.vB = vB;
+            unsigned cw = 0u;
+            if (!c.uniform) {   // this lane's 2-bit codes of the 5 window octets, both quads
+#pragma unroll
+                for (int k = 0; k < 5; ++k) {
+                    cw |= (unsigned)((qcodes[warp][k] >> (2 * lane_p)) & 3ull) << (2 * k);
+                    cw |= (unsigned)((qcodes[warp][5 + k] >> (2 * lane_p)) & 3ull) << (10 + 2 * k);
+                }
+            }
+            lu.codes = cw;
+        }
         for (int ob = U; ob < no; ob += 32) {
             // box pretest of 32 candidate octets at once against the unit's octet box
             const int Oc = ob + lane_p;
@@ -552,6 +710,16 @@ KF_DEV void cluster_pairs_cta(const kf_field_t &f, const ClConst &c, int n, int 
                 const int t = __ffs(cand) - 1;
                 cand &= cand - 1u;
                 const int O = ob + t;
+                if (lean) {
+                    const bool vr = (vmask >> t) & 1u;
+                    if (((genA | genB) >> t) & 1u)
+                        lean_visit<DCONST, NCAP, EALL, true>(c, lu, fx, fy, fz, ee2, ev2, ce, cv, U, O, lane_p, ii, js,
+                                                             sb, cu, vr, close4, wtab, exq, exq_cap, &exq_n);
+                    else
+                        lean_visit<DCONST, NCAP, EALL, false>(c, lu, fx, fy, fz, ee2, ev2, ce, cv, U, O, lane_p, ii,
+                                                              js, sb, cu, vr, close4, wtab, exq, exq_cap, &exq_n);
+                    continue;
+                }
                 const float4 oc = lds4(sb + L::OCT_C + 16 * O);
                 const int j = 8 * O + js;
                 const float4 oj = lds4(sb + L::OQ + 16 * j);
@@ -706,7 +874,7 @@ KF_DEV void cluster_pairs_cta(const kf_field_t &f, const ClConst &c, int n, int 
     }
 }
 
-template <bool DCONST, int NCAP>
+template <bool DCONST, int NCAP, bool EALL>
 __global__ void __launch_bounds__(CL_WARPS * 32, NCAP <= 1536 ? CL_MINB : 1)
 cluster_pair_kernel(const __grid_constant__ kf_field_t f, const __grid_constant__ ClConst c, int n,
                     const double *__restrict__ pos_all, double *__restrict__ forces, double *__restrict__ e_atom,
@@ -715,8 +883,8 @@ cluster_pair_kernel(const __grid_constant__ kf_field_t f, const __grid_constant_
     const int b = blockIdx.x;
     if (status[b].done) return;
     extern __shared__ __align__(16) unsigned char sm[];
-    cluster_pairs_cta<DCONST, NCAP>(f, c, n, b, pos_all, forces, e_atom, pair_count, status, planes, exq_all, exq_cap,
-                                    sm);
+    cluster_pairs_cta<DCONST, NCAP, EALL>(f, c, n, b, pos_all, forces, e_atom, pair_count, status, planes, exq_all,
+                                          exq_cap, sm);
 }
 
 // One whole KCM iteration of trajectory b in one CTA (vacuum ensembles on the
@@ -737,7 +905,7 @@ fold_iteration_kernel(const __grid_constant__ kf_chain_t ch, const __grid_consta
     const int n = ch.n_atoms;
     fk_smem_cta<CL_WARPS * 32>(ch, b, w.theta, w.link_T, w.pos, reinterpret_cast<double *>(sm));
     __syncthreads();
-    cluster_pairs_cta<DCONST, NCAP>(f, c, n, b, w.pos, w.forces, w.e_atom, w.pair_count, w.status, w.pair_fj,
+    cluster_pairs_cta<DCONST, NCAP, false>(f, c, n, b, w.pos, w.forces, w.e_atom, w.pair_count, w.status, w.pair_fj,
                                     reinterpret_cast<unsigned *>(w.s_lo), 2 * n, sm);
     __syncthreads();
     const TorqueArgs ta{w.link_T, w.wrench, w.side_tot, w.bb_suffix, w.tau};
@@ -747,11 +915,14 @@ fold_iteration_kernel(const __grid_constant__ kf_chain_t ch, const __grid_consta
 template <int NCAP>
 inline int launch_cap(bool dconst, const kf_field_t *f, const ClConst &c, kf_batch_t *w, int n, cudaStream_t s) {
     constexpr size_t smem = ClLayout<NCAP>::TOTAL;
-    auto kern = dconst ? cluster_pair_kernel<true, NCAP> : cluster_pair_kernel<false, NCAP>;
-    static bool opted[2] = {false, false};
-    if (!opted[dconst]) {
+    // EALL: the elec threshold is the pair cut-off (elec >= vdW), so every fp32-path pair has the elec term
+    const bool eall = c.te2 >= c.cut2;
+    auto kern = dconst ? (eall ? cluster_pair_kernel<true, NCAP, true> : cluster_pair_kernel<true, NCAP, false>)
+                       : (eall ? cluster_pair_kernel<false, NCAP, true> : cluster_pair_kernel<false, NCAP, false>);
+    static bool opted[4] = {false, false, false, false};
+    if (!opted[2 * dconst + eall]) {
         KF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "cluster smem");
-        opted[dconst] = true;
+        opted[2 * dconst + eall] = true;
     }
     // exact-pair queue + its sorted copy: the SoA low-word buffer ([B][n][4] u32), which
     // the cluster path does not otherwise use (binning writes it, nothing later reads it)
@@ -824,7 +995,7 @@ static ClConst cl_const(const kf_field_t *f) {
     }
     c.band = 1e-3f;
     c.cut2 = (float)f->cut_pair2;
-    c.cutlo = c.cut2 - c.band;
+    c.cutlo = c.cut2 - 0.95f * c.band;   // below the band test's reach, whatever its rounding
     c.tv2 = (float)f->thr_vdw2;
     c.te2 = (float)f->thr_elec2;
     c.pre2 = (float)(f->cut_pair2 + 1e-2);
@@ -837,6 +1008,18 @@ static ClConst cl_const(const kf_field_t *f) {
     c.f64_d2 = f64_below * f64_below;
     c.kap_inv = f->dielectric_const ? (float)(1.0 / f->kappa) : 1.0f;
     c.uniform = f->uniform_weights;
+    {
+        // cut2 = max(elec, vdw)^2 coincides (to an ulp) with the larger per-term
+        // threshold, so there are two distinct thresholds; the third one's distance
+        // to the nearer of them widens the lean band
+        const float t3[3] = {c.cut2, c.tv2, c.te2};
+        const float ta = std::min(std::min(t3[0], t3[1]), t3[2]), tb = std::max(std::max(t3[0], t3[1]), t3[2]);
+        float dev = 0.f;
+        for (float t : t3) dev = std::max(dev, std::min(t - ta, tb - t));
+        c.mid = 0.5f * (ta + tb);
+        c.half = 0.5f * (tb - ta);
+        c.band_l = c.band + dev;
+    }
     c.wnz_mask = 0;
     for (int q = 0; q < 4; ++q) {
         c.kwe[q] = (float)COULOMB_K * c.we[q];
