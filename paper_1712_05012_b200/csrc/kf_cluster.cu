@@ -437,13 +437,6 @@ struct LeanUnit {
     unsigned codes;       // bits 2k..: 4 - class of (iA, j) in window octet U + k; bits 10 + 2k..: iB
 };
 
-template <int NCAP>
-KF_DEV void red_pred(unsigned addr, unsigned v, bool p) {
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q red.shared.add.u32 [%0], %1;\n\t}" ::"r"(addr),
-                 "r"(v), "r"((unsigned)p)
-                 : "memory");
-}
-
 template <bool DCONST, int NCAP, bool EALL, bool GEN>
 KF_DEV void lean_visit(const ClConst &c, const LeanUnit &u, float2 &fx, float2 &fy, float2 &fz, float2 &ee,
                        float2 &ev, int &ce, int &cv, int U, int O, int lane, int ii, int js, unsigned sb, float4 cu,
@@ -538,12 +531,58 @@ KF_DEV void lean_visit(const ClConst &c, const LeanUnit &u, float2 &fx, float2 &
     const float snd = od ? k0 : k1;
     float v = od ? k1 : k0;
     v += __shfl_xor_sync(FULL, snd, 1);
+    // lane ii = 3 holds exactly 0 and adds it to word 3 j + 3 (x of j + 1, or the
+    // first word past the plane): an add of zero changes nothing, and costs less
+    // than a predicated branch around the REDs
     const long long q = __float2ll_rn(-v * FIXF);
-    const unsigned addr = sb + 4 * (3 * j + (ii & 3));
-    const bool p = ii < 3;
-    red_pred<NCAP>(addr + L::ACC_LO, (unsigned)q & 0xfffffu, p);
-    red_pred<NCAP>(addr + L::ACC_MID, (unsigned)(q >> 20) & 0xfffffu, p);
-    red_pred<NCAP>(addr + L::ACC_HI, (unsigned)(int)(q >> 40), p);
+    const unsigned addr = sb + 4 * (3 * j + ii);
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr + L::ACC_LO), "r"((unsigned)q & 0xfffffu) : "memory");
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr + L::ACC_MID), "r"((unsigned)(q >> 20) & 0xfffffu)
+                 : "memory");
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr + L::ACC_HI), "r"((unsigned)(int)(q >> 40)) : "memory");
+}
+
+// The lean sweep of unit U: box pretests of 32 candidate octets at a time (against
+// the unit's octet box, reloaded from shared memory per block), then one lean
+// visit per surviving octet; octets of the first block whose bit is set in gen0
+// (the own octet and class-window octets holding class < 4 pairs) take the
+// general visit.
+template <bool DCONST, int NCAP, bool EALL>
+KF_DEV void lean_sweep(const ClConst &c, const LeanUnit &lu, float2 &fx, float2 &fy, float2 &fz, float2 &ee,
+                       float2 &ev, int &ce, int &cv, int U, int no, int lane, int ii, int js, unsigned sb,
+                       unsigned gen0, float close4, const float4 *wtab, unsigned *exq, int exq_cap, int *exq_n) {
+    using L = ClLayout<NCAP>;
+    for (int ob = U; ob < no; ob += 32) {
+        const float4 cu = lds4(sb + L::OCT_C + 16 * U);
+        unsigned cand, vmask;
+        {
+            const float4 hu = lds4(sb + L::OCT_H + 16 * U);
+            const int Oc = ob + lane;
+            float bd2 = 3.0e38f;
+            if (Oc < no) {
+                const float4 oc = lds4(sb + L::OCT_C + 16 * Oc), oh = lds4(sb + L::OCT_H + 16 * Oc);
+                const float gx = fmaxf(fabsf(cu.x - oc.x) - (hu.x + oh.x), 0.f);
+                const float gy = fmaxf(fabsf(cu.y - oc.y) - (hu.y + oh.y), 0.f);
+                const float gz = fmaxf(fabsf(cu.z - oc.z) - (hu.z + oh.z), 0.f);
+                bd2 = gx * gx + gy * gy + gz * gz;
+            }
+            cand = __ballot_sync(FULL, bd2 <= c.pre2);
+            vmask = __ballot_sync(FULL, bd2 <= c.pre2v);
+        }
+        const unsigned gen = ob == U ? gen0 : 0u;
+        while (cand) {
+            const int t = __ffs(cand) - 1;
+            cand &= cand - 1u;
+            const int O = ob + t;
+            const bool vr = (vmask >> t) & 1u;
+            if ((gen >> t) & 1u)
+                lean_visit<DCONST, NCAP, EALL, true>(c, lu, fx, fy, fz, ee, ev, ce, cv, U, O, lane, ii, js, sb, cu, vr,
+                                                     close4, wtab, exq, exq_cap, exq_n);
+            else
+                lean_visit<DCONST, NCAP, EALL, false>(c, lu, fx, fy, fz, ee, ev, ce, cv, U, O, lane, ii, js, sb, cu,
+                                                      vr, close4, wtab, exq, exq_cap, exq_n);
+        }
+    }
 }
 
 template <bool DCONST, int NCAP, bool EALL>
@@ -672,8 +711,8 @@ KF_DEV void cluster_pairs_cta(const kf_field_t &f, const ClConst &c, int n, int 
         const float2 Ri = make_float2(riA.x, riB.x), wsi = make_float2(c.wv[3] * riA.y, c.wv[3] * riB.y);
         float2 fx = f2(0.f), fy = f2(0.f), fz = f2(0.f), ee2 = f2(0.f), ev2 = f2(0.f);
         const bool lean = CL_LEAN && !slow_u;
-        LeanUnit lu;
         if (lean) {
+            LeanUnit lu;
             lu.ix = oix; lu.iy = oiy; lu.iz = oiz;
             lu.qk = make_float2((float)COULOMB_K * oiA.w, (float)COULOMB_K * oiB.w);
             lu.ri = Ri;
@@ -688,7 +727,9 @@ KF_DEV void cluster_pairs_cta(const kf_field_t &f, const ClConst &c, int n, int 
                 }
             }
             lu.codes = cw;
-        }
+            lean_sweep<DCONST, NCAP, EALL>(c, lu, fx, fy, fz, ee2, ev2, ce, cv, U, no, lane_p, ii, js, sb, winA | winB,
+                                           close4, wtab, exq, exq_cap, &exq_n);
+        } else
         for (int ob = U; ob < no; ob += 32) {
             // box pretest of 32 candidate octets at once against the unit's octet box
             const int Oc = ob + lane_p;
@@ -710,16 +751,6 @@ KF_DEV void cluster_pairs_cta(const kf_field_t &f, const ClConst &c, int n, int 
                 const int t = __ffs(cand) - 1;
                 cand &= cand - 1u;
                 const int O = ob + t;
-                if (lean) {
-                    const bool vr = (vmask >> t) & 1u;
-                    if (((genA | genB) >> t) & 1u)
-                        lean_visit<DCONST, NCAP, EALL, true>(c, lu, fx, fy, fz, ee2, ev2, ce, cv, U, O, lane_p, ii, js,
-                                                             sb, cu, vr, close4, wtab, exq, exq_cap, &exq_n);
-                    else
-                        lean_visit<DCONST, NCAP, EALL, false>(c, lu, fx, fy, fz, ee2, ev2, ce, cv, U, O, lane_p, ii,
-                                                              js, sb, cu, vr, close4, wtab, exq, exq_cap, &exq_n);
-                    continue;
-                }
                 const float4 oc = lds4(sb + L::OCT_C + 16 * O);
                 const int j = 8 * O + js;
                 const float4 oj = lds4(sb + L::OQ + 16 * j);
