@@ -61,6 +61,7 @@ struct ClConst {
     float kwe[4];                 // K w_elec by class
     int uniform, wnz_mask;        // UniformWeights; bit c-1: class c has a nonzero weight
     float mid, half, band_l;      // lean band test: ||d2 - mid| - half| <= band_l (the two distinct thresholds)
+    float close4;                 // class-4 close-pair threshold: f64_d2 if class 4 has a weight, else 1e-4
 };
 
 // j-side / exact-path accumulation into the global planes [lo | hi | fp64]
@@ -136,7 +137,7 @@ __device__ __forceinline__ int2 cl_exact_pair(const kf_field_t &f, const double 
 #define CL_LEAN 1   // lean straight-line visits (off: the general rounds for every unit, A/B)
 #endif
 #ifndef CL_WARPS_N
-#define CL_WARPS_N 12   // measured: 12 (80 registers) 0.99 ms vs 16 (64, spilling) 1.15 ms per C5 launch
+#define CL_WARPS_N 16   // measured (lean visits, C5): 16 warps (64 registers) 0.62 ms vs 14 (72) 0.63, 12 (80) 0.65
 #endif
 #ifndef CL_MINB
 #define CL_MINB 2   // CTAs per SM asked of ptxas for trajectories of <= 1536 atoms
@@ -425,11 +426,12 @@ KF_DEV bool packed_round(const ClConst &c, int n, int O, int iA, int iB, bool vA
 // as one band test (||d2 - mid| - half| <= band), the class weights come from a
 // per-lane register of 2-bit codes and a 4-entry shared table, the force on j is
 // reduced over the quad lanes by a transpose-reduce (3 shuffles), and the
-// fixed-point adds are predicated, not branched.  Only the exact-path queue
-// (pairs in a threshold band or closer than f64_d2: rare) and the vdW term
-// (boxes within the vdW reach) are behind warp-uniform branches.
+// fixed-point adds are unconditional.  Only the exact-path queue (pairs in a
+// threshold band or closer than f64_d2: rare) is behind a warp-uniform branch;
+// whether the vdW term applies (boxes within its reach) is a template argument:
+// the sweep visits the octets of each reach class in separate loops.
 struct LeanUnit {
-    float2 ix, iy, iz;    // i offsets in the unit's octet frame
+    float2 ix, iy, iz;    // i offsets in the unit's octet frame (register pairs)
     float2 qk;            // K q_i (class weight applied per visit)
     float2 ri;            // R_i
     float2 se;            // sqrt(eps_i)
@@ -437,11 +439,24 @@ struct LeanUnit {
     unsigned codes;       // bits 2k..: 4 - class of (iA, j) in window octet U + k; bits 10 + 2k..: iB
 };
 
-template <bool DCONST, int NCAP, bool EALL, bool GEN>
+// the exact-path queue, read only on the rare path (kept out of the registers)
+struct ExQueue { unsigned *q; int cap; int n; };
+
+// two floats as one 64-bit register pair (the packed ops' operand form)
+KF_DEV float2 pair_of(float a, float b) {
+    unsigned long long v;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(v) : "f"(a), "f"(b));
+    float2 r;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+    return r;
+}
+
+template <bool DCONST, int NCAP, bool EALL, bool GEN, bool VDW>
 KF_DEV void lean_visit(const ClConst &c, const LeanUnit &u, float2 &fx, float2 &fy, float2 &fz, float2 &ee,
-                       float2 &ev, int &ce, int &cv, int U, int O, int lane, int ii, int js, unsigned sb, float4 cu,
-                       bool vr, float close4, const float4 *wtab, unsigned *exq, int exq_cap, int *exq_n) {
+                       float2 &ev, int &ce, int &cv, int U, int O, unsigned sb, const float4 &cu, const float4 *wtab,
+                       ExQueue *xq) {
     using L = ClLayout<NCAP>;
+    const int lane = threadIdx.x & 31, ii = lane & 3, js = lane >> 2;
     const int j = 8 * O + js;
     const int iA = 8 * U + ii, iB = iA + 4;
     const float4 oc = lds4(sb + L::OCT_C + 16 * O);
@@ -453,7 +468,7 @@ KF_DEV void lean_visit(const ClConst &c, const LeanUnit &u, float2 &fx, float2 &
     const float2 d2 = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __fmul2_rn(dx, dx)));
     bool vA = u.vA, vB = u.vB;
     float2 qq, weps;
-    float closeA = close4, closeB = close4;
+    float closeA = c.close4, closeB = c.close4;
     int codeA = 0, codeB = 0;
     if (GEN) {
         vA &= j > iA;   // the own octet: each pair once (always true for O > U)
@@ -480,12 +495,14 @@ KF_DEV void lean_visit(const ClConst &c, const LeanUnit &u, float2 &fx, float2 &
     if (__any_sync(FULL, exA | exB)) {   // rare: queue the exact-path pairs
         const unsigned ma = __ballot_sync(FULL, exA), mb = __ballot_sync(FULL, exB);
         int base = 0;
-        if (lane == 0) base = atomicAdd(exq_n, __popc(ma) + __popc(mb));
+        if (lane == 0) base = atomicAdd(&xq->n, __popc(ma) + __popc(mb));
         base = __shfl_sync(FULL, base, 0);
         const int sa = base + __popc(ma & ((1u << lane) - 1u));
         const int sb2 = base + __popc(ma) + __popc(mb & ((1u << lane) - 1u));
-        if (exA && sa < exq_cap) exq[sa] = (unsigned)iA | ((unsigned)j << 12) | ((unsigned)codeA << 24);
-        if (exB && sb2 < exq_cap) exq[sb2] = (unsigned)iB | ((unsigned)j << 12) | ((unsigned)codeB << 24);
+        unsigned *q = xq->q;
+        const int cap = xq->cap;
+        if (exA && sa < cap) q[sa] = (unsigned)iA | ((unsigned)j << 12) | ((unsigned)codeA << 24);
+        if (exB && sb2 < cap) q[sb2] = (unsigned)iB | ((unsigned)j << 12) | ((unsigned)codeB << 24);
     }
     const bool fA = vA & !exA & (d2.x < c.cutlo), fB = vB & !exB & (d2.y < c.cutlo);
     if (!__any_sync(FULL, fA | fB)) return;
@@ -507,14 +524,14 @@ KF_DEV void lean_visit(const ClConst &c, const LeanUnit &u, float2 &fx, float2 &
     }
     ee = __fadd2_rn(ee, e);
     ce += (int)keA + (int)keB;
-    if (vr) {   // boxes within the vdW reach
+    if (VDW) {   // boxes within the vdW reach
         const bool kvA = fA && d2.x <= c.tv2, kvB = fB && d2.y <= c.tv2;
         const float2 ir2v = make_float2(kvA ? ir2.x : 0.f, kvB ? ir2.y : 0.f);
         const float2 D = __fadd2_rn(u.ri, f2(rj.x));
         const float2 sr = __fmul2_rn(__fmul2_rn(D, D), ir2v);
         const float2 s3 = __fmul2_rn(__fmul2_rn(sr, sr), sr);
         const float2 s6 = __fmul2_rn(s3, s3);
-        ev = __ffma2_rn(weps, __ffma2_rn(f2(-2.f), s3, s6), ev);                        // weps (s6 - 2 s3)
+        ev = __ffma2_rn(weps, __ffma2_rn(f2(-2.f), s3, s6), ev);                           // weps (s6 - 2 s3)
         g = __ffma2_rn(__fmul2_rn(__fmul2_rn(f2(12.f), weps), __fadd2_rn(s6, __fmul2_rn(f2(-1.f), s3))), ir2v, g);
         cv += (int)kvA + (int)kvB;
     }
@@ -544,20 +561,21 @@ KF_DEV void lean_visit(const ClConst &c, const LeanUnit &u, float2 &fx, float2 &
 
 // The lean sweep of unit U: box pretests of 32 candidate octets at a time (against
 // the unit's octet box, reloaded from shared memory per block), then one lean
-// visit per surviving octet; octets of the first block whose bit is set in gen0
+// visit per surviving octet.  Octets of the first block whose bit is set in gen0
 // (the own octet and class-window octets holding class < 4 pairs) take the
-// general visit.
+// general visit; the others are visited in two loops, within the vdW reach and
+// beyond it.
 template <bool DCONST, int NCAP, bool EALL>
 KF_DEV void lean_sweep(const ClConst &c, const LeanUnit &lu, float2 &fx, float2 &fy, float2 &fz, float2 &ee,
-                       float2 &ev, int &ce, int &cv, int U, int no, int lane, int ii, int js, unsigned sb,
-                       unsigned gen0, float close4, const float4 *wtab, unsigned *exq, int exq_cap, int *exq_n) {
+                       float2 &ev, int &ce, int &cv, int U, int no, unsigned sb, unsigned gen0, const float4 *wtab,
+                       ExQueue *xq) {
     using L = ClLayout<NCAP>;
     for (int ob = U; ob < no; ob += 32) {
         const float4 cu = lds4(sb + L::OCT_C + 16 * U);
         unsigned cand, vmask;
         {
             const float4 hu = lds4(sb + L::OCT_H + 16 * U);
-            const int Oc = ob + lane;
+            const int Oc = ob + (int)(threadIdx.x & 31);
             float bd2 = 3.0e38f;
             if (Oc < no) {
                 const float4 oc = lds4(sb + L::OCT_C + 16 * Oc), oh = lds4(sb + L::OCT_H + 16 * Oc);
@@ -569,18 +587,33 @@ KF_DEV void lean_sweep(const ClConst &c, const LeanUnit &lu, float2 &fx, float2 
             cand = __ballot_sync(FULL, bd2 <= c.pre2);
             vmask = __ballot_sync(FULL, bd2 <= c.pre2v);
         }
-        const unsigned gen = ob == U ? gen0 : 0u;
-        while (cand) {
-            const int t = __ffs(cand) - 1;
-            cand &= cand - 1u;
-            const int O = ob + t;
-            const bool vr = (vmask >> t) & 1u;
-            if ((gen >> t) & 1u)
-                lean_visit<DCONST, NCAP, EALL, true>(c, lu, fx, fy, fz, ee, ev, ce, cv, U, O, lane, ii, js, sb, cu, vr,
-                                                     close4, wtab, exq, exq_cap, exq_n);
-            else
-                lean_visit<DCONST, NCAP, EALL, false>(c, lu, fx, fy, fz, ee, ev, ce, cv, U, O, lane, ii, js, sb, cu,
-                                                      vr, close4, wtab, exq, exq_cap, exq_n);
+        if (ob == U) {
+            unsigned g = cand & gen0;
+            cand &= ~gen0;
+            while (g) {
+                const int t = __ffs(g) - 1;
+                g &= g - 1u;
+                if ((vmask >> t) & 1u)
+                    lean_visit<DCONST, NCAP, EALL, true, true>(c, lu, fx, fy, fz, ee, ev, ce, cv, U, ob + t, sb, cu,
+                                                               wtab, xq);
+                else
+                    lean_visit<DCONST, NCAP, EALL, true, false>(c, lu, fx, fy, fz, ee, ev, ce, cv, U, ob + t, sb, cu,
+                                                                wtab, xq);
+            }
+        }
+        unsigned m = cand & vmask;
+        while (m) {
+            const int t = __ffs(m) - 1;
+            m &= m - 1u;
+            lean_visit<DCONST, NCAP, EALL, false, true>(c, lu, fx, fy, fz, ee, ev, ce, cv, U, ob + t, sb, cu, wtab,
+                                                        xq);
+        }
+        m = cand & ~vmask;
+        while (m) {
+            const int t = __ffs(m) - 1;
+            m &= m - 1u;
+            lean_visit<DCONST, NCAP, EALL, false, false>(c, lu, fx, fy, fz, ee, ev, ce, cv, U, ob + t, sb, cu, wtab,
+                                                         xq);
         }
     }
 }
@@ -592,7 +625,8 @@ KF_DEV void cluster_pairs_cta(const kf_field_t &f, const ClConst &c, int n, int 
                               unsigned *__restrict__ exq_all, int exq_cap, unsigned char *sm) {
     using L = ClLayout<NCAP>;
     constexpr int CL_THREADS = CL_WARPS * 32;
-    __shared__ int next_q, extent_bad, exq_n;
+    __shared__ int next_q, extent_bad;
+    __shared__ ExQueue xq;   // the exact-path queue: scratch pointer, capacity, count
     __shared__ unsigned cnt_e, cnt_v;
     __shared__ double red_e[CL_WARPS][2];
     __shared__ unsigned long long qcodes[CL_WARPS][10];  // the current unit's window class codes (2 quads)
@@ -610,7 +644,10 @@ KF_DEV void cluster_pairs_cta(const kf_field_t &f, const ClConst &c, int n, int 
     // each quad's (elec, vdW) energy goes to e_atom[quad] (global scratch, read back
     // in quad order at the end; the totals then sit at atom 0)
     double *e_q = e_atom + 2 * (size_t)b * n;
-    if (threadIdx.x == 0) { next_q = CL_WARPS; extent_bad = 0; cnt_e = 0; cnt_v = 0; exq_n = 0; }
+    if (threadIdx.x == 0) {
+        next_q = CL_WARPS; extent_bad = 0; cnt_e = 0; cnt_v = 0;
+        xq.q = exq_all + (size_t)b * exq_cap * 2; xq.cap = exq_cap; xq.n = 0;
+    }
     // exact-path pairs are queued (packed i | j << 12 | class << 24) into this
     // trajectory's share of a scratch buffer and evaluated after the sweep, in
     // sorted order (deterministic), off the hot loop
@@ -680,7 +717,6 @@ KF_DEV void cluster_pairs_cta(const kf_field_t &f, const ClConst &c, int n, int 
     asm volatile("" : "+r"(lane_p), "+r"(sb));
     const int ii = lane_p & 3, js = lane_p >> 2;
     const bool wnz4 = (c.wnz_mask >> 3) & 1;          // class 4 has a nonzero weight
-    const float close4 = wnz4 ? c.f64_d2 : 1e-4f;     // lean class-4 visits: the close-pair threshold
     int ce = 0, cv = 0;                               // pair counts: integers, order-free across units
     int U = warp;
     while (U < no) {
@@ -713,10 +749,10 @@ KF_DEV void cluster_pairs_cta(const kf_field_t &f, const ClConst &c, int n, int 
         const bool lean = CL_LEAN && !slow_u;
         if (lean) {
             LeanUnit lu;
-            lu.ix = oix; lu.iy = oiy; lu.iz = oiz;
-            lu.qk = make_float2((float)COULOMB_K * oiA.w, (float)COULOMB_K * oiB.w);
-            lu.ri = Ri;
-            lu.se = make_float2(riA.y, riB.y);
+            lu.ix = pair_of(oiA.x, oiB.x); lu.iy = pair_of(oiA.y, oiB.y); lu.iz = pair_of(oiA.z, oiB.z);
+            lu.qk = pair_of((float)COULOMB_K * oiA.w, (float)COULOMB_K * oiB.w);
+            lu.ri = pair_of(riA.x, riB.x);
+            lu.se = pair_of(riA.y, riB.y);
             lu.vA = vA; lu.vB = vB;
             unsigned cw = 0u;
             if (!c.uniform) {   // this lane's 2-bit codes of the 5 window octets, both quads
@@ -727,8 +763,7 @@ KF_DEV void cluster_pairs_cta(const kf_field_t &f, const ClConst &c, int n, int 
                 }
             }
             lu.codes = cw;
-            lean_sweep<DCONST, NCAP, EALL>(c, lu, fx, fy, fz, ee2, ev2, ce, cv, U, no, lane_p, ii, js, sb, winA | winB,
-                                           close4, wtab, exq, exq_cap, &exq_n);
+            lean_sweep<DCONST, NCAP, EALL>(c, lu, fx, fy, fz, ee2, ev2, ce, cv, U, no, sb, winA | winB, wtab, &xq);
         } else
         for (int ob = U; ob < no; ob += 32) {
             // box pretest of 32 candidate octets at once against the unit's octet box
@@ -762,15 +797,15 @@ KF_DEV void cluster_pairs_cta(const kf_field_t &f, const ClConst &c, int n, int 
                     // class 4 for both quads: one packed pass over both halves
                     if (!packed_round<DCONST>(c, n, O, iA, iB, vA, vB, lane_p, oix, oiy, oiz, qKw, Ri, wsi, oj, rj, sx,
                                               sy, sz, vr, wnz4, fx, fy, fz, gj_x, gj_y, gj_z, ee2, ev2, ce, cv, exq,
-                                              exq_cap, &exq_n))
+                                              exq_cap, &xq.n))
                         continue;
                 } else {
                     // the class window / own octet: both halves' membership first, one vote,
                     // then the math with predicated lanes
                     const Prep pa = prep(f, c, (genA >> t) & 1u, qcodes[warp], n, O, QA, iA, vA, lane_p, oiA, riA, oj,
-                                         rj, sx, sy, sz, wnz4, exq, exq_cap, &exq_n);
+                                         rj, sx, sy, sz, wnz4, exq, exq_cap, &xq.n);
                     const Prep pb = prep(f, c, (genB >> t) & 1u, qcodes[warp] + 5, n, O, QB, iB, vB, lane_p, oiB, riB,
-                                         oj, rj, sx, sy, sz, wnz4, exq, exq_cap, &exq_n);
+                                         oj, rj, sx, sy, sz, wnz4, exq, exq_cap, &xq.n);
                     const bool anyA = __any_sync(FULL, pa.fast), anyB = __any_sync(FULL, pb.fast);
                     if (!(anyA | anyB)) continue;
                     if (anyA)
@@ -832,7 +867,7 @@ KF_DEV void cluster_pairs_cta(const kf_field_t &f, const ClConst &c, int n, int 
     // ---- 2b. the queued exact-path pairs: sorted (unique keys: a rank sort), then
     // evaluated in fp64 (forces into the global fixed-point planes), energies summed
     // per thread in sorted order and over the block in a fixed tree: deterministic
-    const int m = exq_n;
+    const int m = xq.n;
     double xe = 0.0, xv = 0.0;
     if (m > 0) {
         if (m > exq_cap) {
@@ -1056,6 +1091,7 @@ static ClConst cl_const(const kf_field_t *f) {
         c.kwe[q] = (float)COULOMB_K * c.we[q];
         if (c.we[q] != 0.f || c.wv[q] != 0.f) c.wnz_mask |= 1 << q;
     }
+    c.close4 = ((c.wnz_mask >> 3) & 1) ? c.f64_d2 : 1e-4f;
     return c;
 }
 
