@@ -431,10 +431,12 @@ KF_DEV bool packed_round(const ClConst &c, int n, int O, int iA, int iB, bool vA
 // whether the vdW term applies (boxes within its reach) is a template argument:
 // the sweep visits the octets of each reach class in separate loops.
 struct LeanUnit {
-    float2 ix, iy, iz;    // i offsets in the unit's octet frame (register pairs)
-    float2 qk;            // K q_i (class weight applied per visit)
-    float2 ri;            // R_i
-    float2 se;            // sqrt(eps_i)
+    // packed (quad A, quad B) pairs held as 64-bit registers: the packed ops below
+    // take them as-is (a float2 held in two scalar registers costs two moves per use)
+    unsigned long long ix, iy, iz;   // i offsets in the unit's octet frame
+    unsigned long long qk;           // K q_i (class weight applied per visit)
+    unsigned long long ri;           // R_i
+    unsigned long long se;           // sqrt(eps_i)
     bool vA, vB;
     unsigned codes;       // bits 2k..: 4 - class of (iA, j) in window octet U + k; bits 10 + 2k..: iB
 };
@@ -443,11 +445,28 @@ struct LeanUnit {
 struct ExQueue { unsigned *q; int cap; int n; };
 
 // two floats as one 64-bit register pair (the packed ops' operand form)
-KF_DEV float2 pair_of(float a, float b) {
+KF_DEV unsigned long long pair_of(float a, float b) {
     unsigned long long v;
     asm("mov.b64 %0, {%1, %2};" : "=l"(v) : "f"(a), "f"(b));
+    return v;
+}
+// packed pair (64-bit register) + / * a broadcast scalar, and * a float2
+KF_DEV float2 padd_b(unsigned long long a, float s) {
     float2 r;
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+    asm("{\n\t.reg .b64 t, d;\n\tmov.b64 t, {%3, %3};\n\tadd.rn.f32x2 d, %2, t;\n\tmov.b64 {%0, %1}, d;\n\t}"
+        : "=f"(r.x), "=f"(r.y) : "l"(a), "f"(s));
+    return r;
+}
+KF_DEV float2 pmul_b(unsigned long long a, float s) {
+    float2 r;
+    asm("{\n\t.reg .b64 t, d;\n\tmov.b64 t, {%3, %3};\n\tmul.rn.f32x2 d, %2, t;\n\tmov.b64 {%0, %1}, d;\n\t}"
+        : "=f"(r.x), "=f"(r.y) : "l"(a), "f"(s));
+    return r;
+}
+KF_DEV float2 pmul_p(unsigned long long a, float2 b) {
+    float2 r;
+    asm("{\n\t.reg .b64 t, d;\n\tmov.b64 t, {%3, %4};\n\tmul.rn.f32x2 d, %2, t;\n\tmov.b64 {%0, %1}, d;\n\t}"
+        : "=f"(r.x), "=f"(r.y) : "l"(a), "f"(b.x), "f"(b.y));
     return r;
 }
 
@@ -464,7 +483,7 @@ KF_DEV void lean_visit(const ClConst &c, const LeanUnit &u, float2 &fx, float2 &
     const float2 rj = lds2(sb + L::RS + 8 * j);
     // j in the unit's frame (the frame shift cu - oc is exact: grid centres)
     const float jx = oj.x - (cu.x - oc.x), jy = oj.y - (cu.y - oc.y), jz = oj.z - (cu.z - oc.z);
-    const float2 dx = __fadd2_rn(u.ix, f2(-jx)), dy = __fadd2_rn(u.iy, f2(-jy)), dz = __fadd2_rn(u.iz, f2(-jz));
+    const float2 dx = padd_b(u.ix, -jx), dy = padd_b(u.iy, -jy), dz = padd_b(u.iz, -jz);
     const float2 d2 = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __fmul2_rn(dx, dx)));
     bool vA = u.vA, vB = u.vB;
     float2 qq, weps;
@@ -479,13 +498,13 @@ KF_DEV void lean_visit(const ClConst &c, const LeanUnit &u, float2 &fx, float2 &
             codeB = (int)(u.codes >> (10 + 2 * k)) & 3;
         }
         const float4 wa = wtab[codeA], wb = wtab[codeB];   // (w_elec, w_vdw, close threshold) by 4 - class
-        qq = __fmul2_rn(__fmul2_rn(u.qk, make_float2(wa.x, wb.x)), f2(oj.w));
-        weps = __fmul2_rn(__fmul2_rn(u.se, make_float2(wa.y, wb.y)), f2(rj.y));
+        qq = __fmul2_rn(pmul_p(u.qk, make_float2(wa.x, wb.x)), f2(oj.w));
+        weps = __fmul2_rn(pmul_p(u.se, make_float2(wa.y, wb.y)), f2(rj.y));
         closeA = wa.z;
         closeB = wb.z;
     } else {
-        qq = __fmul2_rn(u.qk, f2(c.we[3] * oj.w));
-        weps = __fmul2_rn(u.se, f2(c.wv[3] * rj.y));
+        qq = pmul_b(u.qk, c.we[3] * oj.w);
+        weps = pmul_b(u.se, c.wv[3] * rj.y);
     }
     // exact path: inside the band around either threshold, or close (see prep())
     const float2 t = __fadd2_rn(d2, f2(-c.mid));
@@ -527,7 +546,7 @@ KF_DEV void lean_visit(const ClConst &c, const LeanUnit &u, float2 &fx, float2 &
     if (VDW) {   // boxes within the vdW reach
         const bool kvA = fA && d2.x <= c.tv2, kvB = fB && d2.y <= c.tv2;
         const float2 ir2v = make_float2(kvA ? ir2.x : 0.f, kvB ? ir2.y : 0.f);
-        const float2 D = __fadd2_rn(u.ri, f2(rj.x));
+        const float2 D = padd_b(u.ri, rj.x);
         const float2 sr = __fmul2_rn(__fmul2_rn(D, D), ir2v);
         const float2 s3 = __fmul2_rn(__fmul2_rn(sr, sr), sr);
         const float2 s6 = __fmul2_rn(s3, s3);
