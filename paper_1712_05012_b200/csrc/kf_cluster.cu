@@ -1051,7 +1051,7 @@ int kf_cluster_clash_report_launch(const kf_field_t *f, kf_batch_t *w, int n, cu
 // moves the batch threshold (measurements).  kf_bin_launch, kf_pairs_launch and
 // kf_torque_launch all consult this, so one launch configuration is consistent.
 #ifndef CL_MIN_B
-#define CL_MIN_B 160   // measured: B=128 0.33 vs 0.29 ms (cluster vs dense half list), B=192 0.39 vs 0.41
+#define CL_MIN_B 32   // measured (lean visits): C2 step at B=32 0.156 vs 0.170 ms (cluster vs dense), B=128 0.175 vs 0.343
 #endif
 
 int kf_cluster_path(const kf_field_t *f, const kf_batch_t *w, int n) {

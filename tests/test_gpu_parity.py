@@ -464,7 +464,9 @@ def test_scans_match_single_point():
     theta[ch.dof_phi(1)] = grid.axes[0][2] + 180.0
     theta[ch.dof_psi(1)] = grid.axes[1][4] + 180.0
     e = P.single_point(ch, P.Conformation(theta, conf.frozen, 2), fld)
-    assert grid.g_total[2, 4] == pytest.approx(e.g_total, rel=1e-12)
+    # the 36-point scan is one batch on the cluster-pair kernel, the single point a
+    # dense-lane launch: equal to the fp32 pair-math bar, not bitwise
+    assert grid.g_total[2, 4] == pytest.approx(e.g_total, rel=1e-6)
 
 
 def test_fold_long_chain_multi_cta_path(fp64_pairs):
