@@ -38,6 +38,8 @@
 // wrote any.
 #include "kf_common.cuh"
 
+#include <cooperative_groups.h>
+
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
@@ -641,9 +643,16 @@ template <bool DCONST, int NCAP, bool EALL>
 KF_DEV void cluster_pairs_cta(const kf_field_t &f, const ClConst &c, int n, int b, const double *__restrict__ pos_all,
                               double *__restrict__ forces, double *__restrict__ e_atom,
                               long long *__restrict__ pair_count, kf_status_t *status, long long *__restrict__ planes,
-                              unsigned *__restrict__ exq_all, int exq_cap, unsigned char *sm) {
+                              unsigned *__restrict__ exq_all, int exq_cap, unsigned char *sm, int nbatch,
+                              int split, int rank) {
     using L = ClLayout<NCAP>;
     constexpr int CL_THREADS = CL_WARPS * 32;
+    // split > 1: the trajectory's units are shared by the `split` CTAs of a thread-block
+    // cluster (rank r takes units r, r + split, ...); each CTA accumulates into its own
+    // shared fixed point and the partial sums are combined through distributed shared
+    // memory at the end.  Each CTA gets 1 / split of the trajectory's exact-pair queue.
+    exq_all += (size_t)b * exq_cap * 2 + (size_t)rank * 2 * (exq_cap / split);
+    exq_cap /= split;
     __shared__ int next_q, extent_bad;
     __shared__ ExQueue xq;   // the exact-path queue: scratch pointer, capacity, count
     __shared__ unsigned cnt_e, cnt_v;
@@ -665,12 +674,12 @@ KF_DEV void cluster_pairs_cta(const kf_field_t &f, const ClConst &c, int n, int 
     double *e_q = e_atom + 2 * (size_t)b * n;
     if (threadIdx.x == 0) {
         next_q = CL_WARPS; extent_bad = 0; cnt_e = 0; cnt_v = 0;
-        xq.q = exq_all + (size_t)b * exq_cap * 2; xq.cap = exq_cap; xq.n = 0;
+        xq.q = exq_all; xq.cap = exq_cap; xq.n = 0;
     }
     // exact-path pairs are queued (packed i | j << 12 | class << 24) into this
     // trajectory's share of a scratch buffer and evaluated after the sweep, in
     // sorted order (deterministic), off the hot loop
-    unsigned *exq = exq_all + (size_t)b * exq_cap * 2;
+    unsigned *exq = exq_all;
 
     // ---- 1. frames: octet and quad grid centres, half-extent boxes, offsets ----
     for (int a0 = 32 * warp; a0 < 8 * no; a0 += 32 * CL_WARPS) {
@@ -737,7 +746,7 @@ KF_DEV void cluster_pairs_cta(const kf_field_t &f, const ClConst &c, int n, int 
     const int ii = lane_p & 3, js = lane_p >> 2;
     const bool wnz4 = (c.wnz_mask >> 3) & 1;          // class 4 has a nonzero weight
     int ce = 0, cv = 0;                               // pair counts: integers, order-free across units
-    int U = warp;
+    int U = rank + split * warp;
     while (U < no) {
         const int QA = 2 * U, QB = 2 * U + 1;
         const int iA = 4 * QA + ii, iB = 4 * QB + ii;
@@ -873,7 +882,7 @@ KF_DEV void cluster_pairs_cta(const kf_field_t &f, const ClConst &c, int n, int 
         if (lane_p == 0) {
             e_q[2 * U] = (double)ee;
             e_q[2 * U + 1] = (double)ev;
-            U = atomicAdd(&next_q, 1);
+            U = rank + split * atomicAdd(&next_q, 1);
         }
         U = __shfl_sync(FULL, U, 0);
     }
@@ -907,7 +916,7 @@ KF_DEV void cluster_pairs_cta(const kf_field_t &f, const ClConst &c, int n, int 
                 sorted[r] = key;
             }
             __syncthreads();
-            const long long plane = 3LL * gridDim.x * n;
+            const long long plane = 3LL * nbatch * n;
             for (int e = threadIdx.x; e < m; e += CL_THREADS) {
                 const unsigned key = sorted[e];
                 double se[2] = {0.0, 0.0};
@@ -924,14 +933,26 @@ KF_DEV void cluster_pairs_cta(const kf_field_t &f, const ClConst &c, int n, int 
     __syncthreads();
 
     // ---- 3. forces out (+ the exact-path planes if any), energies, counts ----
-    const bool with_planes = m > 0;
+    namespace cg = cooperative_groups;
+    if (split > 1) {
+        __threadfence();                 // e_q and the exact-pair planes (global memory)
+        cg::this_cluster().sync();       // every CTA of the trajectory is past its sweep
+    }
+    int mtot = m;
+    for (int r = 1; r < split; ++r)
+        mtot += cg::this_cluster().map_shared_rank(&xq, (rank + r) % split)->n;
+    const bool with_planes = mtot > 0;
     const size_t nb = (size_t)b * n;
-    const long long plane = 3LL * gridDim.x * n;
-    const unsigned *acc_lo = reinterpret_cast<const unsigned *>(sm + L::ACC_LO);
-    const unsigned *acc_mid = reinterpret_cast<const unsigned *>(sm + L::ACC_MID);
-    const int *acc_hi = reinterpret_cast<const int *>(sm + L::ACC_HI);
-    for (int k = threadIdx.x; k < 3 * n; k += CL_THREADS) {
-        const long long a64 = ((long long)acc_hi[k] << 40) + ((long long)acc_mid[k] << 20) + (long long)acc_lo[k];
+    const long long plane = 3LL * nbatch * n;
+    const int k0 = (int)((long long)3 * n * rank / split), k1 = (int)((long long)3 * n * (rank + 1) / split);
+    for (int k = k0 + threadIdx.x; k < k1; k += CL_THREADS) {
+        long long a64 = 0;
+        for (int r = 0; r < split; ++r) {   // integer partial sums: the total is order-free
+            const unsigned char *smr = split > 1 ? cg::this_cluster().map_shared_rank(sm, r) : sm;
+            a64 += ((long long)reinterpret_cast<const int *>(smr + L::ACC_HI)[k] << 40) +
+                   ((long long)reinterpret_cast<const unsigned *>(smr + L::ACC_MID)[k] << 20) +
+                   (long long)reinterpret_cast<const unsigned *>(smr + L::ACC_LO)[k];
+        }
         double v = (double)a64 * FIX_INV;
         if (with_planes) {
             long long *p = planes + 3 * nb + k;
@@ -945,18 +966,25 @@ KF_DEV void cluster_pairs_cta(const kf_field_t &f, const ClConst &c, int n, int 
         }
         forces[3 * nb + k] = v;
     }
-    if (warp == 0) {
+    if (rank == 0 && warp == 0) {
         double de = 0.0, dv = 0.0;
         for (int q = lane; q < no; q += 32) { de += e_q[2 * q]; dv += e_q[2 * q + 1]; }
         de = warp_sum(de);
         dv = warp_sum(dv);
-        for (int w2 = 0; w2 < CL_WARPS; ++w2) { de += red_e[w2][0]; dv += red_e[w2][1]; }   // exact pairs
+        long long te = 0, tv = 0;
+        for (int r = 0; r < split; ++r) {   // exact pairs: each CTA's warps in order, CTAs in rank order
+            const double (*re)[2] = split > 1 ? cg::this_cluster().map_shared_rank(red_e, r) : red_e;
+            for (int w2 = 0; w2 < CL_WARPS; ++w2) { de += re[w2][0]; dv += re[w2][1]; }
+            te += split > 1 ? *cg::this_cluster().map_shared_rank(&cnt_e, r) : cnt_e;
+            tv += split > 1 ? *cg::this_cluster().map_shared_rank(&cnt_v, r) : cnt_v;
+        }
         if (lane == 0) {   // doubled: the energy reduction halves (full-list convention)
             e_atom[2 * nb] = 2.0 * de;
             e_atom[2 * nb + 1] = 2.0 * dv;
-            pair_count[nb] = 2LL * cnt_e + ((2LL * cnt_v) << 32);
+            pair_count[nb] = 2LL * te + ((2LL * tv) << 32);
         }
     }
+    if (split > 1) cg::this_cluster().sync();   // the peers' shared memory outlives every read of it
 }
 
 template <bool DCONST, int NCAP, bool EALL>
@@ -964,12 +992,12 @@ __global__ void __launch_bounds__(CL_WARPS * 32, NCAP <= 1536 ? CL_MINB : 1)
 cluster_pair_kernel(const __grid_constant__ kf_field_t f, const __grid_constant__ ClConst c, int n,
                     const double *__restrict__ pos_all, double *__restrict__ forces, double *__restrict__ e_atom,
                     long long *__restrict__ pair_count, kf_status_t *status, long long *__restrict__ planes,
-                    unsigned *__restrict__ exq_all, int exq_cap) {
-    const int b = blockIdx.x;
+                    unsigned *__restrict__ exq_all, int exq_cap, int nbatch, int split) {
+    const int b = blockIdx.x / split, rank = blockIdx.x % split;   // cluster dims (split, 1, 1)
     if (status[b].done) return;
     extern __shared__ __align__(16) unsigned char sm[];
     cluster_pairs_cta<DCONST, NCAP, EALL>(f, c, n, b, pos_all, forces, e_atom, pair_count, status, planes, exq_all,
-                                          exq_cap, sm);
+                                          exq_cap, sm, nbatch, split, rank);
 }
 
 // One whole KCM iteration of trajectory b in one CTA (vacuum ensembles on the
@@ -991,7 +1019,7 @@ fold_iteration_kernel(const __grid_constant__ kf_chain_t ch, const __grid_consta
     fk_smem_cta<CL_WARPS * 32>(ch, b, w.theta, w.link_T, w.pos, reinterpret_cast<double *>(sm));
     __syncthreads();
     cluster_pairs_cta<DCONST, NCAP, false>(f, c, n, b, w.pos, w.forces, w.e_atom, w.pair_count, w.status, w.pair_fj,
-                                    reinterpret_cast<unsigned *>(w.s_lo), 2 * n, sm);
+                                    reinterpret_cast<unsigned *>(w.s_lo), 2 * n, sm, (int)gridDim.x, 1, 0);
     __syncthreads();
     const TorqueArgs ta{w.link_T, w.wrench, w.side_tot, w.bb_suffix, w.tau};
     torque_step_cta<CL_WARPS * 32>(ch, f, ta, w, step, 1, 1, 1, b, reinterpret_cast<double *>(sm));
@@ -1011,8 +1039,35 @@ inline int launch_cap(bool dconst, const kf_field_t *f, const ClConst &c, kf_bat
     }
     // exact-pair queue + its sorted copy: the SoA low-word buffer ([B][n][4] u32), which
     // the cluster path does not otherwise use (binning writes it, nothing later reads it)
-    kern<<<w->B, CL_WARPS * 32, smem, s>>>(*f, c, n, w->pos, w->forces, w->e_atom, w->pair_count, w->status,
-                                          w->pair_fj, reinterpret_cast<unsigned *>(w->s_lo), 2 * n);
+    // small batches: each trajectory is split over a thread-block cluster of S CTAs so
+    // that the batch still fills two CTAs per SM (S = the largest power of two <= 8
+    // with B S <= 2 x SMs; KFB200_CL_SPLIT overrides)
+    static int sms = 0, env_split = -1;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const char *e = getenv("KFB200_CL_SPLIT");
+        env_split = e ? atoi(e) : 0;
+    }
+    int split = 1;
+    while (split < 8 && (long long)w->B * split * 2 <= 2LL * sms) split *= 2;
+    if (env_split > 0) split = env_split;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(w->B * split);
+    cfg.blockDim = dim3(CL_WARPS * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = split;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    KF_CUDA(cudaLaunchKernelEx(&cfg, kern, *f, c, n, (const double *)w->pos, w->forces, w->e_atom, w->pair_count,
+                               w->status, w->pair_fj, reinterpret_cast<unsigned *>(w->s_lo), 2 * n, w->B, split),
+            "cluster_pair_kernel");
     KF_LAUNCH_CHECK("cluster_pair_kernel");
     return 0;
 }
