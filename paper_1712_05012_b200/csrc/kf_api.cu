@@ -10,7 +10,7 @@
 #include "kf_common.cuh"
 
 // launchers defined in the kernel translation units
-int kf_fk_launch(const kf_chain_t *c, kf_batch_t *w, const kf_status_t *status, cudaStream_t s);
+int kf_fk_launch(const kf_chain_t *c, kf_batch_t *w, const kf_status_t *status, cudaStream_t s, int full_t);
 int kf_bin_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s);
 int kf_pairs_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s);
 int kf_clash_report_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s);
@@ -65,7 +65,7 @@ int enqueue_iteration(const kf_chain_t *c, const kf_field_t *f, kf_batch_t *w, c
     // vacuum ensembles on the cluster path: the whole iteration in one kernel
     const int fused = kf_fused_iteration(c, f, w, st, s);
     if (fused >= 0) return fused;
-    if (kf_fk_launch(c, w, w->status, s)) return 1;
+    if (kf_fk_launch(c, w, w->status, s, 0)) return 1;   // the loop needs P and U only
     if (kf_bin_launch(f, w, n, s)) return 1;
     if (kf_pairs_launch(f, w, n, s)) return 1;
     if (f->solvation && kf_solvation_launch(f, w, n, f->n_solv, f->solv_atoms, s)) return 1;
@@ -108,7 +108,7 @@ int kf_device_sm_count(void) {
 }
 
 int kf_fk(const kf_chain_t *c, kf_batch_t *w, void *stream) {
-    return kf_fk_launch(c, w, w->status, (cudaStream_t)stream);
+    return kf_fk_launch(c, w, w->status, (cudaStream_t)stream, 1);
 }
 
 int kf_nonbonded(const kf_field_t *f, kf_batch_t *w, void *stream) {

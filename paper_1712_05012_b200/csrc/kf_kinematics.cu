@@ -144,10 +144,15 @@ constexpr int FKS_STRIDE = 12;
 
 // The whole FK of trajectory b by one CTA of NT threads in S ([L][12] doubles, then
 // the walk tables): also the first phase of the fused fold iteration (kf_cluster.cu).
+// full_t = 0 (the fold loop): only the second half of each T row is written, which
+// holds the joint point and axis the torque kernel projects with (rows 8-15:
+// M[8], P, U, pad); the API's kinematic_state asks for the whole row.
 template <int NT>
 KF_DEV void fk_smem_cta(const kf_chain_t &c, int b, const double *__restrict__ theta_all,
-                        double *__restrict__ T_all, double *__restrict__ pos_all, double *__restrict__ S) {
+                        double *__restrict__ T_all, double *__restrict__ pos_all, double *__restrict__ S,
+                        int full_t = 1) {
     __shared__ double chunk[NT / 32][12];   // warp totals of the block scan
+    __shared__ int sh_doff[8];               // side-level offsets (side_depth <= 7 staged)
     const int L = c.n_links, D = c.n_dof, n = c.n_atoms, nb = c.n_bb, ns = c.n_side;
     const double *theta = theta_all + (size_t)b * D;
     // the chain tables the serial phases walk, staged once (one global round trip
@@ -156,6 +161,8 @@ KF_DEV void fk_smem_cta(const kf_chain_t &c, int b, const double *__restrict__ t
         *sh_side = sh_bb + nb;
     for (int k = threadIdx.x; k < nb; k += blockDim.x) sh_bb[k] = c.bb_order[k];
     for (int k = threadIdx.x; k < ns; k += blockDim.x) sh_side[k] = c.side_order[k];
+    const int nd = min(c.side_depth, 7);
+    if ((int)threadIdx.x <= nd) sh_doff[threadIdx.x] = c.side_depth_off[threadIdx.x];
 
     {
         // local transforms; the chain tables and angles of U links per thread are
@@ -205,31 +212,46 @@ KF_DEV void fk_smem_cta(const kf_chain_t &c, int b, const double *__restrict__ t
     }
     __syncthreads();
     for (int d = 0; d < c.side_depth; ++d) {
-        for (int k = c.side_depth_off[d] + threadIdx.x; k < c.side_depth_off[d + 1]; k += blockDim.x) {
+        const int k0 = d < nd ? sh_doff[d] : c.side_depth_off[d];
+        const int k1 = d + 1 <= nd ? sh_doff[d + 1] : c.side_depth_off[d + 1];
+        for (int k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
             const int l = sh_side[k];
             double *slot = S + FKS_STRIDE * l;
             xf_store(slot, xf_compose(xf_load(S + FKS_STRIDE * sh_par[l]), xf_load(slot)));
         }
         __syncthreads();
     }
-    // T with the current joint axes U_l = M_l axis0_l (chain.py:257); ground keeps 0
+    // T with the current joint axes U_l = M_l axis0_l (chain.py:257); ground keeps 0.
+    // The axis loads of TU links per thread are issued ahead of the stores.
     double *__restrict__ T = T_all + (size_t)b * L * KF_XF_STRIDE;
-    const int32_t *__restrict__ link_dof = c.link_dof;
     const double *__restrict__ axis0 = c.link_axis0;
-    for (int l = threadIdx.x; l < L; l += blockDim.x) {
-        const double *src = S + FKS_STRIDE * l;
-        double *dst = T + (size_t)KF_XF_STRIDE * l;
-        const bool joint = l != 0 && sh_dof[l] >= 0;
-        const double a0 = axis0[3 * l], a1 = axis0[3 * l + 1], a2 = axis0[3 * l + 2];
-        double v[KF_XF_STRIDE];
+    constexpr int TU = 4;
+    for (int l0 = threadIdx.x; l0 < L; l0 += TU * blockDim.x) {
+        double ax[TU][3];
 #pragma unroll
-        for (int q = 0; q < 12; ++q) v[q] = src[q];
+        for (int u = 0; u < TU; ++u) {
+            const int l = l0 + u * blockDim.x;
 #pragma unroll
-        for (int r = 0; r < 3; ++r) v[12 + r] = joint ? src[3 * r] * a0 + src[3 * r + 1] * a1 + src[3 * r + 2] * a2 : 0.0;
-        v[15] = 0.0;
-        double2 *d2 = reinterpret_cast<double2 *>(dst);
+            for (int q = 0; q < 3; ++q) ax[u][q] = l < L ? axis0[3 * l + q] : 0.0;
+        }
 #pragma unroll
-        for (int q = 0; q < KF_XF_STRIDE / 2; ++q) d2[q] = make_double2(v[2 * q], v[2 * q + 1]);
+        for (int u = 0; u < TU; ++u) {
+            const int l = l0 + u * blockDim.x;
+            if (l >= L) break;
+            const double *src = S + FKS_STRIDE * l;
+            double2 *d2 = reinterpret_cast<double2 *>(T + (size_t)KF_XF_STRIDE * l);
+            const bool joint = l != 0 && sh_dof[l] >= 0;
+            double v[KF_XF_STRIDE];
+#pragma unroll
+            for (int q = 0; q < 12; ++q) v[q] = src[q];
+#pragma unroll
+            for (int r = 0; r < 3; ++r)
+                v[12 + r] = joint ? v[3 * r] * ax[u][0] + v[3 * r + 1] * ax[u][1] + v[3 * r + 2] * ax[u][2] : 0.0;
+            v[15] = 0.0;
+#pragma unroll
+            for (int q = 0; q < KF_XF_STRIDE / 2; ++q)
+                if (full_t || q >= 4) d2[q] = make_double2(v[2 * q], v[2 * q + 1]);
+        }
     }
     // positions pos_a = P_l + M_l zrel_a (fk_positions_kernel's arithmetic);
     // the chain tables are loaded ahead of the stores (no aliasing with pos)
@@ -260,13 +282,14 @@ KF_DEV void fk_smem_cta(const kf_chain_t &c, int b, const double *__restrict__ t
 
 __global__ void __launch_bounds__(FKS_THREADS)
 fk_smem_kernel(const __grid_constant__ kf_chain_t c, const double *__restrict__ theta_all,
-               double *__restrict__ T_all, double *__restrict__ pos_all, const kf_status_t *__restrict__ status) {
+               double *__restrict__ T_all, double *__restrict__ pos_all, const kf_status_t *__restrict__ status,
+               int full_t) {
     kf_pdl_wait();      // after the predecessor (programmatic launch: single trajectories)
     kf_pdl_trigger();
     const int b = blockIdx.x;
     if (status && status[b].done) return;
     extern __shared__ __align__(16) double S[];     // [L][12], then the int tables
-    fk_smem_cta<FKS_THREADS>(c, b, theta_all, T_all, pos_all, S);
+    fk_smem_cta<FKS_THREADS>(c, b, theta_all, T_all, pos_all, S, full_t);
 }
 
 inline size_t fk_smem_bytes(const kf_chain_t &c) {
@@ -414,7 +437,7 @@ __global__ void fk_positions_kernel(kf_chain_t c, int B, const double *__restric
 
 }  // namespace
 
-int kf_fk_launch(const kf_chain_t *c, kf_batch_t *w, const kf_status_t *status, cudaStream_t s) {
+int kf_fk_launch(const kf_chain_t *c, kf_batch_t *w, const kf_status_t *status, cudaStream_t s, int full_t) {
     const int n_seg = (c->n_bb + SEG - 1) / SEG;
     const size_t smem = (size_t)c->n_links * FKS_STRIDE * sizeof(double) +
                         sizeof(int32_t) * (2 * (size_t)c->n_links + c->n_bb + c->n_side);
@@ -426,7 +449,7 @@ int kf_fk_launch(const kf_chain_t *c, kf_batch_t *w, const kf_status_t *status, 
             opted = smem;
         }
         (void)kf_launch(w->B < KF_PDL_B, fk_smem_kernel, dim3(w->B), dim3(FKS_THREADS), smem, s, *c,
-                        (const double *)w->theta, w->link_T, w->pos, status);
+                        (const double *)w->theta, w->link_T, w->pos, status, full_t);
         KF_LAUNCH_CHECK("fk_smem_kernel");
         return 0;
     }

@@ -50,6 +50,46 @@ KF_DEV void link_wrench(const kf_chain_t &c, int l, const double *pos, const dou
     o[0] = F0; o[1] = F1; o[2] = F2; o[3] = T0; o[4] = T1; o[5] = T2;
 }
 
+// Wrench of link l with every load issued before the sums: the first 4 atoms
+// (the synthetic chains have <= 4 per link) come in one round of independent
+// loads instead of a dependent chain per atom.  Same arithmetic and order as
+// link_wrench.
+KF_DEV void link_wrench_pf(const kf_chain_t &c, int l, const double *__restrict__ pos,
+                           const double *__restrict__ frc, double *o) {
+    constexpr int P = 4;
+    const int e0 = c.link_atom_off[l], e1 = c.link_atom_off[l + 1];
+    int a[P];
+    double r[P][3], g[P][3];
+#pragma unroll
+    for (int u = 0; u < P; ++u) a[u] = e0 + u < e1 ? c.link_atoms[e0 + u] : -1;
+#pragma unroll
+    for (int u = 0; u < P; ++u)
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            r[u][q] = a[u] >= 0 ? pos[3 * a[u] + q] : 0.0;
+            g[u][q] = a[u] >= 0 ? frc[3 * a[u] + q] : 0.0;
+        }
+    double F0 = 0.0, F1 = 0.0, F2 = 0.0, T0 = 0.0, T1 = 0.0, T2 = 0.0;
+#pragma unroll
+    for (int u = 0; u < P; ++u) {
+        if (a[u] < 0) break;
+        F0 = xadd(F0, g[u][0]); F1 = xadd(F1, g[u][1]); F2 = xadd(F2, g[u][2]);
+        T0 = xadd(T0, xsub(xmul(r[u][1], g[u][2]), xmul(r[u][2], g[u][1])));
+        T1 = xadd(T1, xsub(xmul(r[u][2], g[u][0]), xmul(r[u][0], g[u][2])));
+        T2 = xadd(T2, xsub(xmul(r[u][0], g[u][1]), xmul(r[u][1], g[u][0])));
+    }
+    for (int e = e0 + P; e < e1; ++e) {   // links with more atoms: the rest in order
+        const int at = c.link_atoms[e];
+        const double r0 = pos[3 * at], r1 = pos[3 * at + 1], r2 = pos[3 * at + 2];
+        const double g0 = frc[3 * at], g1 = frc[3 * at + 1], g2 = frc[3 * at + 2];
+        F0 = xadd(F0, g0); F1 = xadd(F1, g1); F2 = xadd(F2, g2);
+        T0 = xadd(T0, xsub(xmul(r1, g2), xmul(r2, g1)));
+        T1 = xadd(T1, xsub(xmul(r2, g0), xmul(r0, g2)));
+        T2 = xadd(T2, xsub(xmul(r0, g1), xmul(r1, g0)));
+    }
+    o[0] = F0; o[1] = F1; o[2] = F2; o[3] = T0; o[4] = T1; o[5] = T2;
+}
+
 __global__ void wrench_kernel(kf_chain_t c, int B, const double *__restrict__ pos_all,
                               const double *__restrict__ f_all, double *__restrict__ wrench_all,
                               const kf_status_t *status) {
@@ -198,7 +238,7 @@ KF_DEV void torque_step_cta(const kf_chain_t &c, const kf_field_t &f, const Torq
     if (fuse_wrench) {   // wrenches of this iteration straight into shared memory
         const int n = c.n_atoms;
         for (int l = threadIdx.x; l < L; l += blockDim.x)
-            link_wrench(c, l, w.pos + (size_t)b * n * 3, w.forces + (size_t)b * n * 3, wsm + 6 * l);
+            link_wrench_pf(c, l, w.pos + (size_t)b * n * 3, w.forces + (size_t)b * n * 3, wsm + 6 * l);
         __syncthreads();
         Wr = wsm;
     }
@@ -290,7 +330,7 @@ KF_DEV void torque_step_cta(const kf_chain_t &c, const kf_field_t &f, const Torq
 }
 
 template <int NT>
-__global__ void __launch_bounds__(NT)
+__global__ void __launch_bounds__(NT, 1024 / NT)   // 64 registers: 4 CTAs of 256 per SM
 torque_step_kernel(kf_chain_t c, kf_field_t f, TorqueArgs ta, kf_batch_t w, kf_step_t step, int mode,
                    int fuse_wrench, int e_first) {
     kf_pdl_wait();      // after the predecessor (programmatic launch: single trajectories)

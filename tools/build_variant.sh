@@ -1,14 +1,15 @@
 #!/bin/bash
 # Build libkfb200.so with extra -D flags into _variants/NAME.so (A/B measurements:
 # run with KFB200_LIB=$PWD/_variants/NAME.so).
-# usage: [CLSRC=alt_kf_cluster.cu] [REBUILD="kf_xxx ..."] tools/build_variant.sh NAME -DFOO=1 ...
+# usage: [SRCDIR=dir] [CLSRC=alt_kf_cluster.cu] [REBUILD="kf_xxx ..."] tools/build_variant.sh NAME -DFOO=1 ...
 # kf_loop (the unity TU of kinematics, torque and cluster kernels) is always rebuilt.
 set -e
 name=$1; shift
 root=$(cd "$(dirname "$0")/.." && pwd)
 out=$root/_variants/$name
 rm -rf "$out"; mkdir -p "$out/src"
-cp "$root"/paper_1712_05012_b200/csrc/*.cu "$root"/paper_1712_05012_b200/csrc/*.cuh "$out/src/"
+src=${SRCDIR:-$root/paper_1712_05012_b200/csrc}
+cp "$src"/*.cu "$src"/*.cuh "$out/src/"
 [ -n "$CLSRC" ] && cp "$CLSRC" "$out/src/kf_cluster.cu"
 cd "$out/src"
 objs=""
