@@ -9,6 +9,9 @@
 // branches follow level by level.  fp64 throughout; the scan re-associates the
 // products, so positions differ from the sequential walk at the 1e-13 A level.
 #include "kf_common.cuh"
+#ifdef FK_TIMING
+#include <cstdio>
+#endif
 
 namespace {
 
@@ -147,12 +150,21 @@ constexpr int FKS_STRIDE = 12;
 // full_t = 0 (the fold loop): only the second half of each T row is written, which
 // holds the joint point and axis the torque kernel projects with (rows 8-15:
 // M[8], P, U, pad); the API's kinematic_state asks for the whole row.
+#ifdef FK_TIMING   // phase clocks of CTA 0 (measurement builds only)
+#define FKT(k) do { if (b == 0 && threadIdx.x == 0) tk[k] = clock64(); } while (0)
+#else
+#define FKT(k) do { } while (0)
+#endif
 template <int NT>
 KF_DEV void fk_smem_cta(const kf_chain_t &c, int b, const double *__restrict__ theta_all,
                         double *__restrict__ T_all, double *__restrict__ pos_all, double *__restrict__ S,
                         int full_t = 1) {
     __shared__ double chunk[NT / 32][12];   // warp totals of the block scan
     __shared__ int sh_doff[8];               // side-level offsets (side_depth <= 7 staged)
+#ifdef FK_TIMING
+    long long tk[8];
+#endif
+    FKT(0);
     const int L = c.n_links, D = c.n_dof, n = c.n_atoms, nb = c.n_bb, ns = c.n_side;
     const double *theta = theta_all + (size_t)b * D;
     // the chain tables the serial phases walk, staged once (one global round trip
@@ -193,6 +205,7 @@ KF_DEV void fk_smem_cta(const kf_chain_t &c, int b, const double *__restrict__ t
         }
     }
     __syncthreads();
+    FKT(1);
 
     const int per = (nb + blockDim.x - 1) / blockDim.x;
     const int lo = min(nb, (int)threadIdx.x * per), hi = min(nb, lo + per);
@@ -211,6 +224,7 @@ KF_DEV void fk_smem_cta(const kf_chain_t &c, int b, const double *__restrict__ t
         }
     }
     __syncthreads();
+    FKT(2);
     for (int d = 0; d < c.side_depth; ++d) {
         const int k0 = d < nd ? sh_doff[d] : c.side_depth_off[d];
         const int k1 = d + 1 <= nd ? sh_doff[d + 1] : c.side_depth_off[d + 1];
@@ -221,6 +235,7 @@ KF_DEV void fk_smem_cta(const kf_chain_t &c, int b, const double *__restrict__ t
         }
         __syncthreads();
     }
+    FKT(3);
     // T with the current joint axes U_l = M_l axis0_l (chain.py:257); ground keeps 0.
     // The axis loads of TU links per thread are issued ahead of the stores.
     double *__restrict__ T = T_all + (size_t)b * L * KF_XF_STRIDE;
@@ -253,6 +268,10 @@ KF_DEV void fk_smem_cta(const kf_chain_t &c, int b, const double *__restrict__ t
                 if (full_t || q >= 4) d2[q] = make_double2(v[2 * q], v[2 * q + 1]);
         }
     }
+#ifdef FK_TIMING
+    __syncthreads();
+#endif
+    FKT(4);
     // positions pos_a = P_l + M_l zrel_a (fk_positions_kernel's arithmetic);
     // the chain tables are loaded ahead of the stores (no aliasing with pos)
     double *__restrict__ pos = pos_all + (size_t)b * n * 3;
@@ -278,6 +297,13 @@ KF_DEV void fk_smem_cta(const kf_chain_t &c, int b, const double *__restrict__ t
             pos[3 * a + 2] = t[11] + (t[6] * z[u][0] + t[7] * z[u][1] + t[8] * z[u][2]);
         }
     }
+#ifdef FK_TIMING
+    __syncthreads();
+    FKT(5);
+    if (b == 0 && threadIdx.x == 0)
+        printf("FKT tables+local %lld bbscan %lld side %lld Twrite %lld positions %lld total %lld\n", tk[1] - tk[0],
+               tk[2] - tk[1], tk[3] - tk[2], tk[4] - tk[3], tk[5] - tk[4], tk[5] - tk[0]);
+#endif
 }
 
 __global__ void __launch_bounds__(FKS_THREADS)
