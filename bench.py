@@ -568,10 +568,10 @@ def main():
     # algorithmic bytes per trajectory (SURVEY.md §8(d) formulas) x B / phase time
     n_at, L = ch.n_atoms, len(ch.links)
     phase_bytes = {
-        # theta in; link transforms (16 f64) and positions out
-        "fk": 8 * D + 128 * L + 24 * n_at,
-        # transforms, positions, forces, per-atom energies/counts in; tau, theta out
-        "torque": 128 * L + 48 * n_at + 24 * n_at + 16 * D,
+        # theta in; the joint point / axis half of each link row (8 f64) and positions out
+        "fk": 8 * D + 64 * L + 24 * n_at,
+        # joint points / axes, positions, forces, per-atom energies/counts in; tau, theta out
+        "torque": 64 * L + 48 * n_at + 24 * n_at + 16 * D,
     }
     if acc.get("bin", 0.0) > 0.01:   # binning runs only where a cell table is needed (water)
         H = 1 << max(6, int(np.ceil(np.log2(n_at + 1))))
