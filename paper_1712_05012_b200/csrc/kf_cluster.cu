@@ -1026,7 +1026,8 @@ fold_iteration_kernel(const __grid_constant__ kf_chain_t ch, const __grid_consta
 }
 
 template <int NCAP>
-inline int launch_cap(bool dconst, const kf_field_t *f, const ClConst &c, kf_batch_t *w, int n, cudaStream_t s) {
+inline int launch_cap(bool dconst, const kf_field_t *f, const ClConst &c, kf_batch_t *w, int n, cudaStream_t s,
+                      int plane_b) {
     constexpr size_t smem = ClLayout<NCAP>::TOTAL;
     // EALL: the elec threshold is the pair cut-off (elec >= vdW), so every fp32-path pair has the elec term
     const bool eall = c.te2 >= c.cut2;
@@ -1066,7 +1067,7 @@ inline int launch_cap(bool dconst, const kf_field_t *f, const ClConst &c, kf_bat
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     KF_CUDA(cudaLaunchKernelEx(&cfg, kern, *f, c, n, (const double *)w->pos, w->forces, w->e_atom, w->pair_count,
-                               w->status, w->pair_fj, reinterpret_cast<unsigned *>(w->s_lo), 2 * n, w->B, split),
+                               w->status, w->pair_fj, reinterpret_cast<unsigned *>(w->s_lo), 2 * n, plane_b, split),
             "cluster_pair_kernel");
     KF_LAUNCH_CHECK("cluster_pair_kernel");
     return 0;
@@ -1172,14 +1173,17 @@ static ClConst cl_const(const kf_field_t *f) {
     return c;
 }
 
-int kf_cluster_pairs_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s) {
+// plane_b: trajectories in the pair_fj planes' stride (w may be a sub-batch view
+// of a larger batch, see kf_api.cu batch_view); 0 = w->B
+int kf_cluster_pairs_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s, int plane_b) {
     const ClConst c = cl_const(f);
     const bool dc = f->dielectric_const != 0;
-    if (n <= 512) return launch_cap<512>(dc, f, c, w, n, s);
-    if (n <= 1024) return launch_cap<1024>(dc, f, c, w, n, s);
-    if (n <= 1536) return launch_cap<1536>(dc, f, c, w, n, s);
-    if (n <= 2048) return launch_cap<2048>(dc, f, c, w, n, s);
-    return launch_cap<2944>(dc, f, c, w, n, s);
+    if (plane_b <= 0) plane_b = w->B;
+    if (n <= 512) return launch_cap<512>(dc, f, c, w, n, s, plane_b);
+    if (n <= 1024) return launch_cap<1024>(dc, f, c, w, n, s, plane_b);
+    if (n <= 1536) return launch_cap<1536>(dc, f, c, w, n, s, plane_b);
+    if (n <= 2048) return launch_cap<2048>(dc, f, c, w, n, s, plane_b);
+    return launch_cap<2944>(dc, f, c, w, n, s, plane_b);
 }
 
 template <int NCAP>

@@ -854,7 +854,7 @@ int resident_grid(K kern, int threads, size_t dyn) {
 }  // namespace
 
 int kf_cluster_path(const kf_field_t *f, const kf_batch_t *w, int n);
-int kf_cluster_pairs_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s);
+int kf_cluster_pairs_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s, int plane_b);
 int kf_cluster_clash_report_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s);
 
 // The pair kernel a launch of (f, w, n) selects: 0 compacted list (fp64 pair math),
@@ -882,9 +882,9 @@ extern "C" int kf_pair_kernel_kind(const kf_field_t *f, const kf_batch_t *w, int
     return pair_variant(f, w, n);
 }
 
-int kf_pairs_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s) {
+int kf_pairs_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s, int plane_b) {
     // ensembles with fp32 pair math: the cluster-pair kernel (kf_cluster.cu)
-    if (kf_cluster_path(f, w, n)) return kf_cluster_pairs_launch(f, w, n, s);
+    if (kf_cluster_path(f, w, n)) return kf_cluster_pairs_launch(f, w, n, s, plane_b);
     if (g_sms == 0) {
         int dev = 0;
         cudaGetDevice(&dev);
