@@ -568,8 +568,9 @@ def main():
     # algorithmic bytes per trajectory (SURVEY.md §8(d) formulas) x B / phase time
     n_at, L = ch.n_atoms, len(ch.links)
     phase_bytes = {
-        # theta in; the joint point / axis half of each link row (8 f64) and positions out
-        "fk": 8 * D + 64 * L + 24 * n_at,
+        # theta in; link transforms (16 f64: the eager API launch writes whole rows; the fold
+        # loop writes only the joint point / axis half) and positions out
+        "fk": 8 * D + 128 * L + 24 * n_at,
         # joint points / axes, positions, forces, per-atom energies/counts in; tau, theta out
         "torque": 64 * L + 48 * n_at + 24 * n_at + 16 * D,
     }
