@@ -365,13 +365,19 @@ bin_fused_kernel(const __grid_constant__ kf_field_t f, int B, int n, int chunk, 
     __shared__ int wsum[32];
     constexpr int NWB = NT / 32, CAP = bf_cap<NT>();
     __shared__ int buf[NWB][CAP];
+    // the trajectory's hash table (keys, then counts) in shared memory: the CAS
+    // inserts and the warp-aggregated counts are shared-memory atomics; the table is
+    // written out once, coalesced, for the later kernels (solvation, pairs)
+    extern __shared__ __align__(16) unsigned char bf_dyn[];
     const int b = blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const size_t H = (size_t)1 << f.hash_bits;
+    unsigned long long *sk = reinterpret_cast<unsigned long long *>(bf_dyn);
+    int32_t *sc = reinterpret_cast<int32_t *>(sk + H);
     if (!status[b].done) {
         unsigned long long *tk = keys + b * H;
         int32_t *tc = cnt + b * H, *ts = start + b * H, *to = occ + b * H, *tp = chunk_pre + b * H;
-        for (size_t q = threadIdx.x; q < H; q += blockDim.x) { tk[q] = EMPTY; tc[q] = 0; }
+        for (size_t q = threadIdx.x; q < H; q += blockDim.x) { sk[q] = EMPTY; sc[q] = 0; }
         if (threadIdx.x == 0) m_s = 0;
         __syncthreads();
         // insert: cell key per atom, CAS into the table, warp-aggregated counts
@@ -395,7 +401,7 @@ bin_fused_kernel(const __grid_constant__ kf_field_t f, int B, int n, int chunk, 
                 const int leader = __ffs(same) - 1;
                 if (lane == leader) {
                     for (;;) {
-                        const unsigned long long prev = atomicCAS(&tk[slot], EMPTY, key);
+                        const unsigned long long prev = atomicCAS(&sk[slot], EMPTY, key);
                         if (prev == EMPTY) { to[atomicAdd(&m_s, 1)] = (int32_t)slot; break; }
                         if (prev == key) break;
                         slot = (slot + 1) & ((uint32_t)H - 1);
@@ -404,20 +410,21 @@ bin_fused_kernel(const __grid_constant__ kf_field_t f, int B, int n, int chunk, 
                 slot = __shfl_sync(same, slot, leader);
                 const int rank_in = __popc(same & ((1u << lane) - 1u));
                 int base = 0;
-                if (lane == leader) base = atomicAdd(&tc[slot], __popc(same));
+                if (lane == leader) base = atomicAdd(&sc[slot], __popc(same));
                 base = __shfl_sync(same, base, leader);
                 atom_slot[ga] = (int32_t)slot;
                 atom_rank[ga] = base + rank_in;
             }
         }
         __syncthreads();
+        for (size_t q = threadIdx.x; q < H; q += blockDim.x) { tk[q] = sk[q]; tc[q] = sc[q]; }
         // exclusive scans of atom counts and i-chunks over the occupied list
         const int m = m_s;
         const int per = (m + blockDim.x - 1) / blockDim.x;
         const int lo = min(m, (int)threadIdx.x * per), hi = min(m, lo + per);
         int local = 0, lchunk = 0;
         for (int k = lo; k < hi; ++k) {
-            const int c = tc[to[k]];
+            const int c = sc[to[k]];
             local += c;
             lchunk += (c + chunk - 1) / chunk;
         }
@@ -425,7 +432,7 @@ bin_fused_kernel(const __grid_constant__ kf_field_t f, int B, int n, int chunk, 
         int crun = block_excl_scan(lchunk, wsum);
         int32_t *ti = item_cell + b * H;
         for (int k = lo; k < hi; ++k) {
-            const int c = tc[to[k]], nc = (c + chunk - 1) / chunk;
+            const int c = sc[to[k]], nc = (c + chunk - 1) / chunk;
             ts[to[k]] = run; run += c;
             tp[k] = crun;
             for (int q = 0; q < nc; ++q) ti[crun + q] = k;
@@ -591,7 +598,14 @@ int kf_bin_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStream_t s) {
     }
     if (n <= BF_MAX_ATOMS && B >= BF_MIN_B) {   // ensembles: one CTA per trajectory does the whole binning
         auto kern = B < BF_FEW_B ? bin_fused_kernel<BF_THREADS_FEW> : bin_fused_kernel<BF_THREADS>;
-        kern<<<B, B < BF_FEW_B ? BF_THREADS_FEW : BF_THREADS, 0, s>>>(
+        const size_t dyn = (size_t)H * (sizeof(unsigned long long) + sizeof(int32_t));   // the shared hash table
+        static size_t opted[2] = {0, 0};
+        const int few = B < BF_FEW_B;
+        if (dyn > opted[few]) {
+            KF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn), "bin smem");
+            opted[few] = dyn;
+        }
+        kern<<<B, B < BF_FEW_B ? BF_THREADS_FEW : BF_THREADS, dyn, s>>>(
             *f, B, n, kf_pair_chunk(B, n, w->pair_chunk, f->precision), w->pos, w->cell_key, w->cell_cnt,
             w->cell_start, w->occ, w->occ_count, w->chunk_pre, w->item_cell, w->chunk_count, w->occ_offset, w->chunk_offset,
             w->atom_slot, w->atom_rank, w->sorted_atom, reinterpret_cast<float4 *>(w->s_hi),
