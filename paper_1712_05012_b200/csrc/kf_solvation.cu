@@ -263,6 +263,7 @@ struct GroupSmem {
     float4 *cap;       // [cap] u, c1 - margin
     float *c2;         // [cap] c2 - margin
     int32_t *atom;     // [cap]
+    float4 *cone;      // [cap] cos / sin of the enlarged cap, cos / sin of the tightened plain cap
     // staging (aliases acc + masks): unsorted neighbours and their sort keys
     NbSlot *tmp;
     int32_t *tmp_atom;
@@ -278,7 +279,8 @@ KF_DEV GroupSmem carve_group(unsigned char *smem, int cap, int G) {
     S.cap = reinterpret_cast<float4 *>(S.nb + cap);
     S.c2 = reinterpret_cast<float *>(S.cap + cap);
     S.atom = reinterpret_cast<int32_t *>(S.c2 + cap);
-    unsigned char *r1 = reinterpret_cast<unsigned char *>(S.atom + cap);
+    S.cone = reinterpret_cast<float4 *>(S.atom + ((cap + 3) & ~3));
+    unsigned char *r1 = reinterpret_cast<unsigned char *>(S.cone + cap);
     S.tmp = reinterpret_cast<NbSlot *>(r1);
     S.tmp_atom = reinterpret_cast<int32_t *>(S.tmp + cap);
     S.key = reinterpret_cast<float *>(S.tmp_atom + cap);
@@ -289,7 +291,8 @@ KF_DEV GroupSmem carve_group(unsigned char *smem, int cap, int G) {
 }
 
 size_t group_smem(int cap, int G) {
-    const size_t base = (size_t)cap * (sizeof(NbSlot) + sizeof(float4) + sizeof(float) + sizeof(int32_t));
+    const size_t base = (size_t)cap * (sizeof(NbSlot) + 2 * sizeof(float4) + sizeof(float)) +
+                        (size_t)((cap + 3) & ~3) * sizeof(int32_t);
     const size_t stage = (size_t)cap * (sizeof(NbSlot) + sizeof(int32_t) + sizeof(float));
     const size_t work = (size_t)cap * 3 * sizeof(long long) + 2 * (size_t)G * ((cap + 31) / 32) * sizeof(uint32_t);
     return base + (stage > work ? stage : work);
@@ -451,43 +454,68 @@ KF_DEV void solv_atom(const kf_field_t &f, const SolvArgs &A, int b, int i, int 
         if (d2 > 1e-12f) {
             const float d = sqrtf(d2), inv = 1.f / d, r2j = (float)q.r2, rj = sqrtf(r2j);
             const float ri2 = r_i_f * r_i_f, den = 1.f / (2.f * r_i_f * d);
-            S.cap[r] = make_float4(dx * inv, dy * inv, dz * inv, (ri2 + d2 - r2j) * den - CAP_MARGIN);
-            S.c2[r] = (ri2 + d2 - (rj + drf) * (rj + drf)) * den - CAP_MARGIN;
+            const float c1 = (ri2 + d2 - r2j) * den - CAP_MARGIN, c2 = (ri2 + d2 - (rj + drf) * (rj + drf)) * den - CAP_MARGIN;
+            S.cap[r] = make_float4(dx * inv, dy * inv, dz * inv, c1);
+            S.c2[r] = c2;
+            // the mask pass's cone terms: enlarged cap (cos, sin), plain cap tightened
+            // by 1e-3 (c1 is c1 - 1e-3 already) for the full-cover test
+            const float cb = fminf(fmaxf(c2, -1.f), 1.f), sb = sqrtf(fmaxf(0.f, 1.f - cb * cb));
+            float cf = 2.f, sf = 0.f;
+            if (c1 > -2.f) {
+                cf = c1 + 2e-3f;
+                sf = sqrtf(fmaxf(0.f, 1.f - cf * cf));
+            }
+            S.cone[r] = make_float4(cb, sb, cf, sf);
         } else {
             S.cap[r] = make_float4(0.f, 0.f, 0.f, -3.f);
             S.c2[r] = -3.f;
+            S.cone[r] = make_float4(-1.f, 0.f, 2.f, 0.f);   // keep (cb <= -cos alpha), never full
         }
     }
     __syncthreads();
     // ---- candidate bitmasks: group cone vs enlarged cap
     const int G = f.n_groups, W = (count + 31) >> 5;
-    {
+    if (G <= 32) {
+        // lane = sample group (its cone in registers), each warp builds whole
+        // 32-neighbour words, the neighbours' cap terms broadcast from shared memory
+        const int lane = threadIdx.x & 31, g = lane;
+        const bool gl = g < G;
+        const float4 ax = gl ? reinterpret_cast<const float4 *>(f.grp_cone)[2 * g] : make_float4(0.f, 0.f, 0.f, 2.f);
+        const float sin_a = gl ? f.grp_cone[8 * g + 4] : 0.f;
+        for (int w = threadIdx.x >> 5; w < W; w += blockDim.x >> 5) {
+            const int m0 = w << 5, mn = min(32, count - m0);
+            uint32_t bits = 0u, fbits = 0u;
+#pragma unroll 4
+            for (int t = 0; t < mn; ++t) {
+                const float4 cp = S.cap[m0 + t], cn = S.cone[m0 + t];
+                const float dot = ax.x * cp.x + ax.y * cp.y + ax.z * cp.z;
+                // cone (a_g, alpha) meets the enlarged cap (u, beta): angle(a, u) <= alpha + beta
+                const bool keep = cn.x <= -ax.w || dot >= ax.w * cn.x - sin_a * cn.y - 1e-3f;
+                // cone inside the tightened plain cap (beta1 > alpha, angle(a, u) <= beta1 - alpha):
+                // every sample of the group is covered by m, exactly (margins >> rounding)
+                const bool full = cn.z < ax.w && dot >= ax.w * cn.z + sin_a * cn.w + 1e-3f;
+                bits |= (uint32_t)keep << t;
+                fbits |= (uint32_t)full << t;
+            }
+            if (gl) {
+                S.mask[g * W + w] = bits; S.full[g * W + w] = fbits;
+                if (fbits && g < SOLV_MAX_GROUPS) atomicAdd(&gfull_s[g], __popc(fbits));
+            }
+        }
+    } else {
         // lane = neighbour of word w (its cap in registers), warps sweep the groups
         const int lane = threadIdx.x & 31;
         for (int w = 0; w < W; ++w) {
             const int m = (w << 5) + lane;
-            float4 cp = make_float4(0.f, 0.f, 0.f, 0.f);
-            float cb = 1.f, sb = 0.f, cf = 2.f, sf = 0.f;
-            bool live = m < count;
-            if (live) {
-                cp = S.cap[m];
-                cb = fminf(fmaxf(S.c2[m], -1.f), 1.f);
-                sb = sqrtf(fmaxf(0.f, 1.f - cb * cb));
-                // full cover: the plain cap tightened by 1e-3 (cap.w is c1 - 1e-3)
-                if (cp.w > -2.f) {
-                    cf = cp.w + 2e-3f;
-                    sf = sqrtf(fmaxf(0.f, 1.f - cf * cf));
-                }
-            }
+            float4 cp = make_float4(0.f, 0.f, 0.f, 0.f), cn = make_float4(1.f, 0.f, 2.f, 0.f);
+            const bool live = m < count;
+            if (live) { cp = S.cap[m]; cn = S.cone[m]; }
             for (int g = threadIdx.x >> 5; g < G; g += blockDim.x >> 5) {
                 const float4 ax = reinterpret_cast<const float4 *>(f.grp_cone)[2 * g];
                 const float sin_a = f.grp_cone[8 * g + 4];
                 const float dot = ax.x * cp.x + ax.y * cp.y + ax.z * cp.z;
-                // cone (a_g, alpha) meets the enlarged cap (u, beta): angle(a, u) <= alpha + beta
-                const bool keep = live && (cb <= -ax.w || dot >= ax.w * cb - sin_a * sb - 1e-3f);
-                // cone inside the tightened plain cap (beta1 > alpha, angle(a, u) <= beta1 - alpha):
-                // every sample of the group is covered by m, exactly (margins >> rounding)
-                const bool full = live && cf < ax.w && dot >= ax.w * cf + sin_a * sf + 1e-3f;
+                const bool keep = live && (cn.x <= -ax.w || dot >= ax.w * cn.x - sin_a * cn.y - 1e-3f);
+                const bool full = live && cn.z < ax.w && dot >= ax.w * cn.z + sin_a * cn.w + 1e-3f;
                 const uint32_t bits = __ballot_sync(0xffffffffu, keep);
                 const uint32_t fbits = __ballot_sync(0xffffffffu, full);
                 if (lane == 0) {
