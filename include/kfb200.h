@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define KF_ABI_VERSION 12
+#define KF_ABI_VERSION 13
 
 /* ---- static chain tables (uploaded once per chain) ------------------------
  * Links are in the reference's topological order (parent < index, ground = 0),
@@ -106,6 +106,11 @@ typedef struct {
        of the 32 pairs (i = 4Q + l%4, j = 8O + l/4) at bits 2l; host-built from the
        bond tree (topology.py:153-178).  NULL for UniformWeights.               */
     const unsigned long long *class_codes;   /* [ceil(n/4)][5] */
+    /* the same codes per (unit U = octet U = quads 2U, 2U+1; lane l): bits 2k..2k+1
+       quad 2U's code for window octet U + k, bits 10 + 2k.. quad 2U + 1's, bits
+       20-24 / 25-29 which of the 5 window octets hold a class < 4 pair for either
+       quad, bit 30 the unit has a class_slow atom.  NULL for UniformWeights.   */
+    const uint32_t *unit_codes;     /* [ceil(n/8)][32] */
 } kf_field_t;
 
 /* ---- per-trajectory status block ----------------------------------------- */

@@ -14,7 +14,7 @@ from .errors import NativeLibraryError
 
 LIB_PATH = os.environ.get("KFB200_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib",
                                                          "libkfb200.so")   # KFB200_LIB: A/B builds
-ABI_VERSION = 12
+ABI_VERSION = 13
 
 P = C.c_void_p
 I32 = C.c_int32
@@ -43,7 +43,7 @@ class KfField(C.Structure):
         ("gamma", P), ("w_int", P), ("quantum", F64), ("delta_r", F64), ("four_pi", F64),
         ("reach_pad", F64), ("solv_atoms", P), ("n_solv", I32), ("precision", I32),
         ("samples_grp", P), ("grp_cone", P), ("n_groups", I32), ("flat", I32),
-        ("atom_par", P), ("atom_aux", P), ("r_off_max", F64), ("class_codes", P)]
+        ("atom_par", P), ("atom_aux", P), ("r_off_max", F64), ("class_codes", P), ("unit_codes", P)]
 
 
 class KfStatus(C.Structure):

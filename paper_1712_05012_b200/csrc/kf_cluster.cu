@@ -668,7 +668,6 @@ KF_DEV void cluster_pairs_cta(const kf_field_t &f, const ClConst &c, int n, int 
     const unsigned base = smem_u32(sm);
     const double *pos = pos_all + 3 * (size_t)b * n;
     const float4 *apar = reinterpret_cast<const float4 *>(f.atom_par);
-    const int4 *aaux = reinterpret_cast<const int4 *>(f.atom_aux);
     // each quad's (elec, vdW) energy goes to e_atom[quad] (global scratch, read back
     // in quad order at the end; the totals then sit at atom 0)
     double *e_q = e_atom + 2 * (size_t)b * n;
@@ -755,18 +754,19 @@ KF_DEV void cluster_pairs_cta(const kf_field_t &f, const ClConst &c, int n, int 
         const float4 oiB = vB ? lds4(sb + L::OQ + 16 * iB) : make_float4(-FAR, -FAR, -FAR, 0.f);
         const float2 riA = lds2(sb + L::RS + 8 * (vA ? iA : 0)), riB = lds2(sb + L::RS + 8 * (vB ? iB : 0));
         const float4 cu = lds4(sb + L::OCT_C + 16 * U), hu = lds4(sb + L::OCT_H + 16 * U);
-        const bool slow_u = !c.uniform && __any_sync(FULL, (vA && aaux[vA ? iA : 0].w != 0) ||
-                                                           (vB && aaux[vB ? iB : 0].w != 0));
-        // window octets whose 32 pairs are all class 4 (most of k = 3, 4) take the lean path
-        unsigned winA = 1u, winB = 1u;                    // the own octet always (j > i test)
-        if (!c.uniform) {
+        // this lane's class codes of the unit's window octets, which of those octets
+        // hold class < 4 pairs, and whether the unit has a slow atom: one word per lane
+        // (host-built unit_codes).  Window octets whose 32 pairs are all class 4 (most
+        // of k = 3, 4) take the lean path; the own octet always takes the general one
+        // (j > i test).
+        const unsigned uw = c.uniform ? 0u : f.unit_codes[32 * U + lane_p];
+        const bool slow_u = (uw >> 30) & 1u;
+        const unsigned winA = ((uw >> 20) & 0x1fu) | 1u, winB = ((uw >> 25) & 0x1fu) | 1u;
+        if (slow_u) {   // the general rounds read the 64-bit codes from shared memory
             unsigned long long code = 0ull;
             if (lane_p < 5) code = f.class_codes[5 * QA + lane_p];
             else if (lane_p >= 8 && lane_p < 13 && QB < nq) code = f.class_codes[5 * QB + lane_p - 8];
             if (lane_p < 5 || (lane_p >= 8 && lane_p < 13)) qcodes[warp][lane_p < 5 ? lane_p : lane_p - 3] = code;
-            const unsigned m = __ballot_sync(FULL, code != 0ull);
-            winA = (m & 0x1fu) | 1u;
-            winB = ((m >> 8) & 0x1fu) | 1u;
         }
         __syncwarp();
         // packed (quad A, quad B) operands and accumulators of the class-4 rounds
@@ -782,15 +782,7 @@ KF_DEV void cluster_pairs_cta(const kf_field_t &f, const ClConst &c, int n, int 
             lu.ri = pair_of(riA.x, riB.x);
             lu.se = pair_of(riA.y, riB.y);
             lu.vA = vA; lu.vB = vB;
-            unsigned cw = 0u;
-            if (!c.uniform) {   // this lane's 2-bit codes of the 5 window octets, both quads
-#pragma unroll
-                for (int k = 0; k < 5; ++k) {
-                    cw |= (unsigned)((qcodes[warp][k] >> (2 * lane_p)) & 3ull) << (2 * k);
-                    cw |= (unsigned)((qcodes[warp][5 + k] >> (2 * lane_p)) & 3ull) << (10 + 2 * k);
-                }
-            }
-            lu.codes = cw;
+            lu.codes = uw & 0xfffffu;
             lean_sweep<DCONST, NCAP, EALL>(c, lu, fx, fy, fz, ee2, ev2, ce, cv, U, no, sb, winA | winB, wtab, &xq);
         } else
         for (int ob = U; ob < no; ob += 32) {

@@ -322,6 +322,29 @@ def class_codes(tree) -> np.ndarray:
     return code.reshape(nq, 5)
 
 
+def unit_codes(codes, slow) -> np.ndarray:
+    """class_codes regrouped per (unit U = quads 2U, 2U+1; lane l) as the cluster
+    kernel's lanes use them (kfb200.h unit_codes): one coalesced 32-bit load per
+    lane and unit instead of 10 code words and the slow-atom flags."""
+    nq = codes.shape[0]
+    no = (nq + 1) // 2
+    c = np.zeros((2 * no, 5), np.uint64)
+    c[:nq] = codes
+    lane = np.arange(32, dtype=np.uint64)
+    bits = (c[:, :, None] >> (2 * lane)[None, None, :]) & np.uint64(3)      # [2 no][5][32]
+    k2 = (2 * np.arange(5, dtype=np.uint64))[:, None]
+    qa = (bits[0::2] << k2).sum(axis=1, dtype=np.uint64)                       # [no][32]
+    qb = (bits[1::2] << (k2 + np.uint64(10))).sum(axis=1, dtype=np.uint64)
+    nz = (c != 0).astype(np.uint64)
+    win = ((nz[0::2] << np.arange(5, dtype=np.uint64)).sum(axis=1, dtype=np.uint64) << np.uint64(20)) | \
+          ((nz[1::2] << np.arange(5, dtype=np.uint64)).sum(axis=1, dtype=np.uint64) << np.uint64(25))
+    n = len(slow)
+    s = np.zeros(8 * no, bool)
+    s[:n] = slow
+    su = s.reshape(no, 8).any(axis=1).astype(np.uint64) << np.uint64(30)
+    return (qa | qb | (win | su)[:, None]).astype(np.uint32)
+
+
 class ParamTables:
     """Per-atom parameters + pair-weight provider + dielectric on the device."""
 
@@ -351,6 +374,7 @@ class ParamTables:
                      tchain=_up(tree.chain_mask, np.uint8), class_map=_up(cmap, np.int32),
                      class_slow=_up(slow, np.uint8),
                      class_codes=_up(class_codes(tree).view(np.int64), np.int64))
+            t.update(unit_codes=_up(unit_codes(class_codes(tree), slow).view(np.int32), np.int32))
             aux[:, 3] = slow.astype(np.int32)
             s.uniform_weights = 0
             for k, v in enumerate(np.asarray(weights.table.elec_by_class())[1:5]):
