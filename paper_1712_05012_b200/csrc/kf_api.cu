@@ -107,18 +107,21 @@ static kf_batch_t batch_view(const kf_batch_t &w, const kf_chain_t *c, int b0, i
     return v;
 }
 
-// Vacuum ensembles on the cluster path run as independent sub-batches on their own
+// Vacuum ensembles on the cluster path run as independent sub-batches (>= 64
+// trajectories, up to 4) on their own
 // streams inside the graph (graph branches): one sub-batch's latency-bound FK /
 // torque kernels overlap another's issue-bound pair kernel.  KFB200_BRANCHES sets
 // the count (1: off).
 constexpr int KF_MAX_BRANCHES = 4;
 static int graph_branches(const kf_chain_t *c, const kf_field_t *f, const kf_batch_t *w) {
-    static int env = -1;
+    static int env = -1, min_sub = 64;   // measured: B = 256 as 4 x 64 0.223 vs 0.259 ms, B = 512 as 4 x 128 0.362 vs 0.375
     if (env < 0) {
         const char *e = getenv("KFB200_BRANCHES");
         env = std::min(KF_MAX_BRANCHES, e ? atoi(e) : 4);   // measured (C5): 4 0.696, 2 0.711, 1 0.771 ms
+        const char *m = getenv("KFB200_BRANCH_MIN");           // smallest sub-batch
+        if (m) min_sub = std::max(1, atoi(m));
     }
-    const int nbr = std::min(env, w->B / 256);   // sub-batches of >= 256 trajectories
+    const int nbr = std::min(env, w->B / min_sub);
     if (nbr < 2 || f->solvation) return 1;
     kf_batch_t part = *w;
     part.B = w->B / nbr;
