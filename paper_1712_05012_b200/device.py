@@ -892,6 +892,13 @@ class EnsembleRunner:
             th = b.t["theta"][:, :D].cpu().numpy()
             thetas = (b.t["rec_theta"][:, :K].cpu().numpy()
                       if b.t["rec_theta"] is not None else None)
+        # record rows past a trajectory's own stop hold a previous run's values (the
+        # record buffers are reused, not cleared): zero them
+        past = np.arange(K)[None, :] >= iters[:, None]
+        if past.any():
+            rec[past] = 0.0
+            if thetas is not None:
+                thetas[past] = 0.0
         names = {code: N.REASONS.get(int(code), "max_iters") for code in np.unique(sa["reason"])}
         return EnsembleResult(theta=th, energies=rec, iterations=iters,
                               reasons=[names[r] for r in sa["reason"]],

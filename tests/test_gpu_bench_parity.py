@@ -269,3 +269,28 @@ def test_cluster_kernel_variants_match_oracle(variant):
         assert np.all(err <= 1e-5 * np.maximum(scale, 1e-300)), (r, float((err / scale).max()))
         e = res.energies[r, 0, :3]
         assert np.abs(e - np.array(e_ref)).sum() <= 1e-6 * np.abs(np.array(e_ref)).sum(), r
+
+
+def test_graph_branches_equal_separate_sub_batches():
+    """The fold graph of a 256-trajectory vacuum ensemble runs as four 64-trajectory
+    branches (kf_api.cu graph_branches / batch_view).  Each branch must give bitwise
+    what a separate 64-trajectory fold_ensemble gives (same kernel decomposition):
+    final theta, every iteration's energies / tau_max and theta records, iterations
+    and stop reasons, with a stop rule that ends some trajectories early."""
+    from paper_1712_05012_b200 import workloads
+    P = _P()
+    ch, params, w, fld = _system("C2")
+    thetas = workloads.random_thetas(ch, 256, seed=4)
+    confs = [P.Conformation(t, np.zeros(ch.n_dof, bool), ch.n_residues) for t in thetas]
+    step = P.StepConfig(kappa=KAPPA, max_iters=12, torque_tol_rel=0.3, energy_window=0)
+    whole = P.fold_ensemble(ch, confs, fld, step, record_theta=True)
+    for r in range(4):
+        part = P.fold_ensemble(ch, confs[64 * r:64 * (r + 1)], fld, step, record_theta=True)
+        sl = slice(64 * r, 64 * (r + 1))
+        assert np.array_equal(whole.theta[sl], part.theta)
+        K = part.energies.shape[1]   # records are cut at the batch's longest trajectory
+        assert np.array_equal(whole.energies[sl, :K], part.energies)
+        assert not whole.energies[sl, K:].any()
+        assert np.array_equal(whole.thetas[sl, :K], part.thetas)
+        assert np.array_equal(whole.iterations[sl], part.iterations)
+        assert whole.reasons[sl] == part.reasons
