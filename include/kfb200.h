@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define KF_ABI_VERSION 13
+#define KF_ABI_VERSION 14
 
 /* ---- static chain tables (uploaded once per chain) ------------------------
  * Links are in the reference's topological order (parent < index, ground = 0),
@@ -142,6 +142,10 @@ typedef struct {
     int32_t record_theta;           /* store theta per iteration                   */
     int32_t max_records;            /* record ring capacity (iterations)           */
     int32_t pair_chunk;             /* atoms per pair-kernel work item: 4/8/16/32, 0 = auto */
+    int32_t api_eval;               /* 1: a single-conformation API evaluation (Field.evaluate):
+                                       below 32 trajectories it keeps the binned dense lanes,
+                                       whose separate hash phase the API reports; 0: fold loop */
+    int32_t _pad_b;
     double  *theta;                 /* [B][D]                                      */
     const uint8_t *frozen;          /* [B][D]                                      */
     double  *link_T;                /* [B][L][16]: rotation (row-major 9), joint point (3), axis (3), pad */

@@ -14,7 +14,7 @@ from .errors import NativeLibraryError
 
 LIB_PATH = os.environ.get("KFB200_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib",
                                                          "libkfb200.so")   # KFB200_LIB: A/B builds
-ABI_VERSION = 13
+ABI_VERSION = 14
 
 P = C.c_void_p
 I32 = C.c_int32
@@ -55,7 +55,7 @@ class KfStatus(C.Structure):
 
 class KfBatch(C.Structure):
     _fields_ = [("B", I32), ("n_buckets", I32), ("nb_cap", I32), ("record_theta", I32),
-                ("max_records", I32), ("pair_chunk", I32)] + [
+                ("max_records", I32), ("pair_chunk", I32), ("api_eval", I32), ("_pad_b", I32)] + [
         (name, P) for name in (
             "theta", "frozen", "link_T", "fk_scratch", "pos", "forces", "cell_key", "cell_cnt", "cell_start",
             "occ", "occ_count", "occ_offset", "chunk_pre", "item_cell", "chunk_count", "chunk_offset",

@@ -1028,13 +1028,16 @@ inline int launch_cap(bool dconst, const kf_field_t *f, const ClConst &c, kf_bat
     static bool opted[4] = {false, false, false, false};
     if (!opted[2 * dconst + eall]) {
         KF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "cluster smem");
+        // clusters of 16 CTAs (beyond the portable 8) for single short chains
+        KF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1), "cluster size");
         opted[2 * dconst + eall] = true;
     }
     // exact-pair queue + its sorted copy: the SoA low-word buffer ([B][n][4] u32), which
     // the cluster path does not otherwise use (binning writes it, nothing later reads it)
     // small batches: each trajectory is split over a thread-block cluster of S CTAs so
-    // that the batch still fills two CTAs per SM (S = the largest power of two <= 8
-    // with B S <= 2 x SMs; KFB200_CL_SPLIT overrides)
+    // that the batch still fills two CTAs per SM: S = the largest power of two <= 16
+    // with B S <= 2 x SMs and at least 8 units per CTA (C1 single: S = 4 27.9 vs S = 8
+    // 28.9 us; C2 single: S = 16 56.4 vs S = 8 59.4 us); KFB200_CL_SPLIT overrides
     static int sms = 0, env_split = -1;
     if (!sms) {
         int dev = 0;
@@ -1044,7 +1047,8 @@ inline int launch_cap(bool dconst, const kf_field_t *f, const ClConst &c, kf_bat
         env_split = e ? atoi(e) : 0;
     }
     int split = 1;
-    while (split < 8 && (long long)w->B * split * 2 <= 2LL * sms) split *= 2;
+    const int units = (n + 7) / 8;
+    while (split < 16 && (long long)w->B * split * 2 <= 2LL * sms && units >= 16 * split) split *= 2;
     if (env_split > 0) split = env_split;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(w->B * split);
@@ -1094,12 +1098,15 @@ int kf_cluster_clash_report_launch(const kf_field_t *f, kf_batch_t *w, int n, cu
     return 0;
 }
 
-// The cluster path applies to fp32 pair math on ensembles whose trajectories fit
-// one CTA's shared memory; KFB200_CLUSTER=0 disables it, KFB200_CLUSTER_MIN_B
-// moves the batch threshold (measurements).  kf_bin_launch, kf_pairs_launch and
+// The cluster path applies to fp32 pair math on chains that fit one CTA's shared
+// memory, at any batch size (small batches split each trajectory over a cluster of
+// CTAs).  Measured against the dense lanes: C2 step at B = 128 0.175 vs 0.343 ms,
+// B = 32 0.156 vs 0.170; single C2 chain 56.4 vs 60.1 us per iteration (16-CTA
+// clusters), C1 28.9 vs 40.1.  KFB200_CLUSTER=0 disables it, KFB200_CLUSTER_MIN_B
+// sets a batch threshold (measurements).  kf_bin_launch, kf_pairs_launch and
 // kf_torque_launch all consult this, so one launch configuration is consistent.
 #ifndef CL_MIN_B
-#define CL_MIN_B 32   // measured (lean visits): C2 step at B=32 0.156 vs 0.170 ms (cluster vs dense), B=128 0.175 vs 0.343
+#define CL_MIN_B 1
 #endif
 
 int kf_cluster_path(const kf_field_t *f, const kf_batch_t *w, int n) {
@@ -1116,10 +1123,8 @@ int kf_cluster_path(const kf_field_t *f, const kf_batch_t *w, int n) {
         smem_max = (size_t)v;
     }
     if (!f || !w || !env_on || f->precision || f->flat || !w->pair_fj || n < 1) return 0;
-    // short chains take it at any batch size (C1, 301 atoms, one trajectory: 30.7 vs
-    // 40.1 us per iteration, no binning); C2-sized single chains are as fast on the
-    // dense lanes (62 vs 64 us)
-    if (w->B < env_min_b && n > 1024) return 0;
+    if (w->B < env_min_b) return 0;
+    if (w->api_eval && w->B < 32) return 0;   // single API evaluations: cell lists + dense lanes
     return n <= CL_CAPS[CL_NCAPS - 1] && (size_t)ClLayout<2944>::TOTAL <= smem_max ? 1 : 0;
 }
 

@@ -628,6 +628,7 @@ def evaluate(fld, positions, *, energy_only: bool = False):
     if df.solvation:
         check_cav_cutoff(fld.params, fld.config.solvation_cfg, fld.config.cutoffs.cav)
     b = df.batch(None, 1, store_sasa=df.solvation)
+    b.struct.api_eval = 1
     fs = df.struct_for(True)
     s = stream()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
