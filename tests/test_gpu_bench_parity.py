@@ -12,13 +12,12 @@ Each ensemble test runs ``fold_ensemble``'s runner at the batch size that
 selects a given kernel decomposition.  The kernel choice (kf_pairs_launch,
 kf_bin_launch, kf_torque_launch) depends on the batch B:
 
-* B = 1024 is the bench's C5 configuration (cluster-pair kernel);
-* B = 384 is the first B with 256-thread torque CTAs;
-* B = 128 and B = 32 take the cluster-pair kernel with one CTA per SM (B = 32
-  is its first batch size);
-* B = 30 takes the dense half-list kernel with fixed-point j forces (B n >= 40k
-  atoms) and the unfused binning;
-* B = 16 takes the dense full list.
+* B = 1024 is the bench's C5 configuration (cluster-pair kernel, four graph
+  branches of 256);
+* B = 384 is the first B with 256-thread torque CTAs (four branches of 96);
+* B = 128, 32, 30 and 16 split each trajectory over a cluster of 2 (as two
+  64-trajectory branches: 4), 8, 8 and 16 CTAs.
+The dense-lane kernels are covered by the C3 / C4 single-chain tests below.
 
 The comparison covers the first min(B, 32) trajectories, against the goldens.  The
 iteration's forces are read from the batch's force buffer (the test hook).
