@@ -589,8 +589,16 @@ KF_DEV void solv_atom(const kf_field_t &f, const SolvArgs &A, int b, int i, int 
                 bits &= bits - 1u;
                 if (lane == 0) SSTAT(3, 1);
                 if (cnt < 2) {
+                    // |p - r_j|^2 = R_i^2 + d^2 - 2 R_i d (q.u), so j covers p iff q.u >= c1
+                    // exactly; cap.w = c1 - 1e-3.  Outside the +-1e-3 band around c1 the fp32
+                    // test decides (its error is ~1e-6, and so far from the boundary the
+                    // reference's fp64 test agrees); inside it, the reference's exact fp64
+                    // test.  (cap.w = -3: a coincident neighbour, always the exact test.)
                     const float4 cp = S.cap[m];
-                    if (qx * cp.x + qy * cp.y + qz * cp.z >= cp.w && covers(px, py, pz, S.nb[m])) {
+                    const float dot = qx * cp.x + qy * cp.y + qz * cp.z;
+                    bool cov = dot >= cp.w;
+                    if (cov && (dot < cp.w + 2.f * CAP_MARGIN || cp.w < -2.f)) cov = covers(px, py, pz, S.nb[m]);
+                    if (cov) {
                         crit = m;
                         ++cnt;
                     }
