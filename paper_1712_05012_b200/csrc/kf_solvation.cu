@@ -679,14 +679,15 @@ KF_DEV void solv_atom(const kf_field_t &f, const SolvArgs &A, int b, int i, int 
 // capacity CAP (more CTAs per SM); the rare atom with more reachable neighbours
 // is deferred to solv_overflow_kernel.  Two builds: ensembles (many small CTAs
 // resident, CAP 144) and single chains (CAP 256: denser chains overflow less).
-// (MINB 12 for the ensemble build: 42 registers; 16 measured 3 % slower from spills.)
+// (MINB 10 for the ensemble build: 48 registers, 60 B of spill stores, as fast as MINB 12 at 40
+// registers with 128 B of spills (13.10 vs 13.11 ms per C5 water step); 8 (64 registers) 14.26 ms.)
 template <int CAP, int MINB>
 __global__ void __launch_bounds__(SOLV_GROUP_THREADS, MINB)
 solv_group_kernel(const __grid_constant__ kf_field_t f, const SolvArgs A, int n_solv, const int32_t *__restrict__ solv_atoms) {
     solv_atom<false>(f, A, blockIdx.x / n_solv, solv_atoms[blockIdx.x % n_solv], min(CAP, A.fast_cap));
 }
 #ifndef SOLV_MINB_ENS
-#define SOLV_MINB_ENS 12
+#define SOLV_MINB_ENS 10
 #endif
 constexpr int SOLV_CAP_ENSEMBLE = 144, SOLV_MINB_ENSEMBLE = SOLV_MINB_ENS;
 constexpr int SOLV_CAP_SINGLE = 256, SOLV_MINB_SINGLE = 8;
