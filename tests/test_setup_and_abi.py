@@ -141,3 +141,37 @@ def test_sample_groups_partition_and_cones(n):
         assert cones[g, 5] == len(ix)
         assert np.all(pts[ix] @ cones[g, :3].astype(float) >= cones[g, 3] - 1e-6)
         assert abs(cones[g, 3] ** 2 + cones[g, 4] ** 2 - 1.0) < 1e-5
+
+
+@pytest.mark.parametrize("seq", [["ALA", "CYS", "SER"] * 12, (["GLY", "ALA"] * 9) + ["SER"]])
+def test_class_codes_match_tree_classes(seq):
+    """The cluster kernel's host-built class tables (device.class_codes per (quad,
+    window octet) and device.unit_codes per (unit, lane)) against the bond tree's
+    classes as the oracle restates them (topology.py:153-195), pair by pair: the 2-bit
+    code of lane l is 4 - class(i, j) with i = 4Q + l % 4, j = 8(Q // 2 + k) + l // 4,
+    the unit words regroup quads 2U and 2U + 1, and their window bits flag the
+    octets holding a class < 4 pair."""
+    from paper_1712_05012_b200 import device as DV
+    ch = P.build_chain(seq)
+    tree = P.build_tree(ch)
+    n = ch.n_atoms
+    codes = DV.class_codes(tree)
+    _, slow = DV.class_window(tree)
+    units = DV.unit_codes(codes, slow)
+    nq, no = (n + 3) // 4, (n + 7) // 8
+    assert codes.shape == (nq, 5) and units.shape == (no, 32)
+    for Q in range(nq):
+        for k in range(5):
+            for lane in range(32):
+                i, j = 4 * Q + lane % 4, 8 * (Q // 2 + k) + lane // 4
+                want = 0 if (i >= n or j >= n or i == j) else 4 - int(O.classes(tree, np.array([i]), np.array([j]))[0])
+                got = (int(codes[Q, k]) >> (2 * lane)) & 3
+                assert got == want, (Q, k, lane, got, want)
+                U, half = divmod(Q, 2)
+                assert (int(units[U, lane]) >> (10 * half + 2 * k)) & 3 == want
+    for U in range(no):
+        for half in range(2):
+            Q = 2 * U + half
+            win = [(Q < nq and codes[Q, k] != 0) for k in range(5)]
+            assert all(((int(units[U, 0]) >> (20 + 5 * half + k)) & 1) == w for k, w in enumerate(win))
+        assert ((int(units[U, 0]) >> 30) & 1) == bool(slow[8 * U:8 * U + 8].any())
