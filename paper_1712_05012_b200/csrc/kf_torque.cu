@@ -12,6 +12,9 @@
 // trajectory); tau_max is an exact max-reduction and the step reproduces
 // numpy's float remainder twice, so theta' is bit-identical given tau.
 #include "kf_common.cuh"
+#ifdef TQ_TIMING
+#include <cstdio>
+#endif
 
 namespace {
 
@@ -235,6 +238,13 @@ KF_DEV void torque_step_cta(const kf_chain_t &c, const kf_field_t &f, const Torq
     const int L = c.n_links, D = c.n_dof, R = c.n_res, nb = c.n_bb;
     const double *T = ta.link_T + (size_t)b * L * KF_XF_STRIDE;
     const double *Wr = ta.wrench + (size_t)b * L * 6;
+#ifdef TQ_TIMING   // phase clocks of CTA 0 (measurement builds only)
+    long long tk[8];
+#define TQT(k) do { if (b == 0 && threadIdx.x == 0) tk[k] = clock64(); } while (0)
+#else
+#define TQT(k) do { } while (0)
+#endif
+    TQT(0);
     if (fuse_wrench) {   // wrenches of this iteration straight into shared memory
         const int n = c.n_atoms;
         for (int l = threadIdx.x; l < L; l += blockDim.x)
@@ -242,6 +252,7 @@ KF_DEV void torque_step_cta(const kf_chain_t &c, const kf_field_t &f, const Torq
         __syncthreads();
         Wr = wsm;
     }
+    TQT(1);
     double *side = ta.side_tot + (size_t)b * R * 6;
     double *suf = ta.bb_suffix + (size_t)b * nb * 6;
     double *tau = ta.tau + (size_t)b * D;
@@ -259,6 +270,7 @@ KF_DEV void torque_step_cta(const kf_chain_t &c, const kf_field_t &f, const Torq
     }
     __syncthreads();
 
+    TQT(2);
     // 2. backbone reverse suffix over links in dof order (kcm.py:227-239)
     const int per = (nb + blockDim.x - 1) / blockDim.x;
     const int lo = min(nb, (int)threadIdx.x * per), hi = min(nb, lo + per);
@@ -281,6 +293,7 @@ KF_DEV void torque_step_cta(const kf_chain_t &c, const kf_field_t &f, const Torq
     }
     if (mode == 0) return;
 
+    TQT(3);
     // 3. tau_max over free joints (kcm.py:325-326)
     const uint8_t *frozen = w.frozen + (size_t)b * D;
     double tmax = 0.0;
@@ -326,7 +339,14 @@ KF_DEV void torque_step_cta(const kf_chain_t &c, const kf_field_t &f, const Torq
         }
         return;
     }
+    TQT(4);
     finish_iteration(c, w, step, b, tau, tmax, ge, gv, gc, sp, sp5, &stop_reason);
+#ifdef TQ_TIMING
+    TQT(5);
+    if (b == 0 && threadIdx.x == 0)
+        printf("TQT wrench %lld side %lld backbone %lld tmax+energies %lld step %lld total %lld\n", tk[1] - tk[0],
+               tk[2] - tk[1], tk[3] - tk[2], tk[4] - tk[3], tk[5] - tk[4], tk[5] - tk[0]);
+#endif
 }
 
 template <int NT>
