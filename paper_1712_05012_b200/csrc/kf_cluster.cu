@@ -472,7 +472,24 @@ KF_DEV float2 pmul_p(unsigned long long a, float2 b) {
     return r;
 }
 
-template <bool DCONST, int NCAP, bool EALL, bool GEN, bool VDW>
+// EALL: 0 generic; 1 the elec threshold is the pair cut-off (elec >= vdW: every
+// fp32-path pair has the elec term); 2 as 1 with the default field's constants
+// (9 / 5 A cut-offs, class-4 weights 1, close threshold 1 A^2) as immediates, so
+// the visit loop reloads no constants (checked on the host: kf_cluster.cu
+// default_constants).
+template <int EALL> struct KC {
+    static constexpr bool D = EALL == 2;
+    KF_DEV static float mid(const ClConst &c) { return D ? 53.f : c.mid; }
+    KF_DEV static float half(const ClConst &c) { return D ? 28.f : c.half; }
+    KF_DEV static float band(const ClConst &c) { return D ? 1e-3f : c.band_l; }
+    KF_DEV static float cutlo(const ClConst &c) { return D ? 81.f - 0.95f * 1e-3f : c.cutlo; }
+    KF_DEV static float tv2(const ClConst &c) { return D ? 25.f : c.tv2; }
+    KF_DEV static float close4(const ClConst &c) { return D ? 1.f : c.close4; }
+    KF_DEV static float we4(const ClConst &c) { return D ? 1.f : c.we[3]; }
+    KF_DEV static float wv4(const ClConst &c) { return D ? 1.f : c.wv[3]; }
+};
+
+template <bool DCONST, int NCAP, int EALL, bool GEN, bool VDW>
 KF_DEV void lean_visit(const ClConst &c, const LeanUnit &u, float2 &fx, float2 &fy, float2 &fz, float2 &ee,
                        float2 &ev, int &ce, int &cv, int U, int O, unsigned sb, const float4 &cu, const float4 *wtab,
                        ExQueue *xq) {
@@ -489,7 +506,8 @@ KF_DEV void lean_visit(const ClConst &c, const LeanUnit &u, float2 &fx, float2 &
     const float2 d2 = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __fmul2_rn(dx, dx)));
     bool vA = u.vA, vB = u.vB;
     float2 qq, weps;
-    float closeA = c.close4, closeB = c.close4;
+    using K = KC<EALL>;
+    float closeA = K::close4(c), closeB = K::close4(c);
     int codeA = 0, codeB = 0;
     if (GEN) {
         vA &= j > iA;   // the own octet: each pair once (always true for O > U)
@@ -505,14 +523,14 @@ KF_DEV void lean_visit(const ClConst &c, const LeanUnit &u, float2 &fx, float2 &
         closeA = wa.z;
         closeB = wb.z;
     } else {
-        qq = pmul_b(u.qk, c.we[3] * oj.w);
-        weps = pmul_b(u.se, c.wv[3] * rj.y);
+        qq = pmul_b(u.qk, K::we4(c) * oj.w);
+        weps = pmul_b(u.se, K::wv4(c) * rj.y);
     }
     // exact path: inside the band around either threshold, or close (see prep())
-    const float2 t = __fadd2_rn(d2, f2(-c.mid));
-    const float bA = fabsf(fabsf(t.x) - c.half), bB = fabsf(fabsf(t.y) - c.half);
-    const bool exA = vA & ((bA <= c.band_l) | (d2.x < closeA));
-    const bool exB = vB & ((bB <= c.band_l) | (d2.y < closeB));
+    const float2 t = __fadd2_rn(d2, f2(-K::mid(c)));
+    const float bA = fabsf(fabsf(t.x) - K::half(c)), bB = fabsf(fabsf(t.y) - K::half(c));
+    const bool exA = vA & ((bA <= K::band(c)) | (d2.x < closeA));
+    const bool exB = vB & ((bB <= K::band(c)) | (d2.y < closeB));
     if (__any_sync(FULL, exA | exB)) {   // rare: queue the exact-path pairs
         const unsigned ma = __ballot_sync(FULL, exA), mb = __ballot_sync(FULL, exB);
         int base = 0;
@@ -525,7 +543,7 @@ KF_DEV void lean_visit(const ClConst &c, const LeanUnit &u, float2 &fx, float2 &
         if (exA && sa < cap) q[sa] = (unsigned)iA | ((unsigned)j << 12) | ((unsigned)codeA << 24);
         if (exB && sb2 < cap) q[sb2] = (unsigned)iB | ((unsigned)j << 12) | ((unsigned)codeB << 24);
     }
-    const bool fA = vA & !exA & (d2.x < c.cutlo), fB = vB & !exB & (d2.y < c.cutlo);
+    const bool fA = vA & !exA & (d2.x < K::cutlo(c)), fB = vB & !exB & (d2.y < K::cutlo(c));
     if (!__any_sync(FULL, fA | fB)) return;
     float2 ir;
     asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(ir.x) : "f"(d2.x));
@@ -546,7 +564,7 @@ KF_DEV void lean_visit(const ClConst &c, const LeanUnit &u, float2 &fx, float2 &
     ee = __fadd2_rn(ee, e);
     ce += (int)keA + (int)keB;
     if (VDW) {   // boxes within the vdW reach
-        const bool kvA = fA && d2.x <= c.tv2, kvB = fB && d2.y <= c.tv2;
+        const bool kvA = fA && d2.x <= K::tv2(c), kvB = fB && d2.y <= K::tv2(c);
         const float2 ir2v = make_float2(kvA ? ir2.x : 0.f, kvB ? ir2.y : 0.f);
         const float2 D = padd_b(u.ri, rj.x);
         const float2 sr = __fmul2_rn(__fmul2_rn(D, D), ir2v);
@@ -586,7 +604,7 @@ KF_DEV void lean_visit(const ClConst &c, const LeanUnit &u, float2 &fx, float2 &
 // (the own octet and class-window octets holding class < 4 pairs) take the
 // general visit; the others are visited in two loops, within the vdW reach and
 // beyond it.
-template <bool DCONST, int NCAP, bool EALL>
+template <bool DCONST, int NCAP, int EALL>
 KF_DEV void lean_sweep(const ClConst &c, const LeanUnit &lu, float2 &fx, float2 &fy, float2 &fz, float2 &ee,
                        float2 &ev, int &ce, int &cv, int U, int no, unsigned sb, unsigned gen0, const float4 *wtab,
                        ExQueue *xq) {
@@ -639,7 +657,7 @@ KF_DEV void lean_sweep(const ClConst &c, const LeanUnit &lu, float2 &fx, float2 
     }
 }
 
-template <bool DCONST, int NCAP, bool EALL>
+template <bool DCONST, int NCAP, int EALL>
 KF_DEV void cluster_pairs_cta(const kf_field_t &f, const ClConst &c, int n, int b, const double *__restrict__ pos_all,
                               double *__restrict__ forces, double *__restrict__ e_atom,
                               long long *__restrict__ pair_count, kf_status_t *status, long long *__restrict__ planes,
@@ -979,7 +997,7 @@ KF_DEV void cluster_pairs_cta(const kf_field_t &f, const ClConst &c, int n, int 
     if (split > 1) cg::this_cluster().sync();   // the peers' shared memory outlives every read of it
 }
 
-template <bool DCONST, int NCAP, bool EALL>
+template <bool DCONST, int NCAP, int EALL>
 __global__ void __launch_bounds__(CL_WARPS * 32, NCAP <= 1536 ? CL_MINB : 1)
 cluster_pair_kernel(const __grid_constant__ kf_field_t f, const __grid_constant__ ClConst c, int n,
                     const double *__restrict__ pos_all, double *__restrict__ forces, double *__restrict__ e_atom,
@@ -1010,11 +1028,17 @@ fold_iteration_kernel(const __grid_constant__ kf_chain_t ch, const __grid_consta
     const int n = ch.n_atoms;
     fk_smem_cta<CL_WARPS * 32>(ch, b, w.theta, w.link_T, w.pos, reinterpret_cast<double *>(sm));
     __syncthreads();
-    cluster_pairs_cta<DCONST, NCAP, false>(f, c, n, b, w.pos, w.forces, w.e_atom, w.pair_count, w.status, w.pair_fj,
+    cluster_pairs_cta<DCONST, NCAP, 0>(f, c, n, b, w.pos, w.forces, w.e_atom, w.pair_count, w.status, w.pair_fj,
                                     reinterpret_cast<unsigned *>(w.s_lo), 2 * n, sm, (int)gridDim.x, 1, 0);
     __syncthreads();
     const TorqueArgs ta{w.link_T, w.wrench, w.side_tot, w.bb_suffix, w.tau};
     torque_step_cta<CL_WARPS * 32>(ch, f, ta, w, step, 1, 1, 1, b, reinterpret_cast<double *>(sm));
+}
+
+// The field constants KC<2> bakes in (the FieldConfig / WeightTable defaults)
+inline bool default_constants(const ClConst &c) {
+    return c.mid == 53.f && c.half == 28.f && c.band_l == 1e-3f && c.cutlo == 81.f - 0.95f * 1e-3f &&
+           c.tv2 == 25.f && c.close4 == 1.f && c.we[3] == 1.f && c.wv[3] == 1.f && c.uniform == 0;
 }
 
 template <int NCAP>
@@ -1023,14 +1047,17 @@ inline int launch_cap(bool dconst, const kf_field_t *f, const ClConst &c, kf_bat
     constexpr size_t smem = ClLayout<NCAP>::TOTAL;
     // EALL: the elec threshold is the pair cut-off (elec >= vdW), so every fp32-path pair has the elec term
     const bool eall = c.te2 >= c.cut2;
-    auto kern = dconst ? (eall ? cluster_pair_kernel<true, NCAP, true> : cluster_pair_kernel<true, NCAP, false>)
-                       : (eall ? cluster_pair_kernel<false, NCAP, true> : cluster_pair_kernel<false, NCAP, false>);
-    static bool opted[4] = {false, false, false, false};
-    if (!opted[2 * dconst + eall]) {
+    const bool defc = eall && !dconst && default_constants(c);
+    auto kern = dconst ? (eall ? cluster_pair_kernel<true, NCAP, 1> : cluster_pair_kernel<true, NCAP, 0>)
+                       : (defc ? cluster_pair_kernel<false, NCAP, 2>
+                               : eall ? cluster_pair_kernel<false, NCAP, 1> : cluster_pair_kernel<false, NCAP, 0>);
+    const int oi = defc ? 4 : 2 * dconst + eall;
+    static bool opted[5] = {false, false, false, false, false};
+    if (!opted[oi]) {
         KF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "cluster smem");
         // clusters of 16 CTAs (beyond the portable 8) for single short chains
         KF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1), "cluster size");
-        opted[2 * dconst + eall] = true;
+        opted[oi] = true;
     }
     // exact-pair queue + its sorted copy: the SoA low-word buffer ([B][n][4] u32), which
     // the cluster path does not otherwise use (binning writes it, nothing later reads it)
