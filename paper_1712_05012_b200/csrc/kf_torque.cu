@@ -573,14 +573,19 @@ int kf_torque_launch(const kf_chain_t *c, const kf_field_t *f, kf_batch_t *w, co
     if (fuse_wrench && !fuse) {
         if (kf_wrench_launch(c, w->B, w->pos, w->forces, const_cast<double *>(wrench), w->status, s)) return 1;
     }
-    // one CTA per trajectory: 512 threads while the batch leaves SMs to spare (its
-    // latency is the iteration's; measured B=128: 20.5 vs 24.6 us), 256 for large
-    // ensembles (more trajectories per SM; B=1024: 101 vs 117 us)
+    // one CTA per trajectory: 512 threads for small batches (the chain's latency is the
+    // iteration's), 256 from 64 trajectories: with the fold loop's graph branches a
+    // torque CTA shares the GPU with other branches' pair CTAs, and its registers x
+    // time are what it takes from them (C5 step: 256 0.629 vs 512 0.655 ms; B = 128 as
+    // 2 x 64: 0.128 vs 0.130; 128 threads 0.624 at C5 but 0.148 at B = 128)
+#ifndef TQ_NARROW
+#define TQ_NARROW (TQ_THREADS / 2)
+#endif
 #ifndef TQ_WIDE_B
-#define TQ_WIDE_B 384
+#define TQ_WIDE_B 64
 #endif
     const bool wide = w->B < TQ_WIDE_B;
-    auto kern = wide ? torque_step_kernel<TQ_THREADS> : torque_step_kernel<TQ_THREADS / 2>;
+    auto kern = wide ? torque_step_kernel<TQ_THREADS> : torque_step_kernel<TQ_NARROW>;
     if (fuse) {
         static size_t opted[2] = {0, 0};
         if (wsm > opted[wide]) {
@@ -588,7 +593,7 @@ int kf_torque_launch(const kf_chain_t *c, const kf_field_t *f, kf_batch_t *w, co
             opted[wide] = wsm;
         }
     }
-    (void)kf_launch(w->B < KF_PDL_B, kern, dim3(w->B), dim3(wide ? TQ_THREADS : TQ_THREADS / 2), fuse ? wsm : 0, s, *c, fz, ta,
+    (void)kf_launch(w->B < KF_PDL_B, kern, dim3(w->B), dim3(wide ? TQ_THREADS : TQ_NARROW), fuse ? wsm : 0, s, *c, fz, ta,
                     *w, st, mode, fuse ? 1 : 0, e_first);
     KF_LAUNCH_CHECK("torque_step_kernel");
     return 0;

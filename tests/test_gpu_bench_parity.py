@@ -14,7 +14,7 @@ kf_bin_launch, kf_torque_launch) depends on the batch B:
 
 * B = 1024 is the bench's C5 configuration (cluster-pair kernel, four graph
   branches of 256);
-* B = 384 is the first B with 256-thread torque CTAs (four branches of 96);
+* B = 384 runs as four branches of 96 (256-thread torque CTAs from 64 trajectories);
 * B = 128, 32, 30 and 16 split each trajectory over a cluster of 2 (as two
   64-trajectory branches: 4), 8, 8 and 16 CTAs.
 The dense-lane kernels are covered by the C3 / C4 single-chain tests below.
