@@ -172,8 +172,19 @@ def _ref_init(water: bool):
     (setup is outside every timed task)."""
     from oracle import kcm_oracle as O
     from paper_1712_05012_b200 import workloads
+    _one_thread()   # one process per core: no nested BLAS / OpenMP pools
     ch, params, w, _ = workloads.system("C2")
     _W["ch"], _W["of"] = ch, O.OracleField(params, w, solvation=water)
+
+
+def _one_thread():
+    """Limit numpy's native thread pools to one thread in this process (the
+    reference arm runs one process per core; the 1-core leg is one thread)."""
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(1)
+    except ImportError:
+        pass
 
 
 def _ref_task(theta):
@@ -232,6 +243,11 @@ def cpu_fold_rate(config: str, budget_s: float, min_iters: int = 1, fixed_iters:
     them are timed, as for C1's 1000-iteration run)."""
     from oracle import kcm_oracle as O
     from paper_1712_05012_b200 import workloads
+    try:   # one thread, as reported (cores: 1)
+        from threadpoolctl import threadpool_limits
+        limit = threadpool_limits(1)
+    except ImportError:
+        limit = None
     ch, params, w, fld = workloads.system(config)
     of = O.OracleField(params, w, solvation=fld.config.solvation)
     theta = workloads.start_theta(config, ch)
@@ -245,7 +261,10 @@ def cpu_fold_rate(config: str, budget_s: float, min_iters: int = 1, fixed_iters:
         iters = fixed_iters
     t0 = time.perf_counter()
     O.fold(ch, theta, frozen, of, max_iters=iters, torque_tol_rel=0.0, energy_window=0)
-    return iters / (time.perf_counter() - t0), iters
+    rate = iters / (time.perf_counter() - t0)
+    if limit is not None:
+        limit.restore_original_limits()
+    return rate, iters
 
 
 # --------------------------------------------------------------------------
