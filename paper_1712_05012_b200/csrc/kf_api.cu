@@ -34,7 +34,8 @@ int kf_torque_launch(const kf_chain_t *c, const kf_field_t *f, kf_batch_t *w, co
                      const kf_step_t *step, int mode, cudaStream_t s, int fuse_wrench = 0);
 int kf_kcm_step_launch(const double *tau, const double *theta, const uint8_t *frozen, int D, double kappa,
                        double *theta_out, double *deltas, cudaStream_t s);
-int kf_fused_iteration(const kf_chain_t *c, const kf_field_t *f, kf_batch_t *w, const kf_step_t *st, cudaStream_t s);
+int kf_fused_iteration(const kf_chain_t *c, const kf_field_t *f, kf_batch_t *w, const kf_step_t *st, cudaStream_t s,
+                       int plane_b);
 int kf_cluster_path(const kf_field_t *f, const kf_batch_t *w, int n);
 
 namespace {
@@ -65,7 +66,9 @@ int enqueue_iteration(const kf_chain_t *c, const kf_field_t *f, kf_batch_t *w, c
                       cudaStream_t s, int plane_b = 0) {
     const int n = c->n_atoms;
     // vacuum ensembles on the cluster path: the whole iteration in one kernel
-    const int fused = kf_fused_iteration(c, f, w, st, s);
+    const int fused = kf_fused_iteration(c, f, w, st, s, plane_b);
+    if (fused == 2)   // FK + pairs fused: the torque step follows
+        return kf_torque_launch(c, f, w, w->link_T, w->wrench, w->side_tot, w->bb_suffix, w->tau, st, 1, s, 1);
     if (fused >= 0) return fused;
     if (kf_fk_launch(c, w, w->status, s, 0)) return 1;   // the loop needs P and U only
     if (kf_bin_launch(f, w, n, s)) return 1;

@@ -1017,19 +1017,20 @@ cluster_pair_kernel(const __grid_constant__ kf_field_t f, const __grid_constant_
 // runs its own chain, so one trajectory's latency-bound FK / torque phases
 // overlap the other resident CTA's pair phase, and there is one grid tail per
 // iteration instead of three.  The phases reuse one dynamic shared buffer.
-template <bool DCONST, int NCAP>
+template <bool DCONST, int NCAP, int EALL>
 __global__ void __launch_bounds__(CL_WARPS * 32, NCAP <= 1536 ? CL_MINB : 1)
 fold_iteration_kernel(const __grid_constant__ kf_chain_t ch, const __grid_constant__ kf_field_t f,
                       const __grid_constant__ ClConst c, const __grid_constant__ kf_batch_t w,
-                      const __grid_constant__ kf_step_t step) {
+                      const __grid_constant__ kf_step_t step, int with_torque, int nbatch) {
     const int b = blockIdx.x;
     if (w.status[b].done) return;
     extern __shared__ __align__(16) unsigned char sm[];
     const int n = ch.n_atoms;
-    fk_smem_cta<CL_WARPS * 32>(ch, b, w.theta, w.link_T, w.pos, reinterpret_cast<double *>(sm));
+    fk_smem_cta<CL_WARPS * 32>(ch, b, w.theta, w.link_T, w.pos, reinterpret_cast<double *>(sm), 0);
     __syncthreads();
-    cluster_pairs_cta<DCONST, NCAP, 0>(f, c, n, b, w.pos, w.forces, w.e_atom, w.pair_count, w.status, w.pair_fj,
-                                    reinterpret_cast<unsigned *>(w.s_lo), 2 * n, sm, (int)gridDim.x, 1, 0);
+    cluster_pairs_cta<DCONST, NCAP, EALL>(f, c, n, b, w.pos, w.forces, w.e_atom, w.pair_count, w.status, w.pair_fj,
+                                          reinterpret_cast<unsigned *>(w.s_lo), 2 * n, sm, nbatch, 1, 0);
+    if (!with_torque) return;
     __syncthreads();
     const TorqueArgs ta{w.link_T, w.wrench, w.side_tot, w.bb_suffix, w.tau};
     torque_step_cta<CL_WARPS * 32>(ch, f, ta, w, step, 1, 1, 1, b, reinterpret_cast<double *>(sm));
@@ -1039,6 +1040,26 @@ fold_iteration_kernel(const __grid_constant__ kf_chain_t ch, const __grid_consta
 inline bool default_constants(const ClConst &c) {
     return c.mid == 53.f && c.half == 28.f && c.band_l == 1e-3f && c.cutlo == 81.f - 0.95f * 1e-3f &&
            c.tv2 == 25.f && c.close4 == 1.f && c.we[3] == 1.f && c.wv[3] == 1.f && c.uniform == 0;
+}
+
+// Small batches: each trajectory is split over a thread-block cluster of S CTAs so
+// that the batch still fills two CTAs per SM: S = the largest power of two <= 16
+// with B S <= 2 x SMs and at least 8 units per CTA (C1 single: S = 4 27.9 vs S = 8
+// 28.9 us; C2 single: S = 16 56.4 vs S = 8 59.4 us); KFB200_CL_SPLIT overrides.
+int kf_cluster_split(int B, int n) {
+    static int sms = 0, env_split = -1;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const char *e = getenv("KFB200_CL_SPLIT");
+        env_split = e ? atoi(e) : 0;
+    }
+    if (env_split > 0) return env_split;
+    int split = 1;
+    const int units = (n + 7) / 8;
+    while (split < 16 && (long long)B * split * 2 <= 2LL * sms && units >= 16 * split) split *= 2;
+    return split;
 }
 
 template <int NCAP>
@@ -1061,22 +1082,7 @@ inline int launch_cap(bool dconst, const kf_field_t *f, const ClConst &c, kf_bat
     }
     // exact-pair queue + its sorted copy: the SoA low-word buffer ([B][n][4] u32), which
     // the cluster path does not otherwise use (binning writes it, nothing later reads it)
-    // small batches: each trajectory is split over a thread-block cluster of S CTAs so
-    // that the batch still fills two CTAs per SM: S = the largest power of two <= 16
-    // with B S <= 2 x SMs and at least 8 units per CTA (C1 single: S = 4 27.9 vs S = 8
-    // 28.9 us; C2 single: S = 16 56.4 vs S = 8 59.4 us); KFB200_CL_SPLIT overrides
-    static int sms = 0, env_split = -1;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        const char *e = getenv("KFB200_CL_SPLIT");
-        env_split = e ? atoi(e) : 0;
-    }
-    int split = 1;
-    const int units = (n + 7) / 8;
-    while (split < 16 && (long long)w->B * split * 2 <= 2LL * sms && units >= 16 * split) split *= 2;
-    if (env_split > 0) split = env_split;
+    const int split = kf_cluster_split(w->B, n);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(w->B * split);
     cfg.blockDim = dim3(CL_WARPS * 32);
@@ -1212,21 +1218,21 @@ int kf_cluster_pairs_launch(const kf_field_t *f, kf_batch_t *w, int n, cudaStrea
 
 template <int NCAP>
 static int launch_fused(const kf_chain_t *ch, const kf_field_t *f, kf_batch_t *w, const kf_step_t *st,
-                        cudaStream_t s) {
+                        cudaStream_t s, int with_torque, int plane_b) {
     const ClConst c = cl_const(f);
     const bool dc = f->dielectric_const != 0;
     size_t smem = ClLayout<NCAP>::TOTAL;
     smem = std::max(smem, fk_smem_bytes(*ch));
     smem = std::max(smem, (size_t)ch->n_links * 6 * sizeof(double));
-    auto kern = dc ? fold_iteration_kernel<true, NCAP> : fold_iteration_kernel<false, NCAP>;
-    static size_t opted[2] = {0, 0};
-    if (smem > opted[dc]) {
-        KF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "fused smem");
-        opted[dc] = smem;
-    }
-    kern<<<w->B, CL_WARPS * 32, smem, s>>>(*ch, *f, c, *w, *st);
+    const bool eall = c.te2 >= c.cut2;
+    const bool defc = eall && !dc && default_constants(c);
+    auto kern = dc ? (eall ? fold_iteration_kernel<true, NCAP, 1> : fold_iteration_kernel<true, NCAP, 0>)
+                   : (defc ? fold_iteration_kernel<false, NCAP, 2>
+                           : eall ? fold_iteration_kernel<false, NCAP, 1> : fold_iteration_kernel<false, NCAP, 0>);
+    KF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "fused smem");
+    kern<<<w->B, CL_WARPS * 32, smem, s>>>(*ch, *f, c, *w, *st, with_torque, plane_b > 0 ? plane_b : w->B);
     KF_LAUNCH_CHECK("fold_iteration_kernel");
-    return 0;
+    return with_torque ? 0 : 2;
 }
 
 // The fused iteration (KFB200_FUSED=1) applies to vacuum ensembles on the cluster
@@ -1235,18 +1241,21 @@ static int launch_fused(const kf_chain_t *ch, const kf_field_t *f, kf_batch_t *w
 // ms as three kernels.  Both resident CTAs of an SM tend to sit in their
 // latency-bound FK / torque phases together, and those phases run at 2 CTAs per
 // SM instead of the standalone kernels' 4.
-int kf_fused_iteration(const kf_chain_t *ch, const kf_field_t *f, kf_batch_t *w, const kf_step_t *st, cudaStream_t s) {
+// KFB200_FUSED=2: FK and the pair phase fused (torques a separate kernel; returns 2).
+int kf_fused_iteration(const kf_chain_t *ch, const kf_field_t *f, kf_batch_t *w, const kf_step_t *st, cudaStream_t s,
+                       int plane_b) {
     static int env_on = -1;
     if (env_on < 0) {
         const char *e = getenv("KFB200_FUSED");
         env_on = e ? atoi(e) : 0;
     }
     const int n = ch->n_atoms;
-    if (!env_on || f->solvation || !st || !kf_cluster_path(f, w, n)) return -1;
+    if (!env_on || f->solvation || !st || !kf_cluster_path(f, w, n) || kf_cluster_split(w->B, n) != 1) return -1;
     if (fk_smem_bytes(*ch) > 200 * 1024 || (size_t)ch->n_links * 48 > 200 * 1024) return -1;
-    if (n <= 512) return launch_fused<512>(ch, f, w, st, s);
-    if (n <= 1024) return launch_fused<1024>(ch, f, w, st, s);
-    if (n <= 1536) return launch_fused<1536>(ch, f, w, st, s);
-    if (n <= 2048) return launch_fused<2048>(ch, f, w, st, s);
-    return launch_fused<2944>(ch, f, w, st, s);
+    const int wt = env_on == 2 ? 0 : 1;
+    if (n <= 512) return launch_fused<512>(ch, f, w, st, s, wt, plane_b);
+    if (n <= 1024) return launch_fused<1024>(ch, f, w, st, s, wt, plane_b);
+    if (n <= 1536) return launch_fused<1536>(ch, f, w, st, s, wt, plane_b);
+    if (n <= 2048) return launch_fused<2048>(ch, f, w, st, s, wt, plane_b);
+    return launch_fused<2944>(ch, f, w, st, s, wt, plane_b);
 }
