@@ -19,11 +19,10 @@ constexpr int FK_THREADS = 256;
 
 // Rodrigues R = I + sin(t) K + (1 - cos(t)) K^2 (geometry.py:26-41), t in radians
 // from degrees as math.radians does (x * (pi / 180)).
-KF_DEV Xf local_transform(const double *axis, double theta_deg, const double *body_parent) {
+KF_DEV Xf local_transform_v(double x, double y, double z, double theta_deg, double bx, double by, double bz) {
     const double deg2rad = 0.017453292519943295;
     double s, c;
     sincos(theta_deg * deg2rad, &s, &c);
-    const double x = axis[0], y = axis[1], z = axis[2];
     const double omc = 1.0 - c;
     Xf t;
     // K^2 = a a^T - |a|^2 I, written out as the reference's (k @ k) entries
@@ -32,8 +31,11 @@ KF_DEV Xf local_transform(const double *axis, double theta_deg, const double *bo
     t.m[0] = 1.0 + omc * k00;   t.m[1] = -s * z + omc * k01; t.m[2] = s * y + omc * k02;
     t.m[3] = s * z + omc * k01; t.m[4] = 1.0 + omc * k11;    t.m[5] = -s * x + omc * k12;
     t.m[6] = -s * y + omc * k02; t.m[7] = s * x + omc * k12; t.m[8] = 1.0 + omc * k22;
-    t.p[0] = body_parent[0]; t.p[1] = body_parent[1]; t.p[2] = body_parent[2];
+    t.p[0] = bx; t.p[1] = by; t.p[2] = bz;
     return t;
+}
+KF_DEV Xf local_transform(const double *axis, double theta_deg, const double *body_parent) {
+    return local_transform_v(axis[0], axis[1], axis[2], theta_deg, body_parent[0], body_parent[1], body_parent[2]);
 }
 
 // Block-wide scan of the threads' transforms in thread order (composition is
@@ -177,29 +179,39 @@ KF_DEV void fk_smem_cta(const kf_chain_t &c, int b, const double *__restrict__ t
     if ((int)threadIdx.x <= nd) sh_doff[threadIdx.x] = c.side_depth_off[threadIdx.x];
 
     {
-        // local transforms; the chain tables and angles of U links per thread are
-        // loaded ahead of the math (latency of one round, not U)
+        // local transforms; the chain tables, axes, parent offsets and angles of U
+        // links per thread are loaded ahead of the math (two dependent rounds, not 2 U)
         const int32_t *__restrict__ link_dof = c.link_dof;
         const int32_t *__restrict__ link_parent = c.link_parent;
+        const double *__restrict__ axis0 = c.link_axis0;
+        const double *__restrict__ body0 = c.link_body0;
         constexpr int U = 4;
         for (int l0 = threadIdx.x; l0 < L; l0 += U * blockDim.x) {
             int dof[U], par[U];
-            double th[U];
+            double th[U], ax[U][3], bo[U][3];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const int l = l0 + u * blockDim.x;
                 dof[u] = (l < L && l != 0) ? link_dof[l] : -1;
                 par[u] = (l < L && l != 0) ? link_parent[l] : 0;
-                if (l < L) { sh_dof[l] = dof[u]; sh_par[l] = par[u]; }
+#pragma unroll
+                for (int q = 0; q < 3; ++q) ax[u][q] = l < L ? axis0[3 * l + q] : 0.0;
             }
 #pragma unroll
-            for (int u = 0; u < U; ++u) th[u] = dof[u] >= 0 ? theta[dof[u]] : 0.0;
+            for (int u = 0; u < U; ++u) {
+                th[u] = dof[u] >= 0 ? theta[dof[u]] : 0.0;
+#pragma unroll
+                for (int q = 0; q < 3; ++q) bo[u][q] = dof[u] >= 0 ? body0[3 * par[u] + q] : 0.0;
+            }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const int l = l0 + u * blockDim.x;
                 if (l >= L) break;
+                sh_dof[l] = dof[u];
+                sh_par[l] = par[u];
                 const Xf a = dof[u] < 0 ? xf_identity()
-                                        : local_transform(c.link_axis0 + 3 * l, th[u], c.link_body0 + 3 * par[u]);
+                                        : local_transform_v(ax[u][0], ax[u][1], ax[u][2], th[u], bo[u][0], bo[u][1],
+                                                            bo[u][2]);
                 xf_store(S + FKS_STRIDE * l, a);
             }
         }
