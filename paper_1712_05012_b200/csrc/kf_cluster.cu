@@ -477,6 +477,9 @@ KF_DEV float2 pmul_p(unsigned long long a, float2 b) {
 // (9 / 5 A cut-offs, class-4 weights 1, close threshold 1 A^2) as immediates, so
 // the visit loop reloads no constants (checked on the host: kf_cluster.cu
 // default_constants).
+#ifndef CL_VDW_NOVOTE
+#define CL_VDW_NOVOTE 1
+#endif
 template <int EALL> struct KC {
     static constexpr bool D = EALL == 2;
     KF_DEV static float mid(const ClConst &c) { return D ? 53.f : c.mid; }
@@ -544,7 +547,8 @@ KF_DEV void lean_visit(const ClConst &c, const LeanUnit &u, float2 &fx, float2 &
         if (exB && sb2 < cap) q[sb2] = (unsigned)iB | ((unsigned)j << 12) | ((unsigned)codeB << 24);
     }
     const bool fA = vA & !exA & (d2.x < K::cutlo(c)), fB = vB & !exB & (d2.y < K::cutlo(c));
-    if (!__any_sync(FULL, fA | fB)) return;
+    // (boxes within the vdW reach almost always hold a pair inside the cut-off: no vote)
+    if (!(VDW && CL_VDW_NOVOTE) && !__any_sync(FULL, fA | fB)) return;
     float2 ir;
     asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(ir.x) : "f"(d2.x));
     asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(ir.y) : "f"(d2.y));

@@ -228,7 +228,6 @@ KF_DEV void torque_step_cta(const kf_chain_t &c, const kf_field_t &f, const Torq
                             const kf_step_t &step, int mode, int fuse_wrench, int e_first, int b, double *wsm) {
     kf_status_t *st = w.status ? w.status + b : nullptr;
     if (st && st->done) return;
-    __shared__ double red[32];
     __shared__ double chunk[NT / 32][6];   // warp totals of the suffix scan
     __shared__ int stop_reason;
     if (st && st->error) {   // domain error this iteration: freeze, no record, no step
