@@ -439,8 +439,8 @@ struct LeanUnit {
     unsigned long long qk;           // K q_i (class weight applied per visit)
     unsigned long long ri;           // R_i
     unsigned long long se;           // sqrt(eps_i)
-    bool vA, vB;
-    unsigned codes;       // bits 2k..: 4 - class of (iA, j) in window octet U + k; bits 10 + 2k..: iB
+    unsigned codes;       // bits 2k..: 4 - class of (iA, j) in window octet U + k; bits 10 + 2k..: iB;
+                          // bits 30 / 31: atoms iA / iB exist (one register, not two predicates)
 };
 
 // the exact-path queue, read only on the rare path (kept out of the registers)
@@ -510,7 +510,7 @@ KF_DEV void lean_visit(const ClConst &c, const LeanUnit &u, float2 &fx, float2 &
     const float jx = oj.x - (cu.x - oc.x), jy = oj.y - (cu.y - oc.y), jz = oj.z - (cu.z - oc.z);
     const float2 dx = padd_b(u.ix, -jx), dy = padd_b(u.iy, -jy), dz = padd_b(u.iz, -jz);
     const float2 d2 = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __fmul2_rn(dx, dx)));
-    bool vA = u.vA, vB = u.vB;
+    bool vA = (u.codes >> 30) & 1u, vB = (u.codes >> 31) & 1u;
     float2 qq, weps;
     using K = KC<EALL>;
     float closeA = K::close4(c), closeB = K::close4(c);
@@ -827,8 +827,8 @@ KF_DEV void cluster_pairs_cta(const kf_field_t &f, const ClConst &c, int n, int 
             lu.ri = pair_of(riA.x, riB.x);
             lu.se = pair_of(riA.y, riB.y);
 #endif
-            lu.vA = vA; lu.vB = vB;
-            lu.codes = uw & 0xfffffu;
+            lu.codes = (uw & 0xfffffu) | ((unsigned)vA << 30) | ((unsigned)vB << 31);
+            asm volatile("" : "+r"(lu.codes));   // opaque: the visits test its bits, not re-derive iA < n
             lean_sweep<DCONST, NCAP, EALL>(c, lu, fx, fy, fz, ee2, ev2, ce, cv, U, no, sb, winA | winB, wtab, &xq);
         } else
         for (int ob = U; ob < no; ob += 32) {
