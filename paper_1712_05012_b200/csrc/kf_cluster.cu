@@ -465,6 +465,12 @@ KF_DEV float2 pmul_b(unsigned long long a, float s) {
         : "=f"(r.x), "=f"(r.y) : "l"(a), "f"(s));
     return r;
 }
+KF_DEV float2 pmul_pp(unsigned long long a, unsigned long long b) {
+    float2 r;
+    asm("{\n\t.reg .b64 d;\n\tmul.rn.f32x2 d, %2, %3;\n\tmov.b64 {%0, %1}, d;\n\t}"
+        : "=f"(r.x), "=f"(r.y) : "l"(a), "l"(b));
+    return r;
+}
 KF_DEV float2 pmul_p(unsigned long long a, float2 b) {
     float2 r;
     asm("{\n\t.reg .b64 t, d;\n\tmov.b64 t, {%3, %4};\n\tmul.rn.f32x2 d, %2, t;\n\tmov.b64 {%0, %1}, d;\n\t}"
@@ -497,7 +503,7 @@ template <int EALL> struct KC {
 
 template <bool DCONST, int NCAP, int EALL, bool GEN, bool VDW>
 KF_DEV void lean_visit(const ClConst &c, const LeanUnit &u, float2 &fx, float2 &fy, float2 &fz, float2 &ee,
-                       float2 &ev, int &ce, int &cv, int U, int O, unsigned sb, const float4 &cu, const float4 *wtab,
+                       float2 &ev, int &ce, int &cv, int U, int O, unsigned sb, const float4 &cu, unsigned wtab,
                        ExQueue *xq) {
     using L = ClLayout<NCAP>;
     const int lane = threadIdx.x & 31, ii = lane & 3, js = lane >> 2;
@@ -523,11 +529,16 @@ KF_DEV void lean_visit(const ClConst &c, const LeanUnit &u, float2 &fx, float2 &
             codeA = (int)(u.codes >> (2 * k)) & 3;
             codeB = (int)(u.codes >> (10 + 2 * k)) & 3;
         }
-        const float4 wa = wtab[codeA], wb = wtab[codeB];   // (w_elec, w_vdw, close threshold) by 4 - class
-        qq = __fmul2_rn(pmul_p(u.qk, make_float2(wa.x, wb.x)), f2(oj.w));
-        weps = __fmul2_rn(pmul_p(u.se, make_float2(wa.y, wb.y)), f2(rj.y));
-        closeA = wa.z;
-        closeB = wb.z;
+        // the (quad A, quad B) weights and close thresholds of this code pair, as packed
+        // operands straight from the 16-entry shared table
+        const unsigned e = wtab + 32u * (unsigned)(codeA + 4 * codeB);
+        unsigned long long we, wv;
+        asm("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(we), "=l"(wv) : "r"(e));
+        qq = __fmul2_rn(pmul_pp(u.qk, we), f2(oj.w));
+        weps = __fmul2_rn(pmul_pp(u.se, wv), f2(rj.y));
+        const float2 cl = lds2(e + 16u);
+        closeA = cl.x;
+        closeB = cl.y;
     } else {
         qq = pmul_b(u.qk, K::we4(c) * oj.w);
         weps = pmul_b(u.se, K::wv4(c) * rj.y);
@@ -613,7 +624,7 @@ KF_DEV void lean_visit(const ClConst &c, const LeanUnit &u, float2 &fx, float2 &
 // beyond it.
 template <bool DCONST, int NCAP, int EALL>
 KF_DEV void lean_sweep(const ClConst &c, const LeanUnit &lu, float2 &fx, float2 &fy, float2 &fz, float2 &ee,
-                       float2 &ev, int &ce, int &cv, int U, int no, unsigned sb, unsigned gen0, const float4 *wtab,
+                       float2 &ev, int &ce, int &cv, int U, int no, unsigned sb, unsigned gen0, unsigned wtab,
                        ExQueue *xq) {
     using L = ClLayout<NCAP>;
     for (int ob = U; ob < no; ob += 32) {
@@ -683,13 +694,16 @@ KF_DEV void cluster_pairs_cta(const kf_field_t &f, const ClConst &c, int n, int 
     __shared__ unsigned cnt_e, cnt_v;
     __shared__ double red_e[CL_WARPS][2];
     __shared__ unsigned long long qcodes[CL_WARPS][10];  // the current unit's window class codes (2 quads)
-    __shared__ float4 wtab[4];   // lean visits: (w_elec, w_vdw, close threshold, 0) by 4 - class
+    // lean general visits: by code pair (codeA + 4 codeB): (w_elec A, B, w_vdw A, B), (close A, B, 0, 0)
+    __shared__ __align__(16) float4 wpair[16][2];
 #if CL_PSTAGE
     __shared__ __align__(8) float2 pstage[CL_WARPS][32];   // lean units: packed-operand staging
 #endif
-    if (threadIdx.x < 4) {
-        const int cls = 3 - (int)threadIdx.x;   // index into the by-class arrays
-        wtab[threadIdx.x] = make_float4(c.we[cls], c.wv[cls], ((c.wnz_mask >> cls) & 1) ? c.f64_d2 : 1e-4f, 0.f);
+    if (threadIdx.x < 16) {
+        const int ca = 3 - (int)(threadIdx.x & 3), cb = 3 - (int)(threadIdx.x >> 2);
+        wpair[threadIdx.x][0] = make_float4(c.we[ca], c.we[cb], c.wv[ca], c.wv[cb]);
+        wpair[threadIdx.x][1] = make_float4(((c.wnz_mask >> ca) & 1) ? c.f64_d2 : 1e-4f,
+                                            ((c.wnz_mask >> cb) & 1) ? c.f64_d2 : 1e-4f, 0.f, 0.f);
     }
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int no = (n + 7) / 8, nq = (n + 3) / 4;
@@ -768,8 +782,8 @@ KF_DEV void cluster_pairs_cta(const kf_field_t &f, const ClConst &c, int n, int 
     // (lane and the shared base are pinned in registers: the compiler would
     // otherwise rematerialise them from special registers in every round)
     int lane_p = lane;
-    unsigned sb = base;
-    asm volatile("" : "+r"(lane_p), "+r"(sb));
+    unsigned sb = base, wsb = smem_u32(wpair);
+    asm volatile("" : "+r"(lane_p), "+r"(sb), "+r"(wsb));
     const int ii = lane_p & 3, js = lane_p >> 2;
     const bool wnz4 = (c.wnz_mask >> 3) & 1;          // class 4 has a nonzero weight
     int ce = 0, cv = 0;                               // pair counts: integers, order-free across units
@@ -829,7 +843,7 @@ KF_DEV void cluster_pairs_cta(const kf_field_t &f, const ClConst &c, int n, int 
 #endif
             lu.codes = (uw & 0xfffffu) | ((unsigned)vA << 30) | ((unsigned)vB << 31);
             asm volatile("" : "+r"(lu.codes));   // opaque: the visits test its bits, not re-derive iA < n
-            lean_sweep<DCONST, NCAP, EALL>(c, lu, fx, fy, fz, ee2, ev2, ce, cv, U, no, sb, winA | winB, wtab, &xq);
+            lean_sweep<DCONST, NCAP, EALL>(c, lu, fx, fy, fz, ee2, ev2, ce, cv, U, no, sb, winA | winB, wsb, &xq);
         } else
         for (int ob = U; ob < no; ob += 32) {
             // box pretest of 32 candidate octets at once against the unit's octet box

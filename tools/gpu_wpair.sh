@@ -1,0 +1,4 @@
+# general lean visits: code-pair weight table with packed operands (cur) vs per-class table (base)
+python -m pytest tests/test_gpu_bench_parity.py tests/test_gpu_parity.py -x -q 2>&1 | tail -1
+bash tools/ab.sh 1024 16 cur base 2>&1 | sed 's/env={.*}//'
+bash tools/ab.sh 128 16 cur base 2>&1 | sed 's/env={.*}//'
