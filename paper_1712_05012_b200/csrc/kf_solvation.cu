@@ -31,6 +31,9 @@ namespace {
 
 constexpr int SOLV_THREADS = 256;
 constexpr int SOLV_MAX_GROUPS = 128;   // sample groups tracked in shared memory (N <= 4096)
+#ifndef SOLV_PRED_WALK
+#define SOLV_PRED_WALK 1   // candidate walk as predicated code (see the walk)
+#endif
 #ifndef SOLV_VOTE
 #define SOLV_VOTE 4   // candidates between warp votes on "all samples covered twice"
 #endif
@@ -588,12 +591,28 @@ KF_DEV void solv_atom(const kf_field_t &f, const SolvArgs &A, int b, int i, int 
                 const int m = (w << 5) + __ffs(bits) - 1;
                 bits &= bits - 1u;
                 if (lane == 0) SSTAT(3, 1);
+                // |p - r_j|^2 = R_i^2 + d^2 - 2 R_i d (q.u), so j covers p iff q.u >= c1
+                // exactly; cap.w = c1 - 1e-3.  Outside the +-1e-3 band around c1 the fp32
+                // test decides (its error is ~1e-6, and so far from the boundary the
+                // reference's fp64 test agrees); inside it, the reference's exact fp64
+                // test.  (cap.w = -3: a coincident neighbour, always the exact test.)
+#if SOLV_PRED_WALK
+                // predicated: every lane computes the fp32 test, lanes already covered
+                // twice discard it; the rare exact test behind a warp vote (no divergent
+                // branches, so no reconvergence barriers per candidate)
+                {
+                    const float4 cp = S.cap[m];
+                    const float dot = qx * cp.x + qy * cp.y + qz * cp.z;
+                    const bool open = cnt < 2;
+                    bool cov = open & (dot >= cp.w);
+                    const bool ex = cov & ((dot < cp.w + 2.f * CAP_MARGIN) | (cp.w < -2.f));
+                    if (__any_sync(0xffffffffu, ex))
+                        if (ex) cov = covers(px, py, pz, S.nb[m]);
+                    crit = cov ? m : crit;
+                    cnt += cov ? 1 : 0;
+                }
+#else
                 if (cnt < 2) {
-                    // |p - r_j|^2 = R_i^2 + d^2 - 2 R_i d (q.u), so j covers p iff q.u >= c1
-                    // exactly; cap.w = c1 - 1e-3.  Outside the +-1e-3 band around c1 the fp32
-                    // test decides (its error is ~1e-6, and so far from the boundary the
-                    // reference's fp64 test agrees); inside it, the reference's exact fp64
-                    // test.  (cap.w = -3: a coincident neighbour, always the exact test.)
                     const float4 cp = S.cap[m];
                     const float dot = qx * cp.x + qy * cp.y + qz * cp.z;
                     bool cov = dot >= cp.w;
@@ -603,6 +622,7 @@ KF_DEV void solv_atom(const kf_field_t &f, const SolvArgs &A, int b, int i, int 
                         ++cnt;
                     }
                 }
+#endif
                 if (++since_vote == SOLV_VOTE) {
                     since_vote = 0;
                     if (__all_sync(0xffffffffu, cnt >= 2)) { all_done = true; break; }
