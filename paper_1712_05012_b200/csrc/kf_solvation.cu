@@ -482,17 +482,19 @@ KF_DEV void solv_atom(const kf_field_t &f, const SolvArgs &A, int b, int i, int 
         for (int w = threadIdx.x >> 5; w < W; w += blockDim.x >> 5) {
             const int m0 = w << 5, mn = min(32, count - m0);
             uint32_t bits = 0u, fbits = 0u;
+            // neighbours in reverse order, each bit shifted in from the bottom (bit t ends at
+            // position t); both tests evaluated without short-circuit (no predicated chains)
 #pragma unroll 4
-            for (int t = 0; t < mn; ++t) {
+            for (int t = mn - 1; t >= 0; --t) {
                 const float4 cp = S.cap[m0 + t], cn = S.cone[m0 + t];
                 const float dot = ax.x * cp.x + ax.y * cp.y + ax.z * cp.z;
                 // cone (a_g, alpha) meets the enlarged cap (u, beta): angle(a, u) <= alpha + beta
-                const bool keep = cn.x <= -ax.w || dot >= ax.w * cn.x - sin_a * cn.y - 1e-3f;
+                const bool keep = (cn.x <= -ax.w) | (dot >= ax.w * cn.x - sin_a * cn.y - 1e-3f);
                 // cone inside the tightened plain cap (beta1 > alpha, angle(a, u) <= beta1 - alpha):
                 // every sample of the group is covered by m, exactly (margins >> rounding)
-                const bool full = cn.z < ax.w && dot >= ax.w * cn.z + sin_a * cn.w + 1e-3f;
-                bits |= (uint32_t)keep << t;
-                fbits |= (uint32_t)full << t;
+                const bool full = (cn.z < ax.w) & (dot >= ax.w * cn.z + sin_a * cn.w + 1e-3f);
+                bits = (bits << 1) | (uint32_t)keep;
+                fbits = (fbits << 1) | (uint32_t)full;
             }
             if (gl) {
                 S.mask[g * W + w] = bits; S.full[g * W + w] = fbits;
