@@ -329,8 +329,9 @@ KF_DEV void solv_atom(const kf_field_t &f, const SolvArgs &A, int b, int i, int 
     __shared__ int nn, next_group, covered_s;
     __shared__ long long acc_i_s[3];
     __shared__ int gfull_s[SOLV_MAX_GROUPS];   // full coverers per sample group
+    __shared__ int gf0_s[SOLV_MAX_GROUPS];     // the lowest-index full coverer per sample group
     if (threadIdx.x == 0) { nn = 0; next_group = 0; covered_s = 0; acc_i_s[0] = acc_i_s[1] = acc_i_s[2] = 0; }
-    for (int q = threadIdx.x; q < SOLV_MAX_GROUPS; q += blockDim.x) gfull_s[q] = 0;
+    for (int q = threadIdx.x; q < SOLV_MAX_GROUPS; q += blockDim.x) { gfull_s[q] = 0; gf0_s[q] = 0x7fffffff; }
     __syncthreads();
 
     const size_t ai = (size_t)b * n + i;
@@ -498,7 +499,10 @@ KF_DEV void solv_atom(const kf_field_t &f, const SolvArgs &A, int b, int i, int 
             }
             if (gl) {
                 S.mask[g * W + w] = bits; S.full[g * W + w] = fbits;
-                if (fbits && g < SOLV_MAX_GROUPS) atomicAdd(&gfull_s[g], __popc(fbits));
+                if (fbits && g < SOLV_MAX_GROUPS) {
+                    atomicAdd(&gfull_s[g], __popc(fbits));
+                    atomicMin(&gf0_s[g], (w << 5) + __ffs(fbits) - 1);
+                }
             }
         }
     } else {
@@ -519,7 +523,10 @@ KF_DEV void solv_atom(const kf_field_t &f, const SolvArgs &A, int b, int i, int 
                 const uint32_t fbits = __ballot_sync(0xffffffffu, full);
                 if (lane == 0) {
                     S.mask[g * W + w] = bits; S.full[g * W + w] = fbits;
-                    if (fbits && g < SOLV_MAX_GROUPS) atomicAdd(&gfull_s[g], __popc(fbits));
+                    if (fbits && g < SOLV_MAX_GROUPS) {
+                        atomicAdd(&gfull_s[g], __popc(fbits));
+                        atomicMin(&gf0_s[g], (w << 5) + __ffs(fbits) - 1);
+                    }
                 }
             }
         }
@@ -557,12 +564,18 @@ KF_DEV void solv_atom(const kf_field_t &f, const SolvArgs &A, int b, int i, int 
         const int g = use_list ? glist_s[k] : k;
         const bool valid = lane < (int)f.grp_cone[8 * g + 5];
         const uint32_t *gm = S.mask + g * W, *gf = S.full + g * W;
-        // neighbours covering the whole group: two of them settle every sample
+        // neighbours covering the whole group: two of them settle every sample (counted,
+        // with the lowest-index one, in the mask pass when the groups are tracked)
         int nfull = 0, f0 = -1;
-        for (int w = 0; w < W; ++w) {
-            const uint32_t fb = gf[w];
-            if (fb && f0 < 0) f0 = (w << 5) + __ffs(fb) - 1;
-            nfull += __popc(fb);
+        if (use_list) {
+            nfull = gfull_s[g];
+            f0 = nfull ? gf0_s[g] : -1;
+        } else {
+            for (int w = 0; w < W; ++w) {
+                const uint32_t fb = gf[w];
+                if (fb && f0 < 0) f0 = (w << 5) + __ffs(fb) - 1;
+                nfull += __popc(fb);
+            }
         }
         if (lane == 0) { SSTAT(0, 1); SSTAT(7, W); }
         if (nfull >= 2) {
