@@ -411,9 +411,16 @@ KF_DEV void solv_atom(const kf_field_t &f, const SolvArgs &A, int b, int i, int 
                 const double r2j = xmul(pj.w, pj.w);                 // = r_off2[j] (host R_off * R_off)
                 S.tmp[slot] = NbSlot{pj.x, pj.y, pj.z, r2j};
                 S.tmp_atom[slot] = j;
-                // sort key c1 (smaller = larger cap, fp32: ordering only); -3 for a coincident atom
+                // sort key c1 (smaller = larger cap, fp32: ordering only); -3 for a coincident atom.
+                // The visiting order only decides how soon a walk can stop (states, the unique
+                // coverer and the event sums do not depend on it), so the key is c1 mapped to an
+                // order-preserving integer, cut to its top 20 bits, with the slot in the low 12:
+                // unique keys, one integer compare per pair in the rank sort
                 const float d2f = (float)d2, df = sqrtf(d2f);
-                S.key[slot] = d2f > 1e-12f ? (r_i_f * r_i_f + d2f - (float)r2j) / (2.f * r_i_f * df) : -3.f;
+                const float kf = d2f > 1e-12f ? (r_i_f * r_i_f + d2f - (float)r2j) / (2.f * r_i_f * df) : -3.f;
+                unsigned ku = __float_as_uint(kf);
+                ku = (ku & 0x80000000u) ? ~ku : (ku | 0x80000000u);
+                reinterpret_cast<unsigned *>(S.key)[slot] = (ku & 0xfffff000u) | (unsigned)slot;
             }
         }
     }
@@ -433,16 +440,14 @@ KF_DEV void solv_atom(const kf_field_t &f, const SolvArgs &A, int b, int i, int 
         }
         return;
     }
-    // ---- rank sort (largest cap first; ties by arrival) and the caps in sorted order
+    // ---- rank sort (largest cap first; unique integer keys) and the caps in sorted order
     const double dr = f.delta_r;
     const float drf = (float)dr;
+    const unsigned *ukey = reinterpret_cast<const unsigned *>(S.key);
     for (int m = threadIdx.x; m < count; m += blockDim.x) {
-        const float km = S.key[m];
+        const unsigned km = ukey[m];
         int r = 0;
-        for (int t = 0; t < count; ++t) {
-            const float kt = S.key[t];
-            r += (kt < km) || (kt == km && t < m);
-        }
+        for (int t = 0; t < count; ++t) r += ukey[t] < km;
         const NbSlot q = S.tmp[m];
         S.nb[r] = q;
         S.atom[r] = S.tmp_atom[m];
@@ -891,6 +896,8 @@ int kf_solvation_launch(const kf_field_t *f, kf_batch_t *w, int n, int n_solv, c
             fast_cap_env = env ? atoi(env) : 1 << 30;
         }
         A.fast_cap = fast_cap_env;
+        // the rank sort packs the staging slot into 12 key bits
+        if (w->nb_cap > 4096) KF_CUDA(cudaErrorInvalidValue, "solvation neighbour capacity > 4096");
         KF_CUDA(cudaMemsetAsync(w->solv_ovf, 0, sizeof(int32_t), s), "memset solv_ovf");
         const bool ens = B >= SOLV_ENSEMBLE_MIN_B;
         const int cap = ens ? SOLV_CAP_ENSEMBLE : SOLV_CAP_SINGLE;
