@@ -414,13 +414,14 @@ KF_DEV void solv_atom(const kf_field_t &f, const SolvArgs &A, int b, int i, int 
                 // sort key c1 (smaller = larger cap, fp32: ordering only); -3 for a coincident atom.
                 // The visiting order only decides how soon a walk can stop (states, the unique
                 // coverer and the event sums do not depend on it), so the key is c1 mapped to an
-                // order-preserving integer, cut to its top 20 bits, with the slot in the low 12:
-                // unique keys, one integer compare per pair in the rank sort
+                // order-preserving integer, cut to its top 19 bits in bits 12-30, with the slot in
+                // the low 12: unique keys below 2^31, so the rank sort counts smaller keys by the
+                // sign of a difference (a subtract and a shifted add per pair)
                 const float d2f = (float)d2, df = sqrtf(d2f);
                 const float kf = d2f > 1e-12f ? (r_i_f * r_i_f + d2f - (float)r2j) / (2.f * r_i_f * df) : -3.f;
                 unsigned ku = __float_as_uint(kf);
                 ku = (ku & 0x80000000u) ? ~ku : (ku | 0x80000000u);
-                reinterpret_cast<unsigned *>(S.key)[slot] = (ku & 0xfffff000u) | (unsigned)slot;
+                reinterpret_cast<unsigned *>(S.key)[slot] = ((ku >> 1) & 0x7ffff000u) | (unsigned)slot;
             }
         }
     }
@@ -447,7 +448,7 @@ KF_DEV void solv_atom(const kf_field_t &f, const SolvArgs &A, int b, int i, int 
     for (int m = threadIdx.x; m < count; m += blockDim.x) {
         const unsigned km = ukey[m];
         int r = 0;
-        for (int t = 0; t < count; ++t) r += ukey[t] < km;
+        for (int t = 0; t < count; ++t) r += (ukey[t] - km) >> 31;   // keys < 2^31: the sign of the difference
         const NbSlot q = S.tmp[m];
         S.nb[r] = q;
         S.atom[r] = S.tmp_atom[m];
