@@ -543,11 +543,22 @@ KF_DEV void lean_visit(const ClConst &c, const LeanUnit &u, float2 &fx, float2 &
         qq = pmul_b(u.qk, K::we4(c) * oj.w);
         weps = pmul_b(u.se, K::wv4(c) * rj.y);
     }
-    // exact path: inside the band around either threshold, or close (see prep())
-    const float2 t = __fadd2_rn(d2, f2(-K::mid(c)));
-    const float bA = fabsf(fabsf(t.x) - K::half(c)), bB = fabsf(fabsf(t.y) - K::half(c));
-    const bool exA = vA & ((bA <= K::band(c)) | (d2.x < closeA));
-    const bool exB = vB & ((bB <= K::band(c)) | (d2.y < closeB));
+    // exact path: inside the band around either threshold, or close (see prep()).  Beyond
+    // the vdW reach (box distance^2 > tv2 + 1e-2) no pair is close or near the vdW threshold,
+    // and non-vdW visits only exist when the elec threshold is the pair cut-off (mid + half):
+    // one band test (for the default field bitwise the same decision: both differences are
+    // exact there)
+    bool exA, exB;
+    if (!VDW && !GEN && EALL) {
+        const float2 t = __fadd2_rn(d2, f2(-(K::mid(c) + K::half(c))));
+        exA = vA & (fabsf(t.x) <= K::band(c));
+        exB = vB & (fabsf(t.y) <= K::band(c));
+    } else {
+        const float2 t = __fadd2_rn(d2, f2(-K::mid(c)));
+        const float bA = fabsf(fabsf(t.x) - K::half(c)), bB = fabsf(fabsf(t.y) - K::half(c));
+        exA = vA & ((bA <= K::band(c)) | (d2.x < closeA));
+        exB = vB & ((bB <= K::band(c)) | (d2.y < closeB));
+    }
     if (__any_sync(FULL, exA | exB)) {   // rare: queue the exact-path pairs
         const unsigned ma = __ballot_sync(FULL, exA), mb = __ballot_sync(FULL, exB);
         int base = 0;
