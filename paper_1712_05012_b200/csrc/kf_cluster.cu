@@ -516,7 +516,13 @@ KF_DEV void lean_visit(const ClConst &c, const LeanUnit &u, float2 &fx, float2 &
     const float jx = oj.x - (cu.x - oc.x), jy = oj.y - (cu.y - oc.y), jz = oj.z - (cu.z - oc.z);
     const float2 dx = padd_b(u.ix, -jx), dy = padd_b(u.iy, -jy), dz = padd_b(u.iz, -jz);
     const float2 d2 = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __fmul2_rn(dx, dx)));
-    bool vA = (u.codes >> 30) & 1u, vB = (u.codes >> 31) & 1u;
+    // padding atoms (past n) sit at -FAR (i) / +FAR (j) offsets: no pair of theirs meets any
+    // threshold, so outside the own-octet visit the atom-exists bits need no test
+    bool vA = true, vB = true;
+    if (GEN) {
+        vA = (u.codes >> 30) & 1u;
+        vB = (u.codes >> 31) & 1u;
+    }
     float2 qq, weps;
     using K = KC<EALL>;
     float closeA = K::close4(c), closeB = K::close4(c);
